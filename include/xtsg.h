@@ -1,0 +1,229 @@
+/*
+ * xtsg — C ABI of the B200-native Exascale-Tensor compression path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/xts/{compression,cp_als,alignment}.hpp).
+ * Every entry point below names the reference function it replaces
+ * (file:line); the C++ facade in include/xts/xts_b200.hpp re-exposes them
+ * with the reference's exact C++ signatures and exception types.
+ *
+ * Conventions (shared by every function):
+ *  - Plain pointers and sizes only. Matrices are column-major
+ *    ((i,j) at i + rows*j, tensor.hpp:10-20); tensors are column-major
+ *    ((i,j,k) at i + n1*(j + n2*k), tensor.hpp:30-44); "P matrices back to
+ *    back" means replica p starts at p*rows*cols.
+ *  - A pointer may be host memory (pageable or pinned) or device memory of
+ *    the calling thread's current CUDA device; the library detects which and
+ *    stages host buffers itself. Results land where the output pointer points.
+ *  - Return value is a status code. Exceptions never cross the ABI: the
+ *    reference's exception taxonomy (errors.hpp:10-59) maps to the codes
+ *    below, the payload (effective_rank, column, survivors/required) is read
+ *    back with xtsg_last_payload(), the message with xtsg_last_error().
+ *    Both are thread-local.
+ *  - Thread-safe and re-entrant: each host thread gets its own CUDA stream
+ *    (the reference calls comp/cp_als concurrently from parallel_for,
+ *    pipeline.cpp:386-434). There is no CPU fallback: without a usable
+ *    sm_100 device every compute entry point returns XTSG_E_CUDA.
+ */
+#ifndef XTSG_H_
+#define XTSG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:10-59) ---------------------------------- */
+#define XTSG_OK 0
+#define XTSG_E_USAGE 1        /* xts::UsageError */
+#define XTSG_E_DATA 2         /* xts::DataError */
+#define XTSG_E_ILLPOSED 3     /* xts::IllPosedError; payload(0) = effective_rank */
+#define XTSG_E_DEGENERATE 4   /* xts::DegenerateColumnError; payload(0) = column */
+#define XTSG_E_INSUFFICIENT 5 /* xts::InsufficientReplicasError; payload(0)=survivors, (1)=required */
+#define XTSG_E_HALFRANGE 6    /* xts::HalfRangeError */
+#define XTSG_E_STAGE 7        /* xts::StageError; payload(0) = stage index */
+#define XTSG_E_CUDA 8         /* device missing / CUDA runtime failure */
+#define XTSG_E_INTERNAL 99
+
+const char* xtsg_last_error(void);
+int64_t xtsg_last_payload(int32_t which);
+/* Library/ABI version (major*100 + minor). */
+int32_t xtsg_version(void);
+/* 1 when an sm_100 device is usable by this thread, else 0. */
+int32_t xtsg_device_ready(void);
+
+/* ---- ensembles (compression.hpp:13-65, compression.cpp:15-200) --------- */
+#define XTSG_KIND_GAUSSIAN 0
+#define XTSG_KIND_SPARSE 1
+#define XTSG_KIND_TWO_STAGE 2
+
+typedef struct xtsg_ensemble_spec {
+  int32_t kind;       /* EnsembleSpec::Kind */
+  int32_t inner_kind; /* TwoStageSpec::inner_kind: 0 gaussian, 1 sparse */
+  double s;           /* SparseProjectionSpec::s for kind == sparse */
+  double alpha, beta, gamma; /* TwoStageSpec ratios */
+  double inner_s;     /* TwoStageSpec::inner_spec.s */
+} xtsg_ensemble_spec;
+
+/* compute_replica_count (compression.cpp:82-95) */
+int32_t xtsg_replica_count(const int64_t dims[3], const int64_t reduced[3], int64_t slack,
+                           int64_t* out);
+
+/* gen_gaussian (compression.cpp:97-103): one polar stream over all entries. */
+int32_t xtsg_gen_gaussian(int64_t rows, int64_t cols, uint64_t seed, double* out);
+
+/* gen_sparse_projection (compression.cpp:105-113) */
+int32_t xtsg_gen_sparse_projection(int64_t rows, int64_t cols, double s, uint64_t seed,
+                                   double* out);
+
+/* make_ensemble (compression.cpp:115-200). u: count matrices reduced[0] x dims[0]
+ * back to back (likewise v, w). For two-stage, inner_* (alpha*L x I ...) and
+ * outer_* (count matrices L x alpha*L ...) are written when non-null.
+ * Bit-exact with the reference on this image (glibc 2.39 log). */
+int32_t xtsg_make_ensemble(const int64_t dims[3], const int64_t reduced[3], int64_t count,
+                           int64_t shared_rows, const xtsg_ensemble_spec* spec, uint64_t seed,
+                           double* u, double* v, double* w, double* inner_u, double* inner_v,
+                           double* inner_w, double* outer_u, double* outer_v,
+                           double* outer_w);
+
+/* ---- compression, fp64 compatibility path ------------------------------ */
+/* comp (compression.cpp:211-213): y (l x m x n) = t x1 u x2 v x3 w, modes in
+ * the reference order 1 -> 2 -> 3, fp64 on the device. */
+int32_t xtsg_comp(const double* t, int64_t n1, int64_t n2, int64_t n3, const double* u,
+                  int64_t l, const double* v, int64_t m, const double* w, int64_t n, double* y);
+
+/* comp_from_factors (compression.cpp:215-220) */
+int32_t xtsg_comp_from_factors(const double* a, const double* b, const double* c, int64_t i,
+                               int64_t j, int64_t k, int64_t rank, const double* u, int64_t l,
+                               const double* v, int64_t m, const double* w, int64_t n,
+                               double* y);
+
+/* reconstruct (tensor.cpp:133-150) */
+int32_t xtsg_reconstruct(const double* a, const double* b, const double* c, int64_t i,
+                         int64_t j, int64_t k, int64_t rank, double* out);
+
+/* comp_blocked (compression.cpp:332-404) as a push stream. begin() checks the
+ * grid (BlockGrid ctor :222-230) and ensemble shapes; push() validates the
+ * record (:319-328) and rejects duplicates (:344-351, XTSG_E_DATA); finish()
+ * rejects gaps and writes the count replicas back to back. deterministic=1
+ * reassembles and runs one-shot comp (bitwise grid independent, :355-379);
+ * deterministic=0 compresses each block on arrival into fp64 accumulators in
+ * a fixed order (:381-403). */
+typedef struct xtsg_blocked xtsg_blocked;
+int32_t xtsg_blocked_begin(const int64_t dims[3], const int64_t block[3], int64_t count,
+                           const int64_t reduced[3], const double* u, const double* v,
+                           const double* w, int32_t deterministic, xtsg_blocked** out);
+int32_t xtsg_blocked_push(xtsg_blocked* h, const int64_t cell[3], const int64_t shape[3],
+                          const double* data);
+int32_t xtsg_blocked_finish(xtsg_blocked* h, double* y);
+void xtsg_blocked_destroy(xtsg_blocked* h);
+
+/* ---- compression, tensor-core fast path (the B200 hot path) ------------ */
+/* A plan owns the device-resident ensemble of one compression job: the P
+ * replicas' U stacked into one (P*L) x I bf16 operand, V transposed per
+ * replica, W in fp32, all generated on the device from the seed with the
+ * bit-exact RNG above (make_ensemble semantics). It then compresses dense
+ * slabs/blocks of X with the fused tcgen05 TTM kernel. */
+#define XTSG_PREC_FP64 0   /* DFMA chain; reference-order arithmetic */
+#define XTSG_PREC_BF16 1   /* tcgen05 kind::f16, bf16 operands, fp32 accumulation */
+
+#define XTSG_DTYPE_BF16 0
+#define XTSG_DTYPE_F32 1
+#define XTSG_DTYPE_F64 2
+
+typedef struct xtsg_plan_desc {
+  int64_t dims[3];     /* I, J, K */
+  int64_t reduced[3];  /* L, M, N */
+  int64_t count;       /* P */
+  int64_t shared_rows; /* S */
+  xtsg_ensemble_spec spec;
+  uint64_t seed;       /* make_ensemble seed */
+  int32_t precision;   /* XTSG_PREC_* */
+  int32_t reserved;
+} xtsg_plan_desc;
+
+typedef struct xtsg_plan xtsg_plan;
+int32_t xtsg_plan_create(const xtsg_plan_desc* desc, xtsg_plan** out);
+void xtsg_plan_destroy(xtsg_plan* plan);
+
+/* Compress the block of X that starts at offset[3] with extent[3] (a cell of
+ * a BlockGrid, a mode-3 slab, or the whole tensor) into the P replicas y
+ * (P x L x M x N, column-major per replica; fp32 for XTSG_PREC_BF16, fp64 for
+ * XTSG_PREC_FP64), accumulating when accumulate != 0. x points at the block's first element; ld[0] is the
+ * distance between consecutive j (>= extent[0]), ld[1] between consecutive k
+ * (>= ld[0]*extent[1]), in elements. x may be host or device memory, any
+ * XTSG_DTYPE_*; host or non-bf16 input is streamed slab by slab through a
+ * double-buffered H2D/convert pipeline overlapped with the tensor cores.
+ * stream: cudaStream_t to run on (NULL = the thread's stream). Returns
+ * after enqueueing when x and y are device memory, else synchronously. */
+int32_t xtsg_plan_compress(xtsg_plan* plan, const void* x, int32_t x_dtype, const int64_t ld[2],
+                           const int64_t offset[3], const int64_t extent[3], void* y,
+                           int32_t accumulate, void* stream);
+
+/* Same contraction for a tensor given by its CP factors (a: I x R, b: J x R,
+ * c: K x R, fp64): blocks of X are generated on the device slab by slab and
+ * never exist whole (the 10^12-element configs). k range [k0, k1). */
+int32_t xtsg_plan_compress_factors(xtsg_plan* plan, const double* a, const double* b,
+                                   const double* c, int64_t rank, int64_t k0, int64_t k1,
+                                   void* y, int32_t accumulate, void* stream);
+
+/* Sparse COO input (new, no reference counterpart; Eq. 3 restricted to the
+ * nonzeros, duplicates sum): coordinates int32 SoA (i[nnz], j[nnz], k[nnz]),
+ * values fp32. */
+int32_t xtsg_plan_compress_coo(xtsg_plan* plan, const int32_t* i, const int32_t* j,
+                               const int32_t* k, const float* val, int64_t nnz, void* y,
+                               int32_t accumulate, void* stream);
+
+/* Number of this library's kernels launched by the calling thread so far
+ * (evidence for the bench's gpu_launches). */
+int64_t xtsg_launch_count(void);
+
+/* ---- CP-ALS (cp_als.hpp:10-40, cp_als.cpp:22-111) ---------------------- */
+typedef struct xtsg_als_config {
+  int64_t rank;
+  int64_t max_iters;
+  double tol;
+  uint64_t seed;
+  int32_t init; /* 0 normal, 1 nvecs */
+  int32_t reserved;
+} xtsg_als_config;
+
+/* relative_error (cp_als.cpp:37-44) */
+int32_t xtsg_relative_error(const double* t, int64_t n1, int64_t n2, int64_t n3,
+                            const double* a, const double* b, const double* c, int64_t rank,
+                            double* out);
+
+/* cp_als on count tensors at once (each n1 x n2 x n3, back to back), one
+ * config per tensor. a/b/c: count factor matrices back to back. history:
+ * count x max_iters (unused tail untouched), iters/converged per tensor.
+ * count == 1 is the drop-in for xts::cp_als. */
+int32_t xtsg_cp_als_batched(int64_t count, const double* t, int64_t n1, int64_t n2, int64_t n3,
+                            const xtsg_als_config* cfg, double* a, double* b, double* c,
+                            int64_t* iters, int32_t* converged, double* history);
+
+/* ---- alignment & recovery (alignment.hpp:11-77, alignment.cpp) --------- */
+/* normalize_shared (alignment.cpp:66-85) */
+int32_t xtsg_normalize_shared(const double* m, int64_t rows, int64_t cols, int64_t shared_rows,
+                              double* normalized, double* pivots);
+/* max_trace_assignment (alignment.cpp:87-144) */
+int32_t xtsg_max_trace_assignment(const double* objective, int64_t n, int64_t* perm);
+/* align_replicas (alignment.cpp:154-218): factors = count triples back to back,
+ * each (a: dims[0] x r, b: dims[1] x r, c: dims[2] x r). */
+int32_t xtsg_align_replicas(int64_t count, const int64_t dims[3], int64_t r,
+                            const double* factors, int64_t shared_rows, int64_t min_survivors,
+                            double* aligned, int32_t* dropped, int64_t* survivors,
+                            int64_t* n_survivors);
+/* solve_stacked_ls (alignment.cpp:220-252 + linalg.cpp:76-92): column-pivoted
+ * Householder QR on the device, fp64; rank test like Eigen's
+ * ColPivHouseholderQR (|R_ii| > eps * cols * max|R_ii|). */
+int32_t xtsg_solve_stacked_ls(int64_t count, const int64_t* rows, int64_t r, int64_t cols,
+                              const double* f, const double* u, double* x);
+/* recover_perm_scale (alignment.cpp:254-278) */
+int32_t xtsg_recover_perm_scale(const double* global_head, const double* sampled,
+                                int64_t rows, int64_t cols, int64_t* perm, double* scale);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XTSG_H_ */

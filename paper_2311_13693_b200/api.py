@@ -1,0 +1,405 @@
+"""Python mirror of the reference entry points over the xtsg C ABI.
+
+Layout convention follows xts::Matrix / xts::Tensor3 (tensor.hpp:10-44):
+matrices and tensors are numpy arrays in Fortran (column-major) order, so
+``m[i, j]`` is the reference's ``m(i, j)`` and the memory image is identical.
+Device-resident inputs (torch CUDA tensors) are passed through untouched.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from ._lib import (AlsConfig, EnsembleSpec, PlanDesc, DTYPE_BF16, DTYPE_F32, DTYPE_F64,
+                   KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE, PREC_BF16, PREC_FP64, check, lib,
+                   ptr)
+
+_KINDS = {"gaussian": KIND_GAUSSIAN, "sparse": KIND_SPARSE, "two_stage": KIND_TWO_STAGE}
+
+
+def _f64(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _arr3(v) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(v, dtype=np.int64).reshape(3))
+
+
+def device_ready() -> bool:
+    return bool(lib.xtsg_device_ready())
+
+
+def launch_count() -> int:
+    return int(lib.xtsg_launch_count())
+
+
+def compute_replica_count(dims, reduced, slack: int) -> int:
+    """compression.cpp:82-95"""
+    out = np.zeros(1, np.int64)
+    check(lib.xtsg_replica_count(ptr(_arr3(dims)), ptr(_arr3(reduced)), int(slack), ptr(out)))
+    return int(out[0])
+
+
+def gen_gaussian(rows: int, cols: int, seed: int) -> np.ndarray:
+    """compression.cpp:97-103"""
+    out = np.zeros((max(rows, 0), max(cols, 0)), order="F")
+    check(lib.xtsg_gen_gaussian(int(rows), int(cols), C.c_uint64(seed), ptr(out)))
+    return out
+
+
+def gen_sparse_projection(rows: int, cols: int, s: float, seed: int) -> np.ndarray:
+    """compression.cpp:105-113"""
+    out = np.zeros((max(rows, 0), max(cols, 0)), order="F")
+    check(lib.xtsg_gen_sparse_projection(int(rows), int(cols), float(s), C.c_uint64(seed), ptr(out)))
+    return out
+
+
+def _spec(kind="gaussian", s=1.0, alpha=1.6, beta=1.6, gamma=1.6, inner_kind="sparse",
+          inner_s=1.0) -> EnsembleSpec:
+    k = _KINDS[kind] if isinstance(kind, str) else int(kind)
+    ik = _KINDS[inner_kind] if isinstance(inner_kind, str) else int(inner_kind)
+    return EnsembleSpec(k, ik, float(s), float(alpha), float(beta), float(gamma), float(inner_s))
+
+
+@dataclass
+class Ensemble:
+    """CompressionEnsemble (compression.hpp:33-65)."""
+    count: int
+    shared_rows: int
+    seed: int
+    u: list
+    v: list
+    w: list
+    two_stage: Optional[dict] = None
+
+
+def make_ensemble(dims, reduced, count: int, shared_rows: int, seed: int, kind="gaussian",
+                  **spec) -> Ensemble:
+    """compression.cpp:115-200 (bit-exact on the device)."""
+    dims, reduced = _arr3(dims), _arr3(reduced)
+    sp = _spec(kind, **spec)
+    P = max(int(count), 0)
+    bufs = [np.zeros((P, int(reduced[m]), int(dims[m])), np.float64) for m in range(3)]
+    mats = [np.zeros((P, int(reduced[m]), int(dims[m])), np.float64).transpose(0, 2, 1) for m in range(3)]
+    inner = outer = None
+    if sp.kind == KIND_TWO_STAGE:
+        ratio = [sp.alpha, sp.beta, sp.gamma]
+        ir = [int(np.floor(ratio[m] * reduced[m] + 0.5)) for m in range(3)]
+        inner = [np.zeros(ir[m] * int(dims[m])) for m in range(3)]
+        outer = [np.zeros(P * int(reduced[m]) * ir[m]) for m in range(3)]
+    raw = [np.zeros(P * int(reduced[m]) * int(dims[m])) for m in range(3)]
+    args = raw + (inner if inner else [None] * 3) + (outer if outer else [None] * 3)
+    check(lib.xtsg_make_ensemble(ptr(dims), ptr(reduced), int(count), int(shared_rows),
+                                 C.byref(sp), C.c_uint64(seed), *[ptr(a) for a in args]))
+    del bufs, mats
+    per = [int(reduced[m] * dims[m]) for m in range(3)]
+    lists = [[raw[m][p * per[m]:(p + 1) * per[m]].reshape(int(reduced[m]), int(dims[m]), order="F")
+              for p in range(P)] for m in range(3)]
+    ts = None
+    if inner:
+        ts = {
+            "inner": [inner[m].reshape(ir[m], int(dims[m]), order="F") for m in range(3)],
+            "outer": [[outer[m][p * reduced[m] * ir[m]:(p + 1) * reduced[m] * ir[m]].reshape(
+                int(reduced[m]), ir[m], order="F") for p in range(P)] for m in range(3)],
+        }
+    return Ensemble(int(count), int(shared_rows), int(seed), lists[0], lists[1], lists[2], ts)
+
+
+def comp(t, u, v, w) -> np.ndarray:
+    """compression.cpp:211-213 (fp64 on the device)."""
+    t, u, v, w = _f64(t), _f64(u), _f64(v), _f64(w)
+    if t.ndim != 3 or u.shape[1] != t.shape[0] or v.shape[1] != t.shape[1] or w.shape[1] != t.shape[2]:
+        from ._lib import UsageError
+        raise UsageError("comp: compression matrix columns must match tensor dims")
+    y = np.zeros((u.shape[0], v.shape[0], w.shape[0]), order="F")
+    check(lib.xtsg_comp(ptr(t), *t.shape, ptr(u), u.shape[0], ptr(v), v.shape[0], ptr(w),
+                        w.shape[0], ptr(y)))
+    return y
+
+
+def reconstruct(a, b, c) -> np.ndarray:
+    """tensor.cpp:133-150"""
+    a, b, c = _f64(a), _f64(b), _f64(c)
+    out = np.zeros((a.shape[0], b.shape[0], c.shape[0]), order="F")
+    check(lib.xtsg_reconstruct(ptr(a), ptr(b), ptr(c), a.shape[0], b.shape[0], c.shape[0],
+                               a.shape[1], ptr(out)))
+    return out
+
+
+def comp_from_factors(factors, u, v, w) -> np.ndarray:
+    """compression.cpp:215-220"""
+    a, b, c = (_f64(x) for x in factors)
+    u, v, w = _f64(u), _f64(v), _f64(w)
+    if u.shape[1] != a.shape[0] or v.shape[1] != b.shape[0] or w.shape[1] != c.shape[0]:
+        from ._lib import UsageError
+        raise UsageError("comp_from_factors: compression matrix columns must match factors")
+    y = np.zeros((u.shape[0], v.shape[0], w.shape[0]), order="F")
+    check(lib.xtsg_comp_from_factors(ptr(a), ptr(b), ptr(c), a.shape[0], b.shape[0], c.shape[0],
+                                     a.shape[1], ptr(u), u.shape[0], ptr(v), v.shape[0], ptr(w),
+                                     w.shape[0], ptr(y)))
+    return y
+
+
+def comp_blocked(dims, block, source: Iterable, ensemble: Ensemble, deterministic: bool = True):
+    """compression.cpp:332-404. ``source`` yields (cell, block_tensor) records."""
+    dims, block = _arr3(dims), _arr3(block)
+    P = ensemble.count
+    red = _arr3([ensemble.u[0].shape[0], ensemble.v[0].shape[0], ensemble.w[0].shape[0]])
+    src_dims = [ensemble.u[0].shape[1], ensemble.v[0].shape[1], ensemble.w[0].shape[1]]
+    if list(src_dims) != [int(d) for d in dims]:
+        from ._lib import UsageError
+        raise UsageError("comp_blocked: ensemble does not match grid dims")
+    u = np.concatenate([x.ravel(order="F") for x in ensemble.u])
+    v = np.concatenate([x.ravel(order="F") for x in ensemble.v])
+    w = np.concatenate([x.ravel(order="F") for x in ensemble.w])
+    h = C.c_void_p()
+    check(lib.xtsg_blocked_begin(ptr(dims), ptr(block), P, ptr(red), ptr(u), ptr(v), ptr(w),
+                                 1 if deterministic else 0, C.byref(h)))
+    try:
+        for cell, data in source:
+            data = _f64(data)
+            check(lib.xtsg_blocked_push(h, ptr(_arr3(cell)), ptr(_arr3(data.shape)), ptr(data)))
+        out = np.zeros(P * int(np.prod(red)))
+        check(lib.xtsg_blocked_finish(h, ptr(out)))
+    finally:
+        lib.xtsg_blocked_destroy(h)
+    n = int(np.prod(red))
+    return [out[p * n:(p + 1) * n].reshape(tuple(red), order="F") for p in range(P)]
+
+
+def _torch_dtype_code(t):
+    import torch
+    return {torch.bfloat16: DTYPE_BF16, torch.float32: DTYPE_F32, torch.float64: DTYPE_F64}[t.dtype]
+
+
+class Plan:
+    """Device-resident compression plan (include/xtsg.h, xtsg_plan_*)."""
+
+    def __init__(self, dims, reduced, count: int, shared_rows: int, seed: int,
+                 precision: int = PREC_BF16, kind="gaussian", **spec):
+        d = PlanDesc()
+        for m in range(3):
+            d.dims[m] = int(dims[m])
+            d.reduced[m] = int(reduced[m])
+        d.count = int(count)
+        d.shared_rows = int(shared_rows)
+        d.spec = _spec(kind, **spec)
+        d.seed = C.c_uint64(seed).value
+        d.precision = int(precision)
+        self.desc = d
+        self.dims = tuple(int(x) for x in dims)
+        self.reduced = tuple(int(x) for x in reduced)
+        self.count = int(count)
+        self.precision = int(precision)
+        self._h = C.c_void_p()
+        check(lib.xtsg_plan_create(C.byref(d), C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib.xtsg_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def out_shape(self):
+        return (self.count,) + self.reduced
+
+    def compress(self, x, y=None, offset=(0, 0, 0), extent=None, ld=None, accumulate=False,
+                 stream=None):
+        """Compress block ``x`` (column-major (i,j,k) block, numpy or torch) at ``offset``.
+
+        Returns y: (P, L, M, N) with each replica column-major, i.e. an array whose
+        ``y[p]`` memory image is the reference Tensor3 of replica p.
+        """
+        if isinstance(x, np.ndarray):
+            if x.dtype not in (np.float32, np.float64):
+                raise TypeError("numpy input must be float32/float64")
+            xa = np.asfortranarray(x)
+            code = DTYPE_F64 if xa.dtype == np.float64 else DTYPE_F32
+            shape = xa.shape
+            strides = [s // xa.itemsize for s in xa.strides]
+        else:
+            xa = x
+            code = _torch_dtype_code(x)
+            shape = tuple(x.shape)
+            strides = list(x.stride())
+        if extent is None:
+            extent = shape
+        if ld is None:
+            if strides[0] != 1:
+                raise ValueError("x must be column-major (i fastest)")
+            ld = (strides[1], strides[2])
+        ydt = np.float64 if self.precision == PREC_FP64 else np.float32
+        if y is None:
+            if isinstance(x, np.ndarray):
+                y = np.zeros(self.count * int(np.prod(self.reduced)), ydt)
+            else:
+                import torch
+                y = torch.zeros(self.count * int(np.prod(self.reduced)),
+                                dtype=torch.float64 if ydt == np.float64 else torch.float32,
+                                device=x.device)
+        st = None if stream is None else C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else stream)
+        check(lib.xtsg_plan_compress(self._h, ptr(xa), code, ptr(np.asarray(ld, np.int64)),
+                                     ptr(_arr3(offset)), ptr(_arr3(extent)), ptr(y),
+                                     1 if accumulate else 0, st))
+        return y
+
+    @staticmethod
+    def replicas(y, count, reduced):
+        """Split a flat output into per-replica column-major tensors (numpy)."""
+        n = int(np.prod(reduced))
+        y = np.asarray(y)
+        return [y[p * n:(p + 1) * n].reshape(tuple(reduced), order="F") for p in range(count)]
+
+
+# ---------------------------------------------------------------------------
+# CP-ALS (cp_als.hpp:10-40)
+
+@dataclass
+class AlsResult:
+    factors: tuple
+    iters: int
+    error_history: list
+    converged: bool
+
+    def final_error(self) -> float:
+        return self.error_history[-1] if self.error_history else 1.0
+
+
+def cp_als_batched(tensors: Sequence, rank: int, max_iters: int = 500, tol: float = 1e-10,
+                   seeds: Sequence[int] = (0,), init: Sequence[int] | int = 0):
+    ts = [_f64(t) for t in tensors]
+    n = len(ts)
+    n1, n2, n3 = ts[0].shape
+    cfgs = (AlsConfig * n)()
+    inits = [init] * n if isinstance(init, int) else list(init)
+    for q in range(n):
+        cfgs[q] = AlsConfig(int(rank), int(max_iters), float(tol), C.c_uint64(seeds[q]).value,
+                            int(inits[q]), 0)
+    flat = np.concatenate([t.ravel(order="F") for t in ts]) if n else np.zeros(0)
+    a = np.zeros(n * n1 * rank); b = np.zeros(n * n2 * rank); c = np.zeros(n * n3 * rank)
+    iters = np.zeros(n, np.int64); conv = np.zeros(n, np.int32); hist = np.zeros(n * max_iters)
+    check(lib.xtsg_cp_als_batched(n, ptr(flat), n1, n2, n3, cfgs, ptr(a), ptr(b), ptr(c),
+                                  ptr(iters), ptr(conv), ptr(hist)))
+    out = []
+    for q in range(n):
+        fa = a[q * n1 * rank:(q + 1) * n1 * rank].reshape(n1, rank, order="F")
+        fb = b[q * n2 * rank:(q + 1) * n2 * rank].reshape(n2, rank, order="F")
+        fc = c[q * n3 * rank:(q + 1) * n3 * rank].reshape(n3, rank, order="F")
+        it = int(iters[q])
+        out.append(AlsResult((fa, fb, fc), it, list(hist[q * max_iters:q * max_iters + it]), bool(conv[q])))
+    return out
+
+
+def cp_als(t, rank: int, max_iters: int = 500, tol: float = 1e-10, seed: int = 0, init: int = 0):
+    """cp_als.cpp:46-111"""
+    return cp_als_batched([t], rank, max_iters, tol, [seed], [init])[0]
+
+
+def relative_error(t, factors) -> float:
+    """cp_als.cpp:37-44"""
+    t = _f64(t)
+    a, b, c = (_f64(x) for x in factors)
+    out = np.zeros(1)
+    check(lib.xtsg_relative_error(ptr(t), *t.shape, ptr(a), ptr(b), ptr(c), a.shape[1], ptr(out)))
+    return float(out[0])
+
+
+# ---------------------------------------------------------------------------
+# alignment & recovery (alignment.hpp)
+
+def normalize_shared(m, shared_rows: int):
+    m = _f64(m)
+    out = np.zeros_like(m, order="F")
+    piv = np.zeros(m.shape[1])
+    check(lib.xtsg_normalize_shared(ptr(m), m.shape[0], m.shape[1], int(shared_rows), ptr(out), ptr(piv)))
+    return out, piv
+
+
+def max_trace_assignment(objective) -> list:
+    o = _f64(objective)
+    if o.ndim != 2 or o.shape[0] != o.shape[1]:
+        from ._lib import UsageError
+        raise UsageError("max_trace_assignment: objective must be square")
+    perm = np.zeros(o.shape[0], np.int64)
+    check(lib.xtsg_max_trace_assignment(ptr(o), o.shape[0], ptr(perm)))
+    return [int(x) for x in perm]
+
+
+def align_replicas(factors: Sequence, shared_rows: int, min_survivors: int = 1):
+    """alignment.cpp:154-218 -> (aligned, dropped, survivors)"""
+    P = len(factors)
+    if P == 0:
+        from ._lib import UsageError
+        raise UsageError("align_replicas: no replicas")
+    dims = _arr3([f[0].shape[0] for f in [factors[0]]] + [factors[0][1].shape[0], factors[0][2].shape[0]])
+    r = factors[0][0].shape[1]
+    flat = np.concatenate([np.concatenate([_f64(x).ravel(order="F") for x in f]) for f in factors])
+    per = int(dims.sum()) * r
+    aligned = np.zeros(P * per)
+    dropped = np.zeros(P, np.int32)
+    surv = np.zeros(P, np.int64)
+    ns = np.zeros(1, np.int64)
+    check(lib.xtsg_align_replicas(P, ptr(dims), r, ptr(flat), int(shared_rows), int(min_survivors),
+                                  ptr(aligned), ptr(dropped), ptr(surv), ptr(ns)))
+    out = []
+    for i in range(int(ns[0])):
+        base = aligned[i * per:(i + 1) * per]
+        o0 = dims[0] * r
+        o1 = o0 + dims[1] * r
+        out.append((base[:o0].reshape(dims[0], r, order="F"), base[o0:o1].reshape(dims[1], r, order="F"),
+                    base[o1:].reshape(dims[2], r, order="F")))
+    return out, [bool(x) for x in dropped], [int(x) for x in surv[:int(ns[0])]]
+
+
+def solve_stacked_ls(stacked_factors: Sequence, stacked_compressors: Sequence) -> np.ndarray:
+    """alignment.cpp:220-252"""
+    if len(stacked_factors) == 0 or len(stacked_factors) != len(stacked_compressors):
+        from ._lib import UsageError
+        raise UsageError("solve_stacked_ls: factor/compressor counts differ")
+    fs = [_f64(f) for f in stacked_factors]
+    us = [_f64(u) for u in stacked_compressors]
+    r = fs[0].shape[1]
+    cols = us[0].shape[1]
+    rows = np.array([f.shape[0] for f in fs], np.int64)
+    for f, u in zip(fs, us):
+        if f.shape[1] != r or u.shape[1] != cols or f.shape[0] != u.shape[0]:
+            from ._lib import UsageError
+            raise UsageError("solve_stacked_ls: inconsistent block shapes")
+    f = np.concatenate([x.ravel(order="F") for x in fs])
+    u = np.concatenate([x.ravel(order="F") for x in us])
+    x = np.zeros((cols, r), order="F")
+    check(lib.xtsg_solve_stacked_ls(len(fs), ptr(rows), r, cols, ptr(f), ptr(u), ptr(x)))
+    return x
+
+
+def recover_perm_scale(global_head, sampled):
+    g, s = _f64(global_head), _f64(sampled)
+    if g.shape != s.shape:
+        from ._lib import UsageError
+        raise UsageError("recover_perm_scale: blocks must share shape")
+    perm = np.zeros(g.shape[1], np.int64)
+    scale = np.zeros(g.shape[1])
+    check(lib.xtsg_recover_perm_scale(ptr(g), ptr(s), g.shape[0], g.shape[1], ptr(perm), ptr(scale)))
+    return [int(x) for x in perm], [float(x) for x in scale]
+
+
+def apply_forward(m, perm, scale) -> np.ndarray:
+    """alignment.cpp:280-291: column r = m[:, perm[r]] * scale[r]"""
+    m = _f64(m)
+    return np.asfortranarray(m[:, list(perm)] * np.asarray(scale)[None, :])
+
+
+def apply_recovery(m, perm, scale) -> np.ndarray:
+    """alignment.cpp:293-304"""
+    m = _f64(m)
+    out = np.zeros_like(m, order="F")
+    out[:, list(perm)] = m / np.asarray(scale)[None, :]
+    return out

@@ -1,0 +1,427 @@
+// The compression plan: device-resident ensemble + the fast compression path.
+//
+// Reference flow being replaced (pipeline.cpp:360-406): make_ensemble then
+// comp_blocked / comp_from_factors, with P independent mode-product chains
+// per block (compression.cpp:381-403). Here the ensemble is generated once on
+// the device (bit-exact RNG, ensemble.cu) and laid out for the tensor cores:
+//   Ustack : bf16 [ceil(P*Lpad/128)*128][ld_u]   row (p, l), i contiguous
+//   Vt     : bf16 [P*Mpad][ld_v]                 row (p, m), j contiguous
+//   Wf     : fp32 [P][N][K]                      row (p, n), k contiguous
+// Each compress call runs the fused mode-1/mode-2 kernel (ttm_tc.cu) over
+// k-chunks into Z[p][k][m][l] and folds mode 3 in with one batched GEMM per
+// chunk (Y_p += Z_p * W_p^T), accumulating straight into the caller's
+// replicas. Non-bf16 or host-resident input is streamed slab by slab through
+// a double-buffered H2D + convert pipeline on a second stream.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+#include "comp_f64.cuh"
+#include "ensemble.cuh"
+#include "gemm_simt.cuh"
+#include "plan.cuh"
+#include "ttm_tc.cuh"
+#include "xrng.cuh"
+
+namespace xtsg {
+
+namespace {
+
+// P column-major (rows x cols) fp64 matrices -> row-major [p*rows_pad + r][c]
+// with leading dimension ld, converted to T. 32x32 smem transpose tiles.
+template <class T>
+__global__ void pack_rows_kernel(const double* __restrict__ src, int64_t rows, int64_t cols, int64_t rows_pad,
+                                 int64_t ld, T* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int64_t p = blockIdx.z;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const double* s = src + p * rows * cols;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t c = c0 + dy, r = r0 + threadIdx.x;
+    tile[dy][threadIdx.x] = (r < rows && c < cols) ? s[r + rows * c] : 0.0;
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) {
+      const double v = tile[threadIdx.x][dy];
+      T* o = dst + (p * rows_pad + r) * ld + c;
+      if constexpr (std::is_same<T, float>::value) *o = static_cast<float>(v);
+      else *o = __double2bfloat16(v);
+    }
+  }
+}
+
+template <class T>
+void pack_rows(const double* src, int64_t count, int64_t rows, int64_t cols, int64_t rows_pad, int64_t ld, T* dst,
+               cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(rows, 32)),
+            static_cast<unsigned>(count));
+  pack_rows_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, rows_pad, ld, dst);
+  XLAUNCH_CHECK();
+}
+
+template <class T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<double>(double v) { return static_cast<float>(v); }
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// X block (i, j, k) at src[i + ld0*j + ld1*k] -> bf16 dst[(k*nj + j)*ldi + i],
+// zero for ni <= i < ldi.
+template <class T>
+__global__ void stage_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj, int64_t nk, int64_t ld0,
+                               int64_t ld1, int64_t ldi, __nv_bfloat16* __restrict__ dst) {
+  const int64_t rows = nj * nk;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t j = row % nj, k = row / nj;
+    const T* s = src + j * ld0 + k * ld1;
+    __nv_bfloat16* d = dst + row * ldi;
+    for (int64_t i = threadIdx.x; i < ldi; i += blockDim.x)
+      d[i] = __float2bfloat16(i < ni ? to_f(s[i]) : 0.f);
+  }
+}
+
+template <class T>
+__global__ void stage_x64_kernel(const T* __restrict__ src, int64_t ni, int64_t nj, int64_t nk, int64_t ld0,
+                                 int64_t ld1, double* __restrict__ dst) {
+  const int64_t total = ni * nj * nk;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % ni, jk = e / ni, j = jk % nj, k = jk / nj;
+    const T v = src[i + ld0 * j + ld1 * k];
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) dst[e] = static_cast<double>(__bfloat162float(v));
+    else dst[e] = static_cast<double>(v);
+  }
+}
+
+// Ypad (per replica (m*Lpad + l) x N column-major) -> y (l + L*(m + M*n)).
+__global__ void compact_y_kernel(const float* __restrict__ ypad, int64_t count, int64_t L, int64_t M, int64_t N,
+                                 int64_t lpad, int64_t mpad, int32_t accumulate, float* __restrict__ y) {
+  const int64_t per = L * M * N, total = count * per;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t p = e / per, r = e % per;
+    const int64_t l = r % L, mn = r / L, m = mn % M, n = mn / M;
+    const float v = ypad[p * mpad * lpad * N + (m * lpad + l) + mpad * lpad * n];
+    y[e] = accumulate ? y[e] + v : v;
+  }
+}
+
+int grid_for(int64_t work, int per_block = 256) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, per_block), 148 * 16)));
+}
+
+int64_t pad_reduced(int64_t d) {
+  if (d <= 32) return 32;
+  if (d <= 64) return 64;
+  if (d <= 128) return 128;
+  return -1;
+}
+
+int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+size_t dtype_size(int32_t dt) {
+  switch (dt) {
+    case XTSG_DTYPE_BF16: return 2;
+    case XTSG_DTYPE_F32: return 4;
+    case XTSG_DTYPE_F64: return 8;
+    default: usage("plan: unknown x dtype");
+  }
+}
+
+}  // namespace
+
+Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
+  const EnsembleShape sh =
+      validate_ensemble(desc.dims, desc.reduced, desc.count, desc.shared_rows, desc.spec);
+  (void)sh;
+  if (desc.precision != XTSG_PREC_FP64 && desc.precision != XTSG_PREC_BF16) usage("plan: unknown precision");
+  require_device();
+  XCUDA(cudaGetDevice(&device));
+  st = thread_stream();
+  XCUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
+  const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
+  const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
+  // fp64 ensemble in the reference layout (make_ensemble, bit-exact)
+  u64 = DevBuf<double>(static_cast<size_t>(P * L * I), st);
+  v64 = DevBuf<double>(static_cast<size_t>(P * M * J), st);
+  w64 = DevBuf<double>(static_cast<size_t>(P * N * K), st);
+  const int32_t rc = xtsg_make_ensemble(desc.dims, desc.reduced, P, desc.shared_rows, &desc.spec, desc.seed,
+                                        u64.ptr, v64.ptr, w64.ptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                        nullptr);
+  if (rc != XTSG_OK) throw Status(rc, std::string("plan: make_ensemble failed: ") + xtsg_last_error());
+  if (desc.precision == XTSG_PREC_BF16) {
+    lpad = pad_reduced(L);
+    mpad = pad_reduced(M);
+    if (lpad < 0 || mpad < 0) usage("plan: the bf16 tensor-core path supports reduced dims <= 128");
+    rpb = 128 / lpad;
+    n2 = rpb * mpad;
+    if (n2 > 128) usage("plan: (128/Lpad)*Mpad must be <= 128 for the tensor-core path");
+    rows_u = round_up(P * lpad, 128);
+    ld_u = round_up(I, 8);
+    ld_v = round_up(J, 8);
+    ustack = DevBuf<__nv_bfloat16>(static_cast<size_t>(rows_u * ld_u), st);
+    ustack.zero();
+    vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(P * mpad * ld_v), st);
+    vt.zero();
+    wf = DevBuf<float>(static_cast<size_t>(P * N * K), st);
+    pack_rows<__nv_bfloat16>(u64.ptr, P, L, I, lpad, ld_u, ustack.ptr, st);
+    pack_rows<__nv_bfloat16>(v64.ptr, P, M, J, mpad, ld_v, vt.ptr, st);
+    pack_rows<float>(w64.ptr, P, N, K, N, K, wf.ptr, st);
+    // fp64 copies are not needed by the bf16 path any more
+    u64.release();
+    v64.release();
+  }
+  XCUDA(cudaStreamSynchronize(st));
+}
+
+Plan::~Plan() {
+  cudaStreamSynchronize(st);
+  if (copy_st) {
+    cudaStreamSynchronize(copy_st);
+    cudaStreamDestroy(copy_st);
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (ev_copied[b]) cudaEventDestroy(ev_copied[b]);
+    if (ev_consumed[b]) cudaEventDestroy(ev_consumed[b]);
+  }
+}
+
+void Plan::check_block(const int64_t off[3], const int64_t ext[3]) const {
+  for (int m = 0; m < 3; ++m) {
+    if (off[m] < 0 || ext[m] < 1 || off[m] + ext[m] > desc.dims[m])
+      usage("plan_compress: block lies outside the tensor");
+  }
+}
+
+// Z = ttm(X block), Y(+)= Z W^T for k in [kb, kb + nk) of a bf16 device block.
+void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, const int64_t off[3],
+                          const int64_t ext[3], float* ydst, bool first_accumulate, cudaStream_t s) {
+  const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
+  const int64_t K = desc.dims[2];
+  // Operand slices; TMA needs 16-byte aligned bases, so unaligned offsets get
+  // an aligned copy of the slice.
+  const __nv_bfloat16* uop = ustack.ptr + off[0];
+  int64_t ldu = ld_u;
+  DevBuf<__nv_bfloat16> utmp, vtmp;
+  if (off[0] % 8) {
+    ldu = round_up(ext[0], 8);
+    utmp = DevBuf<__nv_bfloat16>(static_cast<size_t>(rows_u * ldu), s);
+    utmp.zero();
+    XCUDA(cudaMemcpy2DAsync(utmp.ptr, ldu * 2, ustack.ptr + off[0], ld_u * 2, ext[0] * 2, rows_u,
+                            cudaMemcpyDeviceToDevice, s));
+    uop = utmp.ptr;
+  }
+  const __nv_bfloat16* vop = vt.ptr + off[1];
+  int64_t ldv = ld_v;
+  if (off[1] % 8) {
+    ldv = round_up(ext[1], 8);
+    vtmp = DevBuf<__nv_bfloat16>(static_cast<size_t>(P * mpad * ldv), s);
+    vtmp.zero();
+    XCUDA(cudaMemcpy2DAsync(vtmp.ptr, ldv * 2, vt.ptr + off[1], ld_v * 2, ext[1] * 2, P * mpad,
+                            cudaMemcpyDeviceToDevice, s));
+    vop = vtmp.ptr;
+  }
+  const int64_t per_k = P * mpad * lpad;  // Z floats per slice
+  const int64_t kc_max = std::max<int64_t>(1, std::min<int64_t>(ext[2], (int64_t(1) << 28) / per_k));
+  ensure_z(kc_max * per_k, s);
+  bool acc = first_accumulate;
+  for (int64_t kb = 0; kb < ext[2]; kb += kc_max) {
+    const int64_t kc = std::min(kc_max, ext[2] - kb);
+    TtmLaunch tl{};
+    tl.u = uop; tl.rows_u = rows_u; tl.ld_u = ldu;
+    tl.x = x; tl.ni = ext[0]; tl.nj = ext[1]; tl.nk = ext[2]; tl.ld_x0 = ld0; tl.ld_x1 = ld1;
+    tl.v = vop; tl.rows_v = P * mpad; tl.ld_v = ldv;
+    tl.mpad = static_cast<int>(mpad);
+    tl.grid_limit = grid_limit;
+    tl.prm.n_rb = static_cast<int32_t>(rows_u / 128);
+    tl.prm.kc = static_cast<int32_t>(kc);
+    tl.prm.k_first = static_cast<int32_t>(kb);
+    tl.prm.j_tiles = static_cast<int32_t>(ceil_div(ext[1], ttm_block_n()));
+    tl.prm.k_steps = static_cast<int32_t>(ceil_div(ext[0], 64));
+    tl.prm.lpad = static_cast<int32_t>(lpad);
+    tl.prm.rpb = static_cast<int32_t>(rpb);
+    tl.prm.n2 = static_cast<int32_t>(n2);
+    tl.prm.count = static_cast<int32_t>(P);
+    tl.prm.z = zbuf.ptr;
+    launch_ttm_fused(tl, s);
+    // mode 3: Y_p (Mpad*Lpad x N) (+)= Z_p (Mpad*Lpad x kc) * W_p[:, k0+kb : +kc]^T
+    GemmArgs<float> g;
+    g.m = mpad * lpad; g.n = N; g.k = kc; g.batch = P;
+    g.a = zbuf.ptr; g.lda = mpad * lpad; g.stride_a = kc * mpad * lpad;
+    g.b = wf.ptr + off[2] + kb; g.ldb = K; g.stride_b = N * K;
+    g.c = ydst; g.ldc = mpad * lpad; g.stride_c = mpad * lpad * N;
+    g.beta = acc ? 1.f : 0.f;
+    gemm_simt(g, s);
+    acc = true;
+  }
+  (void)L;
+  (void)M;
+}
+
+void Plan::ensure_z(int64_t floats, cudaStream_t s) {
+  if (static_cast<int64_t>(zbuf.n) >= floats) return;
+  zbuf = DevBuf<float>(static_cast<size_t>(floats), s);
+}
+
+void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int64_t off[3],
+                    const int64_t ext[3], void* y, bool accumulate, cudaStream_t s) {
+  check_block(off, ext);
+  const size_t es = dtype_size(dtype);
+  if (ld[0] < ext[0] || ld[1] < ld[0] * ext[1]) usage("plan_compress: leading dimensions too small");
+  const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
+  const int64_t ysz = P * L * M * N;
+  const bool x_dev = is_device_ptr(x);
+  const size_t x_span = static_cast<size_t>((ext[2] - 1) * ld[1] + (ext[1] - 1) * ld[0] + ext[0]);
+
+  if (desc.precision == XTSG_PREC_FP64) {
+    OutView<double> yo(static_cast<double*>(y), static_cast<size_t>(ysz), s);
+    if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 8, cudaMemcpyHostToDevice, s));
+    DevBuf<uint8_t> raw;
+    const void* xd = x;
+    if (!x_dev) {
+      raw = DevBuf<uint8_t>(x_span * es, s);
+      XCUDA(cudaMemcpyAsync(raw.ptr, x, x_span * es, cudaMemcpyHostToDevice, s));
+      xd = raw.ptr;
+    }
+    DevBuf<double> x64(static_cast<size_t>(ext[0] * ext[1] * ext[2]), s);
+    const int64_t tot = ext[0] * ext[1] * ext[2];
+    if (dtype == XTSG_DTYPE_F64)
+      stage_x64_kernel<double><<<grid_for(tot), 256, 0, s>>>(static_cast<const double*>(xd), ext[0], ext[1], ext[2],
+                                                             ld[0], ld[1], x64.ptr);
+    else if (dtype == XTSG_DTYPE_F32)
+      stage_x64_kernel<float><<<grid_for(tot), 256, 0, s>>>(static_cast<const float*>(xd), ext[0], ext[1], ext[2],
+                                                            ld[0], ld[1], x64.ptr);
+    else
+      stage_x64_kernel<__nv_bfloat16><<<grid_for(tot), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(xd), ext[0],
+                                                                    ext[1], ext[2], ld[0], ld[1], x64.ptr);
+    XLAUNCH_CHECK();
+    const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
+    for (int64_t p = 0; p < P; ++p)
+      comp_f64_dev(x64.ptr, ext[0], ext[1], ext[2], u64.ptr + p * L * I + off[0] * L, L, L,
+                   v64.ptr + p * M * J + off[1] * M, M, M, w64.ptr + p * N * K + off[2] * N, N, N,
+                   yo.dev + p * L * M * N, accumulate ? 1.0 : 0.0, s);
+    if (yo.host) yo.finish();
+    return;
+  }
+
+  // ---- bf16 tensor-core path ----
+  const bool padded = (lpad != L) || (mpad != M);
+  OutView<float> yo(static_cast<float*>(y), static_cast<size_t>(ysz), s);
+  if (accumulate && yo.host && !padded) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
+  DevBuf<float> ypad;
+  float* ydst = yo.dev;
+  bool acc_first = accumulate;
+  if (padded) {
+    ypad = DevBuf<float>(static_cast<size_t>(P * mpad * lpad * N), s);
+    ydst = ypad.ptr;
+    acc_first = false;
+    if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
+  }
+  const bool direct = x_dev && dtype == XTSG_DTYPE_BF16 && ld[0] % 8 == 0 && ld[1] % 8 == 0 &&
+                      reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  if (direct) {
+    run_bf16_block(static_cast<const __nv_bfloat16*>(x), ld[0], ld[1], off, ext, ydst, acc_first, s);
+  } else {
+    // Slab pipeline: copy_st moves raw slab k-ranges H2D (host input) while s
+    // converts the previous slab to bf16 and runs the tensor cores on it.
+    const int64_t ldi = round_up(ext[0], 8);
+    const int64_t slab_bytes_raw = ld[1] * static_cast<int64_t>(es);
+    const int64_t target = int64_t(1) << 30;  // ~1 GiB of bf16 per slab
+    int64_t ks = std::max<int64_t>(1, target / std::max<int64_t>(1, ldi * ext[1] * 2));
+    ks = std::min(ks, ext[2]);
+    DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * ext[1] * ldi), s);
+    DevBuf<uint8_t> raw[2];
+    if (!x_dev) {
+      for (int b = 0; b < 2; ++b) {
+        raw[b] = DevBuf<uint8_t>(static_cast<size_t>(ks * slab_bytes_raw), s);
+        if (!ev_copied[b]) XCUDA(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
+        if (!ev_consumed[b]) XCUDA(cudaEventCreateWithFlags(&ev_consumed[b], cudaEventDisableTiming));
+      }
+      XCUDA(cudaStreamSynchronize(s));  // raw buffers allocated before copy_st uses them
+    }
+    const uint8_t* xb = static_cast<const uint8_t*>(x);
+    auto issue_copy = [&](int64_t slab, int b) {
+      const int64_t k0 = slab * ks, kn = std::min(ks, ext[2] - k0);
+      const size_t bytes = static_cast<size_t>(((kn - 1) * ld[1] + (ext[1] - 1) * ld[0] + ext[0]) * es);
+      XCUDA(cudaStreamWaitEvent(copy_st, ev_consumed[b], 0));
+      XCUDA(cudaMemcpyAsync(raw[b].ptr, xb + k0 * ld[1] * es, bytes, cudaMemcpyHostToDevice, copy_st));
+      XCUDA(cudaEventRecord(ev_copied[b], copy_st));
+    };
+    const int64_t nslabs = ceil_div(ext[2], ks);
+    if (!x_dev) {
+      // mark both buffers free
+      for (int b = 0; b < 2; ++b) XCUDA(cudaEventRecord(ev_consumed[b], s));
+      issue_copy(0, 0);
+    }
+    bool acc = acc_first;
+    for (int64_t sl = 0; sl < nslabs; ++sl) {
+      const int64_t k0 = sl * ks, kn = std::min(ks, ext[2] - k0);
+      const int b = static_cast<int>(sl & 1);
+      const uint8_t* src;
+      if (!x_dev) {
+        if (sl + 1 < nslabs) issue_copy(sl + 1, 1 - b);
+        XCUDA(cudaStreamWaitEvent(s, ev_copied[b], 0));
+        src = raw[b].ptr;
+      } else {
+        src = xb + k0 * ld[1] * es;
+      }
+      const int64_t rows = kn * ext[1];
+      const int blocks = static_cast<int>(std::min<int64_t>(rows, 148 * 8));
+      if (dtype == XTSG_DTYPE_F64)
+        stage_x_kernel<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
+                                                       ld[0], ld[1], ldi, stage.ptr);
+      else if (dtype == XTSG_DTYPE_F32)
+        stage_x_kernel<float><<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(src), ext[0], ext[1], kn,
+                                                      ld[0], ld[1], ldi, stage.ptr);
+      else
+        stage_x_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(src), ext[0],
+                                                              ext[1], kn, ld[0], ld[1], ldi, stage.ptr);
+      XLAUNCH_CHECK();
+      if (!x_dev) XCUDA(cudaEventRecord(ev_consumed[b], s));
+      const int64_t soff[3] = {off[0], off[1], off[2] + k0};
+      const int64_t sext[3] = {ext[0], ext[1], kn};
+      run_bf16_block(stage.ptr, ldi, ldi * ext[1], soff, sext, ydst, acc, s);
+      acc = true;
+    }
+  }
+  if (padded) {
+    compact_y_kernel<<<grid_for(ysz), 256, 0, s>>>(ypad.ptr, P, L, M, N, lpad, mpad, accumulate ? 1 : 0, yo.dev);
+    XLAUNCH_CHECK();
+  }
+  if (yo.host || !x_dev) yo.finish();
+}
+
+}  // namespace xtsg
+
+using namespace xtsg;
+
+extern "C" {
+
+int32_t xtsg_plan_create(const xtsg_plan_desc* desc, xtsg_plan** out) {
+  return guard([&] {
+    *out = nullptr;
+    auto* p = new Plan(*desc);
+    *out = reinterpret_cast<xtsg_plan*>(p);
+  });
+}
+
+void xtsg_plan_destroy(xtsg_plan* plan) { delete reinterpret_cast<Plan*>(plan); }
+
+int32_t xtsg_plan_compress(xtsg_plan* plan, const void* x, int32_t x_dtype, const int64_t ld[2],
+                           const int64_t offset[3], const int64_t extent[3], void* y, int32_t accumulate,
+                           void* stream) {
+  return guard([&] {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
+    p->compress(x, x_dtype, ld, offset, extent, y, accumulate != 0, s);
+  });
+}
+
+}  // extern "C"

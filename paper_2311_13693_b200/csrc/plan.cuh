@@ -1,0 +1,34 @@
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace xtsg {
+
+struct Plan {
+  xtsg_plan_desc desc;
+  int device = 0;
+  cudaStream_t st = nullptr;       // creation stream
+  cudaStream_t copy_st = nullptr;  // H2D slab stream
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  // fp64 reference-layout ensemble (kept for the fp64 path; W also feeds Wf)
+  DevBuf<double> u64, v64, w64;
+  // tensor-core operands
+  int64_t lpad = 0, mpad = 0, rpb = 0, n2 = 0, rows_u = 0, ld_u = 0, ld_v = 0;
+  DevBuf<__nv_bfloat16> ustack, vt;
+  DevBuf<float> wf;
+  DevBuf<float> zbuf;
+  int grid_limit = 0;  // testing knob: cap on persistent CTAs (0 = #SMs)
+
+  explicit Plan(const xtsg_plan_desc& d);
+  ~Plan();
+  void check_block(const int64_t off[3], const int64_t ext[3]) const;
+  void compress(const void* x, int32_t dtype, const int64_t ld[2], const int64_t off[3], const int64_t ext[3],
+                void* y, bool accumulate, cudaStream_t s);
+  void run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, const int64_t off[3],
+                      const int64_t ext[3], float* ydst, bool first_accumulate, cudaStream_t s);
+  void ensure_z(int64_t floats, cudaStream_t s);
+};
+
+}  // namespace xtsg

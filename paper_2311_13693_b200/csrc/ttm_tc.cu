@@ -1,0 +1,360 @@
+// K2+K3 — fused stacked mode-1 / mode-2 TTM on the 5th-gen tensor cores.
+//
+// Reference semantics: comp_with (compression.cpp:202-209) for all P replicas
+// of an ensemble at once: Y_p = X x1 U_p x2 V_p x3 W_p. This kernel computes
+// the first two mode products for every replica and every mode-3 slice k,
+//   Z_p[:, :, k] = U_p * X[:, :, k] * V_p^T          (L x M per (p, k)),
+// and leaves mode 3 (a K-contraction of Z with W_p, 1/M of mode-2's work) to a
+// follow-up GEMM. The P replicas' U_p are stacked into one (P*L) x I operand
+// so each X tile is multiplied by all replicas straight out of shared memory.
+//
+// Tiling (one CTA per SM, persistent, static schedule):
+//   unit  = (row block rb of 128 stacked U rows = 128/L replicas, slice k)
+//   tile  = 256 consecutive j of that slice; a unit walks all J/256 tiles
+//   mode 1: D1[128 x 256] (fp32, TMEM) = Ustack[rb] (128 x I) * X[:, jtile, k]
+//           K-loop over i in 64-wide chunks, A/B staged by TMA (SWIZZLE_128B)
+//   mode 2: the epilogue warps drain D1 64 columns at a time to bf16 in smem
+//           (A2, K-major SW128) and a second MMA stream computes
+//           D2[128 x RPB*M] = A2 (128 x 256 j) * Vt_block (RPB*M x 256 j)^T
+//           into the *already drained* first columns of the same TMEM buffer,
+//           so TMEM holds two 256-column mode-1 accumulators (double buffer)
+//           and no extra columns. The diagonal RPB blocks of D2 (row replica
+//           == column replica) are accumulated over the unit's j tiles in the
+//           epilogue's registers and written once per unit as Z[p][k][m][l].
+// Warp roles (256 threads): w0 TMA producer (U, X), w1 mode-1 MMA issuer +
+// TMEM owner, w2 TMA producer (Vt), w3 mode-2 MMA issuer, w4-7 epilogue (one
+// TMEM lane quarter each). All hand-offs are mbarriers; tcgen05.commit
+// releases smem stages and signals accumulators.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+#include "ttm_tc.cuh"
+
+namespace xtsg {
+
+namespace {
+
+constexpr int BM = 128;       // stacked U rows per tile (UMMA M)
+constexpr int BN = 256;       // j per tile (UMMA N of mode 1)
+constexpr int BK = 64;        // i per stage (128 B = one SW128 atom row)
+constexpr int S1 = 3;         // mode-1 pipeline stages
+constexpr int A_BYTES = BM * BK * 2;       // 16 KB
+constexpr int B_BYTES = BN * BK * 2;       // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int A2_BYTES = BM * 64 * 2;      // 16 KB (128 rows x 64 j)
+constexpr int B2_BYTES = 128 * 64 * 2;     // up to 128 (p,m) rows x 64 j
+constexpr int CHUNKS = BN / 64;            // mode-2 K chunks per tile
+constexpr int SMEM_DATA = S1 * STAGE_BYTES + 2 * A2_BYTES + 2 * B2_BYTES;
+constexpr int SMEM_TOTAL = SMEM_DATA + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t IDESC1 = ptx::idesc_bf16(BM, BN);
+
+struct Bars {
+  uint64_t full1[S1], empty1[S1];
+  uint64_t tmem_full[2], tmem_empty[2], d2_full[2];
+  uint64_t a2_full[2], a2_empty[2], b2_full[2], b2_empty[2];
+  uint32_t tmem_base;
+};
+
+template <int MPAD>
+__global__ void __launch_bounds__(256, 1)
+    ttm_fused_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_x,
+                     const __grid_constant__ CUtensorMap tm_v, const TtmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  uint8_t* a2_base = smem + S1 * STAGE_BYTES;
+  uint8_t* b2_base = a2_base + 2 * A2_BYTES;
+  Bars* bars = reinterpret_cast<Bars*>(b2_base + 2 * B2_BYTES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S1; ++s) {
+      ptx::mbar_init(&bars->full1[s], 1);
+      ptx::mbar_init(&bars->empty1[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&bars->tmem_full[b], 1);
+      ptx::mbar_init(&bars->tmem_empty[b], 128);
+      ptx::mbar_init(&bars->d2_full[b], 1);
+      ptx::mbar_init(&bars->a2_full[b], 128);
+      ptx::mbar_init(&bars->a2_empty[b], 1);
+      ptx::mbar_init(&bars->b2_full[b], 1);
+      ptx::mbar_init(&bars->b2_empty[b], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tm_u);
+    ptx::tma_prefetch(&tm_x);
+    ptx::tma_prefetch(&tm_v);
+  }
+  if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  const int n_units = p.n_rb * p.kc;
+  const int j_tiles = p.j_tiles;
+  const int k_steps = p.k_steps;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer: U rows and X tiles -------------------------------
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int kk = u / p.n_rb, rb = u % p.n_rb;
+        for (int jt = 0; jt < j_tiles; ++jt) {
+          for (int ks = 0; ks < k_steps; ++ks) {
+            ptx::mbar_wait(&bars->empty1[s], ph ^ 1);
+            uint8_t* st = stage_base + s * STAGE_BYTES;
+            ptx::mbar_arrive_expect_tx(&bars->full1[s], STAGE_BYTES);
+            ptx::tma_load_2d(st, &tm_u, &bars->full1[s], ks * BK, rb * BM);
+            ptx::tma_load_3d(st + A_BYTES, &tm_x, &bars->full1[s], ks * BK, jt * BN, p.k_first + kk);
+            if (++s == S1) { s = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- mode-1 MMA issuer ----------------------------------------------
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t t = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+          const uint32_t b = t & 1, use = t >> 1;
+          ptx::mbar_wait(&bars->tmem_empty[b], (use & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d = tmem + b * 256;
+          for (int ks = 0; ks < k_steps; ++ks) {
+            ptx::mbar_wait(&bars->full1[s], ph);
+            ptx::tc_fence_after();
+            const uint32_t a0 = ptx::smem_u32(stage_base + s * STAGE_BYTES);
+            const uint32_t b0 = a0 + A_BYTES;
+#pragma unroll
+            for (int k4 = 0; k4 < BK / 16; ++k4)
+              ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), IDESC1,
+                            (ks | k4) != 0);
+            ptx::mma_commit(&bars->empty1[s]);
+            if (++s == S1) { s = 0; ph ^= 1; }
+          }
+          ptx::mma_commit(&bars->tmem_full[b]);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // ---- TMA producer: Vt chunks for mode 2 -----------------------------
+      const uint32_t bytes = static_cast<uint32_t>(p.n2) * 128;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int rb = u % p.n_rb;
+        for (int jt = 0; jt < j_tiles; ++jt) {
+          for (int c = 0; c < CHUNKS; ++c) {
+            const int slot = c & 1;
+            const uint32_t par = (c >> 1) & 1;
+            ptx::mbar_wait(&bars->b2_empty[slot], par ^ 1);
+            ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], bytes);
+            ptx::tma_load_2d(b2_base + slot * B2_BYTES, &tm_v, &bars->b2_full[slot], jt * BN + c * 64,
+                             rb * p.n2);
+          }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ---- mode-2 MMA issuer ----------------------------------------------
+      const uint32_t idesc2 = ptx::idesc_bf16(BM, p.n2);
+      uint32_t t = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+          const uint32_t b = t & 1;
+          const uint32_t d = tmem + b * 256;
+          // D2 overwrites D1 columns [0, n2): both of the first two 64-col
+          // chunks must have been drained before the first mode-2 MMA.
+          ptx::mbar_wait(&bars->a2_full[0], 0);
+          ptx::mbar_wait(&bars->a2_full[1], 0);
+          for (int c = 0; c < CHUNKS; ++c) {
+            const int slot = c & 1;
+            const uint32_t par = (c >> 1) & 1;
+            if (c >= 2) ptx::mbar_wait(&bars->a2_full[slot], par);
+            ptx::mbar_wait(&bars->b2_full[slot], par);
+            ptx::tc_fence_after();
+            const uint32_t a0 = ptx::smem_u32(a2_base + slot * A2_BYTES);
+            const uint32_t b0 = ptx::smem_u32(b2_base + slot * B2_BYTES);
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4)
+              ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc2,
+                            (c | k4) != 0);
+            ptx::mma_commit(&bars->a2_empty[slot]);
+            ptx::mma_commit(&bars->b2_empty[slot]);
+          }
+          ptx::mma_commit(&bars->d2_full[b]);
+        }
+      }
+    }
+  } else {
+    // ---- epilogue: 4 warps, one TMEM lane quarter each ---------------------
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // tile row == TMEM lane
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int p_local = r / p.lpad;
+    const int l = r % p.lpad;
+    uint32_t t = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int kk = u / p.n_rb, rb = u % p.n_rb;
+      float zacc[MPAD];
+#pragma unroll
+      for (int m = 0; m < MPAD; ++m) zacc[m] = 0.f;
+      for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+        const uint32_t b = t & 1, use = t >> 1;
+        ptx::mbar_wait(&bars->tmem_full[b], use & 1);
+        ptx::tc_fence_after();
+        for (int c = 0; c < CHUNKS; ++c) {
+          const int slot = c & 1;
+          const uint32_t par = (c >> 1) & 1;
+          ptx::mbar_wait(&bars->a2_empty[slot], par ^ 1);
+          uint8_t* row = a2_base + slot * A2_BYTES + r * 128;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            float v[32];
+            ptx::tmem_ld32(lane_addr + b * 256 + c * 64 + h * 32, v);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int q8 = h * 4 + q4;
+              uint4 pk;
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(v[q4 * 8 + 0], v[q4 * 8 + 1]);
+              __nv_bfloat162 h1 = __floats2bfloat162_rn(v[q4 * 8 + 2], v[q4 * 8 + 3]);
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[q4 * 8 + 4], v[q4 * 8 + 5]);
+              __nv_bfloat162 h3 = __floats2bfloat162_rn(v[q4 * 8 + 6], v[q4 * 8 + 7]);
+              pk.x = *reinterpret_cast<uint32_t*>(&h0);
+              pk.y = *reinterpret_cast<uint32_t*>(&h1);
+              pk.z = *reinterpret_cast<uint32_t*>(&h2);
+              pk.w = *reinterpret_cast<uint32_t*>(&h3);
+              *reinterpret_cast<uint4*>(row + ((q8 ^ (r & 7)) << 4)) = pk;
+            }
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&bars->a2_full[slot]);
+        }
+        ptx::mbar_wait(&bars->d2_full[b], use & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int mc = 0; mc < MPAD / 32; ++mc) {
+          float v[32];
+          ptx::tmem_ld32(lane_addr + b * 256 + p_local * MPAD + mc * 32, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) zacc[mc * 32 + e] += v[e];
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&bars->tmem_empty[b]);
+      }
+      const int prep = rb * p.rpb + p_local;
+      if (prep < p.count) {
+        float* dst = p.z + ((static_cast<int64_t>(prep) * p.kc + kk) * MPAD) * p.lpad + l;
+        const int stride = p.lpad;
+#pragma unroll
+        for (int m = 0; m < MPAD; ++m) {
+          __stcs(dst, zacc[m]);
+          dst += stride;
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      throw Status(XTSG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFn>(f);
+  }();
+  return fn;
+}
+
+void make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              const uint32_t* box) {
+  cuuint64_t d[3], s[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  if (reinterpret_cast<uintptr_t>(base) % 16) usage("tma: base address must be 16-byte aligned");
+  for (int i = 0; i < rank - 1; ++i)
+    if (s[i] % 16) usage("tma: strides must be multiples of 16 bytes");
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, bx, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Status(XTSG_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+template <int MPAD>
+void launch_impl(const TtmLaunch& L, cudaStream_t st) {
+  CUtensorMap mu, mx, mv;
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.rows_u)};
+    const uint64_t str[1] = {static_cast<uint64_t>(L.ld_u) * 2};
+    const uint32_t box[2] = {BK, BM};
+    make_map(&mu, L.u, 2, dims, str, box);
+  }
+  {
+    const uint64_t dims[3] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.nk)};
+    const uint64_t str[2] = {static_cast<uint64_t>(L.ld_x0) * 2, static_cast<uint64_t>(L.ld_x1) * 2};
+    const uint32_t box[3] = {BK, BN, 1};
+    make_map(&mx, L.x, 3, dims, str, box);
+  }
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.rows_v)};
+    const uint64_t str[1] = {static_cast<uint64_t>(L.ld_v) * 2};
+    const uint32_t box[2] = {64, static_cast<uint32_t>(L.prm.n2)};
+    make_map(&mv, L.v, 2, dims, str, box);
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    XCUDA(cudaFuncSetAttribute(ttm_fused_kernel<MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
+    attr_set = true;
+  }
+  const int units = L.prm.n_rb * L.prm.kc;
+  const int grid = std::min(units, L.grid_limit > 0 ? L.grid_limit : sm_count());
+  ttm_fused_kernel<MPAD><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, L.prm);
+  XLAUNCH_CHECK();
+}
+
+}  // namespace
+
+void launch_ttm_fused(const TtmLaunch& L, cudaStream_t st) {
+  if (L.prm.n2 > 128 || L.prm.n2 % 16 || L.prm.lpad * L.prm.rpb != BM)
+    usage("ttm_fused: unsupported reduced dims for the tensor-core path");
+  switch (L.mpad) {
+    case 32: launch_impl<32>(L, st); break;
+    case 64: launch_impl<64>(L, st); break;
+    case 128: launch_impl<128>(L, st); break;
+    default: usage("ttm_fused: M must pad to 32, 64 or 128");
+  }
+}
+
+int ttm_block_n() { return BN; }
+
+}  // namespace xtsg

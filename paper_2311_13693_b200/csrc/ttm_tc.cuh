@@ -1,0 +1,35 @@
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace xtsg {
+
+struct TtmParams {
+  int32_t n_rb;      // row blocks of 128 stacked U rows
+  int32_t kc;        // slices k in this launch (units = n_rb * kc)
+  int32_t k_first;   // first slice (X map coordinate)
+  int32_t j_tiles;   // ceil(nj / 256)
+  int32_t k_steps;   // ceil(ni / 64)
+  int32_t lpad, rpb; // padded L, replicas per row block (lpad * rpb == 128)
+  int32_t n2;        // rpb * mpad (mode-2 MMA N)
+  int32_t count;     // P
+  float* z;          // out: Z[p][kk][m][l], kk in [0, kc)
+};
+
+struct TtmLaunch {
+  const void* u;      // bf16 stacked U: rows_u x ld_u (row-major), columns [0, ni) used
+  int64_t rows_u, ld_u;
+  const void* x;      // bf16 X block: (i, j, k) at i + ld_x0*j + ld_x1*k
+  int64_t ni, nj, nk, ld_x0, ld_x1;
+  const void* v;      // bf16 Vt: rows_v x ld_v (row (p,m), j contiguous)
+  int64_t rows_v, ld_v;
+  int mpad;
+  int grid_limit;     // 0 = number of SMs
+  TtmParams prm;
+};
+
+void launch_ttm_fused(const TtmLaunch& l, cudaStream_t st);
+int ttm_block_n();
+
+}  // namespace xtsg

@@ -1,0 +1,86 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/xtsg.h declares, maps the reference's error taxonomy, and
+refuses compute without a device (no CPU fallback)."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "xtsg.h").read_text()
+    return sorted(set(re.findall(r"\b(xtsg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(xt):
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    lib = C.CDLL(str(ROOT / "paper_2311_13693_b200" / "libxtsg.so"))
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a(xt):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                          str(ROOT / "paper_2311_13693_b200" / "libxtsg.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_replica_count_and_errors(xt):
+    # compression.cpp:82-95 and test_compression.cpp:15-21 (host arithmetic)
+    assert xt.compute_replica_count([1000] * 3, [50] * 3, 10) == 31
+    assert xt.compute_replica_count([300] * 3, [50] * 3, 0) == 7
+    assert xt.compute_replica_count([20] * 3, [20] * 3, 0) == 1
+    with pytest.raises(xt.UsageError):
+        xt.compute_replica_count([10] * 3, [12, 10, 10], 0)
+    with pytest.raises(xt.UsageError):
+        xt.compute_replica_count([10] * 3, [2, 10, 10], 0)
+
+
+def test_host_alignment_entry_points(xt):
+    # alignment.cpp:87-144 vs exhaustive search (test_support.hpp:67-82)
+    import itertools
+    rng = np.random.default_rng(100)
+    for _ in range(50):
+        q = rng.standard_normal((5, 5))
+        best = max(itertools.permutations(range(5)), key=lambda p: sum(q[r, p[r]] for r in range(5)))
+        assert xt.max_trace_assignment(q) == list(best)
+    m = np.array([[1.0], [-2.0], [4.0], [8.0]])
+    norm, piv = xt.normalize_shared(m, 3)
+    assert piv[0] == 4.0 and np.allclose(norm[:, 0], [0.25, -0.5, 1.0, 2.0])
+    with pytest.raises(xt.DegenerateColumnError):
+        xt.normalize_shared(np.array([[0.0, 1.0], [0.0, 0.0], [5.0, 0.0]]), 2)
+    with pytest.raises(xt.UsageError):
+        xt.normalize_shared(m, 0)
+
+
+def test_no_cpu_fallback_without_device(xt):
+    if xt.device_ready():
+        pytest.skip("device present")
+    with pytest.raises(xt.CudaError):
+        xt.gen_gaussian(4, 4, 1)
+    with pytest.raises(xt.CudaError):
+        xt.comp(np.zeros((2, 2, 2)), np.eye(2), np.eye(2), np.eye(2))
+    with pytest.raises(xt.CudaError):
+        xt.Plan([64] * 3, [32] * 3, 4, 2, 1)
+
+
+def test_usage_errors_precede_device_checks(xt):
+    with pytest.raises(xt.UsageError):
+        xt.gen_sparse_projection(100, 100, 40.0, 6)   # test_compression.cpp:61-63
+    with pytest.raises(xt.UsageError):
+        xt.gen_sparse_projection(10, 10, 0.5, 6)
+    with pytest.raises(xt.UsageError):
+        xt.make_ensemble([8, 8, 8], [9, 4, 4], 2, 1, 5)  # :98-100
+    with pytest.raises(xt.UsageError):
+        xt.make_ensemble([8, 8, 8], [4, 4, 4], 0, 1, 5)
+    with pytest.raises(xt.UsageError):
+        xt.make_ensemble([8, 8, 8], [4, 4, 4], 2, 5, 5)
+    with pytest.raises(xt.UsageError):
+        xt.make_ensemble([100] * 3, [50] * 3, 2, 2, 23, kind="two_stage", alpha=1.0)
