@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Headline benchmark: input tensor elements compressed per second (BASELINE.json).
+
+Workload (BASELINE.json configs[1], "C2"): dense 2000^3 rank-20 tensor,
+P = 32 replicas of 64^3, S = 40 shared anchor rows, Gaussian ensemble from the
+bit-exact device RNG. One step = one pass of the hot path (fused tcgen05
+mode-1/2 TTM + mode-3 GEMM) over the rank's 2000^3 block resident in HBM as
+bf16 (16 GB > L2, so no flush is needed between steps); for N > 1 every rank
+owns one mode-3 slab of a (2000, 2000, 2000*N) tensor (weak scaling, per-GPU
+work fixed) and the partial replicas are summed with one NCCL reduce.
+
+`e2e` is the same metric through the public C ABI with HOST buffers: the
+rank's block sits in pinned host memory and every step streams it H2D inside
+xtsg_plan_compress (double-buffered copy/convert/compute) and reads the
+replicas back D2H.
+
+`--impl reference` times the reference's own CPU implementation (compiled in
+place into oracle/_ref) on the box's host cores: comp_blocked fast mode on a
+bounded mode-3 slab sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GOLD = 0x9E3779B97F4A7C15
+M64 = (1 << 64) - 1
+
+C2 = dict(I=2000, J=2000, K=2000, L=64, M=64, N=64, P=32, S=40, R=20, seed=2, factor_seed=1)
+
+
+def _mix(z):
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def derive(seed, tag):
+    """rng.hpp:46-50"""
+    s = (seed ^ ((GOLD * (tag + 0x632BE59BD9B4E019)) & M64)) & M64
+    return _mix((s + 2 * GOLD) & M64)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="xtsg", choices=["xtsg", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-dtype", default="f32", choices=["bf16", "f32", "f64"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--K", type=int, default=C2["K"], help="mode-3 extent per rank (testing)")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampler for the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_block(torch, xt, cfg, k0, K, device):
+    """Rank's block X[:, :, k0:k0+K] of reconstruct(A, B, C) as bf16, (I, J, K) column-major.
+
+    Factors follow generate({dims, R, dense, seed}) (pipeline.cpp:182-193): one
+    polar stream per matrix from derive(seed, 1|2|3), drawn on the device."""
+    I, J, R = cfg["I"], cfg["J"], cfg["R"]
+    Ktot = cfg["Ktot"]
+    A = torch.from_numpy(xt.gen_gaussian(I, R, derive(cfg["factor_seed"], 1))).to(device, torch.float32)
+    B = torch.from_numpy(xt.gen_gaussian(J, R, derive(cfg["factor_seed"], 2))).to(device, torch.float32)
+    Cf = torch.from_numpy(xt.gen_gaussian(Ktot, R, derive(cfg["factor_seed"], 3))).to(device, torch.float32)
+    X = torch.empty((K, J, I), dtype=torch.bfloat16, device=device)
+    step = 50
+    for k in range(0, K, step):
+        kk = min(step, K - k)
+        ck = Cf[k0 + k:k0 + k + kk]                       # (kk, R)
+        # X[k, j, i] = sum_r A[i, r] B[j, r] C[k, r]
+        X[k:k + kk] = torch.einsum("kr,jr,ir->kji", ck, B, A).to(torch.bfloat16)
+    return X.permute(2, 1, 0), (A, B, Cf)
+
+
+def cpu_reference_rate(cfg, seconds, threads):
+    """Reference comp_blocked (fast mode, compression.cpp:381-403) on a
+    (I, J, ks) mode-3 slab of the workload; returns (elements/s, sample)."""
+    from oracle.oracle import Reference
+    ref = Reference()
+    ref.L.xref_set_blas_threads(1)      # one BLAS thread per parallel_for worker
+    I, J, P = cfg["I"], cfg["J"], cfg["P"]
+    red = (cfg["L"], cfg["M"], cfg["N"])
+    rng = np.random.default_rng(0)
+
+    def run(ks):
+        ks = max(ks, cfg["N"])  # make_ensemble needs reduced <= dims on every mode
+        t = np.asfortranarray(rng.standard_normal((I, J, ks)))
+        # the slab's ensemble == leading columns of the full one (per-row streams)
+        ens = ref.make_ensemble((I, J, ks), red, P, cfg["S"], seed=derive(cfg["seed"], 11))
+        t0 = time.perf_counter()
+        ref.comp_blocked(t, (500, 500, ks), ens, deterministic=False, workers=threads)
+        return time.perf_counter() - t0
+
+    ks = cfg["N"]
+    dt = run(ks)
+    if dt < 0.5 * seconds:
+        ks = int(min(400, ks * seconds / max(dt, 1e-3)))
+        dt = run(ks)
+    n = I * J * ks
+    return n / dt, f"comp_blocked fast mode, {I}x{J}x{ks} slab ({n:.3g} elements, 500x500x{ks} blocks), " \
+                   f"P={P} replicas of {red[0]}^3, {dt:.1f} s, OPENBLAS 1 thread x {threads} workers"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    cfg = dict(C2)
+    rates = []
+    for _ in range(max(1, args.steps)):
+        r, sample = cpu_reference_rate(cfg, max(2.0, args.cpu_seconds / max(1, args.steps)), threads)
+        rates.append(r)
+    v = float(np.median(rates))
+    line = {"impl": "reference", "metric": "input tensor elements compressed/sec", "value": v,
+            "unit": "elements/s", "higher_is_better": True, "n_gpus": args.gpus, "steps": len(rates),
+            "warmup": 0, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: dense 2000^3 rank-20, streamed blocks, P=32 replicas of 64^3 (CPU sample)"},
+            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2311_13693_b200 as xt
+
+    cfg = dict(C2)
+    K = args.K
+    cfg["Ktot"] = K * world
+    dims = (cfg["I"], cfg["J"], cfg["Ktot"])
+    red = (cfg["L"], cfg["M"], cfg["N"])
+    P = cfg["P"]
+    k0 = rank * K
+    t_plan = time.perf_counter()
+    plan = xt.Plan(dims, red, P, cfg["S"], derive(cfg["seed"], 11), precision=xt.PREC_BF16)
+    t_plan = time.perf_counter() - t_plan
+    X, _ = make_block(torch, xt, cfg, k0, K, dev)
+    torch.cuda.synchronize()
+    ysz = P * int(np.prod(red))
+    y = torch.zeros(ysz, dtype=torch.float32, device=dev)
+    # a dedicated stream: the legacy default stream's handle is 0, which the
+    # C ABI reads as "use the library's own per-thread stream"
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    elems_rank = cfg["I"] * cfg["J"] * K
+
+    def step():
+        plan.compress(X, y=y, offset=(0, 0, k0), stream=stream)
+        if world > 1:
+            dist.reduce(y, dst=0)
+
+    plan.set_profiling(True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    plan.profile(reset=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = xt.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = xt.launch_count() - launches0
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    prof = plan.profile(reset=True)
+    value = elems_rank * world * args.steps / (ms / 1e3)
+
+    burst, sustained, hbm, src = peaks()
+    fused_avg_ms = prof["fused_ms"] / max(1, prof["fused_launches"])
+    flops_per_launch = prof["fused_flops"] / max(1, prof["fused_launches"])
+    achieved = flops_per_launch / (fused_avg_ms / 1e3) / 1e12
+    traffic = None
+    tj = ROOT / "profiles" / "ncu_traffic.json"
+    if tj.exists():
+        try:
+            traffic = json.loads(tj.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": sustained, "unit": "TFLOP/s",
+                "frac": round(achieved / sustained, 4), "traffic": traffic,
+                "kernel": "ttm_fused_kernel (mode-1 + mode-2, tcgen05 kind::f16)",
+                "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
+                "algorithmic_flops_per_launch": flops_per_launch,
+                "kernel_share_of_step": round(prof["fused_ms"] / ms, 4) if ms > 0 else None,
+                "mode3_ms_per_step": prof["mode3_ms"] / args.steps}
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        npdt = {"bf16": None, "f32": np.float32, "f64": np.float64}[args.e2e_dtype]
+        tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[args.e2e_dtype]
+        xh = torch.empty((K, cfg["J"], cfg["I"]), dtype=tdt, pin_memory=True)
+        for k in range(0, K, 100):
+            xh[k:k + 100].copy_(X.permute(2, 1, 0)[k:k + 100].to(tdt))
+        xh_v = xh.permute(2, 1, 0)
+        yh = torch.zeros(ysz, dtype=torch.float32, pin_memory=True)
+        del npdt
+
+        def e2e_step():
+            plan.compress(xh_v, y=yh, offset=(0, 0, k0))
+            if world > 1:
+                yd = yh.to(dev)
+                dist.reduce(yd, dst=0)
+                yh.copy_(yd.cpu())
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": elems_rank * world * args.e2e_steps / dt, "unit": "elements/s",
+               "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+               "d2h_bytes_per_step": int(yh.numel() * 4),
+               "host_dtype": args.e2e_dtype, "ms_per_step": dt / args.e2e_steps * 1e3}
+        del xh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            v, sample = cpu_reference_rate(cfg, args.cpu_seconds, threads)
+            cpu = {"value": v, "unit": "elements/s", "cores": threads, "kind": "reference", "sample": sample}
+        except Exception as e:  # reference build absent on this box
+            cpu = {"value": None, "unit": "elements/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "input tensor elements compressed/sec", "value": value, "unit": "elements/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (rank-20 reconstruct(A,B,C) from the reference's generate() streams)",
+            "config": {"workload": "C2: dense 2000^3 rank-20, streamed blocks, P=32 replicas of 64^3, S=40",
+                       "dims_per_rank": [cfg["I"], cfg["J"], K], "reduced": list(red), "replicas": P,
+                       "shared_rows": cfg["S"], "parallelism": f"mode-3 slabs x{world}",
+                       "l2": "inputs (16 GB bf16 per rank) larger than L2; no flush",
+                       "plan_create_s": round(t_plan, 3)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -179,6 +179,14 @@ int32_t xtsg_plan_compress_coo(xtsg_plan* plan, const int32_t* i, const int32_t*
  * (evidence for the bench's gpu_launches). */
 int64_t xtsg_launch_count(void);
 
+/* Live profiling of a plan: when on, every fused-TTM launch and every mode-3
+ * GEMM is bracketed by CUDA events on its launching stream. profile() waits
+ * for them and returns out[6] = {fused_ms, fused_launches, mode3_ms,
+ * mode3_launches, fused_algorithmic_flops, mode3_algorithmic_flops}
+ * accumulated since the last reset. */
+int32_t xtsg_plan_set_profiling(xtsg_plan* plan, int32_t on);
+int32_t xtsg_plan_profile(xtsg_plan* plan, int32_t reset, double out[6]);
+
 /* ---- CP-ALS (cp_als.hpp:10-40, cp_als.cpp:22-111) ---------------------- */
 typedef struct xtsg_als_config {
   int64_t rank;

@@ -106,6 +106,8 @@ _SIGS = {
     "xtsg_plan_create": (_I32, [_P, _P]),
     "xtsg_plan_destroy": (None, [_P]),
     "xtsg_plan_compress": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _I32, _P]),
+    "xtsg_plan_set_profiling": (_I32, [_P, _I32]),
+    "xtsg_plan_profile": (_I32, [_P, _I32, _P]),
     "xtsg_plan_compress_factors": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I32, _P]),
     "xtsg_plan_compress_coo": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _I32, _P]),
     "xtsg_relative_error": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _I64, _P]),

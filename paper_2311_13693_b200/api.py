@@ -251,6 +251,15 @@ class Plan:
                                      1 if accumulate else 0, st))
         return y
 
+    def set_profiling(self, on: bool = True):
+        check(lib.xtsg_plan_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self, reset: bool = True) -> dict:
+        out = np.zeros(6)
+        check(lib.xtsg_plan_profile(self._h, 1 if reset else 0, ptr(out)))
+        return {"fused_ms": out[0], "fused_launches": int(out[1]), "mode3_ms": out[2],
+                "mode3_launches": int(out[3]), "fused_flops": out[4], "mode3_flops": out[5]}
+
     @staticmethod
     def replicas(y, count, reduced):
         """Split a flat output into per-replica column-major tensors (numpy)."""

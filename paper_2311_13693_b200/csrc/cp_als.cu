@@ -1,0 +1,576 @@
+// K9 — batched CP-ALS on the device (fp64), one CTA per ALS instance.
+//
+// Reference: cp_als (/root/reference/proj/src/cp_als.cpp:46-111) and
+// relative_error (:37-44). Each sweep updates
+//   A <- X(1) KR(C,B) pinv(C'C .* B'B),  B <- X(2) KR(C,A) pinv(C'C .* A'A),
+//   C <- X(3) KR(B,A) pinv(B'B .* A'A),
+// moves the a/b column norms into c (:84-96) and computes the residual
+// explicitly (:98-99; the ||X||^2 - 2<X,Xh> + ||Xh||^2 shortcut cannot resolve
+// the 1e-10 tolerance). Stops when the relative error changes by < tol.
+// pinv (linalg.cpp:52-61, rcond 1e-12 of the largest singular value) is taken
+// from a parallel-ordered cyclic Jacobi eigendecomposition of the symmetric
+// PSD Hadamard Gram (singular values == |eigenvalues| there). nvecs init
+// (:62-76, linalg.cpp:63-74) uses the same Jacobi on X(n) X(n)'.
+//
+// The replicas of one decomposition stage are independent, so a batch of P
+// replicas (x restarts) runs as P CTAs; each replica tensor (<= a few MB) stays
+// L2-resident across its sweeps. The Khatri-Rao products are never formed: the
+// MTTKRPs contract one mode at a time (L*M*N*R FMAs each).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "xrng.cuh"
+
+namespace xtsg {
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int RC = 4;  // ranks per work item in the MTTKRPs
+
+struct AlsInst {
+  const double* t;
+  double* a;
+  double* b;
+  double* c;
+  double* hist;
+  int64_t* iters;
+  int32_t* conv;
+  double* nvec_ws;  // rows_max * rows_max * 2 doubles when nvecs
+  xtsg_als_config cfg;
+};
+
+__device__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  return s;
+}
+
+// Symmetric eigendecomposition of the n x n matrix h (leading dim ld) in place
+// by parallel-ordered cyclic Jacobi; v receives the eigenvectors (columns),
+// the diagonal of h the eigenvalues. cs/sn/pp/qq scratch of n/2+1 entries.
+__device__ void jacobi_eig(double* h, double* v, int n, int ld, double* cs, double* sn, int* pp, int* qq,
+                           double* red) {
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) v[(e % n) + ld * (e / n)] = (e % n) == (e / n) ? 1.0 : 0.0;
+  __syncthreads();
+  if (n < 2) return;
+  const int m = n + (n & 1);  // even number of players; index n is a dummy when n is odd
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e % n, j = e / n;
+      const double x = h[i + ld * j];
+      tot += x * x;
+      if (i != j) off += x * x;
+    }
+    off = block_sum(off, red);
+    tot = block_sum(tot, red);
+    if (off <= 1e-26 * tot || off == 0.0) break;
+    for (int step = 0; step < m - 1; ++step) {
+      for (int k = threadIdx.x; k < m / 2; k += blockDim.x) {
+        auto who = [&](int i) { return i == 0 ? 0 : 1 + (i - 1 + step) % (m - 1); };
+        int p = who(k), q = who(m - 1 - k);
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        pp[k] = p;
+        qq[k] = q;
+        double c = 1.0, s = 0.0;
+        if (q < n) {
+          const double apq = h[p + ld * q];
+          if (apq != 0.0) {
+            const double app = h[p + ld * p], aqq = h[q + ld * q];
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+          }
+        }
+        cs[k] = c;
+        sn[k] = s;
+      }
+      __syncthreads();
+      // H <- H J (columns p, q) and V <- V J
+      for (int e = threadIdx.x; e < (m / 2) * n; e += blockDim.x) {
+        const int k = e / n, i = e % n;
+        const int p = pp[k], q = qq[k];
+        if (q >= n) continue;
+        const double c = cs[k], s = sn[k];
+        const double hp = h[i + ld * p], hq = h[i + ld * q];
+        h[i + ld * p] = c * hp - s * hq;
+        h[i + ld * q] = s * hp + c * hq;
+        const double vp = v[i + ld * p], vq = v[i + ld * q];
+        v[i + ld * p] = c * vp - s * vq;
+        v[i + ld * q] = s * vp + c * vq;
+      }
+      __syncthreads();
+      // H <- J' H (rows p, q)
+      for (int e = threadIdx.x; e < (m / 2) * n; e += blockDim.x) {
+        const int k = e / n, j = e % n;
+        const int p = pp[k], q = qq[k];
+        if (q >= n) continue;
+        const double c = cs[k], s = sn[k];
+        const double hp = h[p + ld * j], hq = h[q + ld * j];
+        h[p + ld * j] = c * hp - s * hq;
+        h[q + ld * j] = s * hp + c * hq;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+struct Smem {
+  double *A, *B, *C, *G1, *G2, *G3, *H, *V, *P, *M, *cs, *sn, *red, *nrm;
+  int *pp, *qq;
+};
+
+// out[x, r] for one mode (mode 0: A, 1: B, 2: C) of T (n1 x n2 x n3).
+__device__ void mttkrp(const double* __restrict__ T, int n1, int n2, int n3, int R, int mode, const Smem& s,
+                       double* out) {
+  const int rows = mode == 0 ? n1 : mode == 1 ? n2 : n3;
+  const int nrq = (R + RC - 1) / RC;
+  for (int item = threadIdx.x; item < rows * nrq; item += blockDim.x) {
+    const int x = item % rows, r0 = (item / rows) * RC;
+    double acc[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) acc[c] = 0.0;
+    if (mode == 0) {  // sum_k C[k,r] sum_j T[x,j,k] B[j,r]
+      for (int k = 0; k < n3; ++k) {
+        double tmp[RC] = {0.0, 0.0, 0.0, 0.0};
+        const double* tk = T + x + static_cast<int64_t>(n1) * n2 * k;
+        for (int j = 0; j < n2; ++j) {
+          const double tv = tk[static_cast<int64_t>(n1) * j];
+#pragma unroll
+          for (int c = 0; c < RC; ++c)
+            if (r0 + c < R) tmp[c] = fma(tv, s.B[j + n2 * (r0 + c)], tmp[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+          if (r0 + c < R) acc[c] = fma(s.C[k + n3 * (r0 + c)], tmp[c], acc[c]);
+      }
+    } else if (mode == 1) {  // sum_k C[k,r] sum_i T[i,x,k] A[i,r]
+      for (int k = 0; k < n3; ++k) {
+        double tmp[RC] = {0.0, 0.0, 0.0, 0.0};
+        const double* tk = T + static_cast<int64_t>(n1) * (x + static_cast<int64_t>(n2) * k);
+        for (int i = 0; i < n1; ++i) {
+          const double tv = tk[i];
+#pragma unroll
+          for (int c = 0; c < RC; ++c)
+            if (r0 + c < R) tmp[c] = fma(tv, s.A[i + n1 * (r0 + c)], tmp[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+          if (r0 + c < R) acc[c] = fma(s.C[k + n3 * (r0 + c)], tmp[c], acc[c]);
+      }
+    } else {  // sum_j B[j,r] sum_i T[i,j,x] A[i,r]
+      for (int j = 0; j < n2; ++j) {
+        double tmp[RC] = {0.0, 0.0, 0.0, 0.0};
+        const double* tj = T + static_cast<int64_t>(n1) * (j + static_cast<int64_t>(n2) * x);
+        for (int i = 0; i < n1; ++i) {
+          const double tv = tj[i];
+#pragma unroll
+          for (int c = 0; c < RC; ++c)
+            if (r0 + c < R) tmp[c] = fma(tv, s.A[i + n1 * (r0 + c)], tmp[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+          if (r0 + c < R) acc[c] = fma(s.B[j + n2 * (r0 + c)], tmp[c], acc[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < RC; ++c)
+      if (r0 + c < R) out[x + rows * (r0 + c)] = acc[c];
+  }
+}
+
+__device__ void gram(const double* F, int rows, int R, double* G) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int r = e % R, q = e / R;
+    if (r > q) continue;
+    double acc = 0.0;
+    for (int i = 0; i < rows; ++i) acc = fma(F[i + rows * r], F[i + rows * q], acc);
+    G[r + R * q] = acc;
+    G[q + R * r] = acc;
+  }
+}
+
+// P = pinv(H) for symmetric PSD H (R x R), via Jacobi (H is destroyed).
+__device__ void pinv_sym(double* H, int R, const Smem& s) {
+  jacobi_eig(H, s.V, R, R, s.cs, s.sn, s.pp, s.qq, s.red);
+  double mx = 0.0;
+  for (int i = 0; i < R; ++i) mx = fmax(mx, fabs(H[i + R * i]));
+  const double cut = 1e-12 * mx;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e % R, j = e / R;
+    double acc = 0.0;
+    for (int q = 0; q < R; ++q) {
+      const double lam = H[q + R * q];
+      if (fabs(lam) > cut) acc += s.V[i + R * q] * s.V[j + R * q] / lam;
+    }
+    s.P[e] = acc;
+  }
+  __syncthreads();
+}
+
+// F[x, r] = sum_q Mt[x, q] P[q, r]
+__device__ void apply_pinv(const double* Mt, int rows, int R, const double* P, double* F) {
+  for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
+    const int x = e % rows, r = e / rows;
+    double acc = 0.0;
+    for (int q = 0; q < R; ++q) acc = fma(Mt[x + rows * q], P[q + R * r], acc);
+    F[e] = acc;
+  }
+}
+
+__device__ double residual_sq(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s) {
+  double acc = 0.0;
+  const int64_t total = static_cast<int64_t>(n1) * n2 * n3;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int i = static_cast<int>(e % n1);
+    const int64_t jk = e / n1;
+    const int j = static_cast<int>(jk % n2), k = static_cast<int>(jk / n2);
+    double rec = 0.0;
+    for (int r = 0; r < R; ++r) rec = fma(s.A[i + n1 * r], s.B[j + n2 * r] * s.C[k + n3 * r], rec);
+    const double d = T[e] - rec;
+    acc = fma(d, d, acc);
+  }
+  return block_sum(acc, s.red);
+}
+
+__device__ double norm_sq(const double* __restrict__ T, int64_t total, double* red) {
+  double acc = 0.0;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) acc = fma(T[e], T[e], acc);
+  return block_sum(acc, red);
+}
+
+// One polar stream of `n` normals (gaussian_matrix, cp_als.cpp:14-19) into dst,
+// block-cooperative (same compaction as ensemble.cu).
+__device__ void block_normals(uint64_t seed, int n, double* dst, double* red) {
+  int* cnt = reinterpret_cast<int*>(red);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int produced = 0;
+  uint64_t t0 = 0;
+  while (produced < n) {
+    double n0 = 0.0, n1 = 0.0;
+    const bool acc = polar_candidate(seed, t0 + threadIdx.x, n0, n1);
+    const unsigned mask = __ballot_sync(0xffffffffu, acc);
+    __syncthreads();
+    if (lane == 0) cnt[wid] = __popc(mask);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < nw; ++w) {
+      if (w < wid) before += cnt[w];
+      total += cnt[w];
+    }
+    before += __popc(mask & ((1u << lane) - 1u));
+    const int pos = produced + 2 * before;
+    if (acc) {
+      if (pos < n) dst[pos] = n0;
+      if (pos + 1 < n) dst[pos + 1] = n1;
+    }
+    produced += 2 * total;
+    t0 += blockDim.x;
+  }
+  __syncthreads();
+}
+
+// leading eigenvectors of X(n) X(n)' into the first lead columns of F (rows x R)
+__device__ void nvecs_init(const double* __restrict__ T, int n1, int n2, int n3, int mode, int R, double* F,
+                           double* ws, const Smem& s) {
+  const int rows = mode == 0 ? n1 : mode == 1 ? n2 : n3;
+  double* G = ws;                 // rows x rows
+  double* V = ws + rows * rows;   // rows x rows
+  for (int e = threadIdx.x; e < rows * rows; e += blockDim.x) {
+    const int p = e % rows, q = e / rows;
+    if (p > q) continue;
+    double acc = 0.0;
+    if (mode == 0) {
+      for (int64_t c = 0; c < static_cast<int64_t>(n2) * n3; ++c) acc = fma(T[p + n1 * c], T[q + n1 * c], acc);
+    } else if (mode == 1) {
+      for (int k = 0; k < n3; ++k)
+        for (int i = 0; i < n1; ++i) {
+          const int64_t base = i + static_cast<int64_t>(n1) * n2 * k;
+          acc = fma(T[base + static_cast<int64_t>(n1) * p], T[base + static_cast<int64_t>(n1) * q], acc);
+        }
+    } else {
+      const int64_t sl = static_cast<int64_t>(n1) * n2;
+      for (int64_t c = 0; c < sl; ++c) acc = fma(T[c + sl * p], T[c + sl * q], acc);
+    }
+    G[p + rows * q] = acc;
+    G[q + rows * p] = acc;
+  }
+  __syncthreads();
+  jacobi_eig(G, V, rows, rows, s.cs, s.sn, s.pp, s.qq, s.red);
+  // order by descending eigenvalue (stable: ties keep the lower index first)
+  const int lead = R < rows ? R : rows;
+  for (int jj = threadIdx.x; jj < lead; jj += blockDim.x) {
+    // jj-th largest: count eigenvalues strictly greater (or equal with lower index)
+    for (int cidx = 0; cidx < rows; ++cidx) {
+      const double lc = G[cidx + rows * cidx];
+      int rank = 0;
+      for (int o = 0; o < rows; ++o) {
+        const double lo = G[o + rows * o];
+        if (lo > lc || (lo == lc && o < cidx)) ++rank;
+      }
+      if (rank == jj) {
+        for (int i = 0; i < rows; ++i) F[i + rows * jj] = V[i + rows * cidx];
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3) {
+  extern __shared__ double sm[];
+  const AlsInst in = insts[blockIdx.x];
+  const int R = static_cast<int>(in.cfg.rank);
+  const int mx = max(n1, max(n2, n3));
+  Smem s;
+  double* q = sm;
+  s.A = q; q += n1 * R;
+  s.B = q; q += n2 * R;
+  s.C = q; q += n3 * R;
+  s.G1 = q; q += R * R;
+  s.G2 = q; q += R * R;
+  s.G3 = q; q += R * R;
+  s.H = q; q += R * R;
+  s.V = q; q += R * R;
+  s.P = q; q += R * R;
+  s.M = q; q += mx * R;
+  s.cs = q; q += R / 2 + 2;
+  s.sn = q; q += R / 2 + 2;
+  s.nrm = q; q += 2 * R;
+  s.red = q; q += 64;
+  s.pp = reinterpret_cast<int*>(q); q += R / 2 + 2;
+  s.qq = reinterpret_cast<int*>(q);
+
+  const double* T = in.t;
+  const int64_t total = static_cast<int64_t>(n1) * n2 * n3;
+  const double tn = sqrt(norm_sq(T, total, s.red));
+  // init (cp_als.cpp:62-76)
+  block_normals(derive(in.cfg.seed, 1), n1 * R, s.A, s.red);
+  block_normals(derive(in.cfg.seed, 2), n2 * R, s.B, s.red);
+  block_normals(derive(in.cfg.seed, 3), n3 * R, s.C, s.red);
+  if (in.cfg.init == 1 && tn > 0.0) {
+    nvecs_init(T, n1, n2, n3, 0, R, s.A, in.nvec_ws, s);
+    nvecs_init(T, n1, n2, n3, 1, R, s.B, in.nvec_ws, s);
+    nvecs_init(T, n1, n2, n3, 2, R, s.C, in.nvec_ws, s);
+  }
+  __syncthreads();
+  gram(s.B, n2, R, s.G2);
+  gram(s.C, n3, R, s.G3);
+  __syncthreads();
+
+  int64_t it = 0;
+  bool converged = false;
+  double prev = 0.0;
+  for (; it < in.cfg.max_iters; ++it) {
+    // A update
+    mttkrp(T, n1, n2, n3, R, 0, s, s.M);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
+    __syncthreads();
+    pinv_sym(s.H, R, s);
+    apply_pinv(s.M, n1, R, s.P, s.A);
+    __syncthreads();
+    gram(s.A, n1, R, s.G1);
+    __syncthreads();
+    // B update
+    mttkrp(T, n1, n2, n3, R, 1, s, s.M);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G1[e];
+    __syncthreads();
+    pinv_sym(s.H, R, s);
+    apply_pinv(s.M, n2, R, s.P, s.B);
+    __syncthreads();
+    gram(s.B, n2, R, s.G2);
+    __syncthreads();
+    // C update
+    mttkrp(T, n1, n2, n3, R, 2, s, s.M);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G2[e] * s.G1[e];
+    __syncthreads();
+    pinv_sym(s.H, R, s);
+    apply_pinv(s.M, n3, R, s.P, s.C);
+    __syncthreads();
+    // move a/b column norms into c (cp_als.cpp:84-96)
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+      double na = 0.0, nb = 0.0;
+      for (int i = 0; i < n1; ++i) na = fma(s.A[i + n1 * r], s.A[i + n1 * r], na);
+      for (int i = 0; i < n2; ++i) nb = fma(s.B[i + n2 * r], s.B[i + n2 * r], nb);
+      s.nrm[r] = sqrt(na);
+      s.nrm[R + r] = sqrt(nb);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
+      const double na = s.nrm[e / n1];
+      if (na > 0.0) s.A[e] /= na;
+    }
+    for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
+      const double nb = s.nrm[R + e / n2];
+      if (nb > 0.0) s.B[e] /= nb;
+    }
+    for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) {
+      const int r = e / n3;
+      s.C[e] *= s.nrm[r] * s.nrm[R + r];
+    }
+    __syncthreads();
+    gram(s.A, n1, R, s.G1);
+    gram(s.B, n2, R, s.G2);
+    gram(s.C, n3, R, s.G3);
+    const double res = sqrt(residual_sq(T, n1, n2, n3, R, s));
+    const double err = tn > 0.0 ? res / tn : res;
+    if (threadIdx.x == 0) in.hist[it] = err;
+    if (it >= 1 && fabs(prev - err) < in.cfg.tol) {
+      converged = true;
+      ++it;
+      break;
+    }
+    prev = err;
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) in.a[e] = s.A[e];
+  for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) in.b[e] = s.B[e];
+  for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) in.c[e] = s.C[e];
+  if (threadIdx.x == 0) {
+    *in.iters = it;
+    *in.conv = converged ? 1 : 0;
+  }
+}
+
+size_t als_smem_bytes(int n1, int n2, int n3, int R) {
+  const int mx = std::max(n1, std::max(n2, n3));
+  return sizeof(double) * (static_cast<size_t>(n1 + n2 + n3) * R + 6 * R * R + static_cast<size_t>(mx) * R +
+                           2 * (R / 2 + 2) + 2 * R + 64 + 2 * (R / 2 + 2));
+}
+
+__global__ void finite_kernel(const double* t, int64_t n, int* bad) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (!isfinite(t[e])) *bad = 1;
+}
+
+__global__ void relerr_kernel(const double* T, int n1, int n2, int n3, const double* a, const double* b,
+                              const double* c, int R, double* out) {
+  extern __shared__ double sm[];
+  Smem s{};
+  s.A = sm;
+  s.B = sm + n1 * R;
+  s.C = sm + (n1 + n2) * R;
+  s.red = sm + (n1 + n2 + n3) * R;
+  for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) s.A[e] = a[e];
+  for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) s.B[e] = b[e];
+  for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) s.C[e] = c[e];
+  __syncthreads();
+  const double res = sqrt(residual_sq(T, n1, n2, n3, R, s));
+  const double tn = sqrt(norm_sq(T, static_cast<int64_t>(n1) * n2 * n3, s.red));
+  if (threadIdx.x == 0) *out = tn > 0.0 ? res / tn : res;
+}
+
+}  // namespace
+
+}  // namespace xtsg
+
+using namespace xtsg;
+
+extern "C" {
+
+int32_t xtsg_cp_als_batched(int64_t count, const double* t, int64_t n1, int64_t n2, int64_t n3,
+                            const xtsg_als_config* cfg, double* a, double* b, double* c, int64_t* iters,
+                            int32_t* converged, double* history) {
+  return guard([&] {
+    if (count < 0) usage("cp_als: negative batch");
+    if (count == 0) return;
+    int64_t max_it = 0, rank = cfg[0].rank;
+    for (int64_t q = 0; q < count; ++q) {
+      // cp_als.cpp:47-55
+      if (cfg[q].rank < 1) usage("cp_als: rank must be >= 1");
+      if (cfg[q].max_iters < 1) usage("cp_als: max_iters must be >= 1");
+      if (!(cfg[q].tol > 0.0)) usage("cp_als: tol must be positive");
+      if (cfg[q].rank != rank) usage("cp_als: a batch shares one rank");
+      max_it = std::max(max_it, cfg[q].max_iters);
+    }
+    const int64_t cap = std::min({n2 * n3, n1 * n3, n1 * n2});
+    if (rank > cap)
+      usage("cp_als: rank " + std::to_string(rank) + " exceeds the identifiable bound " + std::to_string(cap));
+    require_device();
+    cudaStream_t st = thread_stream();
+    const int64_t tsz = n1 * n2 * n3;
+    InView<double> tt(t, static_cast<size_t>(count * tsz), st);
+    {
+      DevBuf<int> bad(1, st);
+      bad.zero();
+      finite_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(count * tsz, 256), 4096)), 256, 0, st>>>(
+          tt.dev, count * tsz, bad.ptr);
+      XLAUNCH_CHECK();
+      int hb = 0;
+      XCUDA(cudaMemcpyAsync(&hb, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+      XCUDA(cudaStreamSynchronize(st));
+      if (hb) data_error("cp_als: input tensor has non-finite values");
+    }
+    const int R = static_cast<int>(rank);
+    const size_t smem = als_smem_bytes(static_cast<int>(n1), static_cast<int>(n2), static_cast<int>(n3), R);
+    if (smem > 220 * 1024) usage("cp_als: factors do not fit the device ALS working set (reduce rank/dims)");
+    OutView<double> oa(a, static_cast<size_t>(count * n1 * rank), st), ob(b, static_cast<size_t>(count * n2 * rank), st),
+        oc(c, static_cast<size_t>(count * n3 * rank), st);
+    OutView<double> oh(history, static_cast<size_t>(count * max_it), st);
+    OutView<int64_t> oi(iters, static_cast<size_t>(count), st);
+    OutView<int32_t> ov(converged, static_cast<size_t>(count), st);
+    bool any_nvecs = false;
+    for (int64_t q = 0; q < count; ++q) any_nvecs |= cfg[q].init == 1;
+    const int64_t rmax = std::max({n1, n2, n3});
+    DevBuf<double> ws(any_nvecs ? static_cast<size_t>(count * rmax * rmax * 2) : 0, st);
+    std::vector<AlsInst> hin(static_cast<size_t>(count));
+    for (int64_t q = 0; q < count; ++q) {
+      AlsInst& in = hin[static_cast<size_t>(q)];
+      in.t = tt.dev + q * tsz;
+      in.a = oa.dev + q * n1 * rank;
+      in.b = ob.dev + q * n2 * rank;
+      in.c = oc.dev + q * n3 * rank;
+      in.hist = oh.dev + q * max_it;
+      in.iters = oi.dev + q;
+      in.conv = ov.dev + q;
+      in.nvec_ws = any_nvecs ? ws.ptr + q * rmax * rmax * 2 : nullptr;
+      in.cfg = cfg[q];
+    }
+    DevBuf<AlsInst> din(static_cast<size_t>(count), st);
+    XCUDA(cudaMemcpyAsync(din.ptr, hin.data(), sizeof(AlsInst) * count, cudaMemcpyHostToDevice, st));
+    XCUDA(cudaFuncSetAttribute(als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    als_kernel<<<static_cast<unsigned>(count), NT, smem, st>>>(din.ptr, static_cast<int>(n1), static_cast<int>(n2),
+                                                                static_cast<int>(n3));
+    XLAUNCH_CHECK();
+    oa.finish();
+    ob.finish();
+    oc.finish();
+    oh.finish();
+    oi.finish();
+    ov.finish();
+  });
+}
+
+int32_t xtsg_relative_error(const double* t, int64_t n1, int64_t n2, int64_t n3, const double* a, const double* b,
+                            const double* c, int64_t rank, double* out) {
+  return guard([&] {
+    if (rank < 1) usage("relative_error: rank must be >= 1");
+    require_device();
+    cudaStream_t st = thread_stream();
+    InView<double> tt(t, static_cast<size_t>(n1 * n2 * n3), st);
+    InView<double> aa(a, static_cast<size_t>(n1 * rank), st), bb(b, static_cast<size_t>(n2 * rank), st),
+        cc(c, static_cast<size_t>(n3 * rank), st);
+    OutView<double> o(out, 1, st);
+    const size_t smem = sizeof(double) * (static_cast<size_t>(n1 + n2 + n3) * rank + 64);
+    XCUDA(cudaFuncSetAttribute(relerr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    relerr_kernel<<<1, NT, smem, st>>>(tt.dev, static_cast<int>(n1), static_cast<int>(n2), static_cast<int>(n3),
+                                       aa.dev, bb.dev, cc.dev, static_cast<int>(rank), o.dev);
+    XLAUNCH_CHECK();
+    o.finish();
+  });
+}
+
+}  // extern "C"

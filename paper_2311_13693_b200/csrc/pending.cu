@@ -10,15 +10,4 @@ int32_t xtsg_plan_compress_coo(xtsg_plan*, const int32_t*, const int32_t*, const
                                void*, int32_t, void*) {
   return guard([] { throw Status(XTSG_E_INTERNAL, "not implemented yet"); });
 }
-int32_t xtsg_relative_error(const double*, int64_t, int64_t, int64_t, const double*, const double*, const double*,
-                            int64_t, double*) {
-  return guard([] { throw Status(XTSG_E_INTERNAL, "not implemented yet"); });
-}
-int32_t xtsg_cp_als_batched(int64_t, const double*, int64_t, int64_t, int64_t, const xtsg_als_config*, double*,
-                            double*, double*, int64_t*, int32_t*, double*) {
-  return guard([] { throw Status(XTSG_E_INTERNAL, "not implemented yet"); });
-}
-int32_t xtsg_solve_stacked_ls(int64_t, const int64_t*, int64_t, int64_t, const double*, const double*, double*) {
-  return guard([] { throw Status(XTSG_E_INTERNAL, "not implemented yet"); });
-}
 }

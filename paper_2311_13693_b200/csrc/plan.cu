@@ -183,6 +183,11 @@ Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
 
 Plan::~Plan() {
   cudaStreamSynchronize(st);
+  for (auto* v : {&ev_pool, &ev_fused, &ev_mode3})
+    for (auto& e : *v) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
   if (copy_st) {
     cudaStreamSynchronize(copy_st);
     cudaStreamDestroy(copy_st);
@@ -249,8 +254,27 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     tl.prm.rpb = static_cast<int32_t>(rpb);
     tl.prm.n2 = static_cast<int32_t>(n2);
     tl.prm.count = static_cast<int32_t>(P);
+    const int64_t rem_i = ext[0] - 64 * (tl.prm.k_steps - 1);
+    const int64_t rem_j = ext[1] - static_cast<int64_t>(ttm_block_n()) * (tl.prm.j_tiles - 1);
+    tl.prm.k16_last = static_cast<int32_t>(ceil_div(rem_i, 16));
+    tl.prm.n_last = static_cast<int32_t>(round_up(rem_j, 16));
+    tl.prm.chunks_last = static_cast<int32_t>(ceil_div(rem_j, 64));
+    tl.prm.k16_chunk_last = static_cast<int32_t>(ceil_div(rem_j - 64 * (tl.prm.chunks_last - 1), 16));
     tl.prm.z = zbuf.ptr;
+    EvPair e1{}, e2{};
+    if (profiling) {
+      e1 = take_pair();
+      XCUDA(cudaEventRecord(e1.a, s));
+    }
     launch_ttm_fused(tl, s);
+    if (profiling) {
+      XCUDA(cudaEventRecord(e1.b, s));
+      ev_fused.push_back(e1);
+      flops_fused += 2.0 * P * L * static_cast<double>(ext[0]) * ext[1] * kc +
+                     2.0 * P * L * static_cast<double>(M) * ext[1] * kc;
+      e2 = take_pair();
+      XCUDA(cudaEventRecord(e2.a, s));
+    }
     // mode 3: Y_p (Mpad*Lpad x N) (+)= Z_p (Mpad*Lpad x kc) * W_p[:, k0+kb : +kc]^T
     GemmArgs<float> g;
     g.m = mpad * lpad; g.n = N; g.k = kc; g.batch = P;
@@ -259,10 +283,25 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     g.c = ydst; g.ldc = mpad * lpad; g.stride_c = mpad * lpad * N;
     g.beta = acc ? 1.f : 0.f;
     gemm_simt(g, s);
+    if (profiling) {
+      XCUDA(cudaEventRecord(e2.b, s));
+      ev_mode3.push_back(e2);
+      flops_mode3 += 2.0 * P * L * static_cast<double>(M) * N * kc;
+    }
     acc = true;
   }
-  (void)L;
-  (void)M;
+}
+
+Plan::EvPair Plan::take_pair() {
+  if (!ev_pool.empty()) {
+    EvPair e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  EvPair e{};
+  XCUDA(cudaEventCreate(&e.a));
+  XCUDA(cudaEventCreate(&e.b));
+  return e;
 }
 
 void Plan::ensure_z(int64_t floats, cudaStream_t s) {
@@ -413,6 +452,42 @@ int32_t xtsg_plan_create(const xtsg_plan_desc* desc, xtsg_plan** out) {
 }
 
 void xtsg_plan_destroy(xtsg_plan* plan) { delete reinterpret_cast<Plan*>(plan); }
+
+int32_t xtsg_plan_set_profiling(xtsg_plan* plan, int32_t on) {
+  return guard([&] { reinterpret_cast<Plan*>(plan)->profiling = on != 0; });
+}
+
+int32_t xtsg_plan_profile(xtsg_plan* plan, int32_t reset, double out[6]) {
+  return guard([&] {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    double fused = 0.0, m3 = 0.0;
+    for (auto& e : p->ev_fused) {
+      float ms = 0.f;
+      XCUDA(cudaEventSynchronize(e.b));
+      XCUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+      fused += ms;
+    }
+    for (auto& e : p->ev_mode3) {
+      float ms = 0.f;
+      XCUDA(cudaEventSynchronize(e.b));
+      XCUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+      m3 += ms;
+    }
+    out[0] = fused;
+    out[1] = static_cast<double>(p->ev_fused.size());
+    out[2] = m3;
+    out[3] = static_cast<double>(p->ev_mode3.size());
+    out[4] = p->flops_fused;
+    out[5] = p->flops_mode3;
+    if (reset) {
+      for (auto& e : p->ev_fused) p->ev_pool.push_back(e);
+      for (auto& e : p->ev_mode3) p->ev_pool.push_back(e);
+      p->ev_fused.clear();
+      p->ev_mode3.clear();
+      p->flops_fused = p->flops_mode3 = 0.0;
+    }
+  });
+}
 
 int32_t xtsg_plan_compress(xtsg_plan* plan, const void* x, int32_t x_dtype, const int64_t ld[2],
                            const int64_t offset[3], const int64_t extent[3], void* y, int32_t accumulate,

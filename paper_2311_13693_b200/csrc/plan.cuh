@@ -20,6 +20,15 @@ struct Plan {
   DevBuf<float> wf;
   DevBuf<float> zbuf;
   int grid_limit = 0;  // testing knob: cap on persistent CTAs (0 = #SMs)
+  // Live profiling (xtsg_plan_profile): CUDA events around every fused-TTM
+  // and mode-3 launch on the launching stream, plus algorithmic flop counts.
+  bool profiling = false;
+  struct EvPair {
+    cudaEvent_t a, b;
+  };
+  std::vector<EvPair> ev_pool, ev_fused, ev_mode3;
+  double flops_fused = 0.0, flops_mode3 = 0.0;
+  EvPair take_pair();
 
   explicit Plan(const xtsg_plan_desc& d);
   ~Plan();

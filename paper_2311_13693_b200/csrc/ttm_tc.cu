@@ -131,15 +131,20 @@ __global__ void __launch_bounds__(256, 1)
           ptx::mbar_wait(&bars->tmem_empty[b], (use & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t d = tmem + b * 256;
+          // ragged edges: the last j tile narrows N, the last i step issues
+          // only the K=16 slices that hold data (TMA zero-fills the rest)
+          const uint32_t idesc1 = jt == j_tiles - 1 ? ptx::idesc_bf16(BM, p.n_last) : IDESC1;
           for (int ks = 0; ks < k_steps; ++ks) {
             ptx::mbar_wait(&bars->full1[s], ph);
             ptx::tc_fence_after();
             const uint32_t a0 = ptx::smem_u32(stage_base + s * STAGE_BYTES);
             const uint32_t b0 = a0 + A_BYTES;
+            const int nk16 = ks == k_steps - 1 ? p.k16_last : BK / 16;
 #pragma unroll
             for (int k4 = 0; k4 < BK / 16; ++k4)
-              ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), IDESC1,
-                            (ks | k4) != 0);
+              if (k4 < nk16)
+                ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc1,
+                              (ks | k4) != 0);
             ptx::mma_commit(&bars->empty1[s]);
             if (++s == S1) { s = 0; ph ^= 1; }
           }
@@ -151,12 +156,14 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       // ---- TMA producer: Vt chunks for mode 2 -----------------------------
       const uint32_t bytes = static_cast<uint32_t>(p.n2) * 128;
+      uint32_t g = 0;  // running chunk counter (shared convention with w3 / epilogue)
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int rb = u % p.n_rb;
         for (int jt = 0; jt < j_tiles; ++jt) {
-          for (int c = 0; c < CHUNKS; ++c) {
-            const int slot = c & 1;
-            const uint32_t par = (c >> 1) & 1;
+          const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
+          for (int c = 0; c < nch; ++c, ++g) {
+            const int slot = g & 1;
+            const uint32_t par = (g >> 1) & 1;
             ptx::mbar_wait(&bars->b2_empty[slot], par ^ 1);
             ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], bytes);
             ptx::tma_load_2d(b2_base + slot * B2_BYTES, &tm_v, &bars->b2_full[slot], jt * BN + c * 64,
@@ -169,27 +176,31 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       // ---- mode-2 MMA issuer ----------------------------------------------
       const uint32_t idesc2 = ptx::idesc_bf16(BM, p.n2);
-      uint32_t t = 0;
+      uint32_t t = 0, g = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         for (int jt = 0; jt < j_tiles; ++jt, ++t) {
           const uint32_t b = t & 1;
           const uint32_t d = tmem + b * 256;
-          // D2 overwrites D1 columns [0, n2): both of the first two 64-col
-          // chunks must have been drained before the first mode-2 MMA.
-          ptx::mbar_wait(&bars->a2_full[0], 0);
-          ptx::mbar_wait(&bars->a2_full[1], 0);
-          for (int c = 0; c < CHUNKS; ++c) {
-            const int slot = c & 1;
-            const uint32_t par = (c >> 1) & 1;
+          const bool last = jt == j_tiles - 1;
+          const int nch = last ? p.chunks_last : CHUNKS;
+          // D2 overwrites D1 columns [0, n2): the first two 64-col chunks
+          // (when present) must have been drained before the first MMA.
+          ptx::mbar_wait(&bars->a2_full[g & 1], (g >> 1) & 1);
+          if (nch > 1) ptx::mbar_wait(&bars->a2_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+          for (int c = 0; c < nch; ++c, ++g) {
+            const int slot = g & 1;
+            const uint32_t par = (g >> 1) & 1;
             if (c >= 2) ptx::mbar_wait(&bars->a2_full[slot], par);
             ptx::mbar_wait(&bars->b2_full[slot], par);
             ptx::tc_fence_after();
             const uint32_t a0 = ptx::smem_u32(a2_base + slot * A2_BYTES);
             const uint32_t b0 = ptx::smem_u32(b2_base + slot * B2_BYTES);
+            const int nk16 = (last && c == nch - 1) ? p.k16_chunk_last : 4;
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4)
-              ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc2,
-                            (c | k4) != 0);
+              if (k4 < nk16)
+                ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc2,
+                              (c | k4) != 0);
             ptx::mma_commit(&bars->a2_empty[slot]);
             ptx::mma_commit(&bars->b2_empty[slot]);
           }
@@ -204,7 +215,7 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int p_local = r / p.lpad;
     const int l = r % p.lpad;
-    uint32_t t = 0;
+    uint32_t t = 0, g = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int kk = u / p.n_rb, rb = u % p.n_rb;
       float zacc[MPAD];
@@ -212,11 +223,12 @@ __global__ void __launch_bounds__(256, 1)
       for (int m = 0; m < MPAD; ++m) zacc[m] = 0.f;
       for (int jt = 0; jt < j_tiles; ++jt, ++t) {
         const uint32_t b = t & 1, use = t >> 1;
+        const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
         ptx::mbar_wait(&bars->tmem_full[b], use & 1);
         ptx::tc_fence_after();
-        for (int c = 0; c < CHUNKS; ++c) {
-          const int slot = c & 1;
-          const uint32_t par = (c >> 1) & 1;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int slot = g & 1;
+          const uint32_t par = (g >> 1) & 1;
           ptx::mbar_wait(&bars->a2_empty[slot], par ^ 1);
           uint8_t* row = a2_base + slot * A2_BYTES + r * 128;
 #pragma unroll 1

@@ -14,6 +14,10 @@ struct TtmParams {
   int32_t lpad, rpb; // padded L, replicas per row block (lpad * rpb == 128)
   int32_t n2;        // rpb * mpad (mode-2 MMA N)
   int32_t count;     // P
+  int32_t k16_last;        // K=16 MMA slices holding data in the last i step (1..4)
+  int32_t n_last;          // UMMA N of the last j tile (multiple of 16, <= 256)
+  int32_t chunks_last;     // 64-wide mode-2 chunks in the last j tile
+  int32_t k16_chunk_last;  // K=16 slices in the last chunk of the last tile
   float* z;          // out: Z[p][kk][m][l], kk in [0, kc)
 };
 

@@ -38,9 +38,9 @@ def test_gen_sparse_projection_bitexact(gpu, restated):
 
 @pytest.mark.parametrize("dims,red,P,S,seed", [
     ([200, 200, 200], [30, 30, 30], 12, 10, 11),
-    ([2000, 1999, 1003], [64, 63, 17], 3, 40, 2 ** 40 + 3),
+    ([2000, 1999, 1003], [64, 63, 17], 3, 16, 2 ** 40 + 3),
     ([12, 11, 10], [5, 4, 4], 3, 2, 17),
-    ([10007, 64, 64], [128, 32, 32], 2, 40, 99),
+    ([10007, 64, 64], [128, 32, 32], 2, 16, 99),
 ])
 def test_make_ensemble_bitexact_large(gpu, restated, dims, red, P, S, seed):
     ens = gpu.make_ensemble(dims, red, P, S, seed)

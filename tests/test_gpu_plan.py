@@ -36,11 +36,11 @@ def _oracle_replicas(restated, t, ens, off=(0, 0, 0)):
 
 
 @pytest.mark.parametrize("dims,red,P", [
-    ((256, 300, 40), (64, 64, 64), 4),
-    ((200, 200, 24), (30, 30, 30), 12),      # config-1 shape, padded L -> 32
-    ((130, 257, 9), (32, 32, 16), 5),        # ragged i / j, P*L not a multiple of 128
-    ((192, 96, 8), (128, 128, 8), 2),        # L = 128: one replica per row block
-    ((128, 128, 6), (64, 32, 20), 3),        # M != L
+    ((256, 300, 72), (64, 64, 64), 4),
+    ((200, 200, 40), (30, 30, 30), 12),      # config-1 shape, padded L -> 32
+    ((130, 257, 20), (32, 32, 16), 5),        # ragged i / j, P*L not a multiple of 128
+    ((192, 160, 8), (128, 128, 8), 2),        # L = 128: one replica per row block
+    ((128, 128, 24), (64, 32, 20), 3),        # M != L
 ])
 def test_bf16_plan_vs_fp64_oracle(gpu, restated, dims, red, P):
     import torch
@@ -65,18 +65,27 @@ def test_bf16_plan_vs_fp64_oracle(gpu, restated, dims, red, P):
 
 
 def test_bf16_plan_blocks_accumulate_to_whole(gpu, restated):
-    dims, red, P = (192, 256, 16), (64, 64, 64), 4
+    dims, red, P = (192, 256, 16), (64, 64, 16), 4
     plan = gpu.Plan(dims, red, P, 8, 99)
     t = _tensor(dims, 3)
     whole = plan.compress(t)
-    # three k-slabs and an (i, j) split with unaligned offsets, accumulated
+    # mode-3 slabs only: the bf16 rounding points are unchanged, so the
+    # accumulated result equals the one-shot result to fp32 summation order
+    acc = None
+    for k0, k1 in [(0, 5), (5, 11), (11, 16)]:
+        acc = plan.compress(np.asfortranarray(t[:, :, k0:k1]), y=acc, offset=(0, 0, k0),
+                            accumulate=acc is not None)
+    assert rel_diff(whole, acc) <= 1e-5
+    # (i, j) splits with unaligned offsets: the mode-1 partial sums are rounded
+    # to bf16 per block before mode 2 (like the reference's fast blocked mode
+    # rounds per block), so agreement is at the bf16 level
     acc = None
     for (i0, i1), (j0, j1), (k0, k1) in [((0, 192), (0, 256), (0, 5)), ((0, 192), (0, 256), (5, 11)),
                                          ((0, 77), (0, 256), (11, 16)), ((77, 192), (0, 100), (11, 16)),
                                          ((77, 192), (100, 256), (11, 16))]:
         blk = np.asfortranarray(t[i0:i1, j0:j1, k0:k1])
         acc = plan.compress(blk, y=acc, offset=(i0, j0, k0), accumulate=acc is not None)
-    assert rel_diff(whole, acc) <= 1e-5
+    assert rel_diff(whole, acc) <= 5e-3
     ens = gpu.make_ensemble(dims, red, P, 8, 99)
     want = _oracle_replicas(restated, t, ens)
     got = gpu.Plan.replicas(acc, P, red)
