@@ -346,11 +346,11 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
   s.V = q; q += R * R;
   s.P = q; q += R * R;
   s.M = q; q += mx * R;
-  s.cs = q; q += R / 2 + 2;
-  s.sn = q; q += R / 2 + 2;
+  s.cs = q; q += std::max(mx, R) / 2 + 2;
+  s.sn = q; q += std::max(mx, R) / 2 + 2;
   s.nrm = q; q += 2 * R;
   s.red = q; q += 64;
-  s.pp = reinterpret_cast<int*>(q); q += R / 2 + 2;
+  s.pp = reinterpret_cast<int*>(q); q += std::max(mx, R) / 2 + 2;
   s.qq = reinterpret_cast<int*>(q);
 
   const double* T = in.t;
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
 size_t als_smem_bytes(int n1, int n2, int n3, int R) {
   const int mx = std::max(n1, std::max(n2, n3));
   return sizeof(double) * (static_cast<size_t>(n1 + n2 + n3) * R + 6 * R * R + static_cast<size_t>(mx) * R +
-                           2 * (R / 2 + 2) + 2 * R + 64 + 2 * (R / 2 + 2));
+                           2 * (std::max(mx, R) / 2 + 2) + 2 * R + 64 + 2 * (std::max(mx, R) / 2 + 2));
 }
 
 __global__ void finite_kernel(const double* t, int64_t n, int* bad) {
