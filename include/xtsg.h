@@ -231,6 +231,24 @@ int32_t xtsg_solve_stacked_ls(int64_t count, const int64_t* rows, int64_t r, int
 int32_t xtsg_recover_perm_scale(const double* global_head, const double* sampled,
                                 int64_t rows, int64_t cols, int64_t* perm, double* scale);
 
+/* omp_recover (alignment.cpp:306-419): column-wise greedy sparse recovery,
+ * one CTA per measured column. out: atoms x ncols. */
+int32_t xtsg_omp_recover(const double* measured, int64_t rows, int64_t ncols, const double* dictionary,
+                         int64_t atoms, int64_t sparsity, double residual_tol, double* out);
+
+/* ---- dense linear algebra (linalg.hpp:8-24) ---------------------------- */
+/* C (m x n, ldc) = op(A) op(B), fp64 on the device (gemm, linalg.cpp:24-43) */
+int32_t xtsg_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n, int64_t k, const double* a,
+                  int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc);
+/* pseudo_inverse (linalg.cpp:52-61): out is cols x rows */
+int32_t xtsg_pseudo_inverse(const double* m, int64_t rows, int64_t cols, double rcond, double* out);
+/* leading_left_singular_vectors (linalg.cpp:63-74): out is rows x count */
+int32_t xtsg_leading_left_singular_vectors(const double* m, int64_t rows, int64_t cols, int64_t count,
+                                           double* out);
+/* solve_least_squares (linalg.cpp:76-92): x is cols x nrhs */
+int32_t xtsg_solve_least_squares(const double* a, int64_t rows, int64_t cols, const double* rhs,
+                                 int64_t nrhs, double* x);
+
 #ifdef __cplusplus
 }
 #endif
