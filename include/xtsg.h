@@ -52,6 +52,8 @@ int64_t xtsg_last_payload(int32_t which);
 int32_t xtsg_version(void);
 /* 1 when an sm_100 device is usable by this thread, else 0. */
 int32_t xtsg_device_ready(void);
+/* Create the CUDA context and this thread's stream ahead of the first call. */
+int32_t xtsg_warmup(void);
 
 /* ---- ensembles (compression.hpp:13-65, compression.cpp:15-200) --------- */
 #define XTSG_KIND_GAUSSIAN 0

@@ -90,6 +90,12 @@ _SIGS = {
     "xtsg_last_payload": (_I64, [_I32]),
     "xtsg_version": (_I32, []),
     "xtsg_device_ready": (_I32, []),
+    "xtsg_warmup": (_I32, []),
+    "xtsg_gemm": (_I32, [_I32, _I32, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
+    "xtsg_pseudo_inverse": (_I32, [_P, _I64, _I64, _D, _P]),
+    "xtsg_leading_left_singular_vectors": (_I32, [_P, _I64, _I64, _I64, _P]),
+    "xtsg_solve_least_squares": (_I32, [_P, _I64, _I64, _P, _I64, _P]),
+    "xtsg_omp_recover": (_I32, [_P, _I64, _I64, _P, _I64, _I64, _D, _P]),
     "xtsg_launch_count": (_I64, []),
     "xtsg_replica_count": (_I32, [_P, _P, _I64, _P]),
     "xtsg_gen_gaussian": (_I32, [_I64, _I64, _U64, _P]),

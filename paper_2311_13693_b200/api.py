@@ -251,6 +251,40 @@ class Plan:
                                      1 if accumulate else 0, st))
         return y
 
+    def _y(self, like_device, y):
+        if y is not None:
+            return y
+        n = self.count * int(np.prod(self.reduced))
+        if like_device is None:
+            return np.zeros(n, np.float32)
+        import torch
+        return torch.zeros(n, dtype=torch.float32, device=like_device)
+
+    def compress_factors(self, factors, k0=0, k1=None, y=None, accumulate=False, stream=None, device=None):
+        """xtsg_plan_compress_factors: X = reconstruct(a, b, c) generated on the device slab by slab."""
+        a, b, c = (_f64(x) for x in factors)
+        k1 = self.dims[2] if k1 is None else k1
+        y = self._y(device, y)
+        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        check(lib.xtsg_plan_compress_factors(self._h, ptr(a), ptr(b), ptr(c), a.shape[1], int(k0), int(k1), ptr(y),
+                                             1 if accumulate else 0, st))
+        return y
+
+    def compress_coo(self, i, j, k, val, y=None, accumulate=False, stream=None, device=None):
+        """xtsg_plan_compress_coo: COO nonzeros (int32 coordinates, fp32 values; duplicates sum)."""
+        def as_arr(v, dt):
+            if isinstance(v, np.ndarray) or not hasattr(v, "data_ptr"):
+                return np.ascontiguousarray(np.asarray(v, dt))
+            return v
+        i, j, k = as_arr(i, np.int32), as_arr(j, np.int32), as_arr(k, np.int32)
+        val = as_arr(val, np.float32)
+        nnz = int(val.shape[0])
+        y = self._y(device, y)
+        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        check(lib.xtsg_plan_compress_coo(self._h, ptr(i), ptr(j), ptr(k), ptr(val), nnz, ptr(y),
+                                         1 if accumulate else 0, st))
+        return y
+
     def set_profiling(self, on: bool = True):
         check(lib.xtsg_plan_set_profiling(self._h, 1 if on else 0))
 

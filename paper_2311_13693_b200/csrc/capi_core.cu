@@ -95,6 +95,14 @@ int32_t xtsg_device_ready(void) {
   return guard([] { require_device(); }) == XTSG_OK ? 1 : 0;
 }
 
+int32_t xtsg_warmup(void) {
+  return guard([] {
+    require_device();
+    XCUDA(cudaFree(nullptr));
+    (void)thread_stream();
+  });
+}
+
 int32_t xtsg_replica_count(const int64_t dims[3], const int64_t reduced[3], int64_t slack,
                            int64_t* out) {
   // compression.cpp:82-95 (host arithmetic, no device needed)

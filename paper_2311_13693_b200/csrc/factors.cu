@@ -1,0 +1,168 @@
+// K4 — compression of a tensor given by its CP factors, with the tensor
+// blocks generated on the device (reference: comp_from_factors /
+// make_memory_block_source over reconstruct(), compression.cpp:215-278,
+// tensor.cpp:133-150).
+//
+// The 10^12-element configs must never exist in memory: mode-3 slabs of
+// X = sum_r a_r (x) b_r (x) c_r are produced in bf16 by a register-tiled
+// rank-R micro-GEMM (X_k = A diag(c_k) B^T, R FMAs per element) straight into
+// the staging layout the fused tcgen05 TTM consumes, one slab at a time.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "plan.cuh"
+
+namespace xtsg {
+
+namespace {
+
+constexpr int TI = 128, TJ = 64, NT = 256;
+
+// X[kk][j][i] (ld_i) = sum_r A[i,r] B[j,r] C[k0+kk,r]; A/B/C fp32 column-major.
+__global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                      const float* __restrict__ Cm, int64_t I, int64_t J, int64_t K,
+                                                      int R, int64_t k0, int64_t ldi,
+                                                      __nv_bfloat16* __restrict__ X) {
+  extern __shared__ float sm[];
+  float* As = sm;            // R x TI
+  float* Bs = sm + R * TI;   // R x TJ (already scaled by c_k)
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * TI, j0 = static_cast<int64_t>(blockIdx.y) * TJ;
+  const int64_t kk = blockIdx.z, k = k0 + kk;
+  for (int e = threadIdx.x; e < R * TI; e += NT) {
+    const int r = e / TI, ii = e % TI;
+    As[e] = (i0 + ii < I) ? A[(i0 + ii) + I * r] : 0.f;
+  }
+  for (int e = threadIdx.x; e < R * TJ; e += NT) {
+    const int r = e / TJ, jj = e % TJ;
+    Bs[e] = (j0 + jj < J) ? B[(j0 + jj) + J * r] * Cm[k + K * r] : 0.f;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 x 16 threads, 8 x 4 outputs each
+  float acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+  for (int r = 0; r < R; ++r) {
+    float av[8], bv[4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) av[a] = As[r * TI + tx * 8 + a];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bv[b] = Bs[r * TJ + ty + 16 * b];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(av[a], bv[b], acc[a][b]);
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int64_t j = j0 + ty + 16 * b;
+    if (j >= J) continue;
+    __nv_bfloat16* row = X + (kk * J + j) * ldi + i0 + tx * 8;
+    if (i0 + tx * 8 + 8 <= I) {
+      uint4 pk;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(acc[0][b], acc[1][b]);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(acc[2][b], acc[3][b]);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[4][b], acc[5][b]);
+      __nv_bfloat162 h3 = __floats2bfloat162_rn(acc[6][b], acc[7][b]);
+      pk.x = *reinterpret_cast<uint32_t*>(&h0);
+      pk.y = *reinterpret_cast<uint32_t*>(&h1);
+      pk.z = *reinterpret_cast<uint32_t*>(&h2);
+      pk.w = *reinterpret_cast<uint32_t*>(&h3);
+      *reinterpret_cast<uint4*>(row) = pk;
+    } else {
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (i0 + tx * 8 + a < ldi) row[a] = __float2bfloat16(i0 + tx * 8 + a < I ? acc[a][b] : 0.f);
+    }
+  }
+}
+
+__global__ void to_f32_kernel(const double* __restrict__ s, int64_t n, float* __restrict__ d) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[e] = static_cast<float>(s[e]);
+}
+
+__global__ void compact_y3_kernel(const float* __restrict__ ypad, int64_t count, int64_t L, int64_t M, int64_t N,
+                                  int64_t lpad, int64_t mpad, int32_t accumulate, float* __restrict__ y) {
+  const int64_t per = L * M * N, total = count * per;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t p = e / per, r = e % per;
+    const int64_t l = r % L, mn = r / L, m = mn % M, n = mn / M;
+    const float v = ypad[p * mpad * lpad * N + (m * lpad + l) + mpad * lpad * n];
+    y[e] = accumulate ? y[e] + v : v;
+  }
+}
+
+int g1(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 16))); }
+
+}  // namespace
+
+void Plan::compress_factors(const double* a, const double* b, const double* c, int64_t rank, int64_t k0, int64_t k1,
+                            float* y, bool accumulate, cudaStream_t s) {
+  if (desc.precision != XTSG_PREC_BF16) usage("plan_compress_factors: needs a bf16 (tensor-core) plan");
+  const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
+  if (rank < 1 || rank > 64) usage("plan_compress_factors: rank must be in [1, 64]");
+  if (k0 < 0 || k1 > K || k0 >= k1) usage("plan_compress_factors: k range outside the tensor");
+  const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
+  const int64_t ysz = P * L * M * N;
+  const bool padded = (lpad != L) || (mpad != M);
+  OutView<float> yo(y, static_cast<size_t>(ysz), s);
+  if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
+  InView<double> da(a, static_cast<size_t>(I * rank), s), db(b, static_cast<size_t>(J * rank), s),
+      dc(c, static_cast<size_t>(K * rank), s);
+  DevBuf<float> fa(static_cast<size_t>(I * rank), s), fb(static_cast<size_t>(J * rank), s),
+      fc(static_cast<size_t>(K * rank), s);
+  to_f32_kernel<<<g1(I * rank), 256, 0, s>>>(da.dev, I * rank, fa.ptr);
+  to_f32_kernel<<<g1(J * rank), 256, 0, s>>>(db.dev, J * rank, fb.ptr);
+  to_f32_kernel<<<g1(K * rank), 256, 0, s>>>(dc.dev, K * rank, fc.ptr);
+  count_launch(2);
+  XLAUNCH_CHECK();
+  DevBuf<float> ypad;
+  float* ydst = yo.dev;
+  bool acc = accumulate;
+  if (padded) {
+    ypad = DevBuf<float>(static_cast<size_t>(P * mpad * lpad * N), s);
+    ydst = ypad.ptr;
+    acc = false;
+  }
+  const int64_t ldi = ceil_div(I, 8) * 8;
+  const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, (int64_t(1) << 30) / (ldi * J * 2)));
+  DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * J * ldi), s);
+  const size_t smem = static_cast<size_t>(rank) * (TI + TJ) * sizeof(float);
+  XCUDA(cudaFuncSetAttribute(gen_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  for (int64_t kb = k0; kb < k1; kb += ks) {
+    const int64_t kn = std::min(ks, k1 - kb);
+    dim3 grid(static_cast<unsigned>(ceil_div(I, TI)), static_cast<unsigned>(ceil_div(J, TJ)),
+              static_cast<unsigned>(kn));
+    gen_slab_kernel<<<grid, NT, smem, s>>>(fa.ptr, fb.ptr, fc.ptr, I, J, K, static_cast<int>(rank), kb, ldi,
+                                           stage.ptr);
+    XLAUNCH_CHECK();
+    const int64_t off[3] = {0, 0, kb}, ext[3] = {I, J, kn};
+    run_bf16_block(stage.ptr, ldi, ldi * J, off, ext, ydst, acc, s);
+    acc = true;
+  }
+  if (padded) {
+    compact_y3_kernel<<<g1(ysz), 256, 0, s>>>(ypad.ptr, P, L, M, N, lpad, mpad, accumulate ? 1 : 0, yo.dev);
+    XLAUNCH_CHECK();
+  }
+  if (yo.host) yo.finish();
+}
+
+}  // namespace xtsg
+
+using namespace xtsg;
+
+extern "C" int32_t xtsg_plan_compress_factors(xtsg_plan* plan, const double* a, const double* b, const double* c,
+                                              int64_t rank, int64_t k0, int64_t k1, void* y, int32_t accumulate,
+                                              void* stream) {
+  return guard([&] {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
+    p->compress_factors(a, b, c, rank, k0, k1, static_cast<float*>(y), accumulate != 0, s);
+  });
+}

@@ -19,6 +19,7 @@ struct Plan {
   DevBuf<__nv_bfloat16> ustack, vt;
   DevBuf<float> wf;
   DevBuf<float> zbuf;
+  DevBuf<__nv_bfloat16> ut;  // i-major U copy for the sparse path (lazy)
   int grid_limit = 0;  // testing knob: cap on persistent CTAs (0 = #SMs)
   // Live profiling (xtsg_plan_profile): CUDA events around every fused-TTM
   // and mode-3 launch on the launching stream, plus algorithmic flop counts.
@@ -38,6 +39,10 @@ struct Plan {
   void run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, const int64_t off[3],
                       const int64_t ext[3], float* ydst, bool first_accumulate, cudaStream_t s);
   void ensure_z(int64_t floats, cudaStream_t s);
+  void compress_factors(const double* a, const double* b, const double* c, int64_t rank, int64_t k0, int64_t k1,
+                        float* y, bool accumulate, cudaStream_t s);
+  void compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, const float* val, int64_t nnz, float* y,
+                    bool accumulate, cudaStream_t s);
 };
 
 }  // namespace xtsg

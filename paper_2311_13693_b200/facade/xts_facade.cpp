@@ -28,6 +28,10 @@ namespace xts {
 
 namespace {
 
+// Create the CUDA context and the loading thread's stream when the drop-in is
+// loaded, so the first reference call does not pay device initialisation.
+__attribute__((constructor)) void facade_warmup() { (void)xtsg_warmup(); }
+
 [[noreturn]] void rethrow_status(int32_t rc) {
   const std::string msg = xtsg_last_error();
   const int64_t p0 = xtsg_last_payload(0), p1 = xtsg_last_payload(1);
