@@ -163,7 +163,7 @@ Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
     rpb = 128 / lpad;
     n2 = rpb * mpad;
     if (n2 > 128) usage("plan: (128/Lpad)*Mpad must be <= 128 for the tensor-core path");
-    rows_u = round_up(P * lpad, 128);
+    rows_u = round_up(P * lpad, 128);  // odd row-block counts run the kernel without clusters
     ld_u = round_up(I, 8);
     ld_v = round_up(J, 8);
     ustack = DevBuf<__nv_bfloat16>(static_cast<size_t>(rows_u * ld_u), st);

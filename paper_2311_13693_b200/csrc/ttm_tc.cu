@@ -28,6 +28,9 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 #include "sm100_ptx.cuh"
 #include "ttm_tc.cuh"
@@ -37,19 +40,29 @@ namespace xtsg {
 namespace {
 
 constexpr int BM = 128;       // stacked U rows per tile (UMMA M)
-constexpr int BN = 256;       // j per tile (UMMA N of mode 1)
 constexpr int BK = 64;        // i per stage (128 B = one SW128 atom row)
-constexpr int S1 = 3;         // mode-1 pipeline stages
 constexpr int A_BYTES = BM * BK * 2;       // 16 KB
-constexpr int B_BYTES = BN * BK * 2;       // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int A2_BYTES = BM * 64 * 2;      // 16 KB (128 rows x 64 j)
 constexpr int B2_BYTES = 128 * 64 * 2;     // up to 128 (p,m) rows x 64 j
-constexpr int CHUNKS = BN / 64;            // mode-2 K chunks per tile
-constexpr int SMEM_DATA = S1 * STAGE_BYTES + 2 * A2_BYTES + 2 * B2_BYTES;
-constexpr int SMEM_TOTAL = SMEM_DATA + 1024 /*align*/ + 256 /*barriers*/;
-constexpr uint32_t IDESC1 = ptx::idesc_bf16(BM, BN);
 
+// Tile shape / pipeline depth: BN j per tile (UMMA N of mode 1, <= 256 so a
+// TMEM buffer fits twice in 512 columns), S1 TMA stages. 256x3 and 192x4
+// both fit the 227 KB shared-memory budget next to the mode-2 rings.
+template <int BN_, int S1_>
+struct TileCfg {
+  static constexpr int BN = BN_;
+  static constexpr int S1 = S1_;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int CHUNKS = BN / 64;  // mode-2 K chunks per full tile
+  static constexpr int SMEM_DATA = S1 * STAGE_BYTES + 2 * A2_BYTES + 2 * B2_BYTES;
+  static constexpr int SMEM_TOTAL = SMEM_DATA + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t IDESC1 = ptx::idesc_bf16(BM, BN);
+  static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
+  static_assert(BN % 64 == 0 && BN <= 256, "BN");
+};
+
+template <int S1>
 struct Bars {
   uint64_t full1[S1], empty1[S1];
   uint64_t tmem_full[2], tmem_empty[2], d2_full[2];
@@ -57,22 +70,24 @@ struct Bars {
   uint32_t tmem_base;
 };
 
-template <int MPAD>
+template <int MPAD, class Cfg, int CS>
 __global__ void __launch_bounds__(256, 1)
     ttm_fused_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_x,
                      const __grid_constant__ CUtensorMap tm_v, const TtmParams p) {
+  constexpr int BN = Cfg::BN, S1 = Cfg::S1, STAGE_BYTES = Cfg::STAGE_BYTES, CHUNKS = Cfg::CHUNKS;
+  constexpr uint32_t IDESC1 = Cfg::IDESC1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
   uint8_t* a2_base = smem + S1 * STAGE_BYTES;
   uint8_t* b2_base = a2_base + 2 * A2_BYTES;
-  Bars* bars = reinterpret_cast<Bars*>(b2_base + 2 * B2_BYTES);
+  Bars<S1>* bars = reinterpret_cast<Bars<S1>*>(b2_base + 2 * B2_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S1; ++s) {
       ptx::mbar_init(&bars->full1[s], 1);
-      ptx::mbar_init(&bars->empty1[s], 1);
+      ptx::mbar_init(&bars->empty1[s], CS);  // freed by the MMA of every CTA sharing the X tile
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&bars->tmem_full[b], 1);
@@ -93,10 +108,18 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CS > 1) ptx::cluster_sync();  // peers' barriers initialised before any multicast
   ptx::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  const int n_units = p.n_rb * p.kc;
+  // CS CTAs of a cluster take CS consecutive row blocks of the same slice and
+  // tile sequence; each loads BN/CS rows of every X tile and multicasts them
+  // to all CS CTAs, so an X tile crosses the L2->SM fabric once per cluster.
+  const int crank = CS > 1 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+  const int cid = blockIdx.x / CS, n_clusters = gridDim.x / CS;
+  const int n_rbg = p.n_rb / CS;
+  const int n_units = n_rbg * p.kc;
+  const uint16_t cmask = static_cast<uint16_t>((1u << CS) - 1u);
   const int j_tiles = p.j_tiles;
   const int k_steps = p.k_steps;
 
@@ -105,15 +128,19 @@ __global__ void __launch_bounds__(256, 1)
       // ---- TMA producer: U rows and X tiles -------------------------------
       int s = 0;
       uint32_t ph = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const int kk = u / p.n_rb, rb = u % p.n_rb;
+      for (int u = cid; u < n_units; u += n_clusters) {
+        const int kk = u / n_rbg, rb = (u % n_rbg) * CS + crank;
         for (int jt = 0; jt < j_tiles; ++jt) {
           for (int ks = 0; ks < k_steps; ++ks) {
             ptx::mbar_wait(&bars->empty1[s], ph ^ 1);
             uint8_t* st = stage_base + s * STAGE_BYTES;
             ptx::mbar_arrive_expect_tx(&bars->full1[s], STAGE_BYTES);
             ptx::tma_load_2d(st, &tm_u, &bars->full1[s], ks * BK, rb * BM);
-            ptx::tma_load_3d(st + A_BYTES, &tm_x, &bars->full1[s], ks * BK, jt * BN, p.k_first + kk);
+            if constexpr (CS == 1)
+              ptx::tma_load_3d(st + A_BYTES, &tm_x, &bars->full1[s], ks * BK, jt * BN, p.k_first + kk);
+            else
+              ptx::tma_load_3d_mc(st + A_BYTES + crank * (Cfg::B_BYTES / CS), &tm_x, &bars->full1[s], ks * BK,
+                                  jt * BN + crank * (BN / CS), p.k_first + kk, cmask);
             if (++s == S1) { s = 0; ph ^= 1; }
           }
         }
@@ -125,7 +152,7 @@ __global__ void __launch_bounds__(256, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t t = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int u = cid; u < n_units; u += n_clusters) {
         for (int jt = 0; jt < j_tiles; ++jt, ++t) {
           const uint32_t b = t & 1, use = t >> 1;
           ptx::mbar_wait(&bars->tmem_empty[b], (use & 1) ^ 1);
@@ -145,7 +172,10 @@ __global__ void __launch_bounds__(256, 1)
               if (k4 < nk16)
                 ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc1,
                               (ks | k4) != 0);
-            ptx::mma_commit(&bars->empty1[s]);
+            if constexpr (CS == 1)
+              ptx::mma_commit(&bars->empty1[s]);
+            else
+              ptx::mma_commit_mc(&bars->empty1[s], cmask);
             if (++s == S1) { s = 0; ph ^= 1; }
           }
           ptx::mma_commit(&bars->tmem_full[b]);
@@ -157,8 +187,8 @@ __global__ void __launch_bounds__(256, 1)
       // ---- TMA producer: Vt chunks for mode 2 -----------------------------
       const uint32_t bytes = static_cast<uint32_t>(p.n2) * 128;
       uint32_t g = 0;  // running chunk counter (shared convention with w3 / epilogue)
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const int rb = u % p.n_rb;
+      for (int u = cid; u < n_units; u += n_clusters) {
+        const int rb = (u % n_rbg) * CS + crank;
         for (int jt = 0; jt < j_tiles; ++jt) {
           const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
           for (int c = 0; c < nch; ++c, ++g) {
@@ -177,7 +207,7 @@ __global__ void __launch_bounds__(256, 1)
       // ---- mode-2 MMA issuer ----------------------------------------------
       const uint32_t idesc2 = ptx::idesc_bf16(BM, p.n2);
       uint32_t t = 0, g = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int u = cid; u < n_units; u += n_clusters) {
         for (int jt = 0; jt < j_tiles; ++jt, ++t) {
           const uint32_t b = t & 1;
           const uint32_t d = tmem + b * 256;
@@ -216,8 +246,8 @@ __global__ void __launch_bounds__(256, 1)
     const int p_local = r / p.lpad;
     const int l = r % p.lpad;
     uint32_t t = 0, g = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const int kk = u / p.n_rb, rb = u % p.n_rb;
+    for (int u = cid; u < n_units; u += n_clusters) {
+      const int kk = u / n_rbg, rb = (u % n_rbg) * CS + crank;
       float zacc[MPAD];
 #pragma unroll
       for (int m = 0; m < MPAD; ++m) zacc[m] = 0.f;
@@ -282,6 +312,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CS > 1) ptx::cluster_sync();  // no CTA leaves while a peer may still multicast to it
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
@@ -322,8 +353,9 @@ void make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
   if (r != CUDA_SUCCESS) throw Status(XTSG_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
-template <int MPAD>
+template <int MPAD, class Cfg, int CS>
 void launch_impl(const TtmLaunch& L, cudaStream_t st) {
+  constexpr int BN = Cfg::BN;
   CUtensorMap mu, mx, mv;
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.rows_u)};
@@ -334,7 +366,7 @@ void launch_impl(const TtmLaunch& L, cudaStream_t st) {
   {
     const uint64_t dims[3] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.nk)};
     const uint64_t str[2] = {static_cast<uint64_t>(L.ld_x0) * 2, static_cast<uint64_t>(L.ld_x1) * 2};
-    const uint32_t box[3] = {BK, BN, 1};
+    const uint32_t box[3] = {BK, BN / CS, 1};
     make_map(&mx, L.x, 3, dims, str, box);
   }
   {
@@ -345,12 +377,27 @@ void launch_impl(const TtmLaunch& L, cudaStream_t st) {
   }
   static bool attr_set = false;
   if (!attr_set) {
-    XCUDA(cudaFuncSetAttribute(ttm_fused_kernel<MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
+    XCUDA(cudaFuncSetAttribute(ttm_fused_kernel<MPAD, Cfg, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Cfg::SMEM_TOTAL));
     attr_set = true;
   }
-  const int units = L.prm.n_rb * L.prm.kc;
-  const int grid = std::min(units, L.grid_limit > 0 ? L.grid_limit : sm_count());
-  ttm_fused_kernel<MPAD><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, L.prm);
+  if (L.prm.n_rb % CS) usage("ttm_fused: row blocks must be a multiple of the cluster size");
+  const int clusters = (L.prm.n_rb / CS) * L.prm.kc;
+  const int cap = (L.grid_limit > 0 ? L.grid_limit : sm_count()) / CS;
+  const int grid = std::max(1, std::min(clusters, cap)) * CS;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = Cfg::SMEM_TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  XCUDA(cudaLaunchKernelEx(&cfg, ttm_fused_kernel<MPAD, Cfg, CS>, mu, mx, mv, L.prm));
   XLAUNCH_CHECK();
 }
 
@@ -359,14 +406,45 @@ void launch_impl(const TtmLaunch& L, cudaStream_t st) {
 void launch_ttm_fused(const TtmLaunch& L, cudaStream_t st) {
   if (L.prm.n2 > 128 || L.prm.n2 % 16 || L.prm.lpad * L.prm.rpb != BM)
     usage("ttm_fused: unsupported reduced dims for the tensor-core path");
-  switch (L.mpad) {
-    case 32: launch_impl<32>(L, st); break;
-    case 64: launch_impl<64>(L, st); break;
-    case 128: launch_impl<128>(L, st); break;
-    default: usage("ttm_fused: M must pad to 32, 64 or 128");
+  if (ttm_pair_enabled() && ttm_pair_supported(L)) {
+    launch_ttm_pair(L, st);  // cta_group::2 kernel (ttm_tc2.cu)
+    return;
   }
+  const int cs = (L.prm.n_rb % ttm_cluster_size() == 0) ? ttm_cluster_size() : 1;
+  using C = TileCfg<256, 3>;
+  auto go = [&](auto cs_tag) {
+    constexpr int CS = decltype(cs_tag)::value;
+    switch (L.mpad) {
+      case 32: launch_impl<32, C, CS>(L, st); break;
+      case 64: launch_impl<64, C, CS>(L, st); break;
+      case 128: launch_impl<128, C, CS>(L, st); break;
+      default: usage("ttm_fused: M must pad to 32, 64 or 128");
+    }
+  };
+  if (cs == 4) go(std::integral_constant<int, 4>{});
+  else if (cs == 2) go(std::integral_constant<int, 2>{});
+  else go(std::integral_constant<int, 1>{});
 }
 
-int ttm_block_n() { return BN; }
+// Cluster size for the X-tile multicast (XTSG_TTM_CLUSTER=1|2|4, default 2).
+int ttm_cluster_size() {
+  static const int cs = [] {
+    const char* e = std::getenv("XTSG_TTM_CLUSTER");
+    const int v = e ? std::atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
+  }();
+  return cs;
+}
+
+int ttm_block_n() { return 256; }
+
+// CTA-pair kernel on by default (XTSG_TTM_PAIR=0 selects the single-CTA one).
+bool ttm_pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("XTSG_TTM_PAIR");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
 
 }  // namespace xtsg

@@ -35,5 +35,9 @@ struct TtmLaunch {
 
 void launch_ttm_fused(const TtmLaunch& l, cudaStream_t st);
 int ttm_block_n();
+int ttm_cluster_size();
+bool ttm_pair_supported(const TtmLaunch& l);
+void launch_ttm_pair(const TtmLaunch& l, cudaStream_t st);
+bool ttm_pair_enabled();
 
 }  // namespace xtsg

@@ -1,0 +1,382 @@
+// K2+K3 on CTA pairs — the cta_group::2 version of the fused TTM (ttm_tc.cu).
+//
+// Same contraction (Z_p[:, :, k] = U_p X[:, :, k] V_p^T for every replica and
+// slice; reference comp_with, compression.cpp:202-209), but each tcgen05.mma
+// spans the two SMs of a TPC: M = 256 stacked U rows (128 per CTA) x N = 256 j
+// (each CTA stages only its 128 j of the X tile). Per SM this halves the X
+// bytes TMA writes into shared memory and the B bytes the tensor core reads
+// back, which is what capped the single-CTA kernel at ~2/3 tensor-pipe
+// occupancy (ncu: smem shared between TMA fills and UMMA operand reads).
+//
+// Roles per CTA (256 threads): w0 TMA producer (own U rows + own half of the X
+// tile, completing on the LEADER's full barrier), w1 TMEM owner and — leader
+// only — mode-1 MMA issuer, w2 Vt producer, w3 — leader only — mode-2 MMA
+// issuer, w4-7 epilogue over this CTA's 128 TMEM lanes. Commits multicast to
+// both CTAs' barriers; the epilogues arrive remotely on the leader's.
+//
+// Mode 2 runs with the same cta_group (M = 256 rows = 2*RPB replicas,
+// N = 2*RPB*Mpad <= 256 columns): D2 reuses the drained 256-column D1 buffer,
+// so all D1 chunks that D2 overlaps are drained (a 4-deep A2 ring) before the
+// first mode-2 MMA of a tile.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+#include "ttm_tc.cuh"
+
+namespace xtsg {
+
+namespace {
+
+constexpr int BM = 128;                 // rows per CTA (M = 256 per pair)
+constexpr int BN = 256;                 // j per tile (128 staged per CTA)
+constexpr int BNC = BN / 2;
+constexpr int BK = 64;
+constexpr int S = 4;                    // TMA stages
+constexpr int A_BYTES = BM * BK * 2;    // 16 KB
+constexpr int B_BYTES = BNC * BK * 2;   // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int A2_SLOTS = 4;
+constexpr int A2_BYTES = BM * 64 * 2;   // 16 KB
+constexpr int B2_BYTES = 128 * 64 * 2;  // 16 KB (n2 <= 128 rows per CTA)
+constexpr int CHUNKS = BN / 64;
+constexpr int SMEM_DATA = S * STAGE_BYTES + A2_SLOTS * A2_BYTES + 2 * B2_BYTES;
+constexpr int SMEM_TOTAL = SMEM_DATA + 1024 + 512;
+static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
+constexpr uint32_t IDESC1 = ptx::idesc_bf16(2 * BM, BN);
+constexpr uint16_t PAIR = 0x3;
+
+struct Bars2 {
+  uint64_t full1[S], empty1[S];
+  uint64_t tmem_full[2], tmem_empty[2], d2_full[2];
+  uint64_t a2_full[A2_SLOTS], a2_empty[A2_SLOTS];
+  uint64_t b2_full[2], b2_empty[2];
+  uint32_t tmem_base;
+};
+
+template <int MPAD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    ttm_pair_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_x,
+                    const __grid_constant__ CUtensorMap tm_v, const TtmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  uint8_t* a2_base = smem + S * STAGE_BYTES;
+  uint8_t* b2_base = a2_base + A2_SLOTS * A2_BYTES;
+  Bars2* bars = reinterpret_cast<Bars2*>(b2_base + 2 * B2_BYTES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = ptx::cluster_ctarank();
+  const bool leader = crank == 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&bars->full1[s], 1);
+      ptx::mbar_init(&bars->empty1[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&bars->tmem_full[b], 1);
+      ptx::mbar_init(&bars->tmem_empty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy)
+      ptx::mbar_init(&bars->d2_full[b], 1);
+      ptx::mbar_init(&bars->b2_full[b], 1);
+      ptx::mbar_init(&bars->b2_empty[b], 1);
+    }
+    for (int q = 0; q < A2_SLOTS; ++q) {
+      ptx::mbar_init(&bars->a2_full[q], 8);
+      ptx::mbar_init(&bars->a2_empty[q], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tm_u);
+    ptx::tma_prefetch(&tm_x);
+    ptx::tma_prefetch(&tm_v);
+  }
+  if (warp == 1) ptx::tmem_alloc_pair(&bars->tmem_base, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  const int cid = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int n_rb2 = p.n_rb >> 1;
+  const int n_units = n_rb2 * p.kc;
+  const int j_tiles = p.j_tiles, k_steps = p.k_steps;
+  const int n2c = p.n2;            // mode-2 columns contributed by this CTA
+  const int n2 = 2 * n2c;          // mode-2 MMA N
+  const int need = (n2 + 63) / 64; // D1 chunks D2 overlaps
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (both CTAs): own U rows, own half of the X tile -----
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = cid; u < n_units; u += n_clusters) {
+        const int kk = u / n_rb2, rb2 = u % n_rb2;
+        const int urow = rb2 * 2 * BM + crank * BM;
+        for (int jt = 0; jt < j_tiles; ++jt) {
+          for (int ks = 0; ks < k_steps; ++ks) {
+            ptx::mbar_wait(&bars->empty1[s], ph ^ 1);
+            uint8_t* st = stage_base + s * STAGE_BYTES;
+            if (leader) ptx::mbar_arrive_expect_tx(&bars->full1[s], 2 * STAGE_BYTES);
+            const uint32_t fb = ptx::mapa_shared(&bars->full1[s], 0);
+            ptx::tma_load_2d_pair(st, &tm_u, fb, ks * BK, urow);
+            ptx::tma_load_3d_pair(st + A_BYTES, &tm_x, fb, ks * BK, jt * BN + crank * BNC, p.k_first + kk);
+            if (++s == S) { s = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---- mode-1 MMA issuer (leader) -----------------------------------------
+      int s = 0;
+      uint32_t ph = 0, t = 0;
+      for (int u = cid; u < n_units; u += n_clusters) {
+        for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+          const uint32_t b = t & 1, use = t >> 1;
+          ptx::mbar_wait(&bars->tmem_empty[b], (use & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d = tmem + b * 256;
+          for (int ks = 0; ks < k_steps; ++ks) {
+            ptx::mbar_wait(&bars->full1[s], ph);
+            ptx::tc_fence_after();
+            const uint32_t a0 = ptx::smem_u32(stage_base + s * STAGE_BYTES);
+            const uint32_t b0 = a0 + A_BYTES;
+            const int nk16 = ks == k_steps - 1 ? p.k16_last : BK / 16;
+#pragma unroll
+            for (int k4 = 0; k4 < BK / 16; ++k4)
+              if (k4 < nk16)
+                ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), IDESC1,
+                                   (ks | k4) != 0);
+            ptx::mma_commit_pair(&bars->empty1[s], PAIR);
+            if (++s == S) { s = 0; ph ^= 1; }
+          }
+          ptx::mma_commit_pair(&bars->tmem_full[b], PAIR);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // ---- Vt producer (both CTAs): this CTA's replicas' V rows ---------------
+      uint32_t g = 0;
+      const uint32_t bytes = static_cast<uint32_t>(n2c) * 128;
+      for (int u = cid; u < n_units; u += n_clusters) {
+        const int rb2 = u % n_rb2;
+        const int vrow = (rb2 * 2 + static_cast<int>(crank)) * n2c;
+        for (int jt = 0; jt < j_tiles; ++jt) {
+          const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
+          for (int c = 0; c < nch; ++c, ++g) {
+            const int slot = g & 1;
+            ptx::mbar_wait(&bars->b2_empty[slot], ((g >> 1) & 1) ^ 1);
+            if (leader) ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], 2 * bytes);
+            ptx::tma_load_2d_pair(b2_base + slot * B2_BYTES, &tm_v, ptx::mapa_shared(&bars->b2_full[slot], 0),
+                                  jt * BN + c * 64, vrow);
+          }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (leader && lane == 0) {
+      // ---- mode-2 MMA issuer (leader) -----------------------------------------
+      const uint32_t idesc2 = ptx::idesc_bf16(2 * BM, n2);
+      uint32_t t = 0, g = 0;
+      for (int u = cid; u < n_units; u += n_clusters) {
+        for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+          const uint32_t b = t & 1;
+          const uint32_t d = tmem + b * 256;
+          const bool last = jt == j_tiles - 1;
+          const int nch = last ? p.chunks_last : CHUNKS;
+          const int pre = nch < need ? nch : need;
+          for (int c = 0; c < pre; ++c)
+            ptx::mbar_wait(&bars->a2_full[(g + c) % A2_SLOTS], ((g + c) / A2_SLOTS) & 1);
+          for (int c = 0; c < nch; ++c, ++g) {
+            const int slot = g % A2_SLOTS, bslot = g & 1;
+            if (c >= pre) ptx::mbar_wait(&bars->a2_full[slot], (g / A2_SLOTS) & 1);
+            ptx::mbar_wait(&bars->b2_full[bslot], (g >> 1) & 1);
+            ptx::tc_fence_after();
+            const uint32_t a0 = ptx::smem_u32(a2_base + slot * A2_BYTES);
+            const uint32_t b0 = ptx::smem_u32(b2_base + bslot * B2_BYTES);
+            const int nk16 = (last && c == nch - 1) ? p.k16_chunk_last : 4;
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4)
+              if (k4 < nk16)
+                ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc2,
+                                   (c | k4) != 0);
+            ptx::mma_commit_pair(&bars->a2_empty[slot], PAIR);
+            ptx::mma_commit_pair(&bars->b2_empty[bslot], PAIR);
+          }
+          ptx::mma_commit_pair(&bars->d2_full[b], PAIR);
+        }
+      }
+    }
+  } else {
+    // ---- epilogue (both CTAs): this CTA's 128 TMEM lanes ---------------------
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int p_local = r / p.lpad;
+    const int l = r % p.lpad;
+    const uint32_t d2col = crank * n2c + p_local * MPAD;
+    uint32_t t = 0, g = 0;
+    for (int u = cid; u < n_units; u += n_clusters) {
+      const int kk = u / n_rb2, rb2 = u % n_rb2;
+      float zacc[MPAD];
+#pragma unroll
+      for (int m = 0; m < MPAD; ++m) zacc[m] = 0.f;
+      for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+        const uint32_t b = t & 1, use = t >> 1;
+        const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
+        ptx::mbar_wait(&bars->tmem_full[b], use & 1);
+        ptx::tc_fence_after();
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int slot = g % A2_SLOTS;
+          ptx::mbar_wait(&bars->a2_empty[slot], ((g / A2_SLOTS) & 1) ^ 1);
+          uint8_t* row = a2_base + slot * A2_BYTES + r * 128;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            float v[32];
+            ptx::tmem_ld32(lane_addr + b * 256 + c * 64 + h * 32, v);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int q8 = h * 4 + q4;
+              uint4 pk;
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(v[q4 * 8 + 0], v[q4 * 8 + 1]);
+              __nv_bfloat162 h1 = __floats2bfloat162_rn(v[q4 * 8 + 2], v[q4 * 8 + 3]);
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[q4 * 8 + 4], v[q4 * 8 + 5]);
+              __nv_bfloat162 h3 = __floats2bfloat162_rn(v[q4 * 8 + 6], v[q4 * 8 + 7]);
+              pk.x = *reinterpret_cast<uint32_t*>(&h0);
+              pk.y = *reinterpret_cast<uint32_t*>(&h1);
+              pk.z = *reinterpret_cast<uint32_t*>(&h2);
+              pk.w = *reinterpret_cast<uint32_t*>(&h3);
+              *reinterpret_cast<uint4*>(row + ((q8 ^ (r & 7)) << 4)) = pk;
+            }
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(&bars->a2_full[slot], 0));
+        }
+        ptx::mbar_wait(&bars->d2_full[b], use & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int mc = 0; mc < MPAD / 32; ++mc) {
+          float v[32];
+          ptx::tmem_ld32(lane_addr + b * 256 + d2col + mc * 32, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) zacc[mc * 32 + e] += v[e];
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(&bars->tmem_empty[b], 0));
+      }
+      const int prep = (rb2 * 2 + static_cast<int>(crank)) * p.rpb + p_local;
+      if (prep < p.count) {
+        float* dst = p.z + ((static_cast<int64_t>(prep) * p.kc + kk) * MPAD) * p.lpad + l;
+        const int stride = p.lpad;
+#pragma unroll
+        for (int m = 0; m < MPAD; ++m) {
+          __stcs(dst, zacc[m]);
+          dst += stride;
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_pair(tmem, 512);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn2() {
+  static EncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      throw Status(XTSG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFn>(f);
+  }();
+  return fn;
+}
+
+void map_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              const uint32_t* box) {
+  cuuint64_t d[3], s[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  if (reinterpret_cast<uintptr_t>(base) % 16) usage("tma: base address must be 16-byte aligned");
+  for (int i = 0; i < rank - 1; ++i)
+    if (s[i] % 16) usage("tma: strides must be multiples of 16 bytes");
+  const CUresult r = encode_fn2()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, bx, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Status(XTSG_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+template <int MPAD>
+void launch_pair(const TtmLaunch& L, cudaStream_t st) {
+  CUtensorMap mu, mx, mv;
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.rows_u)};
+    const uint64_t str[1] = {static_cast<uint64_t>(L.ld_u) * 2};
+    const uint32_t box[2] = {BK, BM};
+    map_bf16(&mu, L.u, 2, dims, str, box);
+  }
+  {
+    const uint64_t dims[3] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.nk)};
+    const uint64_t str[2] = {static_cast<uint64_t>(L.ld_x0) * 2, static_cast<uint64_t>(L.ld_x1) * 2};
+    const uint32_t box[3] = {BK, BNC, 1};
+    map_bf16(&mx, L.x, 3, dims, str, box);
+  }
+  {
+    const uint64_t dims[2] = {static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.rows_v)};
+    const uint64_t str[1] = {static_cast<uint64_t>(L.ld_v) * 2};
+    const uint32_t box[2] = {64, static_cast<uint32_t>(L.prm.n2)};
+    map_bf16(&mv, L.v, 2, dims, str, box);
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    XCUDA(cudaFuncSetAttribute(ttm_pair_kernel<MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
+    attr_set = true;
+  }
+  const int clusters = (L.prm.n_rb / 2) * L.prm.kc;
+  const int cap = (L.grid_limit > 0 ? L.grid_limit : sm_count()) / 2;
+  const int grid = std::max(1, std::min(clusters, cap)) * 2;
+  ttm_pair_kernel<MPAD><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, L.prm);
+  XLAUNCH_CHECK();
+}
+
+}  // namespace
+
+bool ttm_pair_supported(const TtmLaunch& L) {
+  return L.prm.n_rb % 2 == 0 && L.prm.n2 <= 128 && L.prm.lpad * L.prm.rpb == BM;
+}
+
+void launch_ttm_pair(const TtmLaunch& L, cudaStream_t st) {
+  if (!ttm_pair_supported(L)) usage("ttm_pair: unsupported shape for the CTA-pair kernel");
+  switch (L.mpad) {
+    case 32: launch_pair<32>(L, st); break;
+    case 64: launch_pair<64>(L, st); break;
+    case 128: launch_pair<128>(L, st); break;
+    default: usage("ttm_pair: M must pad to 32, 64 or 128");
+  }
+}
+
+}  // namespace xtsg
