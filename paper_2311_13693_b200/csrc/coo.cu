@@ -200,6 +200,16 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   if (desc.precision != XTSG_PREC_BF16) usage("plan_compress_coo: needs a bf16 (tensor-core) plan");
   if (nnz < 0) usage("plan_compress_coo: negative nnz");
   if (nnz >= (int64_t(1) << 32)) usage("plan_compress_coo: at most 2^32-1 nonzeros per call");
+  if (stage1) {
+    const int64_t ysz = desc.count * desc.reduced[0] * desc.reduced[1] * desc.reduced[2];
+    OutView<float> yo(y, static_cast<size_t>(ysz), s);
+    if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
+    DevBuf<float> zin(static_cast<size_t>(inner_dims[0] * inner_dims[1] * inner_dims[2]), s);
+    stage1->compress_coo(i, j, k, val, nnz, zin.ptr, false, s);
+    stage2(zin.ptr, yo.dev, accumulate, s);
+    if (yo.host) yo.finish();
+    return;
+  }
   const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
   const int64_t ysz = P * L * M * N;

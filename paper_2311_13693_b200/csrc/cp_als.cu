@@ -230,6 +230,67 @@ __device__ void apply_pinv(const double* Mt, int rows, int R, const double* P, d
   }
 }
 
+// F = Mt * pinv(H) for the symmetric Hadamard Gram H (R x R, in s.H).
+// Fast path: Cholesky H = L L' by warp 0 (L into s.P) and one forward/back
+// substitution per row of Mt (no block-wide syncs inside). When H is not
+// safely positive definite (a pivot below 1e-11 of the largest diagonal —
+// well above the reference's rcond = 1e-12 of sigma_max cut, linalg.cpp:56)
+// it falls back to the Jacobi pseudo-inverse, i.e. the reference semantics.
+__device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, double* F, int* ok) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double* Lm = s.P;  // lower triangle, column-major R x R
+    if (R > 64) {  // the per-row substitution keeps R values in registers/local memory
+      if (lane == 0) *ok = 0;
+    } else {
+    double mxd = 0.0;
+    for (int i = 0; i < R; ++i) mxd = fmax(mxd, s.H[i + R * i]);
+    bool good = mxd > 0.0;
+    for (int k = 0; k < R && good; ++k) {
+      double part = 0.0;
+      for (int j = lane; j < k; j += 32) part = fma(Lm[k + R * j], Lm[k + R * j], part);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const double d = s.H[k + R * k] - part;
+      if (!(d > 1e-11 * mxd)) {
+        good = false;
+        break;
+      }
+      const double lkk = sqrt(d);
+      for (int i = k + 1 + lane; i < R; i += 32) {
+        double acc = s.H[i + R * k];
+        for (int j = 0; j < k; ++j) acc = fma(-Lm[i + R * j], Lm[k + R * j], acc);
+        Lm[i + R * k] = acc / lkk;
+      }
+      if (lane == 0) Lm[k + R * k] = lkk;
+      __syncwarp();
+    }
+    if (lane == 0) *ok = good ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (*ok) {
+    // rows of Mt: L L' f' = m'  (f, m row vectors of length R)
+    for (int x = threadIdx.x; x < rows; x += blockDim.x) {
+      double y[64];
+      for (int i = 0; i < R; ++i) {
+        double acc = Mt[x + rows * i];
+        for (int j = 0; j < i; ++j) acc = fma(-s.P[i + R * j], y[j], acc);
+        y[i] = acc / s.P[i + R * i];
+      }
+      for (int i = R - 1; i >= 0; --i) {
+        double acc = y[i];
+        for (int j = i + 1; j < R; ++j) acc = fma(-s.P[j + R * i], y[j], acc);
+        y[i] = acc / s.P[i + R * i];
+      }
+      for (int i = 0; i < R; ++i) F[x + rows * i] = y[i];
+    }
+  } else {
+    pinv_sym(s.H, R, s);
+    apply_pinv(Mt, rows, R, s.P, F);
+  }
+}
+
 __device__ double residual_sq(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s) {
   double acc = 0.0;
   const int64_t total = static_cast<int64_t>(n1) * n2 * n3;
@@ -331,6 +392,7 @@ __device__ void nvecs_init(const double* __restrict__ T, int n1, int n2, int n3,
 
 __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3) {
   extern __shared__ double sm[];
+  __shared__ int s_ok;
   const AlsInst in = insts[blockIdx.x];
   const int R = static_cast<int>(in.cfg.rank);
   const int mx = max(n1, max(n2, n3));
@@ -378,8 +440,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
     mttkrp(T, n1, n2, n3, R, 0, s, s.M);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
     __syncthreads();
-    pinv_sym(s.H, R, s);
-    apply_pinv(s.M, n1, R, s.P, s.A);
+    solve_gram(s.M, n1, R, s, s.A, &s_ok);
     __syncthreads();
     gram(s.A, n1, R, s.G1);
     __syncthreads();
@@ -387,8 +448,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
     mttkrp(T, n1, n2, n3, R, 1, s, s.M);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G1[e];
     __syncthreads();
-    pinv_sym(s.H, R, s);
-    apply_pinv(s.M, n2, R, s.P, s.B);
+    solve_gram(s.M, n2, R, s, s.B, &s_ok);
     __syncthreads();
     gram(s.B, n2, R, s.G2);
     __syncthreads();
@@ -396,8 +456,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
     mttkrp(T, n1, n2, n3, R, 2, s, s.M);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G2[e] * s.G1[e];
     __syncthreads();
-    pinv_sym(s.H, R, s);
-    apply_pinv(s.M, n3, R, s.P, s.C);
+    solve_gram(s.M, n3, R, s, s.C, &s_ok);
     __syncthreads();
     // move a/b column norms into c (cp_als.cpp:84-96)
     for (int r = threadIdx.x; r < R; r += blockDim.x) {

@@ -105,6 +105,16 @@ int g1(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_
 void Plan::compress_factors(const double* a, const double* b, const double* c, int64_t rank, int64_t k0, int64_t k1,
                             float* y, bool accumulate, cudaStream_t s) {
   if (desc.precision != XTSG_PREC_BF16) usage("plan_compress_factors: needs a bf16 (tensor-core) plan");
+  if (stage1) {
+    const int64_t ysz = desc.count * desc.reduced[0] * desc.reduced[1] * desc.reduced[2];
+    OutView<float> yo(y, static_cast<size_t>(ysz), s);
+    if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
+    DevBuf<float> zin(static_cast<size_t>(inner_dims[0] * inner_dims[1] * inner_dims[2]), s);
+    stage1->compress_factors(a, b, c, rank, k0, k1, zin.ptr, false, s);
+    stage2(zin.ptr, yo.dev, accumulate, s);
+    if (yo.host) yo.finish();
+    return;
+  }
   const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
   if (rank < 1 || rank > 64) usage("plan_compress_factors: rank must be in [1, 64]");
   if (k0 < 0 || k1 > K || k0 >= k1) usage("plan_compress_factors: k range outside the tensor");

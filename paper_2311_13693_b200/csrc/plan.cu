@@ -113,6 +113,19 @@ __global__ void compact_y_kernel(const float* __restrict__ ypad, int64_t count, 
   }
 }
 
+__global__ void f32_to_f64_kernel(const float* __restrict__ s, int64_t n, double* __restrict__ d) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[e] = static_cast<double>(s[e]);
+}
+
+__global__ void add_f64_to_f32_kernel(const double* __restrict__ s, int64_t n, int32_t accumulate,
+                                      float* __restrict__ d) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[e] = accumulate ? static_cast<float>(d[e] + s[e]) : static_cast<float>(s[e]);
+}
+
 int grid_for(int64_t work, int per_block = 256) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, per_block), 148 * 16)));
 }
@@ -140,7 +153,6 @@ size_t dtype_size(int32_t dt) {
 Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
   const EnsembleShape sh =
       validate_ensemble(desc.dims, desc.reduced, desc.count, desc.shared_rows, desc.spec);
-  (void)sh;
   if (desc.precision != XTSG_PREC_FP64 && desc.precision != XTSG_PREC_BF16) usage("plan: unknown precision");
   require_device();
   XCUDA(cudaGetDevice(&device));
@@ -148,37 +160,102 @@ Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
   XCUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
   const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
+  const bool two = desc.spec.kind == XTSG_KIND_TWO_STAGE && desc.precision == XTSG_PREC_BF16;
   // fp64 ensemble in the reference layout (make_ensemble, bit-exact)
   u64 = DevBuf<double>(static_cast<size_t>(P * L * I), st);
   v64 = DevBuf<double>(static_cast<size_t>(P * M * J), st);
   w64 = DevBuf<double>(static_cast<size_t>(P * N * K), st);
+  DevBuf<double> inner[3];
+  if (two) {
+    for (int m = 0; m < 3; ++m) {
+      inner[m] = DevBuf<double>(static_cast<size_t>(sh.inner[m] * desc.dims[m]), st);
+      outer[m] = DevBuf<double>(static_cast<size_t>(P * desc.reduced[m] * sh.inner[m]), st);
+      inner_dims[m] = sh.inner[m];
+    }
+  }
   const int32_t rc = xtsg_make_ensemble(desc.dims, desc.reduced, P, desc.shared_rows, &desc.spec, desc.seed,
-                                        u64.ptr, v64.ptr, w64.ptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                        nullptr);
+                                        u64.ptr, v64.ptr, w64.ptr, two ? inner[0].ptr : nullptr,
+                                        two ? inner[1].ptr : nullptr, two ? inner[2].ptr : nullptr,
+                                        two ? outer[0].ptr : nullptr, two ? outer[1].ptr : nullptr,
+                                        two ? outer[2].ptr : nullptr);
   if (rc != XTSG_OK) throw Status(rc, std::string("plan: make_ensemble failed: ") + xtsg_last_error());
-  if (desc.precision == XTSG_PREC_BF16) {
-    lpad = pad_reduced(L);
-    mpad = pad_reduced(M);
-    if (lpad < 0 || mpad < 0) usage("plan: the bf16 tensor-core path supports reduced dims <= 128");
-    rpb = 128 / lpad;
-    n2 = rpb * mpad;
-    if (n2 > 128) usage("plan: (128/Lpad)*Mpad must be <= 128 for the tensor-core path");
-    rows_u = round_up(P * lpad, 128);  // odd row-block counts run the kernel without clusters
-    ld_u = round_up(I, 8);
-    ld_v = round_up(J, 8);
-    ustack = DevBuf<__nv_bfloat16>(static_cast<size_t>(rows_u * ld_u), st);
-    ustack.zero();
-    vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(P * mpad * ld_v), st);
-    vt.zero();
-    wf = DevBuf<float>(static_cast<size_t>(P * N * K), st);
-    pack_rows<__nv_bfloat16>(u64.ptr, P, L, I, lpad, ld_u, ustack.ptr, st);
-    pack_rows<__nv_bfloat16>(v64.ptr, P, M, J, mpad, ld_v, vt.ptr, st);
-    pack_rows<float>(w64.ptr, P, N, K, N, K, wf.ptr, st);
-    // fp64 copies are not needed by the bf16 path any more
+  if (two) {
+    // Two-stage compression as a true two-pass: X is compressed
+    // once by the shared inner matrices (stage 1, tensor cores, a 1-replica
+    // plan of alpha*L x beta*M x gamma*N), then the small intermediate by the
+    // P outer matrices (stage 2, fp64). Mode-1 work per element drops from
+    // 2*P*L to 2*alpha*L. Identity: comp(X, outer*inner) == comp(comp(X, inner), outer)
+    // (test_compression.cpp:187-200).
+    xtsg_plan_desc d1 = desc;
+    d1.count = 1;
+    d1.shared_rows = 0;
+    for (int m = 0; m < 3; ++m) d1.reduced[m] = sh.inner[m];
+    d1.spec.kind = XTSG_KIND_GAUSSIAN;
+    stage1 = std::make_unique<Plan>(d1, inner[0].ptr, inner[1].ptr, inner[2].ptr);
     u64.release();
     v64.release();
+    w64.release();
+  } else if (desc.precision == XTSG_PREC_BF16) {
+    build_tc_operands();
   }
   XCUDA(cudaStreamSynchronize(st));
+}
+
+// Explicit-operand plan (fp64 device matrices in the reference layout).
+Plan::Plan(const xtsg_plan_desc& d, const double* u, const double* v, const double* w) : desc(d) {
+  require_device();
+  XCUDA(cudaGetDevice(&device));
+  st = thread_stream();
+  XCUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
+  const int64_t P = desc.count;
+  u64 = DevBuf<double>(static_cast<size_t>(P * desc.reduced[0] * desc.dims[0]), st);
+  v64 = DevBuf<double>(static_cast<size_t>(P * desc.reduced[1] * desc.dims[1]), st);
+  w64 = DevBuf<double>(static_cast<size_t>(P * desc.reduced[2] * desc.dims[2]), st);
+  XCUDA(cudaMemcpyAsync(u64.ptr, u, u64.n * sizeof(double), cudaMemcpyDefault, st));
+  XCUDA(cudaMemcpyAsync(v64.ptr, v, v64.n * sizeof(double), cudaMemcpyDefault, st));
+  XCUDA(cudaMemcpyAsync(w64.ptr, w, w64.n * sizeof(double), cudaMemcpyDefault, st));
+  if (desc.precision == XTSG_PREC_BF16) build_tc_operands();
+  XCUDA(cudaStreamSynchronize(st));
+}
+
+void Plan::build_tc_operands() {
+  const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
+  const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
+  lpad = pad_reduced(L);
+  mpad = pad_reduced(M);
+  if (lpad < 0 || mpad < 0) usage("plan: the bf16 tensor-core path supports reduced dims <= 128");
+  rpb = 128 / lpad;
+  n2 = rpb * mpad;
+  if (n2 > 128) usage("plan: (128/Lpad)*Mpad must be <= 128 for the tensor-core path");
+  rows_u = round_up(P * lpad, 128);  // odd row-block counts run the kernel without clusters
+  ld_u = round_up(I, 8);
+  ld_v = round_up(J, 8);
+  ustack = DevBuf<__nv_bfloat16>(static_cast<size_t>(rows_u * ld_u), st);
+  ustack.zero();
+  vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(P * mpad * ld_v), st);
+  vt.zero();
+  wf = DevBuf<float>(static_cast<size_t>(P * N * K), st);
+  pack_rows<__nv_bfloat16>(u64.ptr, P, L, I, lpad, ld_u, ustack.ptr, st);
+  pack_rows<__nv_bfloat16>(v64.ptr, P, M, J, mpad, ld_v, vt.ptr, st);
+  pack_rows<float>(w64.ptr, P, N, K, N, K, wf.ptr, st);
+  // the fp64 copies are not needed by the bf16 path any more
+  u64.release();
+  v64.release();
+  w64.release();
+}
+
+// Stage 2 of a two-stage plan: y (+)= comp(zin, outer_u[p], outer_v[p], outer_w[p]).
+void Plan::stage2(const float* zin, float* y, bool accumulate, cudaStream_t s) {
+  const int64_t P = desc.count, L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2];
+  const int64_t a = inner_dims[0], b = inner_dims[1], c = inner_dims[2];
+  DevBuf<double> z64(static_cast<size_t>(a * b * c), s), y64(static_cast<size_t>(P * L * M * N), s);
+  f32_to_f64_kernel<<<grid_for(a * b * c), 256, 0, s>>>(zin, a * b * c, z64.ptr);
+  XLAUNCH_CHECK();
+  for (int64_t p = 0; p < P; ++p)
+    comp_f64_dev(z64.ptr, a, b, c, outer[0].ptr + p * L * a, L, L, outer[1].ptr + p * M * b, M, M,
+                 outer[2].ptr + p * N * c, N, N, y64.ptr + p * L * M * N, 0.0, s);
+  add_f64_to_f32_kernel<<<grid_for(P * L * M * N), 256, 0, s>>>(y64.ptr, P * L * M * N, accumulate ? 1 : 0, y);
+  XLAUNCH_CHECK();
 }
 
 Plan::~Plan() {
@@ -312,6 +389,16 @@ void Plan::ensure_z(int64_t floats, cudaStream_t s) {
 void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int64_t off[3],
                     const int64_t ext[3], void* y, bool accumulate, cudaStream_t s) {
   check_block(off, ext);
+  if (stage1) {
+    const int64_t ysz = desc.count * desc.reduced[0] * desc.reduced[1] * desc.reduced[2];
+    OutView<float> yo(static_cast<float*>(y), static_cast<size_t>(ysz), s);
+    if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
+    DevBuf<float> zin(static_cast<size_t>(inner_dims[0] * inner_dims[1] * inner_dims[2]), s);
+    stage1->compress(x, dtype, ld, off, ext, zin.ptr, false, s);
+    stage2(zin.ptr, yo.dev, accumulate, s);
+    if (yo.host) yo.finish();
+    return;
+  }
   const size_t es = dtype_size(dtype);
   if (ld[0] < ext[0] || ld[1] < ld[0] * ext[1]) usage("plan_compress: leading dimensions too small");
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;

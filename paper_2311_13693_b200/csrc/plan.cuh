@@ -2,6 +2,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <memory>
+#include <vector>
+
 #include "common.cuh"
 
 namespace xtsg {
@@ -31,7 +34,15 @@ struct Plan {
   double flops_fused = 0.0, flops_mode3 = 0.0;
   EvPair take_pair();
 
+  // two-stage plans: stage-1 plan over the shared inner matrices + outer (fp64)
+  std::unique_ptr<Plan> stage1;
+  DevBuf<double> outer[3];
+  int64_t inner_dims[3] = {0, 0, 0};
+
   explicit Plan(const xtsg_plan_desc& d);
+  Plan(const xtsg_plan_desc& d, const double* u, const double* v, const double* w);
+  void build_tc_operands();
+  void stage2(const float* zin, float* y, bool accumulate, cudaStream_t s);
   ~Plan();
   void check_block(const int64_t off[3], const int64_t ext[3]) const;
   void compress(const void* x, int32_t dtype, const int64_t ld[2], const int64_t off[3], const int64_t ext[3],
