@@ -41,6 +41,7 @@ struct AlsInst {
   int64_t* iters;
   int32_t* conv;
   double* nvec_ws;  // rows_max * rows_max * 2 doubles when nvecs
+  double* pbuf;     // n2 * n3 * R doubles: A-contracted tensor of the sweep
   xtsg_als_config cfg;
 };
 
@@ -128,7 +129,7 @@ __device__ void jacobi_eig(double* h, double* v, int n, int ld, double* cs, doub
 }
 
 struct Smem {
-  double *A, *B, *C, *G1, *G2, *G3, *H, *V, *P, *M, *cs, *sn, *red, *nrm;
+  double *A, *B, *C, *G1, *G2, *G3, *H, *V, *P, *M, *cs, *sn, *red, *nrm, *red2;
   int *pp, *qq;
 };
 
@@ -188,6 +189,113 @@ __device__ void mttkrp(const double* __restrict__ T, int n1, int n2, int n3, int
 #pragma unroll
     for (int c = 0; c < RC; ++c)
       if (r0 + c < R) out[x + rows * (r0 + c)] = acc[c];
+  }
+}
+
+// Mode-1 MTTKRP with warp lanes over i (coalesced T reads) and thread groups
+// over k: out[i, r] = sum_k C[k,r] sum_j T[i,j,k] B[j,r]. Per-group partials
+// are reduced in a fixed order (bitwise-deterministic, like the reference).
+constexpr int RCH = 16;          // ranks per register chunk
+constexpr int RED_DOUBLES = 4096;
+__device__ void mttkrp0(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s, double* out,
+                        double* red) {
+  const int n1r = (n1 + 31) & ~31;
+  const int W = n1r < (int)blockDim.x ? n1r : (int)blockDim.x;  // lanes over i per group
+  const int G = (int)blockDim.x / W;                               // groups over k
+  const int gid = threadIdx.x / W;
+  for (int r0 = 0; r0 < R; r0 += RCH) {
+    const int rc = R - r0 < RCH ? R - r0 : RCH;
+    for (int i0 = 0; i0 < n1; i0 += W) {
+      const int i = i0 + (threadIdx.x % W);
+      double acc[RCH];
+#pragma unroll
+      for (int c = 0; c < RCH; ++c) acc[c] = 0.0;
+      if (i < n1) {
+        for (int k = gid; k < n3; k += G) {
+          double tmp[RCH];
+#pragma unroll
+          for (int c = 0; c < RCH; ++c) tmp[c] = 0.0;
+          const double* tk = T + i + static_cast<int64_t>(n1) * n2 * k;
+#pragma unroll 4
+          for (int j = 0; j < n2; ++j) {
+            const double tv = __ldg(tk + static_cast<int64_t>(n1) * j);
+#pragma unroll
+            for (int c = 0; c < RCH; ++c)
+              if (c < rc) tmp[c] = fma(tv, s.B[j + n2 * (r0 + c)], tmp[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < RCH; ++c)
+            if (c < rc) acc[c] = fma(s.C[k + n3 * (r0 + c)], tmp[c], acc[c]);
+        }
+      }
+      // fixed-order reduction over the G groups through shared scratch
+      const int span = W < n1 - i0 ? W : n1 - i0;  // rows in this pass
+      const int per_round = RED_DOUBLES / (G * RCH);
+      for (int base = 0; base < span; base += per_round) {
+        const int li = (threadIdx.x % W) - base;
+        if (li >= 0 && li < per_round && i < n1)
+#pragma unroll
+          for (int c = 0; c < RCH; ++c) red[(gid * per_round + li) * RCH + c] = acc[c];
+        __syncthreads();
+        for (int e = threadIdx.x; e < per_round * rc; e += blockDim.x) {
+          const int row = e / rc, c = e % rc;
+          if (base + row >= span) continue;
+          double v = 0.0;
+          for (int g = 0; g < G; ++g) v += red[(g * per_round + row) * RCH + c];
+          out[(i0 + base + row) + n1 * (r0 + c)] = v;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+// P[r][k][j] = sum_i T[i,j,k] A[i,r] (the A-contracted tensor shared by the B
+// and C updates of a sweep), threads over (j, k) fibers, contiguous i reads.
+__device__ void contract_a(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s,
+                           double* __restrict__ P) {
+  const int fibers = n2 * n3;
+  for (int f = threadIdx.x; f < fibers; f += blockDim.x) {
+    const double* col = T + static_cast<int64_t>(n1) * f;
+    for (int r0 = 0; r0 < R; r0 += RCH) {
+      double acc[RCH];
+#pragma unroll
+      for (int c = 0; c < RCH; ++c) acc[c] = 0.0;
+#pragma unroll 4
+      for (int i = 0; i < n1; ++i) {
+        const double tv = __ldg(col + i);
+#pragma unroll
+        for (int c = 0; c < RCH; ++c)
+          if (r0 + c < R) acc[c] = fma(tv, s.A[i + n1 * (r0 + c)], acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < RCH; ++c)
+        if (r0 + c < R) P[static_cast<int64_t>(r0 + c) * fibers + f] = acc[c];
+    }
+  }
+}
+
+// out_B[j, r] = sum_k C[k,r] P[r][k][j]
+__device__ void mttkrp1_from_p(const double* __restrict__ P, int n2, int n3, int R, const Smem& s, double* out) {
+  for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
+    const int j = e % n2, r = e / n2;
+    const double* pr = P + static_cast<int64_t>(r) * n2 * n3 + j;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < n3; ++k) acc = fma(s.C[k + n3 * r], pr[static_cast<int64_t>(n2) * k], acc);
+    out[e] = acc;
+  }
+}
+
+// out_C[k, r] = sum_j B[j,r] P[r][k][j]
+__device__ void mttkrp2_from_p(const double* __restrict__ P, int n2, int n3, int R, const Smem& s, double* out) {
+  for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) {
+    const int k = e % n3, r = e / n3;
+    const double* pr = P + static_cast<int64_t>(r) * n2 * n3 + static_cast<int64_t>(n2) * k;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < n2; ++j) acc = fma(s.B[j + n2 * r], pr[j], acc);
+    out[e] = acc;
   }
 }
 
@@ -408,6 +516,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
   s.V = q; q += R * R;
   s.P = q; q += R * R;
   s.M = q; q += mx * R;
+  s.red2 = q; q += RED_DOUBLES;
   s.cs = q; q += std::max(mx, R) / 2 + 2;
   s.sn = q; q += std::max(mx, R) / 2 + 2;
   s.nrm = q; q += 2 * R;
@@ -437,7 +546,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
   double prev = 0.0;
   for (; it < in.cfg.max_iters; ++it) {
     // A update
-    mttkrp(T, n1, n2, n3, R, 0, s, s.M);
+    mttkrp0(T, n1, n2, n3, R, s, s.M, s.red2);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
     __syncthreads();
     solve_gram(s.M, n1, R, s, s.A, &s_ok);
@@ -445,7 +554,9 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
     gram(s.A, n1, R, s.G1);
     __syncthreads();
     // B update
-    mttkrp(T, n1, n2, n3, R, 1, s, s.M);
+    contract_a(T, n1, n2, n3, R, s, in.pbuf);
+    __syncthreads();
+    mttkrp1_from_p(in.pbuf, n2, n3, R, s, s.M);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G1[e];
     __syncthreads();
     solve_gram(s.M, n2, R, s, s.B, &s_ok);
@@ -453,7 +564,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
     gram(s.B, n2, R, s.G2);
     __syncthreads();
     // C update
-    mttkrp(T, n1, n2, n3, R, 2, s, s.M);
+    mttkrp2_from_p(in.pbuf, n2, n3, R, s, s.M);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G2[e] * s.G1[e];
     __syncthreads();
     solve_gram(s.M, n3, R, s, s.C, &s_ok);
@@ -505,7 +616,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
 
 size_t als_smem_bytes(int n1, int n2, int n3, int R) {
   const int mx = std::max(n1, std::max(n2, n3));
-  return sizeof(double) * (static_cast<size_t>(n1 + n2 + n3) * R + 6 * R * R + static_cast<size_t>(mx) * R +
+  return sizeof(double) * (static_cast<size_t>(n1 + n2 + n3) * R + 6 * R * R + static_cast<size_t>(mx) * R + 4096 +
                            2 * (std::max(mx, R) / 2 + 2) + 2 * R + 64 + 2 * (std::max(mx, R) / 2 + 2));
 }
 
@@ -585,6 +696,7 @@ int32_t xtsg_cp_als_batched(int64_t count, const double* t, int64_t n1, int64_t 
     for (int64_t q = 0; q < count; ++q) any_nvecs |= cfg[q].init == 1;
     const int64_t rmax = std::max({n1, n2, n3});
     DevBuf<double> ws(any_nvecs ? static_cast<size_t>(count * rmax * rmax * 2) : 0, st);
+    DevBuf<double> pb(static_cast<size_t>(count * n2 * n3 * rank), st);
     std::vector<AlsInst> hin(static_cast<size_t>(count));
     for (int64_t q = 0; q < count; ++q) {
       AlsInst& in = hin[static_cast<size_t>(q)];
@@ -596,6 +708,7 @@ int32_t xtsg_cp_als_batched(int64_t count, const double* t, int64_t n1, int64_t 
       in.iters = oi.dev + q;
       in.conv = ov.dev + q;
       in.nvec_ws = any_nvecs ? ws.ptr + q * rmax * rmax * 2 : nullptr;
+      in.pbuf = pb.ptr + q * n2 * n3 * rank;
       in.cfg = cfg[q];
     }
     DevBuf<AlsInst> din(static_cast<size_t>(count), st);

@@ -111,3 +111,19 @@ def test_bf16_plan_many_units_per_cta(gpu, restated):
     got = gpu.Plan.replicas(plan.compress(t), P, red)
     want = _oracle_replicas(restated, t, ens)
     assert max(rel_diff(w, g) for w, g in zip(want, got)) <= BF16_TOL
+
+
+def test_two_stage_plan_matches_materialized_ensemble(gpu, restated):
+    # two-stage compression as a true two-pass: stage 1 through
+    # the shared inner matrices on the tensor cores, stage 2 by the P outer
+    # matrices; must equal comp with the materialized u[p] = outer[p] * inner
+    # (test_compression.cpp:187-200 identity), to the bf16 tolerance
+    dims, red, P = (200, 180, 160), (40, 40, 40), 5
+    spec = dict(kind="two_stage", alpha=1.6, beta=1.6, gamma=1.6, inner_kind="sparse", inner_s=2.0)
+    plan = gpu.Plan(dims, red, P, 8, 42, **spec)
+    ens = gpu.make_ensemble(dims, red, P, 8, 42, **spec)
+    t = _tensor(dims, 4, rank=4)
+    got = gpu.Plan.replicas(plan.compress(t), P, red)
+    for p in range(P):
+        want = restated.comp(t, ens.u[p], ens.v[p], ens.w[p])
+        assert rel_diff(want, got[p]) <= BF16_TOL
