@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -35,20 +36,19 @@ constexpr int BM = 128;                 // rows per CTA (M = 256 per pair)
 constexpr int BN = 256;                 // j per tile (128 staged per CTA)
 constexpr int BNC = BN / 2;
 constexpr int BK = 64;
-constexpr int S = 4;                    // TMA stages
 constexpr int A_BYTES = BM * BK * 2;    // 16 KB
 constexpr int B_BYTES = BNC * BK * 2;   // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int A2_SLOTS = 4;
 constexpr int A2_BYTES = BM * 64 * 2;   // 16 KB
 constexpr int B2_BYTES = 128 * 64 * 2;  // 16 KB (n2 <= 128 rows per CTA)
 constexpr int CHUNKS = BN / 64;
-constexpr int SMEM_DATA = S * STAGE_BYTES + A2_SLOTS * A2_BYTES + 2 * B2_BYTES;
-constexpr int SMEM_TOTAL = SMEM_DATA + 1024 + 512;
-static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
+// S TMA stages, A2_SLOTS bf16 mode-1 chunks in flight to mode 2
+constexpr int smem_total(int S, int A2_SLOTS) { return S * STAGE_BYTES + A2_SLOTS * A2_BYTES + 2 * B2_BYTES + 1024 + 512; }
+static_assert(smem_total(4, 4) <= 232448 && smem_total(5, 2) <= 232448, "shared memory budget");
 constexpr uint32_t IDESC1 = ptx::idesc_bf16(2 * BM, BN);
 constexpr uint16_t PAIR = 0x3;
 
+template <int S, int A2_SLOTS>
 struct Bars2 {
   uint64_t full1[S], empty1[S];
   uint64_t tmem_full[2], tmem_empty[2], d2_full[2];
@@ -57,7 +57,7 @@ struct Bars2 {
   uint32_t tmem_base;
 };
 
-template <int MPAD>
+template <int MPAD, bool LOCAL2, int S, int A2_SLOTS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     ttm_pair_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_x,
                     const __grid_constant__ CUtensorMap tm_v, const TtmParams p) {
@@ -66,7 +66,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   uint8_t* stage_base = smem;
   uint8_t* a2_base = smem + S * STAGE_BYTES;
   uint8_t* b2_base = a2_base + A2_SLOTS * A2_BYTES;
-  Bars2* bars = reinterpret_cast<Bars2*>(b2_base + 2 * B2_BYTES);
+  auto* bars = reinterpret_cast<Bars2<S, A2_SLOTS>*>(b2_base + 2 * B2_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = ptx::cluster_ctarank();
@@ -84,7 +84,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       ptx::mbar_init(&bars->b2_empty[b], 1);
     }
     for (int q = 0; q < A2_SLOTS; ++q) {
-      ptx::mbar_init(&bars->a2_full[q], 8);
+      ptx::mbar_init(&bars->a2_full[q], LOCAL2 ? 4 : 8);
       ptx::mbar_init(&bars->a2_empty[q], 1);
     }
     ptx::fence_barrier_init();
@@ -106,8 +106,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int n_units = n_rb2 * p.kc;
   const int j_tiles = p.j_tiles, k_steps = p.k_steps;
   const int n2c = p.n2;            // mode-2 columns contributed by this CTA
-  const int n2 = 2 * n2c;          // mode-2 MMA N
-  const int need = (n2 + 63) / 64; // D1 chunks D2 overlaps
+  const int n2 = LOCAL2 ? n2c : 2 * n2c;  // mode-2 MMA N
+  const int need = (n2 + 63) / 64;        // D1 chunks D2 overlaps
 
   if (warp == 0) {
     if (lane == 0) {
@@ -124,7 +124,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             if (leader) ptx::mbar_arrive_expect_tx(&bars->full1[s], 2 * STAGE_BYTES);
             const uint32_t fb = ptx::mapa_shared(&bars->full1[s], 0);
             ptx::tma_load_2d_pair(st, &tm_u, fb, ks * BK, urow);
-            ptx::tma_load_3d_pair(st + A_BYTES, &tm_x, fb, ks * BK, jt * BN + crank * BNC, p.k_first + kk);
+            // the last j tile runs with N = n_last: each CTA holds n_last / 2 of its j
+            const int half = jt == j_tiles - 1 ? (p.n_last >> 1) : BNC;
+            ptx::tma_load_3d_pair(st + A_BYTES, &tm_x, fb, ks * BK, jt * BN + crank * half, p.k_first + kk);
             if (++s == S) { s = 0; ph ^= 1; }
           }
         }
@@ -141,6 +143,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           ptx::mbar_wait(&bars->tmem_empty[b], (use & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t d = tmem + b * 256;
+          const uint32_t idesc1 = jt == j_tiles - 1 ? ptx::idesc_bf16(2 * BM, p.n_last) : IDESC1;
           for (int ks = 0; ks < k_steps; ++ks) {
             ptx::mbar_wait(&bars->full1[s], ph);
             ptx::tc_fence_after();
@@ -150,7 +153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
             for (int k4 = 0; k4 < BK / 16; ++k4)
               if (k4 < nk16)
-                ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), IDESC1,
+                ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc1,
                                    (ks | k4) != 0);
             ptx::mma_commit_pair(&bars->empty1[s], PAIR);
             if (++s == S) { s = 0; ph ^= 1; }
@@ -172,17 +175,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           for (int c = 0; c < nch; ++c, ++g) {
             const int slot = g & 1;
             ptx::mbar_wait(&bars->b2_empty[slot], ((g >> 1) & 1) ^ 1);
-            if (leader) ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], 2 * bytes);
-            ptx::tma_load_2d_pair(b2_base + slot * B2_BYTES, &tm_v, ptx::mapa_shared(&bars->b2_full[slot], 0),
-                                  jt * BN + c * 64, vrow);
+            if (LOCAL2) {
+              ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], bytes);
+              ptx::tma_load_2d(b2_base + slot * B2_BYTES, &tm_v, &bars->b2_full[slot], jt * BN + c * 64, vrow);
+            } else {
+              if (leader) ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], 2 * bytes);
+              ptx::tma_load_2d_pair(b2_base + slot * B2_BYTES, &tm_v, ptx::mapa_shared(&bars->b2_full[slot], 0),
+                                    jt * BN + c * 64, vrow);
+            }
           }
         }
       }
     }
   } else if (warp == 3) {
-    if (leader && lane == 0) {
-      // ---- mode-2 MMA issuer (leader) -----------------------------------------
-      const uint32_t idesc2 = ptx::idesc_bf16(2 * BM, n2);
+    if ((LOCAL2 || leader) && lane == 0) {
+      // ---- mode-2 MMA issuer (leader; every CTA for the per-CTA variant) ------
+      const uint32_t idesc2 = ptx::idesc_bf16(LOCAL2 ? BM : 2 * BM, n2);
       uint32_t t = 0, g = 0;
       for (int u = cid; u < n_units; u += n_clusters) {
         for (int jt = 0; jt < j_tiles; ++jt, ++t) {
@@ -201,15 +209,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             const uint32_t a0 = ptx::smem_u32(a2_base + slot * A2_BYTES);
             const uint32_t b0 = ptx::smem_u32(b2_base + bslot * B2_BYTES);
             const int nk16 = (last && c == nch - 1) ? p.k16_chunk_last : 4;
+            if (LOCAL2) {
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4)
-              if (k4 < nk16)
-                ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc2,
-                                   (c | k4) != 0);
-            ptx::mma_commit_pair(&bars->a2_empty[slot], PAIR);
-            ptx::mma_commit_pair(&bars->b2_empty[bslot], PAIR);
+              for (int k4 = 0; k4 < 4; ++k4)
+                if (k4 < nk16)
+                  ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc2,
+                                (c | k4) != 0);
+              ptx::mma_commit(&bars->a2_empty[slot]);
+              ptx::mma_commit(&bars->b2_empty[bslot]);
+            } else {
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4)
+                if (k4 < nk16)
+                  ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc2,
+                                     (c | k4) != 0);
+              ptx::mma_commit_pair(&bars->a2_empty[slot], PAIR);
+              ptx::mma_commit_pair(&bars->b2_empty[bslot], PAIR);
+            }
           }
-          ptx::mma_commit_pair(&bars->d2_full[b], PAIR);
+          if (LOCAL2)
+            ptx::mma_commit(&bars->d2_full[b]);
+          else
+            ptx::mma_commit_pair(&bars->d2_full[b], PAIR);
         }
       }
     }
@@ -220,7 +241,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int p_local = r / p.lpad;
     const int l = r % p.lpad;
-    const uint32_t d2col = crank * n2c + p_local * MPAD;
+    const uint32_t d2col = (LOCAL2 ? 0u : crank * n2c) + p_local * MPAD;
     uint32_t t = 0, g = 0;
     for (int u = cid; u < n_units; u += n_clusters) {
       const int kk = u / n_rb2, rb2 = u % n_rb2;
@@ -259,7 +280,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           ptx::fence_proxy_async_smem();
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(&bars->a2_full[slot], 0));
+          if (lane == 0) {
+            if (LOCAL2)
+              ptx::mbar_arrive(&bars->a2_full[slot]);
+            else
+              ptx::mbar_arrive_cluster(ptx::mapa_shared(&bars->a2_full[slot], 0));
+          }
         }
         ptx::mbar_wait(&bars->d2_full[b], use & 1);
         ptx::tc_fence_after();
@@ -330,7 +356,7 @@ void map_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
   if (r != CUDA_SUCCESS) throw Status(XTSG_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
-template <int MPAD>
+template <int MPAD, bool LOCAL2, int S, int A2_SLOTS>
 void launch_pair(const TtmLaunch& L, cudaStream_t st) {
   CUtensorMap mu, mx, mv;
   {
@@ -351,15 +377,16 @@ void launch_pair(const TtmLaunch& L, cudaStream_t st) {
     const uint32_t box[2] = {64, static_cast<uint32_t>(L.prm.n2)};
     map_bf16(&mv, L.v, 2, dims, str, box);
   }
+  constexpr int SMEM_TOTAL = smem_total(S, A2_SLOTS);
   static bool attr_set = false;
   if (!attr_set) {
-    XCUDA(cudaFuncSetAttribute(ttm_pair_kernel<MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
+    XCUDA(cudaFuncSetAttribute(ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
     attr_set = true;
   }
   const int clusters = (L.prm.n_rb / 2) * L.prm.kc;
   const int cap = (L.grid_limit > 0 ? L.grid_limit : sm_count()) / 2;
   const int grid = std::max(1, std::min(clusters, cap)) * 2;
-  ttm_pair_kernel<MPAD><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, L.prm);
+  ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, L.prm);
   XLAUNCH_CHECK();
 }
 
@@ -371,10 +398,25 @@ bool ttm_pair_supported(const TtmLaunch& L) {
 
 void launch_ttm_pair(const TtmLaunch& L, cudaStream_t st) {
   if (!ttm_pair_supported(L)) usage("ttm_pair: unsupported shape for the CTA-pair kernel");
+  // 0: mode 2 on the pair (M = 256); 1: mode 2 per CTA (cta_group::1, M = 128,
+  // half the wasted columns), 4 stages; 2: per-CTA mode 2, 5 stages / 2 A2 slots
+  static const int variant = [] {
+    const char* e = std::getenv("XTSG_TTM_PAIR_CFG");
+    return e ? std::atoi(e) : 1;
+  }();
+  auto go = [&](auto mpad_tag) {
+    constexpr int MP = decltype(mpad_tag)::value;
+    if (variant == 0)
+      launch_pair<MP, false, 4, 4>(L, st);
+    else if (variant == 1)
+      launch_pair<MP, true, 4, 4>(L, st);
+    else
+      launch_pair<MP, true, 5, 2>(L, st);
+  };
   switch (L.mpad) {
-    case 32: launch_pair<32>(L, st); break;
-    case 64: launch_pair<64>(L, st); break;
-    case 128: launch_pair<128>(L, st); break;
+    case 32: go(std::integral_constant<int, 32>{}); break;
+    case 64: go(std::integral_constant<int, 64>{}); break;
+    case 128: go(std::integral_constant<int, 128>{}); break;
     default: usage("ttm_pair: M must pad to 32, 64 or 128");
   }
 }
