@@ -251,6 +251,84 @@ int32_t xtsg_leading_left_singular_vectors(const double* m, int64_t rows, int64_
 int32_t xtsg_solve_least_squares(const double* a, int64_t rows, int64_t cols, const double* rhs,
                                  int64_t nrhs, double* x);
 
+/* ---- synthetic problems and the end-to-end pipeline (pipeline.hpp) ------ */
+#define XTSG_LAW_DENSE 0
+#define XTSG_LAW_SPARSE 1
+
+/* generate (pipeline.cpp:176-207) without materialization: the factor triple
+ * (a: dims[0] x rank, ...) of SyntheticSpec{dims, rank, law, nnz_per_col,
+ * seed}, bit-exact with the reference. Host or device outputs. */
+int32_t xtsg_generate_factors(const int64_t dims[3], int64_t rank, int32_t law, int64_t nnz_per_col,
+                              uint64_t seed, double* a, double* b, double* c);
+
+#define XTSG_MODE_DENSE 0
+#define XTSG_MODE_SPARSE 1
+#define XTSG_MODE_TWO_STAGE 2
+
+/* PipelineConfig (pipeline.hpp:16-45) minus dims/block/deterministic/workers
+ * (the device path has no block grid or worker pool), plus the compression
+ * precision: XTSG_PREC_FP64 is the reference's full precision, XTSG_PREC_BF16
+ * the tcgen05 path (then replica_fit_tol must admit the bf16 compression
+ * error, ~1e-2). */
+typedef struct xtsg_pipeline_config {
+  int64_t reduced[3];
+  int64_t rank;
+  int64_t replicas;      /* < 1 -> compute_replica_count(dims, reduced, slack) */
+  int64_t slack;         /* 10 */
+  int64_t shared;        /* < 1 -> min(2 * rank, min reduced) */
+  int32_t mode;          /* XTSG_MODE_* */
+  int32_t precision;     /* XTSG_PREC_FP64 / XTSG_PREC_BF16 */
+  double alpha, beta, gamma;  /* 1.6 */
+  double projection_s;   /* 0 -> max(1, min dims/reduced) */
+  int64_t omp_sparsity;  /* required for sparse and two-stage */
+  double omp_residual_tol;  /* 1e-9 */
+  int64_t sample_b;      /* < 1 -> max(2 * rank, 8) */
+  uint64_t seed;
+  int64_t als_max_iters; /* 500 */
+  double als_tol;        /* 1e-10 */
+  double replica_fit_tol;  /* 1e-6 */
+  int64_t als_restarts;  /* 3 */
+} xtsg_pipeline_config;
+
+/* RunMetrics (metrics.hpp) subset; stages: compression, decomposition,
+ * alignment, recovery. status 0 skipped, 1 ok, 2 error. */
+typedef struct xtsg_pipeline_metrics {
+  double stage_seconds[4];
+  int32_t stage_status[4];
+  int64_t replicas_total;
+  int64_t replicas_dropped;
+  double sample_mse;   /* held-out sample MSE (pipeline.cpp:561-570) */
+  double block_fit;    /* relative error of the sampled-block ALS */
+  int64_t als_sweeps;  /* ALS sweeps over all replicas and restarts */
+} xtsg_pipeline_metrics;
+
+/* decompose (pipeline.cpp:245-573): source = a column-major tensor (host or
+ * device fp64) or, when tensor is NULL, a factor triple of factor_rank
+ * columns (compressed from device-generated slabs on the bf16 path, by
+ * comp_from_factors on the fp64 path). Recovered factors: dims[m] x rank.
+ * Stage failures return XTSG_E_STAGE (payload 0 = stage index, payload 1 =
+ * the inner status). */
+int32_t xtsg_decompose(const xtsg_pipeline_config* cfg, const int64_t dims[3], const double* tensor,
+                       const double* fa, const double* fb, const double* fc, int64_t factor_rank,
+                       double* a_out, double* b_out, double* c_out, xtsg_pipeline_metrics* metrics);
+
+/* Stages 1-3 of decompose on replicas compressed by the caller (e.g. a
+ * mode-3-sharded multi-GPU compression reduced to this rank): count replicas
+ * L x M x N back to back, f32 or f64, host or device. The source is needed
+ * only for the sampled and held-out blocks. */
+int32_t xtsg_decompose_replicas(const xtsg_pipeline_config* cfg, const int64_t dims[3],
+                                const void* replicas, int32_t replicas_dtype, const double* tensor,
+                                const double* fa, const double* fb, const double* fc,
+                                int64_t factor_rank, double* a_out, double* b_out, double* c_out,
+                                xtsg_pipeline_metrics* metrics);
+
+/* evaluate (pipeline.cpp:577-609): joint permutation/scale against the truth,
+ * per-mode relative errors, leading-corner sample MSE. aligned_* optional. */
+int32_t xtsg_evaluate(const int64_t dims[3], int64_t rank, const double* ta, const double* tb,
+                      const double* tc, const double* ra, const double* rb, const double* rc,
+                      int64_t sample, double mode_rel_err[3], double* sample_mse,
+                      double* aligned_a, double* aligned_b, double* aligned_c);
+
 #ifdef __cplusplus
 }
 #endif

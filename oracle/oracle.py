@@ -246,6 +246,15 @@ class Reference:
                                       _ptr(b), _ptr(c)), "generate")
         return a, b, c
 
+    def evaluate(self, truth, recovered):
+        """pipeline.cpp:577-609 -> (mode_rel_err[3], sample_mse)"""
+        t = [_f(x) for x in truth]
+        r = [_f(x) for x in recovered]
+        out = np.zeros(4)
+        self._ok(self.L.xref_evaluate(_ptr(np.asarray([x.shape[0] for x in t], np.int64)), t[0].shape[1],
+                                      *[_ptr(x) for x in t], *[_ptr(x) for x in r], _ptr(out)), "evaluate")
+        return list(out[:3]), float(out[3])
+
     def cp_als(self, t, rank, max_iters=500, tol=1e-10, seed=0, init=0):
         t = _f(t)
         a = np.zeros((t.shape[0], rank), order="F")

@@ -19,12 +19,14 @@ from ._lib import (  # noqa: F401
     InsufficientReplicasError, StageError, UsageError, XtsError, lib, check, ptr,
     KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE, PREC_FP64, PREC_BF16,
     DTYPE_BF16, DTYPE_F32, DTYPE_F64, EnsembleSpec, PlanDesc, AlsConfig,
+    LAW_DENSE, LAW_SPARSE, MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE,
 )
 from .api import (  # noqa: F401
     compute_replica_count, gen_gaussian, gen_sparse_projection, make_ensemble, comp,
     comp_from_factors, reconstruct, comp_blocked, Plan, launch_count, device_ready,
     cp_als, cp_als_batched, relative_error, normalize_shared, max_trace_assignment,
     align_replicas, solve_stacked_ls, recover_perm_scale, apply_forward, apply_recovery,
+    generate_factors, PipelineConfig, RunMetrics, decompose, decompose_replicas, evaluate, EvalReport,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

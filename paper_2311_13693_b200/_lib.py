@@ -15,6 +15,8 @@ LIB_PATH = _PKG / "libxtsg.so"
 KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE = 0, 1, 2
 PREC_FP64, PREC_BF16 = 0, 1
 DTYPE_BF16, DTYPE_F32, DTYPE_F64 = 0, 1, 2
+LAW_DENSE, LAW_SPARSE = 0, 1
+MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE = 0, 1, 2
 
 
 class XtsError(RuntimeError):
@@ -79,6 +81,22 @@ class AlsConfig(C.Structure):
                 ("seed", C.c_uint64), ("init", C.c_int32), ("reserved", C.c_int32)]
 
 
+class PipelineConfigC(C.Structure):
+    _fields_ = [("reduced", C.c_int64 * 3), ("rank", C.c_int64), ("replicas", C.c_int64),
+                ("slack", C.c_int64), ("shared", C.c_int64), ("mode", C.c_int32),
+                ("precision", C.c_int32), ("alpha", C.c_double), ("beta", C.c_double),
+                ("gamma", C.c_double), ("projection_s", C.c_double), ("omp_sparsity", C.c_int64),
+                ("omp_residual_tol", C.c_double), ("sample_b", C.c_int64), ("seed", C.c_uint64),
+                ("als_max_iters", C.c_int64), ("als_tol", C.c_double),
+                ("replica_fit_tol", C.c_double), ("als_restarts", C.c_int64)]
+
+
+class PipelineMetricsC(C.Structure):
+    _fields_ = [("stage_seconds", C.c_double * 4), ("stage_status", C.c_int32 * 4),
+                ("replicas_total", C.c_int64), ("replicas_dropped", C.c_int64),
+                ("sample_mse", C.c_double), ("block_fit", C.c_double), ("als_sweeps", C.c_int64)]
+
+
 _P = C.c_void_p
 _I64 = C.c_int64
 _I32 = C.c_int32
@@ -123,6 +141,10 @@ _SIGS = {
     "xtsg_align_replicas": (_I32, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P]),
     "xtsg_solve_stacked_ls": (_I32, [_I64, _P, _I64, _I64, _P, _P, _P]),
     "xtsg_recover_perm_scale": (_I32, [_P, _P, _I64, _I64, _P, _P]),
+    "xtsg_generate_factors": (_I32, [_P, _I64, _I32, _I64, _U64, _P, _P, _P]),
+    "xtsg_decompose": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
+    "xtsg_decompose_replicas": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
+    "xtsg_evaluate": (_I32, [_P, _I64, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
 }
 
 

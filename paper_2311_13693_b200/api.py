@@ -13,9 +13,9 @@ from typing import Iterable, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (AlsConfig, EnsembleSpec, PlanDesc, DTYPE_BF16, DTYPE_F32, DTYPE_F64,
-                   KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE, PREC_BF16, PREC_FP64, check, lib,
-                   ptr)
+from ._lib import (AlsConfig, EnsembleSpec, PlanDesc, PipelineConfigC, PipelineMetricsC, DTYPE_BF16,
+                   DTYPE_F32, DTYPE_F64, KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE, LAW_DENSE, LAW_SPARSE,
+                   MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE, PREC_BF16, PREC_FP64, check, lib, ptr)
 
 _KINDS = {"gaussian": KIND_GAUSSIAN, "sparse": KIND_SPARSE, "two_stage": KIND_TWO_STAGE}
 
@@ -446,3 +446,153 @@ def apply_recovery(m, perm, scale) -> np.ndarray:
     out = np.zeros_like(m, order="F")
     out[:, list(perm)] = m / np.asarray(scale)[None, :]
     return out
+
+
+# ---------------------------------------------------------------------------
+# synthetic problems and the end-to-end pipeline (pipeline.hpp)
+
+def generate_factors(dims, rank: int, law: str = "dense", nnz_per_col: int = 0, seed: int = 0):
+    """generate (pipeline.cpp:176-207) without materialization: the factor triple."""
+    d = _arr3(dims)
+    outs = [np.zeros((int(d[m]), int(rank)), order="F") for m in range(3)]
+    code = {"dense": LAW_DENSE, "sparse": LAW_SPARSE}[law] if isinstance(law, str) else int(law)
+    check(lib.xtsg_generate_factors(ptr(d), int(rank), code, int(nnz_per_col), C.c_uint64(seed),
+                                    *[ptr(o) for o in outs]))
+    return tuple(outs)
+
+
+_MODES = {"dense": MODE_DENSE, "sparse": MODE_SPARSE, "two_stage": MODE_TWO_STAGE}
+
+
+@dataclass
+class PipelineConfig:
+    """PipelineConfig (pipeline.hpp:16-45) for the device pipeline, same defaults,
+    plus ``precision`` (PREC_FP64 = the reference's full precision, PREC_BF16 =
+    tcgen05 compression; then ``replica_fit_tol`` must admit the bf16 error)."""
+    reduced: tuple = (0, 0, 0)
+    rank: int = 1
+    replicas: int = 0
+    slack: int = 10
+    shared: int = 0
+    mode: str = "dense"
+    precision: int = PREC_FP64
+    alpha: float = 1.6
+    beta: float = 1.6
+    gamma: float = 1.6
+    projection_s: float = 0.0
+    omp_sparsity: int = 0
+    omp_residual_tol: float = 1e-9
+    sample_b: int = 0
+    seed: int = 0
+    als_max_iters: int = 500
+    als_tol: float = 1e-10
+    replica_fit_tol: float = 1e-6
+    als_restarts: int = 3
+
+    def to_c(self) -> PipelineConfigC:
+        c = PipelineConfigC()
+        for m in range(3):
+            c.reduced[m] = int(self.reduced[m])
+        c.rank, c.replicas, c.slack, c.shared = int(self.rank), int(self.replicas), int(self.slack), int(self.shared)
+        c.mode = _MODES[self.mode] if isinstance(self.mode, str) else int(self.mode)
+        c.precision = int(self.precision)
+        c.alpha, c.beta, c.gamma = float(self.alpha), float(self.beta), float(self.gamma)
+        c.projection_s = float(self.projection_s)
+        c.omp_sparsity, c.omp_residual_tol = int(self.omp_sparsity), float(self.omp_residual_tol)
+        c.sample_b = int(self.sample_b)
+        c.seed = C.c_uint64(self.seed).value
+        c.als_max_iters, c.als_tol = int(self.als_max_iters), float(self.als_tol)
+        c.replica_fit_tol, c.als_restarts = float(self.replica_fit_tol), int(self.als_restarts)
+        return c
+
+
+@dataclass
+class RunMetrics:
+    """RunMetrics subset (metrics.hpp): per-stage seconds/status, survivors, sample MSE."""
+    stage_seconds: dict
+    stage_status: dict
+    replicas_total: int
+    replicas_dropped: int
+    sample_mse: float
+    block_fit: float
+    als_sweeps: int
+
+
+_STAGES = ("compression", "decomposition", "alignment", "recovery")
+_STATUS = {0: "skipped", 1: "ok", 2: "error"}
+
+
+def _metrics(m: PipelineMetricsC) -> RunMetrics:
+    return RunMetrics({s: m.stage_seconds[i] for i, s in enumerate(_STAGES)},
+                      {s: _STATUS.get(m.stage_status[i], "?") for i, s in enumerate(_STAGES)},
+                      int(m.replicas_total), int(m.replicas_dropped), float(m.sample_mse),
+                      float(m.block_fit), int(m.als_sweeps))
+
+
+def _source(tensor, factors):
+    if tensor is not None:
+        t = tensor if not isinstance(tensor, np.ndarray) else _f64(tensor)
+        return t, tuple(int(x) for x in t.shape), (None, None, None), 0
+    f = tuple(_f64(x) for x in factors)
+    return None, (f[0].shape[0], f[1].shape[0], f[2].shape[0]), f, f[0].shape[1]
+
+
+def decompose(cfg: PipelineConfig, tensor=None, factors=None):
+    """decompose (pipeline.cpp:245-573) on the device -> (factors, RunMetrics).
+
+    ``tensor``: column-major fp64 array (numpy or a CUDA tensor); or ``factors``
+    (a, b, c) standing in for a tensor too large to hold (TensorSource)."""
+    t, dims, f, frank = _source(tensor, factors)
+    d = _arr3(dims)
+    outs = [np.zeros((int(d[m]), int(cfg.rank)), order="F") for m in range(3)]
+    met = PipelineMetricsC()
+    c = cfg.to_c()
+    rc = lib.xtsg_decompose(C.byref(c), ptr(d), ptr(t), *[ptr(x) for x in f], int(frank),
+                            *[ptr(o) for o in outs], C.byref(met))
+    check(rc)
+    return tuple(outs), _metrics(met)
+
+
+def decompose_replicas(cfg: PipelineConfig, replicas, tensor=None, factors=None):
+    """Stages 1-3 of decompose on caller-compressed replicas (flat P*L*M*N, f32/f64,
+    numpy or CUDA tensor), e.g. after a mode-3-sharded multi-GPU compression."""
+    t, dims, f, frank = _source(tensor, factors)
+    d = _arr3(dims)
+    if isinstance(replicas, np.ndarray):
+        y = np.ascontiguousarray(replicas)
+        code = DTYPE_F64 if y.dtype == np.float64 else DTYPE_F32
+        if y.dtype not in (np.float32, np.float64):
+            raise TypeError("replicas must be float32/float64")
+    else:
+        y = replicas.contiguous()
+        code = _torch_dtype_code(y)
+    outs = [np.zeros((int(d[m]), int(cfg.rank)), order="F") for m in range(3)]
+    met = PipelineMetricsC()
+    c = cfg.to_c()
+    check(lib.xtsg_decompose_replicas(C.byref(c), ptr(d), ptr(y), code, ptr(t), *[ptr(x) for x in f],
+                                      int(frank), *[ptr(o) for o in outs], C.byref(met)))
+    return tuple(outs), _metrics(met)
+
+
+@dataclass
+class EvalReport:
+    mode_rel_err: list
+    sample_mse: float
+    aligned: tuple
+
+
+def evaluate(truth, recovered, sample: int = 0) -> EvalReport:
+    """evaluate (pipeline.cpp:577-609) for a factor-triple truth."""
+    t = [_f64(x) for x in truth]
+    r = [_f64(x) for x in recovered]
+    d = _arr3([x.shape[0] for x in t])
+    rank = t[0].shape[1]
+    if any(x.shape != y.shape for x, y in zip(t, r)):
+        from ._lib import UsageError
+        raise UsageError("evaluate: factor dimensions disagree")
+    errs = np.zeros(3)
+    mse = np.zeros(1)
+    al = [np.zeros_like(x, order="F") for x in t]
+    check(lib.xtsg_evaluate(ptr(d), rank, *[ptr(x) for x in t], *[ptr(x) for x in r], int(sample),
+                            ptr(errs), ptr(mse), *[ptr(x) for x in al]))
+    return EvalReport([float(x) for x in errs], float(mse[0]), tuple(al))
