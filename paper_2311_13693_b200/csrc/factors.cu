@@ -141,7 +141,12 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
     acc = false;
   }
   const int64_t ldi = ceil_div(I, 8) * 8;
-  const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, (int64_t(1) << 30) / (ldi * J * 2)));
+  // slab size: enough slices per TTM launch for many persistent waves (the
+  // last wave's idle SMs amortized), within a quarter of the free HBM
+  size_t free_b = 0, total_b = 0;
+  XCUDA(cudaMemGetInfo(&free_b, &total_b));
+  const int64_t budget = std::min<int64_t>(int64_t(8) << 30, static_cast<int64_t>(free_b / 4));
+  const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, budget / (ldi * J * 2)));
   DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * J * ldi), s);
   const size_t smem = static_cast<size_t>(rank) * (TI + TJ) * sizeof(float);
   XCUDA(cudaFuncSetAttribute(gen_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -337,6 +338,16 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     tl.prm.n_last = static_cast<int32_t>(round_up(rem_j, 16));
     tl.prm.chunks_last = static_cast<int32_t>(ceil_div(rem_j, 64));
     tl.prm.k16_chunk_last = static_cast<int32_t>(ceil_div(rem_j - 64 * (tl.prm.chunks_last - 1), 16));
+    // unit grouping for L2 locality of U (ttm_tc2.cu decode_unit): 8 pairs of
+    // 128-row blocks = 2048 stacked U rows (~40 MB at I = 10^4) per group
+    {
+      static const int grp_env = [] {
+        const char* e = std::getenv("XTSG_TTM_GROUP");
+        return e ? std::atoi(e) : 8;
+      }();
+      const int nrb2 = std::max(1, tl.prm.n_rb / 2);
+      tl.prm.rb_group = std::max(1, std::min(grp_env, nrb2));
+    }
     tl.prm.z = zbuf.ptr;
     EvPair e1{}, e2{};
     if (profiling) {

@@ -18,6 +18,7 @@ struct TtmParams {
   int32_t n_last;          // UMMA N of the last j tile (multiple of 16, <= 256)
   int32_t chunks_last;     // 64-wide mode-2 chunks in the last j tile
   int32_t k16_chunk_last;  // K=16 slices in the last chunk of the last tile
+  int32_t rb_group;        // row blocks (pairs, for the pair kernel) per unit group
   float* z;          // out: Z[p][kk][m][l], kk in [0, kc)
 };
 

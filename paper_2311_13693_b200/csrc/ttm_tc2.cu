@@ -48,6 +48,18 @@ static_assert(smem_total(4, 4) <= 232448 && smem_total(5, 2) <= 232448, "shared 
 constexpr uint32_t IDESC1 = ptx::idesc_bf16(2 * BM, BN);
 constexpr uint16_t PAIR = 0x3;
 
+// Unit u -> (slice kk, row-block pair rb2). Units are grouped by `group`
+// row-block pairs: the ~#SM/2 units in flight at once then share `group`
+// blocks of U (L2-resident however large P*L) while each X tile is read by
+// `group` clusters at the same time (so from DRAM ~n_rb2/group times).
+__device__ __forceinline__ void decode_unit(int u, int n_rb2, int kc, int group, int& kk, int& rb2) {
+  const int g = u / (group * kc);
+  const int rem = u - g * group * kc;
+  const int gsz = min(group, n_rb2 - g * group);
+  kk = rem / gsz;
+  rb2 = g * group + (rem - kk * gsz);
+}
+
 template <int S, int A2_SLOTS>
 struct Bars2 {
   uint64_t full1[S], empty1[S];
@@ -115,7 +127,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int u = cid; u < n_units; u += n_clusters) {
-        const int kk = u / n_rb2, rb2 = u % n_rb2;
+        int kk, rb2;
+        decode_unit(u, n_rb2, p.kc, p.rb_group, kk, rb2);
         const int urow = rb2 * 2 * BM + crank * BM;
         for (int jt = 0; jt < j_tiles; ++jt) {
           for (int ks = 0; ks < k_steps; ++ks) {
@@ -168,7 +181,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t g = 0;
       const uint32_t bytes = static_cast<uint32_t>(n2c) * 128;
       for (int u = cid; u < n_units; u += n_clusters) {
-        const int rb2 = u % n_rb2;
+        int kk, rb2;
+        decode_unit(u, n_rb2, p.kc, p.rb_group, kk, rb2);
         const int vrow = (rb2 * 2 + static_cast<int>(crank)) * n2c;
         for (int jt = 0; jt < j_tiles; ++jt) {
           const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
@@ -244,7 +258,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const uint32_t d2col = (LOCAL2 ? 0u : crank * n2c) + p_local * MPAD;
     uint32_t t = 0, g = 0;
     for (int u = cid; u < n_units; u += n_clusters) {
-      const int kk = u / n_rb2, rb2 = u % n_rb2;
+      int kk, rb2;
+      decode_unit(u, n_rb2, p.kc, p.rb_group, kk, rb2);
       float zacc[MPAD];
 #pragma unroll
       for (int m = 0; m < MPAD; ++m) zacc[m] = 0.f;

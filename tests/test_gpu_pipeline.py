@@ -5,8 +5,11 @@ oracle/_ref, on the reference's own test configurations
 
 Tolerances: the fp64 path differs from the reference only in the
 floating-point order of its GEMM/QR/ALS arithmetic, so recovered factors agree
-to 1e-8 relative (the reference's own pipeline bar, test_pipeline.cpp:281) and
-the per-replica survivor decisions are identical. The bf16 (tcgen05)
+to 1e-8 relative (the reference's own pipeline bar, test_pipeline.cpp:281)
+once the CP sign ambiguity is resolved (a column pair (a_r, b_r) -> (-a_r,
+-b_r) is the same tensor; the signs come from the sampled-block ALS, whose
+nvecs restart takes eigenvector signs that Eigen does not pin), and the
+per-replica survivor decisions are identical. The bf16 (tcgen05)
 compression path is held to 1e-2 on the recovered factors with replica fits
 admitted at 1e-2 (the bf16 compression error is ~3e-3, test_gpu_plan.py).
 """
@@ -20,6 +23,14 @@ pytestmark = pytest.mark.gpu
 
 def _cfg(gpu, **kw):
     return gpu.PipelineConfig(**kw)
+
+
+def _same_cp(gpu, want, got, tol):
+    # got equals want up to the CP column sign/scale ambiguity: align got onto
+    # want with the reference's own evaluate() (pipeline.cpp:577-609)
+    rep = gpu.evaluate(want, got)
+    assert max(rep.mode_rel_err) <= tol, rep.mode_rel_err
+    return rep
 
 
 def _ref_decompose(reference, factors, cfg, tensor=None):
@@ -49,8 +60,7 @@ def test_small_dense_pipeline_from_tensor(gpu, reference):
     assert max(rep.mode_rel_err) <= 1e-8 and rep.sample_mse <= 1e-12
     assert met.stage_status["recovery"] == "ok" and met.sample_mse >= 0.0
     want, st = _ref_decompose(reference, f, cfg, tensor=t)
-    for g, w in zip(rec, want):
-        assert rel_diff(w, g) <= 1e-8
+    _same_cp(gpu, want, rec, 1e-8)
     assert met.replicas_total == int(st[4]) and met.replicas_dropped == int(st[5])
 
 
@@ -60,8 +70,7 @@ def test_dense_pipeline_factored_c1(gpu, reference):
     cfg = _cfg(gpu, reduced=(30, 30, 30), rank=10, replicas=12, shared=10, seed=2)
     rec, met = gpu.decompose(cfg, factors=f)
     want, st = _ref_decompose(reference, f, cfg)
-    for g, w in zip(rec, want):
-        assert rel_diff(w, g) <= 1e-8
+    _same_cp(gpu, want, rec, 1e-8)
     assert met.replicas_dropped == int(st[5])
     rep = gpu.evaluate(f, rec)
     assert max(rep.mode_rel_err) <= 1e-8
@@ -78,9 +87,9 @@ def test_small_sparse_pipeline_exact_supports(gpu, reference):
         assert np.array_equal(f[m] == 0.0, rep.aligned[m] == 0.0)
         assert rep.mode_rel_err[m] <= 1e-8
     want, _ = _ref_decompose(reference, f, cfg)
-    for g, w in zip(rec, want):
+    rep = _same_cp(gpu, want, rec, 1e-8)
+    for g, w in zip(rep.aligned, want):
         assert np.array_equal(g == 0.0, w == 0.0)
-        assert rel_diff(w, g) <= 1e-8
 
 
 def test_small_two_stage_pipeline(gpu, reference):
@@ -91,8 +100,7 @@ def test_small_two_stage_pipeline(gpu, reference):
     rep = gpu.evaluate(f, rec)
     assert max(rep.mode_rel_err) <= 1e-6
     want, _ = _ref_decompose(reference, f, cfg)
-    for g, w in zip(rec, want):
-        assert rel_diff(w, g) <= 1e-6
+    _same_cp(gpu, want, rec, 1e-6)
 
 
 def test_bf16_pipeline_recovers_factors(gpu):
