@@ -54,6 +54,17 @@ void require_device() {
   XCUDA(cudaGetDevice(&dev));
   XCUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
   if (major != 10) throw Status(XTSG_E_CUDA, "xtsg is built for sm_100a (B200) only");
+  // stream-ordered allocations (DevBuf) stay mapped in the device's default
+  // pool across synchronizations instead of being unmapped and remapped on
+  // every call (multi-GB slab buffers otherwise cost ~100 ms per call)
+  static thread_local int pool_dev = -1;
+  if (pool_dev != dev) {
+    cudaMemPool_t pool;
+    XCUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    XCUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    pool_dev = dev;
+  }
 }
 
 int sm_count() {

@@ -323,6 +323,8 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     tl.v = vop; tl.rows_v = P * mpad; tl.ld_v = ldv;
     tl.mpad = static_cast<int>(mpad);
     tl.grid_limit = grid_limit;
+    if (!sync_ctr.ptr) sync_ctr = DevBuf<unsigned>(256, s);
+    tl.sync = sync_ctr.ptr;
     tl.prm.n_rb = static_cast<int32_t>(rows_u / 128);
     tl.prm.kc = static_cast<int32_t>(kc);
     tl.prm.k_first = static_cast<int32_t>(kb);
@@ -347,6 +349,15 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
       }();
       const int nrb2 = std::max(1, tl.prm.n_rb / 2);
       tl.prm.rb_group = std::max(1, std::min(grp_env, nrb2));
+      // U blocks are re-read once per j tile by every unit of the group: keep
+      // them in L2 ahead of the X stream (XTSG_TTM_L2HINT=0 disables)
+      static const int hint_env = [] {
+        const char* e = std::getenv("XTSG_TTM_L2HINT");
+        return e ? std::atoi(e) : 1;
+      }();
+      const uint64_t pol[3] = {0x1000000000000000ull, 0x12F0000000000000ull, 0x14F0000000000000ull};
+      tl.prm.u_policy = hint_env ? pol[2] : pol[0];
+      tl.prm.x_policy = hint_env == 2 ? pol[1] : pol[0];
     }
     tl.prm.z = zbuf.ptr;
     EvPair e1{}, e2{};

@@ -19,6 +19,10 @@ struct TtmParams {
   int32_t chunks_last;     // 64-wide mode-2 chunks in the last j tile
   int32_t k16_chunk_last;  // K=16 slices in the last chunk of the last tile
   int32_t rb_group;        // row blocks (pairs, for the pair kernel) per unit group
+  int32_t lanes;           // pair kernel: static slice lanes (0 = round robin)
+  unsigned* sync;          // pair kernel: per-lane slot counters (null = no lane barrier)
+  int32_t sync_j;          // pair kernel: lane barrier every sync_j j tiles
+  uint64_t u_policy, x_policy;  // L2 cache-policy hints of the U / X tile loads
   float* z;          // out: Z[p][kk][m][l], kk in [0, kc)
 };
 
@@ -31,6 +35,7 @@ struct TtmLaunch {
   int64_t rows_v, ld_v;
   int mpad;
   int grid_limit;     // 0 = number of SMs
+  unsigned* sync;     // >= 256 zeroable counters for the pair kernel's lane barrier (optional)
   TtmParams prm;
 };
 

@@ -60,6 +60,60 @@ __device__ __forceinline__ void decode_unit(int u, int n_rb2, int kc, int group,
   rb2 = g * group + (rem - kk * gsz);
 }
 
+// Persistent-cluster schedule over (slice kk, row-block pair rb2) units.
+// lanes == 0: round robin over the grouped unit order (decode_unit).
+// lanes > 0: static 2-D assignment — cluster c serves row block r = c % group
+// of every group, on the slices kk = lane, lane + lanes, ... (lane = c /
+// group), so the `group` clusters of a lane always work on the same slice and
+// read each X tile together; with p.sync they also re-align at every slot.
+struct UnitSched {
+  int cid, n_clusters, n_rb2, kc, group, lanes, lane, r, ngroups;
+  int u, g, kk, slot;
+  __device__ UnitSched(int c, int nc, int nrb2, const TtmParams& p)
+      : cid(c), n_clusters(nc), n_rb2(nrb2), kc(p.kc), group(p.rb_group), lanes(p.lanes) {
+    lane = lanes ? cid / group : 0;
+    r = lanes ? cid % group : 0;
+    ngroups = (n_rb2 + group - 1) / group;
+    u = cid - n_clusters;
+    g = 0;
+    kk = lane - lanes;
+    slot = -1;
+  }
+  // next slot; active = this cluster has a unit in it
+  __device__ bool next(bool& active, int& ukk, int& urb2) {
+    if (!lanes) {
+      u += n_clusters;
+      if (u >= n_rb2 * kc) return false;
+      decode_unit(u, n_rb2, kc, group, ukk, urb2);
+      active = true;
+      return true;
+    }
+    if (lane >= lanes) return false;
+    kk += lanes;
+    while (kk >= kc) {
+      if (++g >= ngroups) return false;
+      kk = lane;
+    }
+    ++slot;
+    const int gsz = min(group, n_rb2 - g * group);
+    active = r < gsz;
+    ukk = kk;
+    urb2 = g * group + r;
+    return true;
+  }
+};
+
+// Lane barrier between slots (performance only: bounded wait, then proceed).
+__device__ __forceinline__ void lane_barrier(unsigned* ctr, unsigned target) {
+  atomicAdd(ctr, 1u);
+  for (int spin = 0; spin < 40000; ++spin) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    __nanosleep(64);
+  }
+}
+
 template <int S, int A2_SLOTS>
 struct Bars2 {
   uint64_t full1[S], empty1[S];
@@ -115,7 +169,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 
   const int cid = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int n_rb2 = p.n_rb >> 1;
-  const int n_units = n_rb2 * p.kc;
   const int j_tiles = p.j_tiles, k_steps = p.k_steps;
   const int n2c = p.n2;            // mode-2 columns contributed by this CTA
   const int n2 = LOCAL2 ? n2c : 2 * n2c;  // mode-2 MMA N
@@ -126,20 +179,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       // ---- TMA producer (both CTAs): own U rows, own half of the X tile -----
       int s = 0;
       uint32_t ph = 0;
-      for (int u = cid; u < n_units; u += n_clusters) {
-        int kk, rb2;
-        decode_unit(u, n_rb2, p.kc, p.rb_group, kk, rb2);
+      UnitSched us(cid, n_clusters, n_rb2, p);
+      int kk, rb2;
+      bool act;
+      unsigned sync_no = 0;
+      while (us.next(act, kk, rb2)) {
         const int urow = rb2 * 2 * BM + crank * BM;
         for (int jt = 0; jt < j_tiles; ++jt) {
+          // lane barrier every sync_j tiles (idle clusters of a partial group
+          // keep arriving so the counts stay aligned)
+          if (p.sync && jt % p.sync_j == 0) lane_barrier(p.sync + us.lane, 2u * us.group * ++sync_no);
+          if (!act) continue;
           for (int ks = 0; ks < k_steps; ++ks) {
             ptx::mbar_wait(&bars->empty1[s], ph ^ 1);
             uint8_t* st = stage_base + s * STAGE_BYTES;
             if (leader) ptx::mbar_arrive_expect_tx(&bars->full1[s], 2 * STAGE_BYTES);
             const uint32_t fb = ptx::mapa_shared(&bars->full1[s], 0);
-            ptx::tma_load_2d_pair(st, &tm_u, fb, ks * BK, urow);
+            ptx::tma_load_2d_pair_hint(st, &tm_u, fb, ks * BK, urow, p.u_policy);
             // the last j tile runs with N = n_last: each CTA holds n_last / 2 of its j
             const int half = jt == j_tiles - 1 ? (p.n_last >> 1) : BNC;
-            ptx::tma_load_3d_pair(st + A_BYTES, &tm_x, fb, ks * BK, jt * BN + crank * half, p.k_first + kk);
+            ptx::tma_load_3d_pair_hint(st + A_BYTES, &tm_x, fb, ks * BK, jt * BN + crank * half, p.k_first + kk,
+                                       p.x_policy);
             if (++s == S) { s = 0; ph ^= 1; }
           }
         }
@@ -150,7 +210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       // ---- mode-1 MMA issuer (leader) -----------------------------------------
       int s = 0;
       uint32_t ph = 0, t = 0;
-      for (int u = cid; u < n_units; u += n_clusters) {
+      UnitSched us(cid, n_clusters, n_rb2, p);
+      int kk, rb2;
+      bool act;
+      while (us.next(act, kk, rb2)) {
+        if (!act) continue;
         for (int jt = 0; jt < j_tiles; ++jt, ++t) {
           const uint32_t b = t & 1, use = t >> 1;
           ptx::mbar_wait(&bars->tmem_empty[b], (use & 1) ^ 1);
@@ -180,9 +244,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       // ---- Vt producer (both CTAs): this CTA's replicas' V rows ---------------
       uint32_t g = 0;
       const uint32_t bytes = static_cast<uint32_t>(n2c) * 128;
-      for (int u = cid; u < n_units; u += n_clusters) {
-        int kk, rb2;
-        decode_unit(u, n_rb2, p.kc, p.rb_group, kk, rb2);
+      UnitSched us(cid, n_clusters, n_rb2, p);
+      int kk, rb2;
+      bool act;
+      while (us.next(act, kk, rb2)) {
+        if (!act) continue;
         const int vrow = (rb2 * 2 + static_cast<int>(crank)) * n2c;
         for (int jt = 0; jt < j_tiles; ++jt) {
           const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
@@ -206,7 +272,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       // ---- mode-2 MMA issuer (leader; every CTA for the per-CTA variant) ------
       const uint32_t idesc2 = ptx::idesc_bf16(LOCAL2 ? BM : 2 * BM, n2);
       uint32_t t = 0, g = 0;
-      for (int u = cid; u < n_units; u += n_clusters) {
+      UnitSched us(cid, n_clusters, n_rb2, p);
+      int kk, rb2;
+      bool act;
+      while (us.next(act, kk, rb2)) {
+        if (!act) continue;
         for (int jt = 0; jt < j_tiles; ++jt, ++t) {
           const uint32_t b = t & 1;
           const uint32_t d = tmem + b * 256;
@@ -257,9 +327,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const int l = r % p.lpad;
     const uint32_t d2col = (LOCAL2 ? 0u : crank * n2c) + p_local * MPAD;
     uint32_t t = 0, g = 0;
-    for (int u = cid; u < n_units; u += n_clusters) {
-      int kk, rb2;
-      decode_unit(u, n_rb2, p.kc, p.rb_group, kk, rb2);
+    UnitSched us(cid, n_clusters, n_rb2, p);
+    int kk, rb2;
+    bool act;
+    while (us.next(act, kk, rb2)) {
+      if (!act) continue;
       float zacc[MPAD];
 #pragma unroll
       for (int m = 0; m < MPAD; ++m) zacc[m] = 0.f;
@@ -400,8 +472,28 @@ void launch_pair(const TtmLaunch& L, cudaStream_t st) {
   }
   const int clusters = (L.prm.n_rb / 2) * L.prm.kc;
   const int cap = (L.grid_limit > 0 ? L.grid_limit : sm_count()) / 2;
-  const int grid = std::max(1, std::min(clusters, cap)) * 2;
-  ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, L.prm);
+  const int ncl = std::max(1, std::min(clusters, cap));
+  const int grid = ncl * 2;
+  TtmParams prm = L.prm;
+  // schedule (UnitSched): 0 round robin, 1 static lanes, 2 static lanes with a
+  // per-slot lane barrier; static lanes need at least one slice per lane
+  static const int sched_env = [] {
+    const char* e = std::getenv("XTSG_TTM_SCHED");
+    return e ? std::atoi(e) : 2;
+  }();
+  const int lanes = ncl / std::max(1, prm.rb_group);
+  prm.lanes = (sched_env && lanes >= 1 && lanes <= prm.kc) ? lanes : 0;
+  prm.sync = nullptr;
+  static const int syncj_env = [] {
+    const char* e = std::getenv("XTSG_TTM_SYNCJ");
+    return e ? std::atoi(e) : 0;
+  }();
+  prm.sync_j = syncj_env > 0 ? syncj_env : prm.j_tiles;
+  if (prm.lanes && sched_env == 2 && L.sync) {
+    XCUDA(cudaMemsetAsync(L.sync, 0, sizeof(unsigned) * prm.lanes, st));
+    prm.sync = L.sync;
+  }
+  ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, prm);
   XLAUNCH_CHECK();
 }
 

@@ -14,9 +14,9 @@ t = np.einsum("ir,jr,kr->ijk", a, b, c)
 t = t + 3e-3 * np.linalg.norm(t) / np.sqrt(t.size) * rng.standard_normal(t.shape)
 t = np.asfortranarray(t)
 ts = [t] * count
-xt.cp_als_batched(ts[:1], R, max_iters=2, tol=0.0, seeds=[1])
+xt.cp_als_batched(ts[:1], R, max_iters=2, tol=1e-300, seeds=[1])
 for cnt in (1, count):
     t0 = time.perf_counter()
-    res = xt.cp_als_batched(ts[:cnt], R, max_iters=iters, tol=0.0, seeds=list(range(cnt)))
+    res = xt.cp_als_batched(ts[:cnt], R, max_iters=iters, tol=1e-300, seeds=list(range(cnt)))
     dt = time.perf_counter() - t0
     print(f"n={n} R={R} batch={cnt}: {dt / iters * 1e3:.2f} ms/sweep, err {res[0].final_error():.3e}")
