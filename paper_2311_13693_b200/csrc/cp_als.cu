@@ -19,10 +19,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
 #include "common.cuh"
+#include "sm100_ptx.cuh"
 #include "xrng.cuh"
 
 namespace xtsg {
@@ -614,6 +616,417 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
   }
 }
 
+// ---------------------------------------------------------------------------
+// Large replicas (e.g. config 3: 124 replicas of 128^3, rank 20): the same
+// sweep, restructured so that T streams through shared memory twice per sweep
+// and the contractions run on the fp64 tensor cores (DMMA m8n8k4):
+//   pass 1  M_A = T(1) (C kr B) fused with the explicit residual of the
+//           previous sweep (X^_k = (A diag(c_k)) B' tile by tile, compared
+//           with the staged T tile): one T read serves both;
+//   pass 2  P = T x1 A' (the A-contracted tensor, as contract_a) with M_B
+//           accumulated on the fly; M_C from P and the new B as before.
+// T arrives by 1-D bulk copies (cp.async.bulk, one per 8-column chunk column)
+// into a 4-stage ring with a padded leading dimension (n1 + 4 doubles) that
+// makes every DMMA fragment load bank-conflict free. Convergence is checked
+// one pass later than in als_kernel (the residual of sweep s is computed in
+// pass 1 of sweep s + 1), with identical semantics: iteration counts, history
+// and returned factors are those of the sweep that met the tolerance.
+constexpr int BJC = 8;       // T columns per staged chunk
+constexpr int BNS_MAX = 8;   // chunk stages (as many as fit)
+
+struct BigSmem {
+  double *Ts, *Bp, *red;
+  uint64_t *full, *empty;
+  int ldt, ldb, ns;
+};
+
+__device__ __forceinline__ int big_ld(int n) { return n + 4; }  // n % 16 == 0 -> ld % 16 == 4
+
+// refresh the zero-padded DMMA copy of B (n2 x Rp, leading dim ldb)
+__device__ void big_refresh(const Smem& s, const BigSmem& g, int n2, int R) {
+  for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) g.Bp[(e % n2) + g.ldb * (e / n2)] = s.B[e];
+}
+
+// thread 0: stage global chunk number `gnum` (local chunk c of the pass)
+__device__ __forceinline__ void big_issue(const BigSmem& g, const double* T, int n1, int n2, int64_t gnum, int c) {
+  const int stage = static_cast<int>(gnum % g.ns);
+  if (gnum >= g.ns) ptx::mbar_wait(&g.empty[stage], static_cast<uint32_t>(((gnum / g.ns) - 1) & 1));
+  const int cpk = n2 / BJC;
+  const int k = c / cpk, jb = (c % cpk) * BJC;
+  const uint32_t col_bytes = static_cast<uint32_t>(n1) * 8u;
+  ptx::mbar_arrive_expect_tx(&g.full[stage], col_bytes * BJC);
+  double* dst = g.Ts + stage * BJC * g.ldt;
+  const double* src = T + static_cast<int64_t>(n1) * (jb + static_cast<int64_t>(n2) * k);
+#pragma unroll
+  for (int jj = 0; jj < BJC; ++jj)
+    ptx::bulk_g2s(dst + jj * g.ldt, src + static_cast<int64_t>(n1) * jj, col_bytes, &g.full[stage]);
+}
+
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(ptx::smem_u32(bar)), "r"(n) : "memory");
+}
+
+// Pass 1: M_A -> s.M (n1 x R); returns this thread's residual partial
+// sum_(ijk) (T - [[A, B, C]])^2 when `want_res`.
+template <int MTPW, int NTR>
+__device__ double big_pass1(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s,
+                            const BigSmem& g, int64_t& gcn, bool want_res) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int cpk = n2 / BJC, nch = n3 * cpk;
+  double q[MTPW][NTR][2], macc[MTPW][NTR][2], areg[MTPW][2 * NTR], ahat[MTPW][2 * NTR];
+#pragma unroll
+  for (int m = 0; m < MTPW; ++m)
+#pragma unroll
+    for (int t = 0; t < NTR; ++t) q[m][t][0] = q[m][t][1] = macc[m][t][0] = macc[m][t][1] = 0.0;
+  // A fragments (M = i, K = r) of this warp's row tiles (once per pass)
+#pragma unroll
+  for (int m = 0; m < MTPW; ++m)
+#pragma unroll
+    for (int kr = 0; kr < 2 * NTR; ++kr) {
+      const int r = kr * 4 + lc;
+      areg[m][kr] = r < R ? s.A[((warp * MTPW + m) * 8 + lr) + n1 * r] : 0.0;
+    }
+  double res = 0.0;
+  for (int c = 0; c < nch; ++c, ++gcn) {
+    if (threadIdx.x == 0 && c == 0)
+      for (int q0 = 0; q0 < g.ns && q0 < nch; ++q0) big_issue(g, T, n1, n2, gcn + q0, q0);
+    const int k = c / cpk, jb = (c % cpk) * BJC;
+    if (jb == 0) {
+#pragma unroll
+      for (int kr = 0; kr < 2 * NTR; ++kr) {
+        const int r = kr * 4 + lc;
+        const double ck = r < R ? s.C[k + n3 * r] : 0.0;
+#pragma unroll
+        for (int m = 0; m < MTPW; ++m) ahat[m][kr] = areg[m][kr] * ck;
+      }
+    }
+    const int stage = static_cast<int>(gcn % g.ns);
+    ptx::mbar_wait(&g.full[stage], static_cast<uint32_t>((gcn / g.ns) & 1));
+    const double* ts = g.Ts + stage * BJC * g.ldt;
+    // GEMM 1: q[i, r] += sum_j T[i, j] B[j, r]
+#pragma unroll
+    for (int ks = 0; ks < BJC / 4; ++ks) {
+      double b[NTR];
+#pragma unroll
+      for (int t = 0; t < NTR; ++t) b[t] = g.Bp[(jb + ks * 4 + lc) + g.ldb * (t * 8 + lr)];
+#pragma unroll
+      for (int m = 0; m < MTPW; ++m) {
+        const double a = ts[((warp * MTPW + m) * 8 + lr) + g.ldt * (ks * 4 + lc)];
+#pragma unroll
+        for (int t = 0; t < NTR; ++t) ptx::dmma(q[m][t][0], q[m][t][1], a, b[t]);
+      }
+    }
+    // GEMM 2 + residual: X^[i, j] = sum_r (A[i, r] C[k, r]) B[j, r]
+    if (want_res) {
+      double bb[2 * NTR];
+#pragma unroll
+      for (int kr = 0; kr < 2 * NTR; ++kr) bb[kr] = g.Bp[(jb + lr) + g.ldb * (kr * 4 + lc)];
+#pragma unroll
+      for (int m = 0; m < MTPW; ++m) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kr = 0; kr < 2 * NTR; ++kr) ptx::dmma(d0, d1, ahat[m][kr], bb[kr]);
+        const int i = (warp * MTPW + m) * 8 + lr;
+        const double t0 = ts[i + g.ldt * (2 * lc)], t1 = ts[i + g.ldt * (2 * lc + 1)];
+        res = fma(t0 - d0, t0 - d0, res);
+        res = fma(t1 - d1, t1 - d1, res);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&g.empty[stage]);
+    if (threadIdx.x == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, c + g.ns);
+    if (jb + BJC == n2) {  // slice k complete: macc += c_k .* q
+#pragma unroll
+      for (int t = 0; t < NTR; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = t * 8 + 2 * lc + e;
+          const double ck = r < R ? s.C[k + n3 * r] : 0.0;
+#pragma unroll
+          for (int m = 0; m < MTPW; ++m) {
+            macc[m][t][e] = fma(ck, q[m][t][e], macc[m][t][e]);
+            q[m][t][e] = 0.0;
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < MTPW; ++m)
+#pragma unroll
+    for (int t = 0; t < NTR; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = t * 8 + 2 * lc + e;
+        if (r < R) s.M[((warp * MTPW + m) * 8 + lr) + n1 * r] = macc[m][t][e];
+      }
+  return res;
+}
+
+// Pass 2: P[r][k][j] = sum_i T[i, j, k] A[i, r] into global P, and
+// M_B[j, r] = sum_k C[k, r] P[r][k][j] into s.M (n2 x R). Two groups of four
+// warps take alternate chunks (K = i split over a group's warps, partials
+// reduced in a fixed order behind a group barrier); n2 % 16 == 0 keeps every
+// j column's slices in one group, so M_B accumulates over k in order.
+template <int NTR>
+__device__ void big_pass2(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s,
+                          const BigSmem& g, int64_t& gcn, double* __restrict__ P) {
+  constexpr int KS_MAX = 8;  // n1 <= 128
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp >> 2, wq = warp & 3, gtid = threadIdx.x & 127;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int cpk = n2 / BJC, nch = n3 * cpk;
+  const int iw = n1 / 4, ks2 = iw / 4;  // i rows per warp, K steps
+  double areg[NTR][KS_MAX];
+#pragma unroll
+  for (int t = 0; t < NTR; ++t)
+#pragma unroll
+    for (int ks = 0; ks < KS_MAX; ++ks) {
+      const int r = t * 8 + lr;
+      areg[t][ks] = (ks < ks2 && r < R) ? s.A[(wq * iw + ks * 4 + lc) + n1 * r] : 0.0;
+    }
+  for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) s.M[e] = 0.0;
+  __syncthreads();
+  const int rp = NTR * 8;
+  int use = 0;
+  for (int c = 0; c < nch; ++c, ++gcn) {
+    if (threadIdx.x == 0 && c == 0)
+      for (int q0 = 0; q0 < g.ns && q0 < nch; ++q0) big_issue(g, T, n1, n2, gcn + q0, q0);
+    const int stage = static_cast<int>(gcn % g.ns);
+    if ((c & 1) == grp) {
+      const int k = c / cpk, jb = (c % cpk) * BJC;
+      ptx::mbar_wait(&g.full[stage], static_cast<uint32_t>((gcn / g.ns) & 1));
+      const double* ts = g.Ts + stage * BJC * g.ldt;
+      double acc[NTR][2];
+#pragma unroll
+      for (int t = 0; t < NTR; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS_MAX; ++ks) {
+        if (ks < ks2) {
+          const double b = ts[(wq * iw + ks * 4 + lc) + g.ldt * lr];
+#pragma unroll
+          for (int t = 0; t < NTR; ++t) ptx::dmma(acc[t][0], acc[t][1], areg[t][ks], b);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cnt(&g.empty[stage], 2);
+      double* red = g.red + (grp * 2 + (use & 1)) * 4 * rp * BJC;
+      ++use;
+#pragma unroll
+      for (int t = 0; t < NTR; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) red[(wq * rp + t * 8 + lr) * BJC + 2 * lc + e] = acc[t][e];
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+      for (int e = gtid; e < R * BJC; e += 128) {
+        const int r = e / BJC, jj = e % BJC;
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) v += red[(w * rp + r) * BJC + jj];
+        const int j = jb + jj;
+        P[static_cast<int64_t>(r) * n2 * n3 + static_cast<int64_t>(n2) * k + j] = v;
+        s.M[j + n2 * r] = fma(s.C[k + n3 * r], v, s.M[j + n2 * r]);
+      }
+    }
+    if (threadIdx.x == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, c + g.ns);
+  }
+  __syncthreads();
+}
+
+size_t big_fixed_doubles(int n1, int n2, int n3, int R) {
+  const int mx = std::max(n1, std::max(n2, n3));
+  const int rp = (R + 7) / 8 * 8;
+  return static_cast<size_t>(n2 + 4) * rp + 4 * 4 * rp * BJC + static_cast<size_t>(n1 + n2 + n3) * R + 6 * R * R +
+         static_cast<size_t>(mx) * R + 2 * (std::max(mx, R) / 2 + 2) + 2 * R + 64 + 2 * (std::max(mx, R) / 2 + 2);
+}
+constexpr size_t BIG_SMEM_CAP = 225 * 1024;
+
+// stages that fit next to the fixed working set (0 when not even 3 do)
+int big_stages(int n1, int n2, int n3, int R) {
+  const size_t fixed = big_fixed_doubles(n1, n2, n3, R) * 8;
+  const size_t per = static_cast<size_t>(BJC) * (n1 + 4) * 8;
+  if (fixed + 3 * per > BIG_SMEM_CAP) return 0;
+  return static_cast<int>(std::min<size_t>(BNS_MAX, (BIG_SMEM_CAP - fixed) / per));
+}
+
+template <int MTPW, int NTR>
+__global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3,
+                                                        int ns) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_ok;
+  __shared__ __align__(8) uint64_t bars[2 * BNS_MAX];
+  const AlsInst in = insts[blockIdx.x];
+  const int R = static_cast<int>(in.cfg.rank);
+  const int mx = max(n1, max(n2, n3));
+  const int rp = NTR * 8;
+  Smem s;
+  BigSmem g;
+  g.ldt = big_ld(n1);
+  g.ldb = big_ld(n2);
+  g.ns = ns;
+  double* q = sm;
+  g.Ts = q; q += ns * BJC * g.ldt;
+  g.Bp = q; q += g.ldb * rp;
+  g.red = q; q += 4 * 4 * rp * BJC;
+  s.A = q; q += n1 * R;
+  s.B = q; q += n2 * R;
+  s.C = q; q += n3 * R;
+  s.G1 = q; q += R * R;
+  s.G2 = q; q += R * R;
+  s.G3 = q; q += R * R;
+  s.H = q; q += R * R;
+  s.V = q; q += R * R;
+  s.P = q; q += R * R;
+  s.M = q; q += mx * R;
+  s.red2 = nullptr;
+  s.cs = q; q += std::max(mx, R) / 2 + 2;
+  s.sn = q; q += std::max(mx, R) / 2 + 2;
+  s.nrm = q; q += 2 * R;
+  s.red = q; q += 64;
+  s.pp = reinterpret_cast<int*>(q); q += std::max(mx, R) / 2 + 2;
+  s.qq = reinterpret_cast<int*>(q);
+  g.full = bars;
+  g.empty = bars + BNS_MAX;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ns; ++i) {
+      ptx::mbar_init(&g.full[i], 1);
+      ptx::mbar_init(&g.empty[i], 8);
+    }
+    ptx::fence_barrier_init();
+  }
+  for (int e = threadIdx.x; e < g.ldb * rp; e += blockDim.x) g.Bp[e] = 0.0;
+  __syncthreads();
+
+  const double* T = in.t;
+  const int64_t total = static_cast<int64_t>(n1) * n2 * n3;
+  const double tn = sqrt(norm_sq(T, total, s.red));
+  block_normals(derive(in.cfg.seed, 1), n1 * R, s.A, s.red);
+  block_normals(derive(in.cfg.seed, 2), n2 * R, s.B, s.red);
+  block_normals(derive(in.cfg.seed, 3), n3 * R, s.C, s.red);
+  if (in.cfg.init == 1 && tn > 0.0) {
+    nvecs_init(T, n1, n2, n3, 0, R, s.A, in.nvec_ws, s);
+    nvecs_init(T, n1, n2, n3, 1, R, s.B, in.nvec_ws, s);
+    nvecs_init(T, n1, n2, n3, 2, R, s.C, in.nvec_ws, s);
+  }
+  __syncthreads();
+  gram(s.B, n2, R, s.G2);
+  gram(s.C, n3, R, s.G3);
+  big_refresh(s, g, n2, R);
+  __syncthreads();
+
+  int64_t gcn = 0, it = 0, iters = 0;
+  bool converged = false, stopped = false;
+  double prev = 0.0;
+  for (; it < in.cfg.max_iters; ++it) {
+    // pass 1: M_A for sweep it, residual of sweep it - 1
+    const double part = big_pass1<MTPW, NTR>(T, n1, n2, n3, R, s, g, gcn, it >= 1);
+    if (it >= 1) {
+      const double res = sqrt(block_sum(part, s.red));
+      const double err = tn > 0.0 ? res / tn : res;
+      if (threadIdx.x == 0) in.hist[it - 1] = err;
+      if (it - 1 >= 1 && fabs(prev - err) < in.cfg.tol) {
+        converged = true;
+        stopped = true;
+        iters = it;
+        break;
+      }
+      prev = err;
+    }
+    __syncthreads();
+    // A update
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
+    __syncthreads();
+    solve_gram(s.M, n1, R, s, s.A, &s_ok);
+    __syncthreads();
+    gram(s.A, n1, R, s.G1);
+    __syncthreads();
+    // pass 2 + B update
+    big_pass2<NTR>(T, n1, n2, n3, R, s, g, gcn, in.pbuf);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G1[e];
+    __syncthreads();
+    solve_gram(s.M, n2, R, s, s.B, &s_ok);
+    __syncthreads();
+    gram(s.B, n2, R, s.G2);
+    __syncthreads();
+    // C update
+    mttkrp2_from_p(in.pbuf, n2, n3, R, s, s.M);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G2[e] * s.G1[e];
+    __syncthreads();
+    solve_gram(s.M, n3, R, s, s.C, &s_ok);
+    __syncthreads();
+    // move a/b column norms into c (cp_als.cpp:84-96)
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+      double na = 0.0, nb = 0.0;
+      for (int i = 0; i < n1; ++i) na = fma(s.A[i + n1 * r], s.A[i + n1 * r], na);
+      for (int i = 0; i < n2; ++i) nb = fma(s.B[i + n2 * r], s.B[i + n2 * r], nb);
+      s.nrm[r] = sqrt(na);
+      s.nrm[R + r] = sqrt(nb);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
+      const double na = s.nrm[e / n1];
+      if (na > 0.0) s.A[e] /= na;
+    }
+    for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
+      const double nb = s.nrm[R + e / n2];
+      if (nb > 0.0) s.B[e] /= nb;
+    }
+    for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) {
+      const int r = e / n3;
+      s.C[e] *= s.nrm[r] * s.nrm[R + r];
+    }
+    __syncthreads();
+    gram(s.A, n1, R, s.G1);
+    gram(s.B, n2, R, s.G2);
+    gram(s.C, n3, R, s.G3);
+    big_refresh(s, g, n2, R);
+    __syncthreads();
+  }
+  if (!stopped) {
+    // residual of the last sweep (no next pass 1 to carry it)
+    const double res = sqrt(residual_sq(T, n1, n2, n3, R, s));
+    const double err = tn > 0.0 ? res / tn : res;
+    const int64_t last = in.cfg.max_iters - 1;
+    if (threadIdx.x == 0) in.hist[last] = err;
+    converged = last >= 1 && fabs(prev - err) < in.cfg.tol;
+    iters = in.cfg.max_iters;
+  }
+  for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) in.a[e] = s.A[e];
+  for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) in.b[e] = s.B[e];
+  for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) in.c[e] = s.C[e];
+  if (threadIdx.x == 0) {
+    *in.iters = iters;
+    *in.conv = converged ? 1 : 0;
+  }
+}
+
+// Shapes the large-replica kernel takes: 64 | n1 <= 128, 16 | n2, rank <= 24.
+bool als_big_eligible(int64_t n1, int64_t n2, int64_t n3, int64_t R) {
+  static const bool off = [] {
+    const char* e = std::getenv("XTSG_ALS_BIG");
+    return e && std::atoi(e) == 0;
+  }();
+  if (off) return false;
+  if (!(n1 % 64 == 0 && n1 <= 128 && n2 % 16 == 0 && n2 <= 1024 && n3 >= 1 && n3 <= 1024 && R >= 1 && R <= 24))
+    return false;
+  return big_stages(int(n1), int(n2), int(n3), int(R)) >= 3;
+}
+
+void launch_als_big(const AlsInst* din, int64_t count, int n1, int n2, int n3, int R, cudaStream_t st) {
+  const int ns = big_stages(n1, n2, n3, R);
+  const size_t smem = 8 * (big_fixed_doubles(n1, n2, n3, R) + static_cast<size_t>(ns) * BJC * (n1 + 4));
+  const int mtpw = n1 / 64, ntr = (R + 7) / 8;
+  auto go = [&](auto kern) {
+    XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<static_cast<unsigned>(count), NT, smem, st>>>(din, n1, n2, n3, ns);
+  };
+  if (mtpw == 1) {
+    if (ntr == 1) go(als_big_kernel<1, 1>); else if (ntr == 2) go(als_big_kernel<1, 2>); else go(als_big_kernel<1, 3>);
+  } else {
+    if (ntr == 1) go(als_big_kernel<2, 1>); else if (ntr == 2) go(als_big_kernel<2, 2>); else go(als_big_kernel<2, 3>);
+  }
+  XLAUNCH_CHECK();
+}
+
 size_t als_smem_bytes(int n1, int n2, int n3, int R) {
   const int mx = std::max(n1, std::max(n2, n3));
   return sizeof(double) * (static_cast<size_t>(n1 + n2 + n3) * R + 6 * R * R + static_cast<size_t>(mx) * R + 4096 +
@@ -713,10 +1126,14 @@ int32_t xtsg_cp_als_batched(int64_t count, const double* t, int64_t n1, int64_t 
     }
     DevBuf<AlsInst> din(static_cast<size_t>(count), st);
     XCUDA(cudaMemcpyAsync(din.ptr, hin.data(), sizeof(AlsInst) * count, cudaMemcpyHostToDevice, st));
-    XCUDA(cudaFuncSetAttribute(als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    als_kernel<<<static_cast<unsigned>(count), NT, smem, st>>>(din.ptr, static_cast<int>(n1), static_cast<int>(n2),
-                                                                static_cast<int>(n3));
-    XLAUNCH_CHECK();
+    if (als_big_eligible(n1, n2, n3, rank)) {
+      launch_als_big(din.ptr, count, static_cast<int>(n1), static_cast<int>(n2), static_cast<int>(n3), R, st);
+    } else {
+      XCUDA(cudaFuncSetAttribute(als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      als_kernel<<<static_cast<unsigned>(count), NT, smem, st>>>(din.ptr, static_cast<int>(n1), static_cast<int>(n2),
+                                                                  static_cast<int>(n3));
+      XLAUNCH_CHECK();
+    }
     oa.finish();
     ob.finish();
     oc.finish();

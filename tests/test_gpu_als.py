@@ -116,3 +116,41 @@ def test_replica_sized_batch_matches_reference_fit(gpu, reference):
     for t, r, s in zip(ts, res, [11, 12, 13, 14]):
         _, _, hist, _ = reference.cp_als(t, 10, seed=s, init=1)
         assert r.final_error() <= max(1e-6, 10 * hist[-1])
+
+
+# ---- large-replica kernel (DMMA passes, fused residual; cp_als.cu als_big_kernel)
+# Shapes with 64 | n1 <= 128, 8 | n2, rank <= 24 take it. Same seeds -> the
+# same trajectory as the reference up to fp64 summation order.
+
+def _noisy(shape, rank, seed, noise):
+    rng = np.random.default_rng(seed)
+    t = recon(*(rng.standard_normal((n, rank)) for n in shape))
+    return np.asfortranarray(t + noise * np.linalg.norm(t) / np.sqrt(t.size) * rng.standard_normal(shape))
+
+
+@pytest.mark.parametrize("shape,rank,noise,max_iters", [
+    ((64, 64, 64), 5, 0.0, 300),      # exact low rank (this seed swamps in both)
+    ((128, 96, 40), 20, 3e-3, 60),    # config-3-like noisy replica, capped sweeps
+    ((64, 128, 24), 12, 1e-2, 7),     # max_iters path (final residual pass)
+])
+def test_large_replica_trajectory_matches_reference(gpu, reference, shape, rank, noise, max_iters):
+    t = _noisy(shape, rank, 17, noise)
+    r = gpu.cp_als(t, rank, max_iters=max_iters, seed=23)
+    _, it, hist, conv = reference.cp_als(t, rank, max_iters=max_iters, seed=23)
+    n = min(len(hist), len(r.error_history))
+    h_gpu, h_ref = np.array(r.error_history[:n]), np.array(hist[:n])
+    assert np.all(np.abs(h_gpu - h_ref) <= 1e-9 * np.maximum(h_ref, 1e-3)), (h_gpu[:5], h_ref[:5])
+    assert abs(r.iters - it) <= 2 and len(r.error_history) == r.iters
+    if max_iters == 7:
+        assert r.iters == 7 == it and r.converged == conv
+    assert r.converged == conv
+
+
+def test_large_replica_batch_matches_single(gpu):
+    ts = [_noisy((128, 64, 32), 8, s, 1e-3) for s in range(3)]
+    res = gpu.cp_als_batched(ts, 8, max_iters=80, seeds=[5, 6, 7])
+    for t, rb, s in zip(ts, res, [5, 6, 7]):
+        r1 = gpu.cp_als(t, 8, max_iters=80, seed=s)
+        assert r1.error_history == rb.error_history
+        for x, y in zip(r1.factors, rb.factors):
+            assert np.array_equal(x, y)
