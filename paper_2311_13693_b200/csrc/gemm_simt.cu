@@ -186,6 +186,92 @@ __global__ void __launch_bounds__(256) gemm_f32_nn_kernel(GemmArgs<float> g) {
   }
 }
 
+// fp64 on the tensor cores (DMMA m8n8k4): 64 x 64 block tile, 16-deep K
+// chunks staged k-major in shared memory with a 68-double row stride (every
+// fragment load bank-conflict free), 8 warps of 32 x 16, register-staged
+// prefetch of the next chunk. Fixed K order per output (deterministic).
+constexpr int DM = 64, DN = 64, DK = 16, DLD = 68;
+
+__global__ void __launch_bounds__(256) gemm_f64_dmma_kernel(GemmArgs<double> g) {
+  __shared__ __align__(16) double As[DK][DLD];
+  __shared__ __align__(16) double Bs[DK][DLD];
+  const int64_t bz = blockIdx.z;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * DM, n0 = static_cast<int64_t>(blockIdx.y) * DN;
+  if (g.lower_only && m0 + DM <= n0) return;
+  const double* A = g.a + bz * g.stride_a;
+  const double* B = g.b + bz * g.stride_b;
+  double* C = g.c + bz * g.stride_c;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps of 32 x 16
+  double ra[4], rb[4];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      int mi, ki;
+      if (!g.trans_a) { mi = idx % DM; ki = idx / DM; } else { ki = idx % DK; mi = idx / DK; }
+      const int64_t gm = m0 + mi, gk = k0 + ki;
+      ra[e] = (gm < g.m && gk < g.k) ? (g.trans_a ? A[gk + gm * g.lda] : A[gm + gk * g.lda]) : 0.0;
+      int ni, kj;
+      if (g.trans_b) { ni = idx % DN; kj = idx / DN; } else { kj = idx % DK; ni = idx / DK; }
+      const int64_t gn = n0 + ni, gk2 = k0 + kj;
+      rb[e] = (gn < g.n && gk2 < g.k) ? (g.trans_b ? B[gn + gk2 * g.ldb] : B[gk2 + gn * g.ldb]) : 0.0;
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      int mi, ki;
+      if (!g.trans_a) { mi = idx % DM; ki = idx / DM; } else { ki = idx % DK; mi = idx / DK; }
+      As[ki][mi] = ra[e];
+      int ni, kj;
+      if (g.trans_b) { ni = idx % DN; kj = idx / DN; } else { kj = idx % DK; ni = idx / DK; }
+      Bs[kj][ni] = rb[e];
+    }
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  load(0);
+  for (int64_t k0 = 0; k0 < g.k; k0 += DK) {
+    __syncthreads();
+    store();
+    __syncthreads();
+    if (k0 + DK < g.k) load(k0 + DK);
+#pragma unroll
+    for (int ks = 0; ks < DK / 4; ++ks) {
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[ks * 4 + lc][wm * 32 + i * 8 + lr];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bs[ks * 4 + lc][wn * 16 + j * 8 + lr];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(a[i]), "d"(b[j]));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t gm = m0 + wm * 32 + i * 8 + lr, gn = n0 + wn * 16 + j * 8 + 2 * lc + e;
+        if (gm >= g.m || gn >= g.n) continue;
+        double* dst = C + gm + gn * g.ldc;
+        const double v = g.alpha * acc[i][j][e];
+        *dst = g.beta == 0.0 ? v : v + g.beta * *dst;
+      }
+}
+
 }  // namespace
 
 template <class T>
@@ -201,6 +287,26 @@ void gemm_simt(const GemmArgs<T>& g, cudaStream_t st) {
         dim3 grid(static_cast<unsigned>(ceil_div(g.m, FM)), static_cast<unsigned>(ceil_div(g.n, FN)),
                   static_cast<unsigned>(nb));
         gemm_f32_nn_kernel<<<grid, 256, 0, st>>>(part);
+        XLAUNCH_CHECK();
+        part.a += nb * g.stride_a;
+        part.b += nb * g.stride_b;
+        part.c += nb * g.stride_c;
+        left -= nb;
+      }
+      return;
+    }
+  }
+  if constexpr (std::is_same<T, double>::value) {
+    if (g.k > 0) {
+      int64_t left = g.batch;
+      GemmArgs<double> part = g;
+      while (left > 0) {
+        const int64_t nb = std::min<int64_t>(left, 65535);
+        part.batch = nb;
+        dim3 grid(static_cast<unsigned>(ceil_div(g.m, DM)), static_cast<unsigned>(ceil_div(g.n, DN)),
+                  static_cast<unsigned>(nb));
+        if (grid.y > 65535) throw Status(XTSG_E_USAGE, "gemm: n too large for one launch");
+        gemm_f64_dmma_kernel<<<grid, 256, 0, st>>>(part);
         XLAUNCH_CHECK();
         part.a += nb * g.stride_a;
         part.b += nb * g.stride_b;

@@ -22,6 +22,7 @@ struct GemmArgs {
   T* c = nullptr;
   int64_t ldc = 0, stride_c = 0;
   T alpha = T(1), beta = T(0);
+  bool lower_only = false;  // skip output tiles strictly above the diagonal (m == n, batch 1)
 };
 
 // C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b]

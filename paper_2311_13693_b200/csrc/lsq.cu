@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -190,7 +191,160 @@ __global__ void stack_kernel(const double* src, int64_t rows, int64_t cols, doub
   }
 }
 
+// ---- normal-equations fast path (large, well-conditioned stacks) ---------
+
+constexpr int CNB = 64;  // Cholesky block
+
+// Factor the nb x nb diagonal block at (j0, j0) of the lower Cholesky in place
+// (right-looking, in shared memory) and write its triangular inverse to Linv
+// (nb x nb, leading dim CNB). Pivots <= tau flag `fail`.
+__global__ void __launch_bounds__(256) potrf_block_kernel(double* G, int64_t n, int64_t j0, int nb, double* Linv,
+                                                          int* fail, double tau) {
+  extern __shared__ double shm[];
+  double* L = shm;                   // CNB x (CNB + 1), row i col j at L[i * (CNB + 1) + j]
+  double* V = shm + CNB * (CNB + 1);  // inverse, same layout
+  constexpr int LD = CNB + 1;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    L[i * LD + j] = i >= j ? G[(j0 + i) + n * (j0 + j)] : 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < nb; ++k) {
+    if (threadIdx.x == 0) {
+      double d = L[k * LD + k];
+      if (!(d > tau)) {
+        *fail = 1;
+        d = 1.0;
+      }
+      L[k * LD + k] = sqrt(d);
+    }
+    __syncthreads();
+    const double dk = L[k * LD + k];
+    for (int i = k + 1 + threadIdx.x; i < nb; i += blockDim.x) L[i * LD + k] /= dk;
+    __syncthreads();
+    const int rem = nb - k - 1;
+    for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+      const int i = k + 1 + e % rem, j = k + 1 + e / rem;
+      if (i >= j) L[i * LD + j] = fma(-L[i * LD + k], L[j * LD + k], L[i * LD + j]);
+    }
+    __syncthreads();
+  }
+  // inverse by forward substitution, one column per thread
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+    for (int i = 0; i < nb; ++i) {
+      double acc = i == c ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) acc = fma(-L[i * LD + k], V[k * LD + c], acc);
+      V[i * LD + c] = i < c ? 0.0 : acc / L[i * LD + i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    if (i >= j) G[(j0 + i) + n * (j0 + j)] = L[i * LD + j];
+    Linv[i + CNB * j] = V[i * LD + j];
+  }
+}
+
+__global__ void axpy_kernel(double* y, const double* x, int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[e] += x[e];
+}
+
+void gemm_d(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda,
+            const double* b, int64_t ldb, double beta, double* c, int64_t ldc, cudaStream_t st, bool lower = false) {
+  if (m <= 0 || n <= 0) return;
+  GemmArgs<double> g;
+  g.m = m; g.n = n; g.k = k;
+  g.a = a; g.lda = lda; g.trans_a = ta;
+  g.b = b; g.ldb = ldb; g.trans_b = tb;
+  g.c = c; g.ldc = ldc;
+  g.alpha = alpha; g.beta = beta;
+  g.lower_only = lower;
+  gemm_simt(g, st);
+}
+
+// Y (n x r, ld n) <- L^-T L^-1 Y with L the blocked Cholesky factor in G.
+void chol_solve(const double* G, int64_t n, const double* Linv, double* Y, int64_t r, double* tmp, cudaStream_t st) {
+  const int64_t nblk = ceil_div(n, CNB);
+  for (int64_t b = 0; b < nblk; ++b) {  // forward: L z = y
+    const int64_t j0 = b * CNB, nb = std::min<int64_t>(CNB, n - j0), n2 = n - j0 - nb;
+    gemm_d(false, false, nb, r, nb, 1.0, Linv + b * CNB * CNB, CNB, Y + j0, n, 0.0, tmp, CNB, st);
+    XCUDA(cudaMemcpy2DAsync(Y + j0, n * 8, tmp, CNB * 8, nb * 8, r, cudaMemcpyDeviceToDevice, st));
+    gemm_d(false, false, n2, r, nb, -1.0, G + (j0 + nb) + n * j0, n, Y + j0, n, 1.0, Y + j0 + nb, n, st);
+  }
+  for (int64_t b = nblk - 1; b >= 0; --b) {  // backward: L' x = z
+    const int64_t j0 = b * CNB, nb = std::min<int64_t>(CNB, n - j0), n2 = n - j0 - nb;
+    gemm_d(true, false, nb, r, n2, -1.0, G + (j0 + nb) + n * j0, n, Y + j0 + nb, n, 1.0, Y + j0, n, st);
+    gemm_d(true, false, nb, r, nb, 1.0, Linv + b * CNB * CNB, CNB, Y + j0, n, 0.0, tmp, CNB, st);
+    XCUDA(cudaMemcpy2DAsync(Y + j0, n * 8, tmp, CNB * 8, nb * 8, r, cudaMemcpyDeviceToDevice, st));
+  }
+}
+
 }  // namespace
+
+// Least squares through the normal equations A'A x = A'b with a blocked
+// Cholesky (DMMA GEMMs for the Gram, the trailing updates and the solves) and
+// two steps of iterative refinement on the true residual b - A x. Taken only
+// when every pivot of A'A exceeds 1e-6 of its largest diagonal (cond(A) of at
+// most ~10^3, far from the QR rank threshold eps * n): then the system has
+// full rank in the reference's sense and the refined solution matches the
+// QR solution to ~cond * eps. Returns false (nothing written) otherwise.
+bool lsq_chol_dev(const double* A, int64_t m, int64_t n, const double* B, int64_t r, double* X, cudaStream_t st) {
+  const int64_t nblk = ceil_div(n, CNB);
+  DevBuf<double> G(static_cast<size_t>(n * n), st), W(static_cast<size_t>(n * CNB), st),
+      Linv(static_cast<size_t>(nblk * CNB * CNB), st), tmp(static_cast<size_t>(CNB * r), st),
+      Rm(static_cast<size_t>(m * r), st), dX(static_cast<size_t>(n * r), st), diag(static_cast<size_t>(n), st);
+  DevBuf<int> fail(1, st);
+  fail.zero();
+  gemm_d(true, false, n, n, m, 1.0, A, m, A, m, 0.0, G.ptr, n, st, true);
+  diag_kernel<<<static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 1024))), 256, 0, st>>>(
+      G.ptr, n, n, diag.ptr);
+  XLAUNCH_CHECK();
+  std::vector<double> hd(static_cast<size_t>(n));
+  XCUDA(cudaMemcpyAsync(hd.data(), diag.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  XCUDA(cudaStreamSynchronize(st));
+  double mx = 0.0;
+  for (double v : hd) mx = std::max(mx, v);
+  if (!(mx > 0.0)) return false;
+  const double tau = 1e-6 * mx;
+  const size_t smem = sizeof(double) * 2 * CNB * (CNB + 1);
+  static bool attr = false;
+  if (!attr) {
+    XCUDA(cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = true;
+  }
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t j0 = b * CNB, nb = std::min<int64_t>(CNB, n - j0), n2 = n - j0 - nb;
+    potrf_block_kernel<<<1, 256, smem, st>>>(G.ptr, n, j0, static_cast<int>(nb), Linv.ptr + b * CNB * CNB, fail.ptr,
+                                             tau);
+    XLAUNCH_CHECK();
+    if (n2 > 0) {
+      // panel L21 = A21 L11^-T, then the trailing update A22 -= L21 L21'
+      gemm_d(false, true, n2, nb, nb, 1.0, G.ptr + (j0 + nb) + n * j0, n, Linv.ptr + b * CNB * CNB, CNB, 0.0, W.ptr,
+             n2, st);
+      XCUDA(cudaMemcpy2DAsync(G.ptr + (j0 + nb) + n * j0, n * 8, W.ptr, n2 * 8, n2 * 8, nb, cudaMemcpyDeviceToDevice,
+                              st));
+      gemm_d(false, true, n2, n2, nb, -1.0, W.ptr, n2, W.ptr, n2, 1.0, G.ptr + (j0 + nb) * (n + 1), n, st, true);
+    }
+  }
+  int hf = 0;
+  XCUDA(cudaMemcpyAsync(&hf, fail.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  XCUDA(cudaStreamSynchronize(st));
+  if (hf) return false;
+  // x = (A'A)^-1 A'b, then refine twice: x += (A'A)^-1 A'(b - A x)
+  gemm_d(true, false, n, r, m, 1.0, A, m, B, m, 0.0, X, n, st);
+  chol_solve(G.ptr, n, Linv.ptr, X, r, tmp.ptr, st);
+  for (int it = 0; it < 2; ++it) {
+    XCUDA(cudaMemcpyAsync(Rm.ptr, B, sizeof(double) * m * r, cudaMemcpyDeviceToDevice, st));
+    gemm_d(false, false, m, r, n, -1.0, A, m, X, n, 1.0, Rm.ptr, m, st);
+    gemm_d(true, false, n, r, m, 1.0, A, m, Rm.ptr, m, 0.0, dX.ptr, n, st);
+    chol_solve(G.ptr, n, Linv.ptr, dX.ptr, r, tmp.ptr, st);
+    axpy_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(n * r, 256), 4096)), 256, 0, st>>>(X, dX.ptr, n * r);
+    XLAUNCH_CHECK();
+  }
+  return true;
+}
 
 // Column-pivoted QR least squares of the device system A (m x n) X = B (m x r).
 // Returns the numerical rank; X (n x r) is written only when rank == n.
@@ -288,6 +442,14 @@ extern "C" int32_t xtsg_solve_stacked_ls(int64_t count, const int64_t* rows, int
       row0 += rp;
     }
     OutView<double> xo(x, static_cast<size_t>(cols * r), st);
+    static const bool chol_on = [] {
+      const char* e = std::getenv("XTSG_LS_CHOL");
+      return !(e && std::atoi(e) == 0);
+    }();
+    if (chol_on && cols >= 512 && m >= cols && lsq_chol_dev(A.ptr, m, cols, B.ptr, r, xo.dev, st)) {
+      xo.finish();
+      return;
+    }
     const int64_t rank = lsq_colpiv_dev(A.ptr, m, cols, B.ptr, r, xo.dev, st);
     if (rank < cols)
       throw Status(XTSG_E_ILLPOSED,

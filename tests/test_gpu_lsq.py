@@ -74,3 +74,34 @@ def test_large_stack_matches_numpy(gpu):
     g = rng.standard_normal((700, 20))
     sol = gpu.solve_stacked_ls([u @ g for u in us], us)
     assert rel_diff(g, sol) <= 1e-9
+
+
+# ---- large stacks take the normal-equations fast path (blocked Cholesky with
+# refinement, lsq.cu lsq_chol_dev); rank-deficient ones fall back to the
+# column-pivoted QR and report the reference's rank
+
+def _stack(cols, P, L, S, seed):
+    from oracle.oracle import Restated
+    ens = Restated().make_ensemble([cols, 16, 16], [L, 8, 8], P, S, seed=seed)
+    return ens[0]
+
+
+def test_large_stack_fast_path_matches_reference(gpu, reference):
+    us = _stack(640, 12, 64, 8, 5)            # 768 x 640, well conditioned
+    g = rmat(640, 7, 901)
+    rng = np.random.default_rng(3)
+    fs = [u @ g + 1e-3 * rng.standard_normal((u.shape[0], 7)) for u in us]   # inconsistent system
+    sol = gpu.solve_stacked_ls(fs, us)
+    rc, _, want = reference.solve_stacked_ls(fs, us)
+    assert rc == 0
+    assert rel_diff(want, sol) <= 1e-9
+
+
+def test_large_rank_deficient_falls_back_to_qr(gpu, reference):
+    us = _stack(600, 12, 64, 40, 6)           # 12 * 24 + 40 = 328 distinct rows < 600
+    g = rmat(600, 3, 902)
+    fs = [u @ g for u in us]
+    with pytest.raises(gpu.IllPosedError) as e:
+        gpu.solve_stacked_ls(fs, us)
+    rc, rank, _ = reference.solve_stacked_ls(fs, us)
+    assert rc != 0 and e.value.effective_rank == rank == 328
