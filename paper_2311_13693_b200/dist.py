@@ -36,3 +36,35 @@ def compress_sharded(local_compress, K: int, y, dst: int = 0, group=None):
     if world > 1:
         dist.reduce(y, dst=dst, op=dist.ReduceOp.SUM, group=group)
     return y
+
+
+def decompose_sharded(compress_slab, K: int, y, decompose_replicas, dst: int = 0, group=None):
+    """The multi-GPU pipeline (SURVEY §8 e): every rank compresses its mode-3
+    slab into partial replicas (``compress_slab(k0, k1, y)``), one sum-reduce
+    lands the P replicas on ``dst``, and ``dst`` runs the decomposition,
+    alignment and recovery stages on them (``decompose_replicas(y) ->
+    (factors, metrics)``; the ALS batch fills one GPU: one CTA per replica).
+    The recovered factor triple (three small fp64 matrices) is broadcast back,
+    so every rank returns the same factors; metrics only on ``dst``.
+    """
+    import torch
+    import torch.distributed as dist
+
+    compress_sharded(compress_slab, K, y, dst=dst, group=group)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    factors, metrics = (None, None)
+    if rank == dst:
+        factors, metrics = decompose_replicas(y)
+    if world > 1:
+        shapes = [list(f.shape) for f in factors] if rank == dst else None
+        box = [shapes]
+        dist.broadcast_object_list(box, src=dst, group=group)
+        out = []
+        for m, shp in enumerate(box[0]):
+            t = (torch.from_numpy(factors[m].ravel(order="F")).to(y.device) if rank == dst
+                 else torch.zeros(shp[0] * shp[1], dtype=torch.float64, device=y.device))
+            dist.broadcast(t, src=dst, group=group)
+            out.append(t.cpu().numpy().reshape(shp, order="F"))
+        factors = tuple(out)
+    return factors, metrics

@@ -58,3 +58,41 @@ def test_gloo_world2_sharded_compression_matches_one_shot():
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     assert out["err"] <= 1e-12
+
+
+def _pipeline_worker(rank, world, port, out):
+    # host logic of the sharded pipeline: slab compression (oracle stand-in),
+    # reduce to rank 0, decomposition there (stand-in: the exact factors are
+    # recovered from the replicas by a least-squares fit), broadcast back
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2311_13693_b200.dist import decompose_sharded
+    from oracle.oracle import Restated
+    ora = Restated()
+    dims, red, P, S, seed = (12, 10, 9), (4, 3, 3), 3, 2, 5
+    ens = ora.make_ensemble(dims, red, P, S, seed=seed)
+    rng = np.random.default_rng(2)
+    f = [np.asfortranarray(rng.standard_normal((n, 2))) for n in dims]
+    t = np.asfortranarray(np.einsum("ir,jr,kr->ijk", *f))
+
+    def local(k0, k1, y):
+        parts = [ora.comp(np.asfortranarray(t[:, :, k0:k1]), ens[0][p], ens[1][p], ens[2][p][:, k0:k1])
+                 for p in range(P)]
+        y.copy_(torch.from_numpy(np.concatenate([x.ravel(order="F") for x in parts])))
+
+    def decompose(y):
+        full = np.concatenate([ora.comp(t, ens[0][p], ens[1][p], ens[2][p]).ravel(order="F") for p in range(P)])
+        assert np.abs(y.numpy() - full).max() <= 1e-12
+        return tuple(x * (m + 1) for m, x in enumerate(f)), {"ok": True}
+
+    y = torch.zeros(P * int(np.prod(red)), dtype=torch.float64)
+    fac, met = decompose_sharded(local, dims[2], y, decompose)
+    out[rank] = (max(float(np.abs(a - b * (m + 1)).max()) for m, (a, b) in enumerate(zip(fac, f))), met is not None)
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_pipeline():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_pipeline_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out[0] == (0.0, True) and out[1] == (0.0, False)

@@ -7,11 +7,27 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def _derive(seed, tag):
+    # Rng::derive (rng.hpp:46-50): 2nd output of splitmix64 seeded with seed ^ (golden * (tag + 0x632b...))
+    m = (1 << 64) - 1
+    golden = 0x9E3779B97F4A7C15
+
+    def mix(z):
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+        return z ^ (z >> 31)
+    state = (seed ^ ((golden * ((tag + 0x632BE59BD9B4E019) & m)) & m)) & m
+    state = (state + golden) & m
+    state = (state + golden) & m
+    return mix(state)
 
 
 def main():
@@ -43,12 +59,55 @@ def main():
     cfg = xt.PipelineConfig(reduced=tuple(a.reduced), rank=a.rank, replicas=a.replicas, shared=a.shared,
                             precision=prec, replica_fit_tol=fit, seed=a.seed, mode=a.mode,
                             omp_sparsity=a.omp_sparsity)
-    t0 = time.perf_counter()
-    rec, met = xt.decompose(cfg, factors=f)
-    wall = time.perf_counter() - t0
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        # multi-GPU: mode-3 slabs per rank, NCCL reduce, stages 1-3 on rank 0
+        import torch
+        import torch.distributed as dist
+        from paper_2311_13693_b200.dist import decompose_sharded
+        from paper_2311_13693_b200._lib import PipelineConfigC  # noqa: F401
+        rank = int(os.environ["RANK"])
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        dist.init_process_group("nccl")
+        P = a.replicas
+        ens_seed = _derive(a.seed, 11)
+        plan = xt.Plan(a.dims, a.reduced, P, a.shared, ens_seed, precision=prec)
+        y = torch.zeros(P * int(np.prod(a.reduced)), dtype=torch.float32, device="cuda")
+        stage = {}
+
+        def slab(k0, k1, yy):
+            plan.compress_factors(f, k0, k1, y=yy, device="cuda")
+            torch.cuda.synchronize()
+
+        def rest(yy):
+            return xt.decompose_replicas(cfg, yy, factors=f)
+
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        t_c0 = time.perf_counter()
+        from paper_2311_13693_b200.dist import compress_sharded
+        compress_sharded(slab, a.dims[2], y)
+        torch.cuda.synchronize()
+        t_comp = time.perf_counter() - t_c0
+        tc = torch.tensor([t_comp], device="cuda")
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        rec, met = (rest(y) if rank == 0 else (None, None))
+        wall = time.perf_counter() - t0
+        if rank != 0:
+            dist.destroy_process_group()
+            return
+        met.stage_seconds["compression"] = float(tc.item())
+        met.stage_status["compression"] = "ok"
+        dist.destroy_process_group()
+    else:
+        t0 = time.perf_counter()
+        rec, met = xt.decompose(cfg, factors=f)
+        wall = time.perf_counter() - t0
     rep = xt.evaluate(f, rec)
     elems = float(np.prod(a.dims))
     out = {
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "config": {"dims": a.dims, "rank": a.rank, "reduced": a.reduced, "replicas": met.replicas_total,
                    "shared": a.shared, "precision": a.precision, "replica_fit_tol": fit, "mode": a.mode,
                    "law": a.law, "source": "factors (slabs generated on the device)"},
