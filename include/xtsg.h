@@ -121,6 +121,40 @@ int32_t xtsg_blocked_push(xtsg_blocked* h, const int64_t cell[3], const int64_t 
 int32_t xtsg_blocked_finish(xtsg_blocked* h, double* y);
 void xtsg_blocked_destroy(xtsg_blocked* h);
 
+/* ---- precision model (half.hpp, mixed.hpp) ----------------------------- */
+/* Device replays of the reference's binary16 arithmetic, bit-identical to it:
+ * values are binary16 numbers carried as doubles, every product is a
+ * half_gemm (fixed k-inner order, one rounding per product and per add). */
+#define XTSG_SPLIT_ROUND 0   /* round_to_half only (residual unused) */
+#define XTSG_SPLIT_FULL 1    /* fp16_split: half + residual == x exactly */
+#define XTSG_SPLIT_STORED 2  /* fp16_split_stored: residual itself binary16 (scaled 2^11) */
+
+/* split_matrix / split_tensor / round_matrix_to_half / round_tensor_to_half
+ * (mixed.cpp:11-61) over n values; XTSG_E_HALFRANGE like double_to_half_bits
+ * (half.cpp:10-47) for NaN, Inf or magnitudes rounding above 65504. */
+int32_t xtsg_split_half(const double* x, int64_t n, int32_t mode, double* half, double* residual);
+
+/* half_gemm (mixed.cpp:63-76): out (rows x cols) = a (rows x inner) * b (b_rows x cols). */
+int32_t xtsg_half_gemm(const double* a, int64_t rows, int64_t inner, const double* b, int64_t b_rows,
+                       int64_t cols, double* out);
+
+/* comp_with(t, u, v, w, &half_gemm) (compression.cpp:202-209, mixed.cpp:84-86) */
+int32_t xtsg_comp_half(const double* t, int64_t n1, int64_t n2, int64_t n3, const double* u, int64_t l,
+                       const double* v, int64_t m, const double* w, int64_t n, double* y);
+
+/* comp_mixed (mixed.cpp:88-98, the paper's Eq. 5): the half x half x half x
+ * half term plus the four single-residual terms, summed in the reference's
+ * order. Inputs are the half/residual parts of split_tensor / split_matrix. */
+int32_t xtsg_comp_mixed(const double* t_half, const double* t_res, int64_t n1, int64_t n2, int64_t n3,
+                        const double* u_half, const double* u_res, int64_t l, const double* v_half,
+                        const double* v_res, int64_t m, const double* w_half, const double* w_res,
+                        int64_t n, double* y);
+
+/* comp_naive_half (mixed.cpp:100-104) */
+int32_t xtsg_comp_naive_half(const double* t, int64_t n1, int64_t n2, int64_t n3, const double* u,
+                             int64_t l, const double* v, int64_t m, const double* w, int64_t n,
+                             double* y);
+
 /* ---- compression, tensor-core fast path (the B200 hot path) ------------ */
 /* A plan owns the device-resident ensemble of one compression job: the P
  * replicas' U stacked into one (P*L) x I bf16 operand, V transposed per

@@ -61,6 +61,10 @@ class Restated:
             "or_comp_from_factors": (None, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
             "or_comp_triple_sum": (None, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
             "or_generate_dense": (None, [_P, _I64, _U64, _P, _P, _P]),
+            "or_half_bits": (C.c_int32, [_D]),
+            "or_split": (C.c_int, [_P, _I64, C.c_int, _P, _P]),
+            "or_comp_half": (None, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
+            "or_comp_mixed": (None, [_P, _P, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P]),
         }
         for n, (r, a) in sig.items():
             fn = getattr(L, n)
@@ -132,6 +136,35 @@ class Restated:
                                     _ptr(u), u.shape[0], _ptr(v), v.shape[0], _ptr(w), w.shape[0], _ptr(y))
         return y
 
+    def half_bits(self, x):
+        """double_to_half_bits (half.cpp:10-47); None for HalfRangeError."""
+        b = self.L.or_half_bits(float(x))
+        return None if b < 0 else b
+
+    def split(self, x, mode):
+        """mode 0 round_to_half, 1 fp16_split, 2 fp16_split_stored (mixed.cpp:11-61)."""
+        x = _f(x)
+        half = np.zeros(x.shape, order="F")
+        res = np.zeros(x.shape, order="F")
+        if self.L.or_split(_ptr(x), x.size, mode, _ptr(half), _ptr(res)):
+            raise OverflowError("HalfRangeError")
+        return half, res
+
+    def comp_half(self, t, u, v, w):
+        t, u, v, w = _f(t), _f(u), _f(v), _f(w)
+        y = np.zeros((u.shape[0], v.shape[0], w.shape[0]), order="F")
+        self.L.or_comp_half(_ptr(t), *t.shape, _ptr(u), u.shape[0], _ptr(v), v.shape[0], _ptr(w), w.shape[0],
+                            _ptr(y))
+        return y
+
+    def comp_mixed(self, t, u, v, w):
+        """comp_mixed from (half, residual) pairs."""
+        (th, tr), (uh, ur), (vh, vr), (wh, wr) = [(_f(a), _f(b)) for a, b in (t, u, v, w)]
+        y = np.zeros((uh.shape[0], vh.shape[0], wh.shape[0]), order="F")
+        self.L.or_comp_mixed(_ptr(th), _ptr(tr), *th.shape, _ptr(uh), _ptr(ur), uh.shape[0], _ptr(vh), _ptr(vr),
+                             vh.shape[0], _ptr(wh), _ptr(wr), wh.shape[0], _ptr(y))
+        return y
+
     def generate_dense(self, dims, rank, seed):
         a = np.zeros((dims[0], rank), order="F")
         b = np.zeros((dims[1], rank), order="F")
@@ -176,6 +209,12 @@ class Reference:
             "xref_generate": (C.c_int, [_P, _I64, C.c_int, _I64, _U64, _P, _P, _P]),
             "xref_decompose": (C.c_int, [_P, _P, _P, _P, _I64, _P, _P, _P, _U64, _P, _P, _P, _P]),
             "xref_evaluate": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+            "xref_double_to_half_bits": (C.c_int, [_D, _P]),
+            "xref_split": (C.c_int, [_P, _I64, C.c_int, _P, _P]),
+            "xref_half_gemm": (C.c_int, [_P, _I64, _I64, _P, _I64, _P]),
+            "xref_comp_half": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
+            "xref_comp_naive_half": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
+            "xref_comp_mixed": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, C.c_int, _P]),
         }
         for n, (r, a) in sig.items():
             fn = getattr(L, n)
@@ -216,6 +255,43 @@ class Reference:
         self._ok(self.L.xref_comp(_ptr(t), *t.shape, _ptr(u), u.shape[0], _ptr(v), v.shape[0], _ptr(w),
                                   w.shape[0], _ptr(y)), "comp")
         return y
+
+    def half_bits(self, x):
+        out = np.zeros(1, np.uint16)
+        rc = self.L.xref_double_to_half_bits(float(x), _ptr(out))
+        return None if rc != 0 else int(out[0])
+
+    def split(self, x, mode):
+        x = _f(x)
+        half = np.zeros(x.shape, order="F")
+        res = np.zeros(x.shape, order="F")
+        if self.L.xref_split(_ptr(x), x.size, mode, _ptr(half), _ptr(res)) != 0:
+            raise OverflowError("HalfRangeError")
+        return half, res
+
+    def half_gemm(self, a, b):
+        a, b = _f(a), _f(b)
+        out = np.zeros((a.shape[0], b.shape[1]), order="F")
+        self._ok(self.L.xref_half_gemm(_ptr(a), a.shape[0], a.shape[1], _ptr(b), b.shape[1], _ptr(out)),
+                 "half_gemm")
+        return out
+
+    def _comp3(self, fn, t, u, v, w, *extra):
+        t, u, v, w = _f(t), _f(u), _f(v), _f(w)
+        y = np.zeros((u.shape[0], v.shape[0], w.shape[0]), order="F")
+        self._ok(fn(_ptr(t), *t.shape, _ptr(u), u.shape[0], _ptr(v), v.shape[0], _ptr(w), w.shape[0], *extra,
+                    _ptr(y)), fn.__name__)
+        return y
+
+    def comp_half(self, t, u, v, w):
+        return self._comp3(self.L.xref_comp_half, t, u, v, w)
+
+    def comp_naive_half(self, t, u, v, w):
+        return self._comp3(self.L.xref_comp_naive_half, t, u, v, w)
+
+    def comp_mixed(self, t, u, v, w, stored_residual=False):
+        """comp_mixed(split_tensor(t), split_matrix(u), ...) from the unsplit operands."""
+        return self._comp3(self.L.xref_comp_mixed, t, u, v, w, int(stored_residual))
 
     def comp_from_factors(self, a, b, c, u, v, w):
         a, b, c, u, v, w = map(_f, (a, b, c, u, v, w))

@@ -59,12 +59,12 @@ int guard(F&& f) {
 
 Matrix mat(const double* p, int64_t r, int64_t c) {
   Matrix m(r, c);
-  if (r * c) std::memcpy(m.values.data(), p, sizeof(double) * r * c);
+  if (r * c != 0) std::memcpy(m.values.data(), p, sizeof(double) * r * c);
   return m;
 }
 Tensor3 ten(const double* p, int64_t a, int64_t b, int64_t c) {
   Tensor3 t(a, b, c);
-  if (a * b * c) std::memcpy(t.values.data(), p, sizeof(double) * a * b * c);
+  if (a * b * c != 0) std::memcpy(t.values.data(), p, sizeof(double) * a * b * c);
   return t;
 }
 void put(double* dst, const std::vector<double>& v) {
@@ -420,6 +420,41 @@ int xref_evaluate(const int64_t* dims, int64_t r, const double* ta, const double
 // half.cpp:10-47
 int xref_double_to_half_bits(double x, uint16_t* out) {
   return guard([&] { *out = double_to_half_bits(x); });
+}
+
+// mixed.cpp:47-61 (mode 0) and split_tensor (mode 1 full, 2 stored residual)
+int xref_split(const double* x, int64_t n, int mode, double* half, double* res) {
+  return guard([&] {
+    const Tensor3 t = ten(x, n, 1, 1);
+    if (mode == 0) {
+      put(half, round_tensor_to_half(t).values);
+    } else {
+      const SplitTensor3 s = split_tensor(t, mode == 2);
+      put(half, s.half.values);
+      put(res, s.residual.values);
+    }
+  });
+}
+
+// mixed.cpp:63-76
+int xref_half_gemm(const double* a, int64_t rows, int64_t inner, const double* b, int64_t cols, double* out) {
+  return guard([&] { put(out, half_gemm(mat(a, rows, inner), mat(b, inner, cols)).values); });
+}
+
+// comp_with(..., &half_gemm) (compression.cpp:202-209)
+int xref_comp_half(const double* t, int64_t n1, int64_t n2, int64_t n3, const double* u, int64_t l,
+                   const double* v, int64_t m, const double* w, int64_t n, double* y) {
+  return guard([&] {
+    put(y, comp_with(ten(t, n1, n2, n3), mat(u, l, n1), mat(v, m, n2), mat(w, n, n3), &half_gemm).values);
+  });
+}
+
+// mixed.cpp:100-104
+int xref_comp_naive_half(const double* t, int64_t n1, int64_t n2, int64_t n3, const double* u, int64_t l,
+                         const double* v, int64_t m, const double* w, int64_t n, double* y) {
+  return guard([&] {
+    put(y, comp_naive_half(ten(t, n1, n2, n3), mat(u, l, n1), mat(v, m, n2), mat(w, n, n3)).values);
+  });
 }
 
 }  // extern "C"

@@ -235,3 +235,100 @@ void or_generate_dense(const int64_t* dims, int64_t rank, uint64_t seed, double*
   or_gen_gaussian(dims[1], rank, or_derive(seed, 2), b);
   or_gen_gaussian(dims[2], rank, or_derive(seed, 3), c);
 }
+
+/* ---- precision model (half.cpp, mixed.cpp) ---------------------------- */
+
+/* double_to_half_bits (half.cpp:10-47); returns -1 for HalfRangeError. */
+int32_t or_half_bits(double x) {
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  const uint32_t sign = (uint32_t)((b >> 63) << 15);
+  const uint64_t dexp = (b >> 52) & 0x7ff, dman = b & ((1ULL << 52) - 1);
+  if (dexp == 0x7ff) return -1;
+  if (dexp == 0) return (int32_t)sign;
+  const int e = (int)dexp - 1023;
+  if (e >= 16) return -1;
+  if (e <= -26) return (int32_t)sign;
+  if (e >= -14) {
+    uint64_t r = dman >> 42;
+    const uint64_t rem = dman & ((1ULL << 42) - 1), hp = 1ULL << 41;
+    if (rem > hp || (rem == hp && (r & 1))) ++r;
+    int he = e;
+    if (r == 1024) { r = 0; ++he; }
+    if (he > 15) return -1;
+    return (int32_t)(sign | (uint32_t)((he + 15) << 10) | (uint32_t)r);
+  }
+  const uint64_t full = (1ULL << 52) | dman;
+  const int shift = 28 - e;
+  uint64_t r = full >> shift;
+  const uint64_t rem = full & ((1ULL << shift) - 1), hp = 1ULL << (shift - 1);
+  if (rem > hp || (rem == hp && (r & 1))) ++r;
+  if (r == 1024) return (int32_t)(sign | (1u << 10));
+  return (int32_t)(sign | (uint32_t)r);
+}
+
+/* half_bits_to_double (half.cpp:49-60) */
+double or_half_value(int32_t bits) {
+  const int e = (bits >> 10) & 0x1f, man = bits & 0x3ff;
+  double v = e == 0 ? ldexp((double)man, -24) : ldexp((double)(1024 + man), e - 25);
+  return (bits >> 15) & 1 ? -v : v;
+}
+
+/* round_to_half / fp16_split / fp16_split_stored over n values (mixed.cpp:11-25);
+ * mode 0 round, 1 split, 2 stored split. Returns 1 on HalfRangeError. */
+int or_split(const double* x, int64_t n, int mode, double* half, double* res) {
+  for (int64_t e = 0; e < n; ++e) {
+    const int32_t hb = or_half_bits(x[e]);
+    if (hb < 0) return 1;
+    half[e] = or_half_value(hb);
+    if (mode >= 1) {
+      double r = x[e] - half[e];
+      if (mode == 2) {
+        const int32_t rb = or_half_bits(ldexp(r, 11));
+        if (rb < 0) return 1;
+        r = ldexp(or_half_value(rb), -11);
+      }
+      res[e] = r;
+    }
+  }
+  return 0;
+}
+
+/* half_gemm (mixed.cpp:63-76) applied to one unfolding: out(a,c,b) = sum_x A(c,x) in(a,x,b) */
+static void mode_seq(const double* A, int64_t nc, int64_t nx, const double* in, int64_t na, int64_t nb,
+                     double* out) {
+  for (int64_t b = 0; b < nb; ++b)
+    for (int64_t c = 0; c < nc; ++c)
+      for (int64_t a = 0; a < na; ++a) {
+        double acc = 0.0;
+        for (int64_t x = 0; x < nx; ++x) acc += A[c + nc * x] * in[a + na * (x + nx * b)];
+        out[a + na * (c + nc * b)] = acc;
+      }
+}
+
+/* comp_with(t, u, v, w, &half_gemm) (compression.cpp:202-209, mixed.cpp:84-86) */
+void or_comp_half(const double* t, int64_t n1, int64_t n2, int64_t n3, const double* u, int64_t l,
+                  const double* v, int64_t m, const double* w, int64_t n, double* y) {
+  double* s1 = malloc(sizeof(double) * (size_t)(l * n2 * n3 + 1));
+  double* s2 = malloc(sizeof(double) * (size_t)(l * m * n3 + 1));
+  mode_seq(u, l, n1, t, 1, n2 * n3, s1);
+  mode_seq(v, m, n2, s1, l, n3, s2);
+  mode_seq(w, n, n3, s2, l * m, 1, y);
+  free(s1);
+  free(s2);
+}
+
+/* comp_mixed (mixed.cpp:88-98) from split parts: five comp_half terms, add_inplace order */
+void or_comp_mixed(const double* th, const double* tr, int64_t n1, int64_t n2, int64_t n3, const double* uh,
+                   const double* ur, int64_t l, const double* vh, const double* vr, int64_t m, const double* wh,
+                   const double* wr, int64_t n, double* y) {
+  const int64_t yn = l * m * n;
+  double* tmp = malloc(sizeof(double) * (size_t)(yn + 1));
+  or_comp_half(th, n1, n2, n3, uh, l, vh, m, wh, n, y);
+  const double* terms[4][4] = {{th, ur, vh, wh}, {th, uh, vr, wh}, {th, uh, vh, wr}, {tr, uh, vh, wh}};
+  for (int q = 0; q < 4; ++q) {
+    or_comp_half(terms[q][0], n1, n2, n3, terms[q][1], l, terms[q][2], m, terms[q][3], n, tmp);
+    for (int64_t e = 0; e < yn; ++e) y[e] += tmp[e];
+  }
+  free(tmp);
+}

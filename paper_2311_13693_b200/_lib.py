@@ -123,6 +123,11 @@ _SIGS = {
     "xtsg_comp_from_factors": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _I64,
                                       _P, _I64, _P]),
     "xtsg_reconstruct": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _P]),
+    "xtsg_split_half": (_I32, [_P, _I64, _I32, _P, _P]),
+    "xtsg_half_gemm": (_I32, [_P, _I64, _I64, _P, _I64, _I64, _P]),
+    "xtsg_comp_half": (_I32, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
+    "xtsg_comp_mixed": (_I32, [_P, _P, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P]),
+    "xtsg_comp_naive_half": (_I32, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
     "xtsg_blocked_begin": (_I32, [_P, _P, _I64, _P, _P, _P, _P, _I32, _P]),
     "xtsg_blocked_push": (_I32, [_P, _P, _P, _P]),
     "xtsg_blocked_finish": (_I32, [_P, _P]),

@@ -120,6 +120,67 @@ def comp(t, u, v, w) -> np.ndarray:
     return y
 
 
+def _split(x, mode):
+    x = _f64(x)
+    half = np.zeros(x.shape, order="F")
+    res = np.zeros(x.shape, order="F") if mode else None
+    check(lib.xtsg_split_half(ptr(x), x.size, mode, ptr(half), ptr(res) if mode else None))
+    return half, res
+
+
+def round_to_half(x) -> np.ndarray:
+    """round_matrix_to_half / round_tensor_to_half (mixed.cpp:47-61); HalfRangeError out of range."""
+    return _split(x, 0)[0]
+
+
+def split_half(x, stored_residual: bool = False):
+    """split_matrix / split_tensor (mixed.cpp:27-45): (half, residual) arrays."""
+    return _split(x, 2 if stored_residual else 1)
+
+
+def half_gemm(a, b) -> np.ndarray:
+    """half_gemm (mixed.cpp:63-76), bit-exact on the device."""
+    a, b = _f64(a), _f64(b)
+    out = np.zeros((a.shape[0], b.shape[1]), order="F")
+    check(lib.xtsg_half_gemm(ptr(a), a.shape[0], a.shape[1], ptr(b), b.shape[0], b.shape[1], ptr(out)))
+    return out
+
+
+def _comp_shapes(t, u, v, w):
+    if t.ndim != 3 or u.shape[1] != t.shape[0] or v.shape[1] != t.shape[1] or w.shape[1] != t.shape[2]:
+        from ._lib import UsageError
+        raise UsageError("comp: compression matrix columns must match tensor dims")
+    return np.zeros((u.shape[0], v.shape[0], w.shape[0]), order="F")
+
+
+def comp_half(t, u, v, w) -> np.ndarray:
+    """comp_with(t, u, v, w, &half_gemm) (mixed.cpp:84-86)."""
+    t, u, v, w = _f64(t), _f64(u), _f64(v), _f64(w)
+    y = _comp_shapes(t, u, v, w)
+    check(lib.xtsg_comp_half(ptr(t), *t.shape, ptr(u), u.shape[0], ptr(v), v.shape[0], ptr(w),
+                             w.shape[0], ptr(y)))
+    return y
+
+
+def comp_mixed(t, u, v, w) -> np.ndarray:
+    """comp_mixed (mixed.cpp:88-98). Each argument is a (half, residual) pair
+    as returned by split_half."""
+    (th, tr), (uh, ur), (vh, vr), (wh, wr) = [(_f64(a), _f64(b)) for a, b in (t, u, v, w)]
+    y = _comp_shapes(th, uh, vh, wh)
+    check(lib.xtsg_comp_mixed(ptr(th), ptr(tr), *th.shape, ptr(uh), ptr(ur), uh.shape[0], ptr(vh), ptr(vr),
+                              vh.shape[0], ptr(wh), ptr(wr), wh.shape[0], ptr(y)))
+    return y
+
+
+def comp_naive_half(t, u, v, w) -> np.ndarray:
+    """comp_naive_half (mixed.cpp:100-104)."""
+    t, u, v, w = _f64(t), _f64(u), _f64(v), _f64(w)
+    y = _comp_shapes(t, u, v, w)
+    check(lib.xtsg_comp_naive_half(ptr(t), *t.shape, ptr(u), u.shape[0], ptr(v), v.shape[0], ptr(w),
+                                   w.shape[0], ptr(y)))
+    return y
+
+
 def reconstruct(a, b, c) -> np.ndarray:
     """tensor.cpp:133-150"""
     a, b, c = _f64(a), _f64(b), _f64(c)

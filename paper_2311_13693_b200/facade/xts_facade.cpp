@@ -19,7 +19,9 @@
 #include "xts/compression.hpp"
 #include "xts/cp_als.hpp"
 #include "xts/errors.hpp"
+#include "xts/half.hpp"
 #include "xts/linalg.hpp"
+#include "xts/mixed.hpp"
 #include "xts/rng.hpp"
 #include "xts/tensor.hpp"
 #include "xtsg.h"
@@ -69,7 +71,7 @@ std::vector<Matrix> split(const std::vector<double>& flat, index_t count, index_
   out.reserve(static_cast<std::size_t>(count));
   for (index_t p = 0; p < count; ++p) {
     Matrix m(rows, cols);
-    if (rows * cols) std::memcpy(m.values.data(), flat.data() + p * rows * cols, sizeof(double) * rows * cols);
+    if (rows * cols != 0) std::memcpy(m.values.data(), flat.data() + p * rows * cols, sizeof(double) * rows * cols);
     out.push_back(std::move(m));
   }
   return out;
@@ -158,11 +160,19 @@ Tensor3 comp(const Tensor3& t, const Matrix& u, const Matrix& v, const Matrix& w
   return y;
 }
 
-// The GemmFn hook swaps the arithmetic model (mixed.cpp:84-86): the caller's
-// host multiply runs the fixed mode-1 -> 2 -> 3 skeleton (compression.cpp:202-209).
+// The GemmFn hook swaps the arithmetic model (mixed.cpp:84-86). The
+// reference's own models run on the device (half_gemm: bit-exact chain,
+// gemm: the fp64 chain); any other caller-supplied multiply runs the fixed
+// mode-1 -> 2 -> 3 skeleton (compression.cpp:202-209) on the host.
 Tensor3 comp_with(const Tensor3& t, const Matrix& u, const Matrix& v, const Matrix& w, GemmFn multiply) {
   if (u.cols != t.n1 || v.cols != t.n2 || w.cols != t.n3)
     throw UsageError("comp: compression matrix columns must match tensor dims");
+  if (multiply == &half_gemm) {
+    Tensor3 y(u.rows, v.rows, w.rows);
+    ok(xtsg_comp_half(t.values.data(), t.n1, t.n2, t.n3, u.values.data(), u.rows, v.values.data(), v.rows,
+                      w.values.data(), w.rows, y.values.data()));
+    return y;
+  }
   const Tensor3 s1 = fold(multiply(u, matricize(t, 1)), 1, u.rows, t.n2, t.n3);
   const Tensor3 s2 = fold(multiply(v, matricize(s1, 2)), 2, u.rows, v.rows, t.n3);
   return fold(multiply(w, matricize(s2, 3)), 3, u.rows, v.rows, w.rows);
@@ -500,6 +510,86 @@ Matrix solve_least_squares(const Matrix& a, const Matrix& rhs) {
   Matrix x(a.cols, rhs.cols);
   ok(xtsg_solve_least_squares(a.values.data(), a.rows, a.cols, rhs.values.data(), rhs.cols, x.values.data()));
   return x;
+}
+
+// ---- precision model (mixed.hpp): the reference's mixed.cpp is replaced by
+// device replays that are bit-identical to it (csrc/mixed.cu); the scalar
+// conversions of half.cpp stay the reference's own host code.
+
+SplitValue fp16_split(double x) {
+  SplitValue s;
+  s.half = round_to_half(x);
+  s.residual = x - s.half;
+  return s;
+}
+
+SplitValue fp16_split_stored(double x) {
+  SplitValue s = fp16_split(x);
+  s.residual = std::ldexp(round_to_half(std::ldexp(s.residual, 11)), -11);
+  return s;
+}
+
+namespace {
+
+void split_values(const std::vector<double>& in, int32_t mode, std::vector<double>& half,
+                  std::vector<double>* res) {
+  ok(xtsg_split_half(in.data(), static_cast<int64_t>(in.size()), mode, half.data(),
+                     res ? res->data() : nullptr));
+}
+
+}  // namespace
+
+SplitMatrix split_matrix(const Matrix& m, bool stored_residual) {
+  SplitMatrix out{Matrix(m.rows, m.cols), Matrix(m.rows, m.cols)};
+  split_values(m.values, stored_residual ? XTSG_SPLIT_STORED : XTSG_SPLIT_FULL, out.half.values,
+               &out.residual.values);
+  return out;
+}
+
+SplitTensor3 split_tensor(const Tensor3& t, bool stored_residual) {
+  SplitTensor3 out{Tensor3(t.n1, t.n2, t.n3), Tensor3(t.n1, t.n2, t.n3)};
+  split_values(t.values, stored_residual ? XTSG_SPLIT_STORED : XTSG_SPLIT_FULL, out.half.values,
+               &out.residual.values);
+  return out;
+}
+
+Matrix round_matrix_to_half(const Matrix& m) {
+  Matrix out(m.rows, m.cols);
+  split_values(m.values, XTSG_SPLIT_ROUND, out.values, nullptr);
+  return out;
+}
+
+Tensor3 round_tensor_to_half(const Tensor3& t) {
+  Tensor3 out(t.n1, t.n2, t.n3);
+  split_values(t.values, XTSG_SPLIT_ROUND, out.values, nullptr);
+  return out;
+}
+
+Matrix half_gemm(const Matrix& a, const Matrix& b) {
+  if (a.cols != b.rows) throw UsageError("half_gemm: inner dimensions differ");
+  Matrix out(a.rows, b.cols);
+  ok(xtsg_half_gemm(a.values.data(), a.rows, a.cols, b.values.data(), b.rows, b.cols, out.values.data()));
+  return out;
+}
+
+Tensor3 comp_mixed(const SplitTensor3& t, const SplitMatrix& u, const SplitMatrix& v, const SplitMatrix& w) {
+  if (u.half.cols != t.half.n1 || v.half.cols != t.half.n2 || w.half.cols != t.half.n3)
+    throw UsageError("comp: compression matrix columns must match tensor dims");
+  Tensor3 y(u.half.rows, v.half.rows, w.half.rows);
+  ok(xtsg_comp_mixed(t.half.values.data(), t.residual.values.data(), t.half.n1, t.half.n2, t.half.n3,
+                     u.half.values.data(), u.residual.values.data(), u.half.rows, v.half.values.data(),
+                     v.residual.values.data(), v.half.rows, w.half.values.data(), w.residual.values.data(),
+                     w.half.rows, y.values.data()));
+  return y;
+}
+
+Tensor3 comp_naive_half(const Tensor3& t, const Matrix& u, const Matrix& v, const Matrix& w) {
+  if (u.cols != t.n1 || v.cols != t.n2 || w.cols != t.n3)
+    throw UsageError("comp: compression matrix columns must match tensor dims");
+  Tensor3 y(u.rows, v.rows, w.rows);
+  ok(xtsg_comp_naive_half(t.values.data(), t.n1, t.n2, t.n3, u.values.data(), u.rows, v.values.data(), v.rows,
+                          w.values.data(), w.rows, y.values.data()));
+  return y;
 }
 
 }  // namespace xts

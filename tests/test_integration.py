@@ -54,3 +54,7 @@ def test_reference_acceptance_against_dropin(gpu):
     # unattainable coherence precondition, independent of the compression path
     for crit in (1, 2, 3, 4, 5, 6, 8, 9, 10):
         assert res.get(crit), (crit, r.stdout)
+    # criterion 8 runs comp_mixed / comp_naive_half on the device, bit-exact
+    # with the reference, so the logged ratio is reproduced (test_output.txt:14)
+    m = re.search(r"median error ratio ([0-9.eE+-]+)", r.stdout)
+    assert m and abs(float(m.group(1)) - 0.000253996) < 5e-10, r.stdout

@@ -129,3 +129,30 @@ def test_golden_vectors_match_oracle(restated):
 def _golden_cfgs():
     from tests.golden.make_golden import CONFIGS
     return CONFIGS
+
+
+# ---- precision model (half.cpp / mixed.cpp): restatement pinned bitwise ----
+
+def test_half_bits_restatement_matches_reference(restated, reference):
+    from tests.test_gpu_mixed import TABLE
+    for v, bits in TABLE:                       # test_mixed_precision.cpp:15-48
+        assert restated.half_bits(v) == bits == reference.half_bits(v)
+    rng = np.random.default_rng(42)
+    xs = np.concatenate([rng.standard_normal(1000) * np.exp2(rng.integers(-30, 18, 1000)),
+                         [65519.0, 65520.0, 65536.0, np.nan, np.inf, -1e300, 2.9802322387695312e-08]])
+    for x in xs:
+        assert restated.half_bits(x) == reference.half_bits(x), x
+
+
+def test_comp_mixed_restatement_bitexact(restated, reference):
+    rng = np.random.default_rng(5)
+    t = np.asfortranarray(rng.standard_normal((9, 7, 6)))
+    u, v, w = rng.standard_normal((3, 9)), rng.standard_normal((4, 7)), rng.standard_normal((2, 6))
+    for stored in (False, True):
+        parts = [restated.split(a, 2 if stored else 1) for a in (t, u, v, w)]
+        for a, (h, r) in zip((t, u, v, w), parts):
+            rh, rr = reference.split(a, 2 if stored else 1)
+            assert np.array_equal(h, rh) and np.array_equal(r, rr)
+        assert np.array_equal(restated.comp_mixed(*parts), reference.comp_mixed(t, u, v, w, stored))
+    rounded = [restated.split(a, 0)[0] for a in (t, u, v, w)]
+    assert np.array_equal(restated.comp_half(*rounded), reference.comp_naive_half(t, u, v, w))
