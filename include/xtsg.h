@@ -211,6 +211,18 @@ int32_t xtsg_plan_compress_coo(xtsg_plan* plan, const int32_t* i, const int32_t*
                                const int32_t* k, const float* val, int64_t nnz, void* y,
                                int32_t accumulate, void* stream);
 
+/* Out-of-core .xts source (io.hpp:9-12, io.cpp:55-125).
+ * xts_header reads and validates a file's header: kind 0 dense tensor, 1
+ * factor triple; dims; rank (factors). plan_compress_file compresses the
+ * file's tensor (dims must equal the plan's) straight from disk: dense
+ * payloads stream as mode-3 slabs of ~slab_bytes (0 = 512 MiB) through a
+ * reader thread and a ring of pinned buffers into the plan's H2D/convert/
+ * tensor-core pipeline; factor files generate their slabs on the device.
+ * Malformed / truncated files: XTSG_E_DATA with the reference's messages. */
+int32_t xtsg_xts_header(const char* path, int32_t* kind, int64_t dims[3], int64_t* rank);
+int32_t xtsg_plan_compress_file(xtsg_plan* plan, const char* path, int64_t slab_bytes, void* y,
+                                int32_t accumulate, void* stream);
+
 /* Number of this library's kernels launched by the calling thread so far
  * (evidence for the bench's gpu_launches). */
 int64_t xtsg_launch_count(void);

@@ -210,6 +210,8 @@ class Reference:
             "xref_decompose": (C.c_int, [_P, _P, _P, _P, _I64, _P, _P, _P, _U64, _P, _P, _P, _P]),
             "xref_evaluate": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
             "xref_double_to_half_bits": (C.c_int, [_D, _P]),
+            "xref_write_tensor_file": (C.c_int, [C.c_char_p, _P, _I64, _I64, _I64]),
+            "xref_write_factor_file": (C.c_int, [C.c_char_p, _P, _P, _P, _I64, _I64, _I64, _I64]),
             "xref_split": (C.c_int, [_P, _I64, C.c_int, _P, _P]),
             "xref_half_gemm": (C.c_int, [_P, _I64, _I64, _P, _I64, _P]),
             "xref_comp_half": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
@@ -255,6 +257,15 @@ class Reference:
         self._ok(self.L.xref_comp(_ptr(t), *t.shape, _ptr(u), u.shape[0], _ptr(v), v.shape[0], _ptr(w),
                                   w.shape[0], _ptr(y)), "comp")
         return y
+
+    def write_tensor_file(self, path, t):
+        t = _f(t)
+        self._ok(self.L.xref_write_tensor_file(str(path).encode(), _ptr(t), *t.shape), "write_tensor_file")
+
+    def write_factor_file(self, path, a, b, c):
+        a, b, c = _f(a), _f(b), _f(c)
+        self._ok(self.L.xref_write_factor_file(str(path).encode(), _ptr(a), _ptr(b), _ptr(c), a.shape[0], b.shape[0],
+                                               c.shape[0], a.shape[1]), "write_factor_file")
 
     def half_bits(self, x):
         out = np.zeros(1, np.uint16)

@@ -17,6 +17,7 @@
 #include "xts/cp_als.hpp"
 #include "xts/errors.hpp"
 #include "xts/linalg.hpp"
+#include "xts/io.hpp"
 #include "xts/mixed.hpp"
 #include "xts/half.hpp"
 #include "xts/pipeline.hpp"
@@ -455,6 +456,16 @@ int xref_comp_naive_half(const double* t, int64_t n1, int64_t n2, int64_t n3, co
   return guard([&] {
     put(y, comp_naive_half(ten(t, n1, n2, n3), mat(u, l, n1), mat(v, m, n2), mat(w, n, n3)).values);
   });
+}
+
+// io.cpp:55-89 (fixtures for the out-of-core source tests)
+int xref_write_tensor_file(const char* path, const double* t, int64_t n1, int64_t n2, int64_t n3) {
+  return guard([&] { write_tensor_file(path, ten(t, n1, n2, n3)); });
+}
+
+int xref_write_factor_file(const char* path, const double* a, const double* b, const double* c, int64_t i,
+                           int64_t j, int64_t k, int64_t r) {
+  return guard([&] { write_factor_file(path, FactorTriple(mat(a, i, r), mat(b, j, r), mat(c, k, r))); });
 }
 
 }  // extern "C"

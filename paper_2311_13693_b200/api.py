@@ -346,6 +346,21 @@ class Plan:
                                          1 if accumulate else 0, st))
         return y
 
+    def compress_file(self, path, y=None, accumulate=False, stream=None, device=None, slab_bytes=0):
+        """xtsg_plan_compress_file: compress a .xts file (dense or factor triple) straight from disk."""
+        ydt = np.float64 if self.precision == PREC_FP64 else np.float32
+        if y is None:
+            n = self.count * int(np.prod(self.reduced))
+            if device is None:
+                y = np.zeros(n, ydt)
+            else:
+                import torch
+                y = torch.zeros(n, dtype=torch.float64 if ydt == np.float64 else torch.float32, device=device)
+        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        check(lib.xtsg_plan_compress_file(self._h, str(path).encode(), int(slab_bytes), ptr(y),
+                                          1 if accumulate else 0, st))
+        return y
+
     def set_profiling(self, on: bool = True):
         check(lib.xtsg_plan_set_profiling(self._h, 1 if on else 0))
 
@@ -511,6 +526,15 @@ def apply_recovery(m, perm, scale) -> np.ndarray:
 
 # ---------------------------------------------------------------------------
 # synthetic problems and the end-to-end pipeline (pipeline.hpp)
+
+def xts_header(path):
+    """Header of a .xts file (io.cpp:94-125): (kind 'tensor'|'factors', dims, rank)."""
+    kind = C.c_int32()
+    dims = np.zeros(3, np.int64)
+    rank = C.c_int64()
+    check(lib.xtsg_xts_header(str(path).encode(), C.byref(kind), ptr(dims), C.byref(rank)))
+    return ("tensor" if kind.value == 0 else "factors"), tuple(int(d) for d in dims), int(rank.value)
+
 
 def generate_factors(dims, rank: int, law: str = "dense", nnz_per_col: int = 0, seed: int = 0):
     """generate (pipeline.cpp:176-207) without materialization: the factor triple."""
