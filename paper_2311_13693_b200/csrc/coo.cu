@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
@@ -29,17 +30,18 @@ namespace xtsg {
 namespace {
 
 constexpr int NT = 256;
-constexpr int CHUNK = 256;
 
 __global__ void coo_keys_kernel(const int32_t* __restrict__ jj, const int32_t* __restrict__ kk, int64_t nnz,
-                                int64_t J, uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
-                                int* __restrict__ bad, int64_t I, int64_t K, const int32_t* __restrict__ ii) {
+                                int64_t J, uint64_t* __restrict__ keys, uint64_t* __restrict__ payload,
+                                int* __restrict__ bad, int64_t I, int64_t K, const int32_t* __restrict__ ii,
+                                const float* __restrict__ vv) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t i = ii[e], j = jj[e], k = kk[e];
     if (i < 0 || i >= I || j < 0 || j >= J || k < 0 || k >= K) *bad = 1;
     keys[e] = static_cast<uint64_t>(k) * static_cast<uint64_t>(J) + static_cast<uint64_t>(j);
-    idx[e] = static_cast<uint32_t>(e);
+    // the sort carries (i, value) with the key: no random gather afterwards
+    payload[e] = (static_cast<uint64_t>(static_cast<uint32_t>(i)) << 32) | __float_as_uint(vv[e]);
   }
 }
 
@@ -49,120 +51,173 @@ __global__ void unsorted_kernel(const uint64_t* keys, int64_t nnz, int* flag) {
     if (keys[e] > keys[e + 1]) *flag = 1;
 }
 
-__global__ void coo_gather_kernel(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx,
-                                  const int32_t* __restrict__ ii, const float* __restrict__ vv, int64_t nnz, int64_t J,
-                                  int32_t* __restrict__ oi, int32_t* __restrict__ oj, int32_t* __restrict__ ok,
-                                  float* __restrict__ ov) {
+// sorted (key, payload) -> SoA i, j, k, value (one streaming pass)
+__global__ void coo_unpack_kernel(const uint64_t* __restrict__ skeys, const uint64_t* __restrict__ spay, int64_t nnz,
+                                  int64_t J, int32_t* __restrict__ oi, int32_t* __restrict__ oj,
+                                  int32_t* __restrict__ ok, float* __restrict__ ov) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t key = skeys[e];
-    const uint32_t src = sidx[e];
-    oi[e] = ii[src];
-    ov[e] = vv[src];
+    const uint64_t key = skeys[e], pl = spay[e];
+    oi[e] = static_cast<int32_t>(pl >> 32);
+    ov[e] = __uint_as_float(static_cast<uint32_t>(pl));
     oj[e] = static_cast<int32_t>(key % static_cast<uint64_t>(J));
     ok[e] = static_cast<int32_t>(key / static_cast<uint64_t>(J));
   }
 }
 
-// Ustack [rows_u][ld_u] (row (p,l), i contiguous) -> Ut [I][plpad] (i-major)
-__global__ void transpose_u_kernel(const __nv_bfloat16* __restrict__ u, int64_t rows, int64_t ld, int64_t I,
-                                   __nv_bfloat16* __restrict__ ut) {
+// bf16 [rows][ld] (row-major, cols contiguous) -> [cols][ld_out] (transposed;
+// rows <= ld_out, the caller zero-fills the padding). Builds the i-major U
+// copy Ut[i][(p, l)] and the j-major V copy Vtj[j][(p, m)] of the sparse path.
+__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ u, int64_t rows, int64_t ld, int64_t cols,
+                                      int64_t ld_out, __nv_bfloat16* __restrict__ ut) {
   __shared__ __nv_bfloat16 tile[32][34];
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const int64_t r = r0 + dy, c = c0 + threadIdx.x;
-    tile[dy][threadIdx.x] = (r < rows && c < I) ? u[r * ld + c] : __float2bfloat16(0.f);
+    tile[dy][threadIdx.x] = (r < rows && c < cols) ? u[r * ld + c] : __float2bfloat16(0.f);
   }
   __syncthreads();
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const int64_t c = c0 + dy, r = r0 + threadIdx.x;
-    if (r < rows && c < I) ut[c * rows + r] = tile[threadIdx.x][dy];
+    if (r < rows && c < cols) ut[c * ld_out + r] = tile[threadIdx.x][dy];
   }
 }
 
-// One CTA per slice (persistent). G stacked rows per pass (RPL per lane).
-template <int RPL>
-__global__ void __launch_bounds__(NT) coo_slice_kernel(
+__device__ __forceinline__ void bf16x8(const uint4& raw, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 v = __bfloat1622float2(h[q]);
+    f[2 * q] = v.x;
+    f[2 * q + 1] = v.y;
+  }
+}
+
+// y[q] += x * u[q] for the 8 bf16 of u: sm_100's mixed-precision FMA
+// (fma.rn.f32.bf16 -> FHFMA.BF16, half-select operands), no unpacking.
+__device__ __forceinline__ void fma8(float* y, const uint4& u, uint16_t x) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n fma.rn.f32.bf16 %0, %3, lo, %0;\n"
+        " fma.rn.f32.bf16 %1, %3, hi, %1;\n}"
+        : "+f"(y[2 * q]), "+f"(y[2 * q + 1])
+        : "r"(w[q]), "h"(x));
+}
+
+// Warp-level segmented accumulation over the (k, j)-sorted nonzeros of a
+// slice. A pass covers G = 256*C stacked rows (p, l); lane `lane` owns rows
+// c*256 + lane*8 + t (t < 8) of it, so one nonzero is one 16-byte gather per
+// row group from Ut[i] (the warp reads 512 contiguous bytes) and 8*C fp32
+// FMAs. The 8 warps of a CTA take contiguous eighths of the slice's nonzeros
+// (fibers may straddle: partial fibers simply fold separately) and run
+// UNROLL nonzeros ahead with all gathers in flight before the FMAs. At each
+// fiber change (j) the lane folds its y1 into the slice's Z (Mpad x G, shared
+// memory) with V_p[:, j] from the j-major copy: Z[m][r] += y1[r] * V_p[m, j],
+// shared-memory atomics (warps of the CTA share Z rows), rows skewed by r/8 so
+// the 32 lanes hit 32 banks.
+template <int C>
+__global__ void __launch_bounds__(NT) coo_fiber_kernel(
     const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, const float* __restrict__ cv,
     const int64_t* __restrict__ slice_off, const int32_t* __restrict__ slice_cnt, int64_t n_slices,
-    const __nv_bfloat16* __restrict__ ut, int64_t plrows, const __nv_bfloat16* __restrict__ vt, int64_t ld_v,
-    int mpad, int lpad, int64_t count, float* __restrict__ z) {
-  constexpr int G = NT * RPL;  // stacked rows handled per pass
-  extern __shared__ float zs[];  // G x mpad
-  __shared__ int32_t s_i[CHUNK], s_j[CHUNK];
-  __shared__ float s_v[CHUNK];
+    const __nv_bfloat16* __restrict__ ut, int64_t ld_ut, int64_t plrows, const __nv_bfloat16* __restrict__ vtj,
+    int64_t ld_vtj, int mpad, int lpad, int64_t count, float* __restrict__ z) {
+  constexpr int G = 256 * C, GS = G + G / 8, UNROLL = 8;
+  extern __shared__ float zs[];  // [mpad][GS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = warp * (G / 8) + lane * RPL;  // rows of this lane within the pass
   for (int64_t s = blockIdx.x; s < n_slices; s += gridDim.x) {
-    const int64_t b0 = slice_off[s], b1 = b0 + slice_cnt[s];
+    const int64_t b0 = slice_off[s], n = slice_cnt[s];
+    const int64_t per = (n + 7) / 8;
+    const int64_t w0 = b0 + (warp * per < n ? warp * per : n), w1 = b0 + ((warp + 1) * per < n ? (warp + 1) * per : n);
     for (int64_t g0 = 0; g0 < plrows; g0 += G) {
-      for (int e = threadIdx.x; e < G * mpad; e += NT) zs[e] = 0.f;
-      float y1[RPL];
+      for (int e = threadIdx.x; e < mpad * GS; e += NT) zs[e] = 0.f;
+      __syncthreads();
+      float y1[C][8];
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) y1[q] = 0.f;
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) y1[c][t] = 0.f;
       int32_t cur_j = -1;
       auto flush = [&]() {
-        if (cur_j < 0) return;
+        if (cur_j >= 0) {
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-          const int64_t gr = g0 + row0 + q;
-          if (gr < plrows && y1[q] != 0.f) {
-            const int64_t p = gr / lpad;
-            const __nv_bfloat16* vcol = vt + (p * mpad) * ld_v + cur_j;
-            float* zr = zs + (row0 + q) * mpad;
-            for (int m = 0; m < mpad; ++m) zr[m] = fmaf(y1[q], __bfloat162float(vcol[m * ld_v]), zr[m]);
-          }
-          y1[q] = 0.f;
-        }
-      };
-      __syncthreads();
-      for (int64_t c0 = b0; c0 < b1; c0 += CHUNK) {
-        const int n = static_cast<int>(b1 - c0 < CHUNK ? b1 - c0 : CHUNK);
-        if (threadIdx.x < n) {
-          s_i[threadIdx.x] = ci[c0 + threadIdx.x];
-          s_j[threadIdx.x] = cj[c0 + threadIdx.x];
-          s_v[threadIdx.x] = cv[c0 + threadIdx.x];
-        }
-        __syncthreads();
-        for (int e = 0; e < n; ++e) {
-          const int32_t j = s_j[e];
-          if (j != cur_j) {
-            flush();
-            cur_j = j;
-          }
-          const float x = s_v[e];
-          const __nv_bfloat16* ucol = ut + static_cast<int64_t>(s_i[e]) * plrows + g0 + row0;
-          if (g0 + row0 + RPL <= plrows) {
-            if constexpr (RPL == 4) {
-              const uint2 raw = *reinterpret_cast<const uint2*>(ucol);
-              const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
-              const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
-              y1[0] = fmaf(x, __low2float(a), y1[0]);
-              y1[1] = fmaf(x, __high2float(a), y1[1]);
-              y1[2] = fmaf(x, __low2float(b), y1[2]);
-              y1[3] = fmaf(x, __high2float(b), y1[3]);
-            } else {
+          for (int c = 0; c < C; ++c) {
+            const int rl = c * 256 + lane * 8;  // local row of t = 0
+            const int64_t rg = g0 + rl;
+            if (rg < plrows) {
+              const int64_t p = rg / lpad;
+              const __nv_bfloat16* vrow = vtj + static_cast<int64_t>(cur_j) * ld_vtj + p * mpad;
+              float* zr = zs + rl + rl / 8;
+              for (int m0 = 0; m0 < mpad; m0 += 8) {
+                float v[8];
+                bf16x8(*reinterpret_cast<const uint4*>(vrow + m0), v);
 #pragma unroll
-              for (int q = 0; q < RPL; ++q) y1[q] = fmaf(x, __bfloat162float(ucol[q]), y1[q]);
+                for (int mm = 0; mm < 8; ++mm)
+#pragma unroll
+                  for (int t = 0; t < 8; ++t) atomicAdd(zr + (m0 + mm) * GS + t, y1[c][t] * v[mm]);
+              }
             }
-          } else {
-#pragma unroll
-            for (int q = 0; q < RPL; ++q)
-              if (g0 + row0 + q < plrows) y1[q] = fmaf(x, __bfloat162float(ucol[q]), y1[q]);
           }
         }
-        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+#pragma unroll
+          for (int t = 0; t < 8; ++t) y1[c][t] = 0.f;
+      };
+      const __nv_bfloat16* ubase = ut + g0 + lane * 8;
+      for (int64_t e0 = w0; e0 < w1; e0 += UNROLL) {
+        // lanes < UNROLL fetch one nonzero each; the value is rounded to bf16
+        // (the dense path's X precision) for the mixed bf16 x bf16 + f32 FMA
+        int32_t li = 0, lj = -2;
+        uint32_t lx = 0;
+        if (lane < UNROLL && e0 + lane < w1) {
+          li = __ldg(ci + e0 + lane);
+          lj = __ldg(cj + e0 + lane);
+          lx = __bfloat16_as_ushort(__float2bfloat16_rn(__ldg(cv + e0 + lane)));
+        }
+        uint4 u[UNROLL][C];
+#pragma unroll
+        for (int t = 0; t < UNROLL; ++t) {
+          const int32_t it = __shfl_sync(0xffffffffu, li, t);
+          const __nv_bfloat16* col = ubase + static_cast<int64_t>(it) * ld_ut;
+#pragma unroll
+          for (int c = 0; c < C; ++c) u[t][c] = __ldg(reinterpret_cast<const uint4*>(col + c * 256));
+        }
+        // common case: the whole batch continues the current fiber
+        const bool same = __all_sync(0xffffffffu, lane >= UNROLL || lj == cur_j || lj == -2);
+        if (same) {
+#pragma unroll
+          for (int t = 0; t < UNROLL; ++t) {
+            const uint16_t xt = static_cast<uint16_t>(__shfl_sync(0xffffffffu, lx, t));
+#pragma unroll
+            for (int c = 0; c < C; ++c) fma8(y1[c], u[t][c], xt);
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < UNROLL; ++t) {
+            const int32_t jt = __shfl_sync(0xffffffffu, lj, t);
+            const uint16_t xt = static_cast<uint16_t>(__shfl_sync(0xffffffffu, lx, t));
+            if (jt != -2) {
+              if (jt != cur_j) {
+                flush();
+                cur_j = jt;
+              }
+#pragma unroll
+              for (int c = 0; c < C; ++c) fma8(y1[c], u[t][c], xt);
+            }
+          }
+        }
       }
       flush();
       __syncthreads();
       // Z[p][s][m][l] for the rows of this pass
       for (int e = threadIdx.x; e < G * mpad; e += NT) {
-        const int r = e / mpad, m = e % mpad;
+        const int m = e / G, r = e % G;
         const int64_t gr = g0 + r;
         if (gr >= plrows) continue;
         const int64_t p = gr / lpad, l = gr % lpad;
         if (p >= count) continue;
-        z[((p * n_slices + s) * mpad + m) * lpad + l] = zs[e];
+        z[((p * n_slices + s) * mpad + m) * lpad + l] = zs[m * GS + r + r / 8];
       }
       __syncthreads();
     }
@@ -190,6 +245,8 @@ __global__ void compact_y2_kernel(const float* __restrict__ ypad, int64_t count,
     y[e] = accumulate ? y[e] + v : v;
   }
 }
+
+int64_t round_up256(int64_t a) { return (a + 255) / 256 * 256; }
 
 int gridn(int64_t work) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * 16))); }
 
@@ -222,20 +279,28 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     return;
   }
   const int64_t plrows = P * lpad;
+  const int64_t ld_ut = round_up256(plrows), ld_vtj = P * mpad;
   if (!ut.ptr) {
-    ut = DevBuf<__nv_bfloat16>(static_cast<size_t>(I * plrows), s);
+    // i-major U (rows padded to 256 with zeros) and j-major V copies
+    ut = DevBuf<__nv_bfloat16>(static_cast<size_t>(I * ld_ut), s);
+    ut.zero();
     dim3 grid(static_cast<unsigned>(ceil_div(I, 32)), static_cast<unsigned>(ceil_div(plrows, 32)));
-    transpose_u_kernel<<<grid, dim3(32, 8), 0, s>>>(ustack.ptr, plrows, ld_u, I, ut.ptr);
+    transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(ustack.ptr, plrows, ld_u, I, ld_ut, ut.ptr);
+    XLAUNCH_CHECK();
+    vtj = DevBuf<__nv_bfloat16>(static_cast<size_t>(J * ld_vtj), s);
+    dim3 gv(static_cast<unsigned>(ceil_div(J, 32)), static_cast<unsigned>(ceil_div(ld_vtj, 32)));
+    transpose_bf16_kernel<<<gv, dim3(32, 8), 0, s>>>(vt.ptr, ld_vtj, ld_v, J, ld_vtj, vtj.ptr);
     XLAUNCH_CHECK();
   }
   InView<int32_t> di(i, static_cast<size_t>(nnz), s), dj(j, static_cast<size_t>(nnz), s), dk(k, static_cast<size_t>(nnz), s);
   InView<float> dv(val, static_cast<size_t>(nnz), s);
   // 1. keys, validation, sortedness
   DevBuf<uint64_t> keys(static_cast<size_t>(nnz), s);
-  DevBuf<uint32_t> idx(static_cast<size_t>(nnz), s);
+  DevBuf<uint64_t> idx(static_cast<size_t>(nnz), s);  // packed (i, value)
   DevBuf<int> flags(2, s);
   flags.zero();
-  coo_keys_kernel<<<gridn(nnz), 256, 0, s>>>(dj.dev, dk.dev, nnz, J, keys.ptr, idx.ptr, flags.ptr, I, K, di.dev);
+  coo_keys_kernel<<<gridn(nnz), 256, 0, s>>>(dj.dev, dk.dev, nnz, J, keys.ptr, idx.ptr, flags.ptr, I, K, di.dev,
+                                             dv.dev);
   XLAUNCH_CHECK();
   unsorted_kernel<<<gridn(nnz), 256, 0, s>>>(keys.ptr, nnz, flags.ptr + 1);
   XLAUNCH_CHECK();
@@ -249,7 +314,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   DevBuf<float> bv;
   if (hf[1]) {
     DevBuf<uint64_t> keys2(static_cast<size_t>(nnz), s);
-    DevBuf<uint32_t> idx2(static_cast<size_t>(nnz), s);
+    DevBuf<uint64_t> idx2(static_cast<size_t>(nnz), s);
     size_t tmp_bytes = 0;
     int end_bit = 1;
     while (end_bit < 64 && (uint64_t(1) << end_bit) < static_cast<uint64_t>(K) * static_cast<uint64_t>(J)) ++end_bit;
@@ -261,8 +326,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     bj = DevBuf<int32_t>(static_cast<size_t>(nnz), s);
     bk = DevBuf<int32_t>(static_cast<size_t>(nnz), s);
     bv = DevBuf<float>(static_cast<size_t>(nnz), s);
-    coo_gather_kernel<<<gridn(nnz), 256, 0, s>>>(keys2.ptr, idx2.ptr, di.dev, dv.dev, nnz, J, bi.ptr, bj.ptr, bk.ptr,
-                                                  bv.ptr);
+    coo_unpack_kernel<<<gridn(nnz), 256, 0, s>>>(keys2.ptr, idx2.ptr, nnz, J, bi.ptr, bj.ptr, bk.ptr, bv.ptr);
     XLAUNCH_CHECK();
     si = bi.ptr; sj = bj.ptr; sk = bk.ptr; sv = bv.ptr;
   }
@@ -290,24 +354,26 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   }
   // 3. fibers -> Z[p][kd][m][l]
   DevBuf<float> z(static_cast<size_t>(P * kd * mpad * lpad), s);
-  const int rpl_max = mpad <= 32 ? 4 : mpad <= 64 ? 2 : 1;
-  int rpl = 1;
-  while (rpl < rpl_max && NT * rpl < plrows) rpl *= 2;
-  const size_t smem = static_cast<size_t>(NT * rpl * mpad) * sizeof(float);
-  const int grid = static_cast<int>(std::min<int64_t>(kd, sm_count() * 2));
-  if (rpl == 4) {
-    XCUDA(cudaFuncSetAttribute(coo_slice_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    coo_slice_kernel<4><<<grid, NT, smem, s>>>(si, sj, sv, off.ptr, cnt.ptr, kd, ut.ptr, plrows, vt.ptr, ld_v,
-                                               static_cast<int>(mpad), static_cast<int>(lpad), P, z.ptr);
-  } else if (rpl == 2) {
-    XCUDA(cudaFuncSetAttribute(coo_slice_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    coo_slice_kernel<2><<<grid, NT, smem, s>>>(si, sj, sv, off.ptr, cnt.ptr, kd, ut.ptr, plrows, vt.ptr, ld_v,
-                                               static_cast<int>(mpad), static_cast<int>(lpad), P, z.ptr);
-  } else {
-    XCUDA(cudaFuncSetAttribute(coo_slice_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    coo_slice_kernel<1><<<grid, NT, smem, s>>>(si, sj, sv, off.ptr, cnt.ptr, kd, ut.ptr, plrows, vt.ptr, ld_v,
-                                               static_cast<int>(mpad), static_cast<int>(lpad), P, z.ptr);
-  }
+  // C groups of 256 rows per pass, Z pass in shared memory (mpad x 1.125*G fp32)
+  static const int cenv = [] {
+    const char* e = std::getenv("XTSG_COO_C");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int cmax = (mpad <= 64 ? 2 : 1) < (cenv > 0 ? cenv : 2) ? (mpad <= 64 ? 2 : 1) : (cenv > 0 ? cenv : 2);
+  const int cg = plrows > 256 ? cmax : 1;
+  const size_t smem = static_cast<size_t>(mpad) * (256 * cg + 32 * cg) * sizeof(float);
+  auto launch = [&](auto kern) {
+    XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 1;
+    XCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    const int grid = static_cast<int>(std::min<int64_t>(kd, static_cast<int64_t>(sm_count()) * std::max(1, per_sm)));
+    kern<<<grid, NT, smem, s>>>(si, sj, sv, off.ptr, cnt.ptr, kd, ut.ptr, ld_ut, plrows, vtj.ptr, ld_vtj,
+                                static_cast<int>(mpad), static_cast<int>(lpad), P, z.ptr);
+  };
+  if (cg == 2)
+    launch(coo_fiber_kernel<2>);
+  else
+    launch(coo_fiber_kernel<1>);
   XLAUNCH_CHECK();
   // 4. mode 3 over the distinct slices
   DevBuf<float> wg(static_cast<size_t>(P * N * kd), s);

@@ -23,7 +23,8 @@ struct Plan {
   DevBuf<float> wf;
   DevBuf<float> zbuf;
   DevBuf<unsigned> sync_ctr;  // lane-barrier counters of the pair TTM kernel
-  DevBuf<__nv_bfloat16> ut;  // i-major U copy for the sparse path (lazy)
+  DevBuf<__nv_bfloat16> ut;   // i-major U copy for the sparse path (lazy)
+  DevBuf<__nv_bfloat16> vtj;  // j-major V copy for the sparse path (lazy)
   int grid_limit = 0;  // testing knob: cap on persistent CTAs (0 = #SMs)
   // Live profiling (xtsg_plan_profile): CUDA events around every fused-TTM
   // and mode-3 launch on the launching stream, plus algorithmic flop counts.
