@@ -384,28 +384,45 @@ void decompose_stages(const xtsg_pipeline_config& cfg, const Resolved& rs, const
   run_stage(met, 1, "decomposition", st, [&] {
     if (cfg.als_max_iters < 1) usage("cp_als: max_iters must be >= 1");
     DevBuf<double> gather;
-    for (int64_t attempt = 0; attempt <= std::max<int64_t>(cfg.als_restarts, 0); ++attempt) {
+    const int64_t last_attempt = std::max<int64_t>(cfg.als_restarts, 0);
+    for (int64_t attempt = 0; attempt <= last_attempt; ++attempt) {
       std::vector<int64_t> pend;
       for (int64_t p = 0; p < P; ++p)
         if (!(have[p] && best_conv[p] && best_err[p] <= cfg.replica_fit_tol)) pend.push_back(p);
       if (pend.empty()) break;
-      const int64_t n = static_cast<int64_t>(pend.size());
+      // Restart rounds are sequential per replica (pipeline.cpp:413-432): the
+      // next attempt runs only if every earlier one failed. Once the pending
+      // replicas' remaining attempts fit the SMs, they all run in ONE batched
+      // launch (speculatively) and the sequential rule is replayed on the
+      // results below — same factors, same survivors, but the failing
+      // replicas' restarts no longer serialise into one round each.
+      const int64_t rounds_left = last_attempt - attempt + 1;
+      const bool all_at_once = rounds_left > 1 && static_cast<int64_t>(pend.size()) * rounds_left <= sm_count();
+      const int64_t span = all_at_once ? rounds_left : 1;
+      std::vector<int64_t> item_p, item_a;
+      for (int64_t a = attempt; a < attempt + span; ++a)
+        for (int64_t p : pend) {
+          item_p.push_back(p);
+          item_a.push_back(a);
+        }
+      const int64_t n = static_cast<int64_t>(item_p.size());
       const double* t = Yd;
       if (n != P) {
-        if (!gather.ptr) gather = DevBuf<double>(static_cast<size_t>(P * lmn), st);
+        if (!gather.ptr || static_cast<int64_t>(gather.n) < n * lmn)
+          gather = DevBuf<double>(static_cast<size_t>(std::max(P, n) * lmn), st);
         for (int64_t q = 0; q < n; ++q)
-          XCUDA(cudaMemcpyAsync(gather.ptr + q * lmn, Yd + pend[q] * lmn, sizeof(double) * lmn,
+          XCUDA(cudaMemcpyAsync(gather.ptr + q * lmn, Yd + item_p[q] * lmn, sizeof(double) * lmn,
                                 cudaMemcpyDeviceToDevice, st));
         t = gather.ptr;
       }
       std::vector<xtsg_als_config> cfgs(static_cast<size_t>(n));
       for (int64_t q = 0; q < n; ++q) {
-        const uint64_t replica_seed = derive(cfg.seed, 500 + static_cast<uint64_t>(pend[q]));
+        const uint64_t replica_seed = derive(cfg.seed, 500 + static_cast<uint64_t>(item_p[q]));
         cfgs[q].rank = R;
         cfgs[q].max_iters = cfg.als_max_iters;
         cfgs[q].tol = cfg.als_tol;
-        cfgs[q].seed = derive(replica_seed, static_cast<uint64_t>(attempt));
-        cfgs[q].init = attempt == 1 ? 1 : 0;
+        cfgs[q].seed = derive(replica_seed, static_cast<uint64_t>(item_a[q]));
+        cfgs[q].init = item_a[q] == 1 ? 1 : 0;
         cfgs[q].reserved = 0;
       }
       std::vector<double> fa(static_cast<size_t>(n * red[0] * R)), fb(static_cast<size_t>(n * red[1] * R)),
@@ -414,8 +431,11 @@ void decompose_stages(const xtsg_pipeline_config& cfg, const Resolved& rs, const
       std::vector<int32_t> conv(static_cast<size_t>(n));
       ck(xtsg_cp_als_batched(n, t, red[0], red[1], red[2], cfgs.data(), fa.data(), fb.data(), fc.data(), iters.data(),
                              conv.data(), hist.data()));
+      // items are attempt-major, so this walk replays each replica's attempts
+      // in order and skips the ones the sequential loop would not have run
       for (int64_t q = 0; q < n; ++q) {
-        const int64_t p = pend[q];
+        const int64_t p = item_p[q];
+        if (have[p] && best_conv[p] && best_err[p] <= cfg.replica_fit_tol) continue;
         sweeps += iters[q];
         const double err = iters[q] > 0 ? hist[q * cfg.als_max_iters + iters[q] - 1] : 1.0;
         if (!have[p] || err < best_err[p]) {
@@ -429,6 +449,7 @@ void decompose_stages(const xtsg_pipeline_config& cfg, const Resolved& rs, const
           have[p] = 1;
         }
       }
+      attempt += span - 1;
     }
     for (int64_t p = 0; p < P; ++p)
       if (best_conv[p] && best_err[p] <= cfg.replica_fit_tol) {
