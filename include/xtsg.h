@@ -368,6 +368,25 @@ int32_t xtsg_decompose_replicas(const xtsg_pipeline_config* cfg, const int64_t d
                                 int64_t factor_rank, double* a_out, double* b_out, double* c_out,
                                 xtsg_pipeline_metrics* metrics);
 
+/* decompose split at the stage-1 boundary, for multi-GPU pipelines that
+ * spread the per-replica CP-ALS over ranks (SURVEY §8 e).
+ * stage1: stage 1 (pipeline.cpp:410-446) for n replicas (L x M x N back to
+ * back, f32/f64, host or device) whose global indices are ids[n] (restart
+ * seeds derive(derive(cfg.seed, 500 + id), attempt)); per replica: the best
+ * attempt's factors (per_f = (L + M + N) * rank doubles: A, then B, then C,
+ * column-major), its relative fit error, its convergence flag and the sweeps
+ * of every attempt the reference's sequential restart loop runs.
+ * finish: stages 1 (survivor rule) - 3 on those results for all `replicas`
+ * replicas in index order; identical output to xtsg_decompose_replicas. */
+int32_t xtsg_decompose_stage1(const xtsg_pipeline_config* cfg, const int64_t dims[3], int64_t n,
+                              const int64_t* ids, const void* replicas, int32_t replicas_dtype,
+                              double* factors, double* fit_err, int32_t* converged, int64_t* sweeps);
+int32_t xtsg_decompose_finish(const xtsg_pipeline_config* cfg, const int64_t dims[3], const double* factors,
+                              const double* fit_err, const int32_t* converged, const int64_t* sweeps,
+                              const double* tensor, const double* fa, const double* fb, const double* fc,
+                              int64_t factor_rank, double* a_out, double* b_out, double* c_out,
+                              xtsg_pipeline_metrics* metrics);
+
 /* evaluate (pipeline.cpp:577-609): joint permutation/scale against the truth,
  * per-mode relative errors, leading-corner sample MSE. aligned_* optional. */
 int32_t xtsg_evaluate(const int64_t dims[3], int64_t rank, const double* ta, const double* tb,

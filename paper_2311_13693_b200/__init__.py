@@ -27,7 +27,8 @@ from .api import (  # noqa: F401
     comp_naive_half, comp_blocked, Plan, launch_count, device_ready,
     cp_als, cp_als_batched, relative_error, normalize_shared, max_trace_assignment,
     align_replicas, solve_stacked_ls, recover_perm_scale, apply_forward, apply_recovery,
-    generate_factors, xts_header, PipelineConfig, RunMetrics, decompose, decompose_replicas, evaluate, EvalReport,
+    generate_factors, xts_header, PipelineConfig, RunMetrics, decompose, decompose_replicas, decompose_stage1,
+    decompose_finish, Stage1Result, evaluate, EvalReport,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

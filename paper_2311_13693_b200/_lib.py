@@ -151,6 +151,8 @@ _SIGS = {
     "xtsg_generate_factors": (_I32, [_P, _I64, _I32, _I64, _U64, _P, _P, _P]),
     "xtsg_decompose": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "xtsg_decompose_replicas": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
+    "xtsg_decompose_stage1": (_I32, [_P, _P, _I64, _P, _P, _I32, _P, _P, _P, _P]),
+    "xtsg_decompose_finish": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "xtsg_evaluate": (_I32, [_P, _I64, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
 }
 

@@ -659,6 +659,59 @@ def decompose_replicas(cfg: PipelineConfig, replicas, tensor=None, factors=None)
     return tuple(outs), _metrics(met)
 
 
+def _replicas_arg(replicas):
+    if isinstance(replicas, np.ndarray):
+        if replicas.dtype not in (np.float32, np.float64):
+            raise TypeError("replicas must be float32/float64")
+        y = np.ascontiguousarray(replicas)
+        return y, (DTYPE_F64 if y.dtype == np.float64 else DTYPE_F32)
+    y = replicas.contiguous()
+    return y, _torch_dtype_code(y)
+
+
+@dataclass
+class Stage1Result:
+    """Per-replica stage-1 results (xtsg_decompose_stage1): factors (n, (L+M+N)*R),
+    fit errors, convergence flags, sweeps — the exchange unit of a multi-GPU pipeline."""
+    ids: np.ndarray
+    factors: np.ndarray
+    fit_err: np.ndarray
+    converged: np.ndarray
+    sweeps: np.ndarray
+
+
+def decompose_stage1(cfg: PipelineConfig, dims, replicas, ids) -> Stage1Result:
+    """Stage 1 of decompose (pipeline.cpp:410-446) for the replicas with global indices ``ids``
+    (``replicas``: len(ids) replicas back to back)."""
+    d = _arr3(dims)
+    ids = np.ascontiguousarray(np.asarray(ids, np.int64))
+    n = int(ids.size)
+    per_f = int(sum(cfg.reduced)) * int(cfg.rank)
+    out = Stage1Result(ids, np.zeros((n, per_f)), np.ones(n), np.zeros(n, np.int32), np.zeros(n, np.int64))
+    y, code = _replicas_arg(replicas)
+    c = cfg.to_c()
+    check(lib.xtsg_decompose_stage1(C.byref(c), ptr(d), n, ptr(ids), ptr(y), code, ptr(out.factors),
+                                    ptr(out.fit_err), ptr(out.converged), ptr(out.sweeps)))
+    return out
+
+
+def decompose_finish(cfg: PipelineConfig, stage1: Stage1Result, tensor=None, factors=None):
+    """Stages 1 (survivor rule) - 3 from the stage-1 results of all replicas (any order of ids)."""
+    t, dims, f, frank = _source(tensor, factors)
+    d = _arr3(dims)
+    order = np.argsort(stage1.ids, kind="stable")
+    fac = np.ascontiguousarray(stage1.factors[order])
+    err = np.ascontiguousarray(stage1.fit_err[order])
+    conv = np.ascontiguousarray(stage1.converged[order].astype(np.int32))
+    sw = np.ascontiguousarray(stage1.sweeps[order].astype(np.int64))
+    outs = [np.zeros((int(d[m]), int(cfg.rank)), order="F") for m in range(3)]
+    met = PipelineMetricsC()
+    c = cfg.to_c()
+    check(lib.xtsg_decompose_finish(C.byref(c), ptr(d), ptr(fac), ptr(err), ptr(conv), ptr(sw), ptr(t),
+                                    *[ptr(x) for x in f], int(frank), *[ptr(o) for o in outs], C.byref(met)))
+    return tuple(outs), _metrics(met)
+
+
 @dataclass
 class EvalReport:
     mode_rel_err: list

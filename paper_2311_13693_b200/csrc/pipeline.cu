@@ -365,97 +365,133 @@ void run_stage(xtsg_pipeline_metrics* met, int idx, const char* name, cudaStream
   done(1);
 }
 
-// Stages 1-3 of decompose (pipeline.cpp:410-572) on device-resident fp64 replicas.
-void decompose_stages(const xtsg_pipeline_config& cfg, const Resolved& rs, const EnsembleDev& ens, const double* Yd,
-                      const Source& src, double* a_out, double* b_out, double* c_out, xtsg_pipeline_metrics* met,
-                      cudaStream_t st) {
-  const int64_t P = rs.replicas, R = rs.rank;
+// Stage-1 result of one replica: the best attempt's factors (A | B | C,
+// column-major) and its fit error / convergence, plus the sweeps of every
+// attempt the reference's sequential restart loop would have run.
+struct Stage1Out {
+  std::vector<double> f;
+  double err = 1.0;
+  int32_t conv = 0, have = 0;
+  int64_t sweeps = 0;
+};
+
+// Stage 1 of decompose (pipeline.cpp:410-446) for n replicas with global
+// indices ids[q] (seeds derive(cfg.seed, 500 + ids[q])), fp64 on the device
+// back to back at Yd. Restart rounds run batched; once the pending replicas'
+// remaining attempts fit the SMs they all run in ONE launch (speculatively)
+// and the sequential rule is replayed on the results: same factors, errors
+// and sweep counts as the reference's per-replica loop.
+std::vector<Stage1Out> run_stage1(const xtsg_pipeline_config& cfg, const Resolved& rs, int64_t n_rep,
+                                  const int64_t* ids, const double* Yd, cudaStream_t st) {
+  const int64_t R = rs.rank;
   const int64_t* red = rs.reduced;
   const int64_t lmn = red[0] * red[1] * red[2];
   const int64_t per_f = (red[0] + red[1] + red[2]) * R;
+  if (cfg.als_max_iters < 1) usage("cp_als: max_iters must be >= 1");
+  std::vector<Stage1Out> out(static_cast<size_t>(n_rep));
+  auto done = [&](int64_t q) {
+    const Stage1Out& o = out[static_cast<size_t>(q)];
+    return o.have && o.conv && o.err <= cfg.replica_fit_tol;
+  };
+  DevBuf<double> gather;
+  const int64_t last_attempt = std::max<int64_t>(cfg.als_restarts, 0);
+  for (int64_t attempt = 0; attempt <= last_attempt; ++attempt) {
+    std::vector<int64_t> pend;
+    for (int64_t q = 0; q < n_rep; ++q)
+      if (!done(q)) pend.push_back(q);
+    if (pend.empty()) break;
+    const int64_t rounds_left = last_attempt - attempt + 1;
+    const bool all_at_once = rounds_left > 1 && static_cast<int64_t>(pend.size()) * rounds_left <= sm_count();
+    const int64_t span = all_at_once ? rounds_left : 1;
+    std::vector<int64_t> item_q, item_a;
+    for (int64_t a = attempt; a < attempt + span; ++a)
+      for (int64_t q : pend) {
+        item_q.push_back(q);
+        item_a.push_back(a);
+      }
+    const int64_t n = static_cast<int64_t>(item_q.size());
+    const double* t = Yd;
+    bool identity = n == n_rep;
+    for (int64_t k = 0; identity && k < n; ++k) identity = item_q[k] == k;
+    if (!identity) {
+      if (!gather.ptr || static_cast<int64_t>(gather.n) < n * lmn)
+        gather = DevBuf<double>(static_cast<size_t>(std::max(n_rep, n) * lmn), st);
+      for (int64_t k = 0; k < n; ++k)
+        XCUDA(cudaMemcpyAsync(gather.ptr + k * lmn, Yd + item_q[k] * lmn, sizeof(double) * lmn,
+                              cudaMemcpyDeviceToDevice, st));
+      t = gather.ptr;
+    }
+    std::vector<xtsg_als_config> cfgs(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) {
+      const uint64_t replica_seed = derive(cfg.seed, 500 + static_cast<uint64_t>(ids[item_q[k]]));
+      cfgs[k].rank = R;
+      cfgs[k].max_iters = cfg.als_max_iters;
+      cfgs[k].tol = cfg.als_tol;
+      cfgs[k].seed = derive(replica_seed, static_cast<uint64_t>(item_a[k]));
+      cfgs[k].init = item_a[k] == 1 ? 1 : 0;
+      cfgs[k].reserved = 0;
+    }
+    std::vector<double> fa(static_cast<size_t>(n * red[0] * R)), fb(static_cast<size_t>(n * red[1] * R)),
+        fc(static_cast<size_t>(n * red[2] * R)), hist(static_cast<size_t>(n * cfg.als_max_iters));
+    std::vector<int64_t> iters(static_cast<size_t>(n));
+    std::vector<int32_t> conv(static_cast<size_t>(n));
+    ck(xtsg_cp_als_batched(n, t, red[0], red[1], red[2], cfgs.data(), fa.data(), fb.data(), fc.data(), iters.data(),
+                           conv.data(), hist.data()));
+    // items are attempt-major: this walk replays each replica's attempts in
+    // order and skips the ones the sequential loop would not have run
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t q = item_q[k];
+      if (done(q)) continue;
+      Stage1Out& o = out[static_cast<size_t>(q)];
+      o.sweeps += iters[k];
+      const double err = iters[k] > 0 ? hist[k * cfg.als_max_iters + iters[k] - 1] : 1.0;
+      if (!o.have || err < o.err) {
+        o.f.resize(static_cast<size_t>(per_f));
+        std::copy_n(fa.data() + k * red[0] * R, red[0] * R, o.f.data());
+        std::copy_n(fb.data() + k * red[1] * R, red[1] * R, o.f.data() + red[0] * R);
+        std::copy_n(fc.data() + k * red[2] * R, red[2] * R, o.f.data() + (red[0] + red[1]) * R);
+        o.err = err;
+        o.conv = conv[k] != 0;
+        o.have = 1;
+      }
+    }
+    attempt += span - 1;
+  }
+  return out;
+}
+
+// Stages 1-3 of decompose (pipeline.cpp:410-572) on device-resident fp64
+// replicas (Yd, all P of them), or — when `pre` is given — stages 2-3 on the
+// stage-1 results of all P replicas computed elsewhere (multi-GPU: each rank
+// ran stage 1 on its share of the replicas).
+void decompose_stages(const xtsg_pipeline_config& cfg, const Resolved& rs, const EnsembleDev& ens, const double* Yd,
+                      const Source& src, double* a_out, double* b_out, double* c_out, xtsg_pipeline_metrics* met,
+                      cudaStream_t st, const std::vector<Stage1Out>* pre = nullptr) {
+  const int64_t P = rs.replicas, R = rs.rank;
+  const int64_t* red = rs.reduced;
+  const int64_t per_f = (red[0] + red[1] + red[2]) * R;
 
   // ---- stage 1: decomposition (pipeline.cpp:410-446) ----------------------
-  std::vector<std::vector<double>> best(static_cast<size_t>(P));
-  std::vector<double> best_err(static_cast<size_t>(P), 1.0);
-  std::vector<char> have(static_cast<size_t>(P), 0), best_conv(static_cast<size_t>(P), 0);
   std::vector<double> flat_surv;
   std::vector<int64_t> decomp_survivors;
   int64_t sweeps = 0;
   run_stage(met, 1, "decomposition", st, [&] {
-    if (cfg.als_max_iters < 1) usage("cp_als: max_iters must be >= 1");
-    DevBuf<double> gather;
-    const int64_t last_attempt = std::max<int64_t>(cfg.als_restarts, 0);
-    for (int64_t attempt = 0; attempt <= last_attempt; ++attempt) {
-      std::vector<int64_t> pend;
-      for (int64_t p = 0; p < P; ++p)
-        if (!(have[p] && best_conv[p] && best_err[p] <= cfg.replica_fit_tol)) pend.push_back(p);
-      if (pend.empty()) break;
-      // Restart rounds are sequential per replica (pipeline.cpp:413-432): the
-      // next attempt runs only if every earlier one failed. Once the pending
-      // replicas' remaining attempts fit the SMs, they all run in ONE batched
-      // launch (speculatively) and the sequential rule is replayed on the
-      // results below — same factors, same survivors, but the failing
-      // replicas' restarts no longer serialise into one round each.
-      const int64_t rounds_left = last_attempt - attempt + 1;
-      const bool all_at_once = rounds_left > 1 && static_cast<int64_t>(pend.size()) * rounds_left <= sm_count();
-      const int64_t span = all_at_once ? rounds_left : 1;
-      std::vector<int64_t> item_p, item_a;
-      for (int64_t a = attempt; a < attempt + span; ++a)
-        for (int64_t p : pend) {
-          item_p.push_back(p);
-          item_a.push_back(a);
-        }
-      const int64_t n = static_cast<int64_t>(item_p.size());
-      const double* t = Yd;
-      if (n != P) {
-        if (!gather.ptr || static_cast<int64_t>(gather.n) < n * lmn)
-          gather = DevBuf<double>(static_cast<size_t>(std::max(P, n) * lmn), st);
-        for (int64_t q = 0; q < n; ++q)
-          XCUDA(cudaMemcpyAsync(gather.ptr + q * lmn, Yd + item_p[q] * lmn, sizeof(double) * lmn,
-                                cudaMemcpyDeviceToDevice, st));
-        t = gather.ptr;
-      }
-      std::vector<xtsg_als_config> cfgs(static_cast<size_t>(n));
-      for (int64_t q = 0; q < n; ++q) {
-        const uint64_t replica_seed = derive(cfg.seed, 500 + static_cast<uint64_t>(item_p[q]));
-        cfgs[q].rank = R;
-        cfgs[q].max_iters = cfg.als_max_iters;
-        cfgs[q].tol = cfg.als_tol;
-        cfgs[q].seed = derive(replica_seed, static_cast<uint64_t>(item_a[q]));
-        cfgs[q].init = item_a[q] == 1 ? 1 : 0;
-        cfgs[q].reserved = 0;
-      }
-      std::vector<double> fa(static_cast<size_t>(n * red[0] * R)), fb(static_cast<size_t>(n * red[1] * R)),
-          fc(static_cast<size_t>(n * red[2] * R)), hist(static_cast<size_t>(n * cfg.als_max_iters));
-      std::vector<int64_t> iters(static_cast<size_t>(n));
-      std::vector<int32_t> conv(static_cast<size_t>(n));
-      ck(xtsg_cp_als_batched(n, t, red[0], red[1], red[2], cfgs.data(), fa.data(), fb.data(), fc.data(), iters.data(),
-                             conv.data(), hist.data()));
-      // items are attempt-major, so this walk replays each replica's attempts
-      // in order and skips the ones the sequential loop would not have run
-      for (int64_t q = 0; q < n; ++q) {
-        const int64_t p = item_p[q];
-        if (have[p] && best_conv[p] && best_err[p] <= cfg.replica_fit_tol) continue;
-        sweeps += iters[q];
-        const double err = iters[q] > 0 ? hist[q * cfg.als_max_iters + iters[q] - 1] : 1.0;
-        if (!have[p] || err < best_err[p]) {
-          auto& b = best[p];
-          b.resize(static_cast<size_t>(per_f));
-          std::copy_n(fa.data() + q * red[0] * R, red[0] * R, b.data());
-          std::copy_n(fb.data() + q * red[1] * R, red[1] * R, b.data() + red[0] * R);
-          std::copy_n(fc.data() + q * red[2] * R, red[2] * R, b.data() + (red[0] + red[1]) * R);
-          best_err[p] = err;
-          best_conv[p] = conv[q] != 0;
-          have[p] = 1;
-        }
-      }
-      attempt += span - 1;
+    std::vector<Stage1Out> res;
+    if (pre) {
+      res = *pre;
+    } else {
+      std::vector<int64_t> ids(static_cast<size_t>(P));
+      for (int64_t p = 0; p < P; ++p) ids[p] = p;
+      res = run_stage1(cfg, rs, P, ids.data(), Yd, st);
     }
-    for (int64_t p = 0; p < P; ++p)
-      if (best_conv[p] && best_err[p] <= cfg.replica_fit_tol) {
-        flat_surv.insert(flat_surv.end(), best[p].begin(), best[p].end());
+    for (int64_t p = 0; p < P; ++p) {
+      const Stage1Out& o = res[static_cast<size_t>(p)];
+      sweeps += o.sweeps;
+      if (o.have && o.conv && o.err <= cfg.replica_fit_tol) {
+        flat_surv.insert(flat_surv.end(), o.f.begin(), o.f.end());
         decomp_survivors.push_back(p);
       }
+    }
     if (decomp_survivors.empty())
       throw Status(XTSG_E_INSUFFICIENT, "decompose: every replica failed to fit", 0, rs.min_survivors);
   });
@@ -553,27 +589,38 @@ void decompose_stages(const xtsg_pipeline_config& cfg, const Resolved& rs, const
     std::vector<double> bbest[3];
     double bbest_err = 1.0;
     bool have_block = false;
-    for (int attempt = 0; attempt < 3; ++attempt) {
-      xtsg_als_config als{};
-      als.rank = R;
-      als.max_iters = cfg.als_max_iters;
-      als.tol = cfg.als_tol;
-      als.seed = derive(cfg.seed, 31 + static_cast<uint64_t>(attempt));
-      als.init = attempt == 1 ? 1 : 0;
-      std::vector<double> f[3];
-      for (int m = 0; m < 3; ++m) f[m].resize(static_cast<size_t>(bn[m] * R));
-      std::vector<double> hist(static_cast<size_t>(cfg.als_max_iters));
-      int64_t it = 0;
-      int32_t conv = 0;
-      ck(xtsg_cp_als_batched(1, block.data(), bn[0], bn[1], bn[2], &als, f[0].data(), f[1].data(), f[2].data(), &it,
-                             &conv, hist.data()));
-      const double err = it > 0 ? hist[it - 1] : 1.0;
-      if (!have_block || err < bbest_err) {
-        for (int m = 0; m < 3; ++m) bbest[m] = std::move(f[m]);
-        bbest_err = err;
-        have_block = true;
+    {
+      // the sampled block's 3 attempts (pipeline.cpp:524-537) run in one
+      // batched launch; the sequential rule (keep the best, stop once it
+      // fits to 1e-6) is replayed on the results in attempt order
+      const int64_t bsz = bn[0] * bn[1] * bn[2];
+      std::vector<double> blocks(static_cast<size_t>(3 * bsz));
+      for (int q = 0; q < 3; ++q) std::copy(block.begin(), block.end(), blocks.begin() + q * bsz);
+      xtsg_als_config als[3] = {};
+      for (int q = 0; q < 3; ++q) {
+        als[q].rank = R;
+        als[q].max_iters = cfg.als_max_iters;
+        als[q].tol = cfg.als_tol;
+        als[q].seed = derive(cfg.seed, 31 + static_cast<uint64_t>(q));
+        als[q].init = q == 1 ? 1 : 0;
       }
-      if (bbest_err <= 1e-6) break;
+      std::vector<double> f[3];
+      for (int m = 0; m < 3; ++m) f[m].resize(static_cast<size_t>(3 * bn[m] * R));
+      std::vector<double> hist(static_cast<size_t>(3 * cfg.als_max_iters));
+      int64_t it[3] = {0, 0, 0};
+      int32_t conv[3] = {0, 0, 0};
+      ck(xtsg_cp_als_batched(3, blocks.data(), bn[0], bn[1], bn[2], als, f[0].data(), f[1].data(), f[2].data(), it,
+                             conv, hist.data()));
+      for (int q = 0; q < 3; ++q) {
+        const double err = it[q] > 0 ? hist[q * cfg.als_max_iters + it[q] - 1] : 1.0;
+        if (!have_block || err < bbest_err) {
+          for (int m = 0; m < 3; ++m)
+            bbest[m].assign(f[m].begin() + q * bn[m] * R, f[m].begin() + (q + 1) * bn[m] * R);
+          bbest_err = err;
+          have_block = true;
+        }
+        if (bbest_err <= 1e-6) break;
+      }
     }
     if (met) met->block_fit = bbest_err;
     std::vector<double> heads[3];
@@ -661,6 +708,84 @@ int32_t xtsg_generate_factors(const int64_t dims[3], int64_t rank, int32_t law, 
       else
         std::copy(f.begin(), f.end(), outs[m]);
     }
+  });
+}
+
+namespace {
+
+// replicas (host or device, f32 or f64) -> device fp64
+const double* replicas_f64(const void* replicas, int32_t dtype, int64_t n, DevBuf<double>& keep, cudaStream_t st) {
+  if (dtype == XTSG_DTYPE_F64) {
+    InView<double> v(static_cast<const double*>(replicas), static_cast<size_t>(n), st);
+    if (v.tmp.ptr) {
+      keep = std::move(v.tmp);
+      return keep.ptr;
+    }
+    return v.dev;
+  }
+  if (dtype == XTSG_DTYPE_F32) {
+    InView<float> v(static_cast<const float*>(replicas), static_cast<size_t>(n), st);
+    keep = DevBuf<double>(static_cast<size_t>(n), st);
+    widen_kernel<<<static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 148 * 16)), 256, 0, st>>>(v.dev, n, keep.ptr);
+    XLAUNCH_CHECK();
+    return keep.ptr;
+  }
+  usage("decompose: replicas must be f32 or f64");
+}
+
+}  // namespace
+
+int32_t xtsg_decompose_stage1(const xtsg_pipeline_config* cfg, const int64_t dims[3], int64_t n, const int64_t* ids,
+                              const void* replicas, int32_t replicas_dtype, double* factors, double* fit_err,
+                              int32_t* converged, int64_t* sweeps) {
+  return guard([&] {
+    const Resolved rs = resolve(*cfg, dims);
+    if (n < 0) usage("decompose_stage1: negative replica count");
+    for (int64_t q = 0; q < n; ++q)
+      if (ids[q] < 0 || ids[q] >= rs.replicas) usage("decompose_stage1: replica index outside [0, replicas)");
+    if (n == 0) return;
+    require_device();
+    cudaStream_t st = thread_stream();
+    const int64_t lmn = rs.reduced[0] * rs.reduced[1] * rs.reduced[2];
+    const int64_t per_f = (rs.reduced[0] + rs.reduced[1] + rs.reduced[2]) * rs.rank;
+    DevBuf<double> keep;
+    const double* y = replicas_f64(replicas, replicas_dtype, n * lmn, keep, st);
+    const std::vector<Stage1Out> res = run_stage1(*cfg, rs, n, ids, y, st);
+    for (int64_t q = 0; q < n; ++q) {
+      const Stage1Out& o = res[static_cast<size_t>(q)];
+      if (o.have) std::copy(o.f.begin(), o.f.end(), factors + q * per_f);
+      else std::fill_n(factors + q * per_f, per_f, 0.0);
+      fit_err[q] = o.err;
+      converged[q] = o.have && o.conv ? 1 : 0;
+      sweeps[q] = o.sweeps;
+    }
+  });
+}
+
+int32_t xtsg_decompose_finish(const xtsg_pipeline_config* cfg, const int64_t dims[3], const double* factors,
+                              const double* fit_err, const int32_t* converged, const int64_t* sweeps,
+                              const double* tensor, const double* fa, const double* fb, const double* fc,
+                              int64_t factor_rank, double* a_out, double* b_out, double* c_out,
+                              xtsg_pipeline_metrics* metrics) {
+  return guard([&] {
+    if (metrics) *metrics = xtsg_pipeline_metrics{};
+    const Resolved rs = resolve(*cfg, dims);
+    require_device();
+    cudaStream_t st = thread_stream();
+    const Source src = make_source(dims, tensor, fa, fb, fc, factor_rank, st);
+    EnsembleDev ens;
+    make_ensemble_dev(rs, ens, st);
+    const int64_t per_f = (rs.reduced[0] + rs.reduced[1] + rs.reduced[2]) * rs.rank;
+    std::vector<Stage1Out> pre(static_cast<size_t>(rs.replicas));
+    for (int64_t p = 0; p < rs.replicas; ++p) {
+      Stage1Out& o = pre[static_cast<size_t>(p)];
+      o.f.assign(factors + p * per_f, factors + (p + 1) * per_f);
+      o.err = fit_err[p];
+      o.conv = converged[p];
+      o.have = 1;
+      o.sweeps = sweeps[p];
+    }
+    decompose_stages(*cfg, rs, ens, nullptr, src, a_out, b_out, c_out, metrics, st, &pre);
   });
 }
 

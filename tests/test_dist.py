@@ -96,3 +96,70 @@ def test_gloo_world2_sharded_pipeline():
     out = mgr.dict()
     mp.spawn(_pipeline_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     assert out[0] == (0.0, True) and out[1] == (0.0, False)
+
+
+def test_replica_ranges_partition():
+    from paper_2311_13693_b200.dist import replica_range
+    for P in (1, 5, 124, 128):
+        for world in (1, 2, 3, 8):
+            spans = [replica_range(P, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == P
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def _distributed_worker(rank, world, port, out):
+    # host logic of the ALS-sharded pipeline: slab compression (oracle
+    # stand-in), reduce-scatter of the replicas, stage 1 per rank on its own
+    # replicas (stand-in: a deterministic function of the replica and its id),
+    # gather of the per-replica results on rank 0, finish there, broadcast
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2311_13693_b200.api import Stage1Result
+    from paper_2311_13693_b200.dist import decompose_distributed
+    from oracle.oracle import Restated
+    ora = Restated()
+    dims, red, P, S, seed = (12, 10, 9), (4, 3, 3), 5, 2, 5
+    lmn = int(np.prod(red))
+    ens = ora.make_ensemble(dims, red, P, S, seed=seed)
+    t = np.asfortranarray(np.random.default_rng(3).standard_normal(dims))
+    full = [ora.comp(t, ens[0][p], ens[1][p], ens[2][p]).ravel(order="F") for p in range(P)]
+    per = -(-P // world)
+
+    def local(k0, k1, y):
+        y.zero_()
+        for p in range(P):
+            part = ora.comp(np.asfortranarray(t[:, :, k0:k1]), ens[0][p], ens[1][p], ens[2][p][:, k0:k1])
+            y[p * lmn:(p + 1) * lmn] = torch.from_numpy(part.ravel(order="F"))
+
+    seen = {}
+
+    def stage1(reps, ids):
+        reps = reps.numpy().reshape(len(ids), lmn)
+        for q, p in enumerate(ids):
+            seen[int(p)] = float(np.abs(reps[q] - full[p]).max())
+        return Stage1Result(ids, reps * 2.0, ids * 0.5, np.ones(len(ids), np.int32), ids + 100)
+
+    def finish(merged):
+        assert list(merged.ids) == list(range(P))
+        want = np.stack([2.0 * full[p] for p in range(P)])
+        assert np.abs(merged.factors - want).max() <= 1e-12
+        assert list(merged.sweeps) == [p + 100 for p in range(P)]
+        return (merged.factors[:, :3].copy(order="F"), merged.factors[:, 3:5].copy(order="F"),
+                merged.factors[:, 5:6].copy(order="F")), {"ok": True}
+
+    y = torch.zeros(per * world * lmn, dtype=torch.float64)
+    fac, met, _ = decompose_distributed(local, dims[2], P, lmn, y, stage1, finish)
+    want = np.stack([2.0 * full[p] for p in range(P)])
+    out[rank] = (max(seen.values()) if seen else 0.0, sorted(seen),
+                 float(np.abs(fac[0] - want[:, :3]).max()), met is not None)
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_als_sharded_pipeline():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_distributed_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out[0][0] <= 1e-12 and out[1][0] <= 1e-12
+    assert out[0][1] == [0, 1, 2] and out[1][1] == [3, 4]   # ceil(5 / 2) replicas per rank
+    assert out[0][2] <= 1e-12 and out[1][2] <= 1e-12   # slab sums vs one-shot: rounding only
+    assert out[0][3] and not out[1][3]

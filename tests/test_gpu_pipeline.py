@@ -145,3 +145,29 @@ def _derive(gpu, seed, tag):
     from oracle.oracle import Restated
     return Restated().derive(seed, tag)
 
+
+
+def test_stage1_split_matches_decompose_replicas(gpu):
+    # the multi-GPU split (stage 1 per rank on its share of the replicas, the
+    # rest on one rank) gives exactly the single-process decompose_replicas
+    import torch
+    dims, R = (96, 90, 80), 4
+    f = gpu.generate_factors(dims, R, seed=7)
+    cfg = _cfg(gpu, reduced=(24, 24, 24), rank=R, seed=9, precision=gpu.PREC_BF16, replica_fit_tol=1e-2)
+    P = gpu.compute_replica_count(dims, cfg.reduced, 10)
+    ens_seed = None
+    from bench import derive
+    plan = gpu.Plan(dims, cfg.reduced, P, 2 * R, derive(9, 11), precision=gpu.PREC_BF16)
+    y = plan.compress_factors(f, device="cuda")
+    torch.cuda.synchronize()
+    want, met = gpu.decompose_replicas(cfg, y, factors=f)
+    lmn = int(np.prod(cfg.reduced))
+    cut = P // 3
+    parts = [gpu.decompose_stage1(cfg, dims, y[a * lmn:b * lmn], np.arange(a, b)) for a, b in ((cut, P), (0, cut))]
+    merged = gpu.Stage1Result(*(np.concatenate([getattr(r, k) for r in parts])
+                                for k in ("ids", "factors", "fit_err", "converged", "sweeps")))
+    got, met2 = gpu.decompose_finish(cfg, merged, factors=f)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+    assert met2.als_sweeps == met.als_sweeps and met2.replicas_dropped == met.replicas_dropped
+    assert max(gpu.evaluate(f, got).mode_rel_err) <= 1e-2
