@@ -16,6 +16,7 @@
 // replicas (x restarts) runs as P CTAs; each replica tensor (<= a few MB) stays
 // L2-resident across its sweeps. The Khatri-Rao products are never formed: the
 // MTTKRPs contract one mode at a time (L*M*N*R FMAs each).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -197,8 +198,10 @@ __device__ void mttkrp(const double* __restrict__ T, int n1, int n2, int n3, int
 // Mode-1 MTTKRP with warp lanes over i (coalesced T reads) and thread groups
 // over k: out[i, r] = sum_k C[k,r] sum_j T[i,j,k] B[j,r]. Per-group partials
 // are reduced in a fixed order (bitwise-deterministic, like the reference).
-constexpr int RCH = 16;          // ranks per register chunk
 constexpr int RED_DOUBLES = 4096;
+// RCH: ranks per register chunk, chosen per launch to waste the fewest
+// predicated FMA slots for the batch's rank (rch_for below)
+template <int RCH>
 __device__ void mttkrp0(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s, double* out,
                         double* red) {
   const int n1r = (n1 + 31) & ~31;
@@ -254,6 +257,7 @@ __device__ void mttkrp0(const double* __restrict__ T, int n1, int n2, int n3, in
 
 // P[r][k][j] = sum_i T[i,j,k] A[i,r] (the A-contracted tensor shared by the B
 // and C updates of a sweep), threads over (j, k) fibers, contiguous i reads.
+template <int RCH>
 __device__ void contract_a(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s,
                            double* __restrict__ P) {
   const int fibers = n2 * n3;
@@ -301,14 +305,30 @@ __device__ void mttkrp2_from_p(const double* __restrict__ P, int n2, int n3, int
   }
 }
 
+// G = F' F (R x R, symmetric): four lanes per (r, q) pair, each summing every
+// fourth row, combined by two xor-shuffles (a fixed, symmetric order).
 __device__ void gram(const double* F, int rows, int R, double* G) {
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int r = e % R, q = e / R;
-    if (r > q) continue;
-    double acc = 0.0;
-    for (int i = 0; i < rows; ++i) acc = fma(F[i + rows * r], F[i + rows * q], acc);
-    G[r + R * q] = acc;
-    G[q + R * r] = acc;
+  const int npair = R * (R + 1) / 2;
+  for (int t0 = 0; t0 < 4 * npair; t0 += blockDim.x) {
+    const int t = t0 + static_cast<int>(threadIdx.x);
+    const int pidx = t >> 2, part = t & 3;
+    double v = 0.0;
+    int r = 0, q = 0;
+    if (pidx < npair) {
+      q = static_cast<int>((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
+      while (q * (q + 1) / 2 > pidx) --q;
+      while ((q + 1) * (q + 2) / 2 <= pidx) ++q;
+      r = pidx - q * (q + 1) / 2;
+      const double* fr = F + rows * r;
+      const double* fq = F + rows * q;
+      for (int i = part; i < rows; i += 4) v = fma(fr[i], fq[i], v);
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (pidx < npair && part == 0) {
+      G[r + R * q] = v;
+      G[q + R * r] = v;
+    }
   }
 }
 
@@ -353,26 +373,28 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
     if (R > 64) {  // the per-row substitution keeps R values in registers/local memory
       if (lane == 0) *ok = 0;
     } else {
+    // right-looking Cholesky in place (lower triangle of s.P), warp-synchronous
+    for (int e = lane; e < R * R; e += 32) Lm[e] = s.H[e];
+    __syncwarp();
     double mxd = 0.0;
-    for (int i = 0; i < R; ++i) mxd = fmax(mxd, s.H[i + R * i]);
+    for (int i = 0; i < R; ++i) mxd = fmax(mxd, Lm[i + R * i]);
     bool good = mxd > 0.0;
     for (int k = 0; k < R && good; ++k) {
-      double part = 0.0;
-      for (int j = lane; j < k; j += 32) part = fma(Lm[k + R * j], Lm[k + R * j], part);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      const double d = s.H[k + R * k] - part;
+      const double d = Lm[k + R * k];
+      __syncwarp();
       if (!(d > 1e-11 * mxd)) {
         good = false;
         break;
       }
       const double lkk = sqrt(d);
-      for (int i = k + 1 + lane; i < R; i += 32) {
-        double acc = s.H[i + R * k];
-        for (int j = 0; j < k; ++j) acc = fma(-Lm[i + R * j], Lm[k + R * j], acc);
-        Lm[i + R * k] = acc / lkk;
-      }
+      for (int i = k + 1 + lane; i < R; i += 32) Lm[i + R * k] /= lkk;
       if (lane == 0) Lm[k + R * k] = lkk;
+      __syncwarp();
+      const int m = R - k - 1;
+      for (int t = lane; t < m * m; t += 32) {
+        const int i = k + 1 + t % m, j = k + 1 + t / m;
+        if (i >= j) Lm[i + R * j] = fma(-Lm[i + R * k], Lm[j + R * k], Lm[i + R * j]);
+      }
       __syncwarp();
     }
     if (lane == 0) *ok = good ? 1 : 0;
@@ -380,20 +402,31 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
   }
   __syncthreads();
   if (*ok) {
-    // rows of Mt: L L' f' = m'  (f, m row vectors of length R)
-    for (int x = threadIdx.x; x < rows; x += blockDim.x) {
-      double y[64];
-      for (int i = 0; i < R; ++i) {
-        double acc = Mt[x + rows * i];
-        for (int j = 0; j < i; ++j) acc = fma(-s.P[i + R * j], y[j], acc);
-        y[i] = acc / s.P[i + R * i];
+    // H^-1 = L^-T L^-1: lane c of warp 0 forms column c of L^-1 (into s.V),
+    // then H^-1 (into s.H) and F = Mt H^-1 run over all threads
+    if (threadIdx.x < 32) {
+      for (int c = threadIdx.x; c < R; c += 32) {
+        s.V[c + R * c] = 1.0 / s.P[c + R * c];
+        for (int i = c + 1; i < R; ++i) {
+          double acc = 0.0;
+          for (int j = c; j < i; ++j) acc = fma(s.P[i + R * j], s.V[j + R * c], acc);
+          s.V[i + R * c] = -acc / s.P[i + R * i];
+        }
       }
-      for (int i = R - 1; i >= 0; --i) {
-        double acc = y[i];
-        for (int j = i + 1; j < R; ++j) acc = fma(-s.P[j + R * i], y[j], acc);
-        y[i] = acc / s.P[i + R * i];
-      }
-      for (int i = 0; i < R; ++i) F[x + rows * i] = y[i];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int a = e % R, b = e / R;
+      double acc = 0.0;
+      for (int i = a > b ? a : b; i < R; ++i) acc = fma(s.V[i + R * a], s.V[i + R * b], acc);
+      s.H[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
+      const int x = e % rows, r = e / rows;
+      double acc = 0.0;
+      for (int q = 0; q < R; ++q) acc = fma(Mt[x + rows * q], s.H[q + R * r], acc);
+      F[e] = acc;
     }
   } else {
     pinv_sym(s.H, R, s);
@@ -401,17 +434,31 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
   }
 }
 
+// sum over (i, j, k) of (T - [[A, B, C]])^2: lanes over i, warps over (j, k)
+// fibers (no 64-bit index arithmetic per element), two interleaved rank
+// chains per element.
 __device__ double residual_sq(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int fibers = n2 * n3;
   double acc = 0.0;
-  const int64_t total = static_cast<int64_t>(n1) * n2 * n3;
-  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-    const int i = static_cast<int>(e % n1);
-    const int64_t jk = e / n1;
-    const int j = static_cast<int>(jk % n2), k = static_cast<int>(jk / n2);
-    double rec = 0.0;
-    for (int r = 0; r < R; ++r) rec = fma(s.A[i + n1 * r], s.B[j + n2 * r] * s.C[k + n3 * r], rec);
-    const double d = T[e] - rec;
-    acc = fma(d, d, acc);
+  for (int i0 = 0; i0 < n1; i0 += 32) {
+    const int i = i0 + lane;
+    const bool on = i < n1;
+    const double* Ai = s.A + (on ? i : 0);
+    for (int f = warp; f < fibers; f += nw) {
+      const int j = f % n2, k = f / n2;
+      const double* Bj = s.B + j;
+      const double* Ck = s.C + k;
+      double r0 = 0.0, r1 = 0.0;
+      int r = 0;
+      for (; r + 1 < R; r += 2) {
+        r0 = fma(Ai[n1 * r], Bj[n2 * r] * Ck[n3 * r], r0);
+        r1 = fma(Ai[n1 * (r + 1)], Bj[n2 * (r + 1)] * Ck[n3 * (r + 1)], r1);
+      }
+      if (r < R) r0 = fma(Ai[n1 * r], Bj[n2 * r] * Ck[n3 * r], r0);
+      const double d = on ? T[i + static_cast<int64_t>(n1) * f] - (r0 + r1) : 0.0;
+      acc = fma(d, d, acc);
+    }
   }
   return block_sum(acc, s.red);
 }
@@ -500,6 +547,7 @@ __device__ void nvecs_init(const double* __restrict__ T, int n1, int n2, int n3,
   __syncthreads();
 }
 
+template <int RCH>
 __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3) {
   extern __shared__ double sm[];
   __shared__ int s_ok;
@@ -548,7 +596,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
   double prev = 0.0;
   for (; it < in.cfg.max_iters; ++it) {
     // A update
-    mttkrp0(T, n1, n2, n3, R, s, s.M, s.red2);
+    mttkrp0<RCH>(T, n1, n2, n3, R, s, s.M, s.red2);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
     __syncthreads();
     solve_gram(s.M, n1, R, s, s.A, &s_ok);
@@ -556,7 +604,7 @@ __global__ void __launch_bounds__(NT) als_kernel(const AlsInst* __restrict__ ins
     gram(s.A, n1, R, s.G1);
     __syncthreads();
     // B update
-    contract_a(T, n1, n2, n3, R, s, in.pbuf);
+    contract_a<RCH>(T, n1, n2, n3, R, s, in.pbuf);
     __syncthreads();
     mttkrp1_from_p(in.pbuf, n2, n3, R, s, s.M);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G1[e];
@@ -1000,6 +1048,329 @@ __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restric
 }
 
 // Shapes the large-replica kernel takes: 64 | n1 <= 128, 16 | n2, rank <= 24.
+// ---------------------------------------------------------------------------
+// Small replicas on CTA clusters (config 1's 30^3 replicas, the sampled
+// blocks): the single-CTA kernel is latency-bound (every pass re-reads T from
+// L2, ~150 us per sweep at 30^3). Here a cluster of CL CTAs owns one ALS
+// instance: CTA c keeps the mode-3 slab k in [c*kc, (c+1)*kc) of T resident in
+// its shared memory, the factors are replicated, and the three updates
+// exchange only R-column partials through distributed shared memory:
+//   M_A = sum_c (slab-c partial of T(1) (C kr B))       reduced in rank order
+//   P_c = T_c x1 A' (own slab), M_B = sum_c (P_c with C) reduced in rank order
+//   C rows of slab c solved by CTA c, all-gathered from the owners
+//   residual = sum_c (slab-c partial), every CTA takes the same decision.
+// Every reduction runs in a fixed order, so results are deterministic. The
+// sweep, normalisation, residual and convergence rule are als_kernel's
+// (cp_als.cpp:77-104); initial factors come from als_init_kernel.
+namespace cg = cooperative_groups;
+
+// init (cp_als.cpp:62-76): normals, nvecs on attempt 1, and ||T||
+__global__ void __launch_bounds__(NT) als_init_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3,
+                                                      double* ia, double* ib, double* ic, double* tnorm) {
+  extern __shared__ double sm[];
+  const AlsInst in = insts[blockIdx.x];
+  const int R = static_cast<int>(in.cfg.rank);
+  const int mx = max(n1, max(n2, n3));
+  Smem s{};
+  double* q = sm;
+  s.red = q; q += 64;
+  s.cs = q; q += max(mx, R) / 2 + 2;
+  s.sn = q; q += max(mx, R) / 2 + 2;
+  s.pp = reinterpret_cast<int*>(q); q += max(mx, R) / 2 + 2;
+  s.qq = reinterpret_cast<int*>(q);
+  double* A = ia + static_cast<int64_t>(blockIdx.x) * n1 * R;
+  double* B = ib + static_cast<int64_t>(blockIdx.x) * n2 * R;
+  double* C = ic + static_cast<int64_t>(blockIdx.x) * n3 * R;
+  const double tn = sqrt(norm_sq(in.t, static_cast<int64_t>(n1) * n2 * n3, s.red));
+  block_normals(derive(in.cfg.seed, 1), n1 * R, A, s.red);
+  block_normals(derive(in.cfg.seed, 2), n2 * R, B, s.red);
+  block_normals(derive(in.cfg.seed, 3), n3 * R, C, s.red);
+  if (in.cfg.init == 1 && tn > 0.0) {
+    nvecs_init(in.t, n1, n2, n3, 0, R, A, in.nvec_ws, s);
+    nvecs_init(in.t, n1, n2, n3, 1, R, B, in.nvec_ws, s);
+    nvecs_init(in.t, n1, n2, n3, 2, R, C, in.nvec_ws, s);
+  }
+  if (threadIdx.x == 0) tnorm[blockIdx.x] = tn;
+}
+
+struct ClusterLayout {
+  int kc;
+  size_t doubles;
+};
+
+__host__ __device__ inline ClusterLayout cluster_layout(int n1, int n2, int n3, int R, int CL) {
+  const int kc = (n3 + CL - 1) / CL;
+  const int mx = n1 > n2 ? (n1 > n3 ? n1 : n3) : (n2 > n3 ? n2 : n3);
+  const int jac = (mx > R ? mx : R) / 2 + 2;
+  size_t d = static_cast<size_t>(n1) * n2 * kc            // T slab
+             + static_cast<size_t>(n1 + n2 + n3) * R      // A, B, C
+             + static_cast<size_t>(kc) * R                // own C rows
+             + static_cast<size_t>(n1 + n2) * R           // M_A / M_B partials
+             + static_cast<size_t>(mx) * R                // reduced M
+             + 6 * static_cast<size_t>(R) * R             // G1..G3, H, V, P
+             + static_cast<size_t>(R) * n2 * kc           // P of the slab
+             + 64 + 2 * R + 2 + 4 * jac;
+  return {kc, d};
+}
+
+template <int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
+    als_cluster_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3, const double* __restrict__ ia,
+                       const double* __restrict__ ib, const double* __restrict__ ic,
+                       const double* __restrict__ tnorm) {
+  extern __shared__ double sm[];
+  __shared__ int s_ok;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = static_cast<int>(cl.block_rank());
+  const int item = blockIdx.x / CL;
+  const AlsInst in = insts[item];
+  const int R = static_cast<int>(in.cfg.rank);
+  const int mx = max(n1, max(n2, n3));
+  const ClusterLayout lay = cluster_layout(n1, n2, n3, R, CL);
+  const int kc = lay.kc;
+  const int k0 = min(n3, crank * kc), nk = min(n3, k0 + kc) - k0;
+  const int jac = max(mx, R) / 2 + 2;
+  Smem s{};
+  double* q = sm;
+  double* Ts = q; q += static_cast<int64_t>(n1) * n2 * kc;
+  s.A = q; q += n1 * R;
+  s.B = q; q += n2 * R;
+  s.C = q; q += n3 * R;
+  double* Cown = q; q += kc * R;
+  double* MAp = q; q += n1 * R;
+  double* MBp = q; q += n2 * R;
+  s.M = q; q += mx * R;
+  s.G1 = q; q += R * R;
+  s.G2 = q; q += R * R;
+  s.G3 = q; q += R * R;
+  s.H = q; q += R * R;
+  s.V = q; q += R * R;
+  s.P = q; q += R * R;
+  double* Pl = q; q += R * n2 * kc;
+  s.red = q; q += 64;
+  s.nrm = q; q += 2 * R;
+  double* rs = q; q += 2;
+  s.cs = q; q += jac;
+  s.sn = q; q += jac;
+  s.pp = reinterpret_cast<int*>(q); q += jac;
+  s.qq = reinterpret_cast<int*>(q);
+  // the slab is contiguous in the column-major replica
+  const int64_t slab = static_cast<int64_t>(n1) * n2 * nk;
+  const double* Tg = in.t + static_cast<int64_t>(n1) * n2 * k0;
+  for (int64_t e = threadIdx.x; e < slab; e += blockDim.x) Ts[e] = Tg[e];
+  for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) s.A[e] = ia[static_cast<int64_t>(item) * n1 * R + e];
+  for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) s.B[e] = ib[static_cast<int64_t>(item) * n2 * R + e];
+  for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) s.C[e] = ic[static_cast<int64_t>(item) * n3 * R + e];
+  const double tn = tnorm[item];
+  __syncthreads();
+  gram(s.B, n2, R, s.G2);
+  gram(s.C, n3, R, s.G3);
+  __syncthreads();
+  const int n12 = n1 * n2;
+
+  int64_t it = 0;
+  bool converged = false;
+  double prev = 0.0;
+  for (; it < in.cfg.max_iters; ++it) {
+    // ---- A update: slab partial of T(1) (C kr B), reduced over the cluster
+    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
+      const int i = e % n1, r = e / n1;
+      const double* Br = s.B + n2 * r;
+      double acc = 0.0;
+      for (int kk = 0; kk < nk; ++kk) {
+        const double* tk = Ts + i + n12 * kk;
+        double t0 = 0.0, t1 = 0.0;
+        int j = 0;
+        for (; j + 1 < n2; j += 2) {
+          t0 = fma(tk[n1 * j], Br[j], t0);
+          t1 = fma(tk[n1 * (j + 1)], Br[j + 1], t1);
+        }
+        if (j < n2) t0 = fma(tk[n1 * j], Br[j], t0);
+        acc = fma(s.C[(k0 + kk) + n3 * r], t0 + t1, acc);
+      }
+      MAp[e] = acc;
+    }
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
+    cl.sync();
+    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < CL; ++c) v += cl.map_shared_rank(MAp, c)[e];
+      s.M[e] = v;
+    }
+    __syncthreads();
+    solve_gram(s.M, n1, R, s, s.A, &s_ok);
+    __syncthreads();
+    gram(s.A, n1, R, s.G1);
+    __syncthreads();
+    // ---- P = T_c x1 A' on the slab (fibers (j, kk), r fastest), M_B partial
+    for (int e = threadIdx.x; e < R * n2 * nk; e += blockDim.x) {
+      const int r = e % R, f = e / R;  // f = j + n2 * kk
+      const double* col = Ts + static_cast<int64_t>(n1) * f;
+      const double* Ar = s.A + n1 * r;
+      double p0 = 0.0, p1 = 0.0;
+      int i = 0;
+      for (; i + 1 < n1; i += 2) {
+        p0 = fma(col[i], Ar[i], p0);
+        p1 = fma(col[i + 1], Ar[i + 1], p1);
+      }
+      if (i < n1) p0 = fma(col[i], Ar[i], p0);
+      Pl[static_cast<int64_t>(r) * n2 * kc + f] = p0 + p1;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
+      const int j = e % n2, r = e / n2;
+      const double* pr = Pl + static_cast<int64_t>(r) * n2 * kc + j;
+      double acc = 0.0;
+      for (int kk = 0; kk < nk; ++kk) acc = fma(s.C[(k0 + kk) + n3 * r], pr[n2 * kk], acc);
+      MBp[e] = acc;
+    }
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G1[e];
+    cl.sync();
+    for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < CL; ++c) v += cl.map_shared_rank(MBp, c)[e];
+      s.M[e] = v;
+    }
+    __syncthreads();
+    solve_gram(s.M, n2, R, s, s.B, &s_ok);
+    __syncthreads();
+    gram(s.B, n2, R, s.G2);
+    __syncthreads();
+    // ---- C rows of this slab: M_C[kk, r] = sum_j B[j, r] P[r][kk][j]
+    for (int e = threadIdx.x; e < nk * R; e += blockDim.x) {
+      const int kk = e % nk, r = e / nk;
+      const double* pr = Pl + static_cast<int64_t>(r) * n2 * kc + n2 * kk;
+      const double* Br = s.B + n2 * r;
+      double acc = 0.0;
+      for (int j = 0; j < n2; ++j) acc = fma(Br[j], pr[j], acc);
+      s.M[e] = acc;
+    }
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G2[e] * s.G1[e];
+    __syncthreads();
+    solve_gram(s.M, nk, R, s, Cown, &s_ok);
+    cl.sync();
+    // all-gather the new C rows from their owners
+    for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) {
+      const int k = e % n3, r = e / n3;
+      const int c = k / kc, kk = k - c * kc;
+      const int nkc = min(n3, (c + 1) * kc) - c * kc;
+      s.C[e] = cl.map_shared_rank(Cown, c)[kk + nkc * r];
+    }
+    __syncthreads();
+    // ---- move a/b column norms into c (cp_als.cpp:84-96)
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+      double na = 0.0, nb = 0.0;
+      for (int i = 0; i < n1; ++i) na = fma(s.A[i + n1 * r], s.A[i + n1 * r], na);
+      for (int i = 0; i < n2; ++i) nb = fma(s.B[i + n2 * r], s.B[i + n2 * r], nb);
+      s.nrm[r] = sqrt(na);
+      s.nrm[R + r] = sqrt(nb);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
+      const double na = s.nrm[e / n1];
+      if (na > 0.0) s.A[e] /= na;
+    }
+    for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
+      const double nb = s.nrm[R + e / n2];
+      if (nb > 0.0) s.B[e] /= nb;
+    }
+    for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) {
+      const int r = e / n3;
+      s.C[e] *= s.nrm[r] * s.nrm[R + r];
+    }
+    __syncthreads();
+    gram(s.A, n1, R, s.G1);
+    gram(s.B, n2, R, s.G2);
+    gram(s.C, n3, R, s.G3);
+    // ---- residual of the slab (lanes over i, warps over fibers)
+    {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      double acc = 0.0;
+      for (int i0 = 0; i0 < n1; i0 += 32) {
+        const int i = i0 + lane;
+        const bool on = i < n1;
+        const double* Ai = s.A + (on ? i : 0);
+        for (int f = warp; f < n2 * nk; f += nw) {
+          const int j = f % n2, kk = f / n2;
+          const double* Bj = s.B + j;
+          const double* Ck = s.C + k0 + kk;
+          double r0 = 0.0, r1 = 0.0;
+          int r = 0;
+          for (; r + 1 < R; r += 2) {
+            r0 = fma(Ai[n1 * r], Bj[n2 * r] * Ck[n3 * r], r0);
+            r1 = fma(Ai[n1 * (r + 1)], Bj[n2 * (r + 1)] * Ck[n3 * (r + 1)], r1);
+          }
+          if (r < R) r0 = fma(Ai[n1 * r], Bj[n2 * r] * Ck[n3 * r], r0);
+          const double d = on ? Ts[i + static_cast<int64_t>(n1) * f] - (r0 + r1) : 0.0;
+          acc = fma(d, d, acc);
+        }
+      }
+      acc = block_sum(acc, s.red);
+      if (threadIdx.x == 0) rs[0] = acc;
+    }
+    cl.sync();
+    double res2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < CL; ++c) res2 += cl.map_shared_rank(rs, c)[0];
+    const double res = sqrt(res2);
+    const double err = tn > 0.0 ? res / tn : res;
+    if (crank == 0 && threadIdx.x == 0) in.hist[it] = err;
+    if (it >= 1 && fabs(prev - err) < in.cfg.tol) {
+      converged = true;
+      ++it;
+      break;
+    }
+    prev = err;
+  }
+  if (crank == 0) {
+    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) in.a[e] = s.A[e];
+    for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) in.b[e] = s.B[e];
+    for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) in.c[e] = s.C[e];
+    if (threadIdx.x == 0) {
+      *in.iters = it;
+      *in.conv = converged ? 1 : 0;
+    }
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
+// cluster size for the small-replica kernel: the smallest CL in {2, 4, 8}
+// whose per-CTA working set fits 110 KB (two clusters' CTAs per SM); 0 when
+// none does (or XTSG_ALS_CLUSTER=0)
+int als_cluster_size(int64_t n1, int64_t n2, int64_t n3, int64_t R) {
+  static const int env = [] {
+    const char* e = std::getenv("XTSG_ALS_CLUSTER");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (env == 0 || R > 32 || n1 > 64 || n2 > 64 || n3 > 64 || n3 < 2) return 0;
+  for (int cl : {2, 4, 8}) {
+    if (env > 0 && cl != env) continue;
+    if (cl > n3) break;
+    if (cluster_layout(int(n1), int(n2), int(n3), int(R), cl).doubles * 8 <= 110 * 1024) return cl;
+  }
+  return 0;
+}
+
+void launch_als_cluster(const AlsInst* din, int64_t count, int n1, int n2, int n3, int R, int CL, cudaStream_t st) {
+  DevBuf<double> ia(static_cast<size_t>(count * n1 * R), st), ib(static_cast<size_t>(count * n2 * R), st),
+      ic(static_cast<size_t>(count * n3 * R), st), tn(static_cast<size_t>(count), st);
+  const int mx = std::max(n1, std::max(n2, n3));
+  const size_t ismem = sizeof(double) * (64 + 4 * (std::max(mx, R) / 2 + 2));
+  als_init_kernel<<<static_cast<unsigned>(count), NT, ismem, st>>>(din, n1, n2, n3, ia.ptr, ib.ptr, ic.ptr, tn.ptr);
+  XLAUNCH_CHECK();
+  const size_t smem = cluster_layout(n1, n2, n3, R, CL).doubles * 8;
+  auto go = [&](auto kern) {
+    XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<static_cast<unsigned>(count * CL), NT, smem, st>>>(din, n1, n2, n3, ia.ptr, ib.ptr, ic.ptr, tn.ptr);
+  };
+  if (CL == 2) go(als_cluster_kernel<2>);
+  else if (CL == 4) go(als_cluster_kernel<4>);
+  else go(als_cluster_kernel<8>);
+  XLAUNCH_CHECK();
+}
+
 bool als_big_eligible(int64_t n1, int64_t n2, int64_t n3, int64_t R) {
   static const bool off = [] {
     const char* e = std::getenv("XTSG_ALS_BIG");
@@ -1025,6 +1396,20 @@ void launch_als_big(const AlsInst* din, int64_t count, int n1, int n2, int n3, i
     if (ntr == 1) go(als_big_kernel<2, 1>); else if (ntr == 2) go(als_big_kernel<2, 2>); else go(als_big_kernel<2, 3>);
   }
   XLAUNCH_CHECK();
+}
+
+// register chunk of ranks for the small-replica kernel: fewest wasted
+// (predicated) FMA slots over ceil(R / RCH) chunks, larger chunks on ties
+int rch_for(int R) {
+  int best = 16, waste = 1 << 30;
+  for (int c : {16, 12, 10, 8, 4}) {
+    const int w = ((R + c - 1) / c) * c - R;
+    if (w < waste) {
+      waste = w;
+      best = c;
+    }
+  }
+  return best;
 }
 
 size_t als_smem_bytes(int n1, int n2, int n3, int R) {
@@ -1126,12 +1511,25 @@ int32_t xtsg_cp_als_batched(int64_t count, const double* t, int64_t n1, int64_t 
     }
     DevBuf<AlsInst> din(static_cast<size_t>(count), st);
     XCUDA(cudaMemcpyAsync(din.ptr, hin.data(), sizeof(AlsInst) * count, cudaMemcpyHostToDevice, st));
-    if (als_big_eligible(n1, n2, n3, rank)) {
+    const int ccl = als_cluster_size(n1, n2, n3, rank);
+    if (ccl > 0) {
+      launch_als_cluster(din.ptr, count, static_cast<int>(n1), static_cast<int>(n2), static_cast<int>(n3), R, ccl,
+                         st);
+    } else if (als_big_eligible(n1, n2, n3, rank)) {
       launch_als_big(din.ptr, count, static_cast<int>(n1), static_cast<int>(n2), static_cast<int>(n3), R, st);
     } else {
-      XCUDA(cudaFuncSetAttribute(als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      als_kernel<<<static_cast<unsigned>(count), NT, smem, st>>>(din.ptr, static_cast<int>(n1), static_cast<int>(n2),
-                                                                  static_cast<int>(n3));
+      auto go = [&](auto kern) {
+        XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<static_cast<unsigned>(count), NT, smem, st>>>(din.ptr, static_cast<int>(n1), static_cast<int>(n2),
+                                                             static_cast<int>(n3));
+      };
+      switch (rch_for(R)) {
+        case 4: go(als_kernel<4>); break;
+        case 8: go(als_kernel<8>); break;
+        case 10: go(als_kernel<10>); break;
+        case 12: go(als_kernel<12>); break;
+        default: go(als_kernel<16>); break;
+      }
       XLAUNCH_CHECK();
     }
     oa.finish();
