@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-dtype", default="f32", choices=["bf16", "f32", "f64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cp-time", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--K", type=int, default=C2["K"], help="mode-3 extent per rank (testing)")
     return ap.parse_args()
@@ -176,6 +177,44 @@ def cpu_reference_rate(cfg, seconds, threads):
                    f"P={P} replicas of {red[0]}^3, {dt:.1f} s, OPENBLAS 1 thread x {threads} workers"
 
 
+def cp_time_c1():
+    """The metric's second half, end-to-end CP time, on the reference's own
+    CPU-runnable config (BASELINE configs[0], C1): decompose from the rank-10
+    factors on the device (fp64 compression, the reference's precision) next
+    to the reference's decompose on the host cores (oracle/_ref), with the
+    recovered-factor errors of both (evaluate, pipeline.cpp:577-609)."""
+    import paper_2311_13693_b200 as xt
+    dims, R, red, P, S = (200, 200, 200), 10, (30, 30, 30), 12, 10
+    f = xt.generate_factors(dims, R, seed=1)
+    cfg = xt.PipelineConfig(reduced=red, rank=R, replicas=P, shared=S, precision=xt.PREC_FP64, seed=2)
+    xt.decompose(cfg, factors=f)
+    walls = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        rec, met = xt.decompose(cfg, factors=f)
+        walls.append(time.perf_counter() - t0)
+    out = {"config": "C1: dense 200^3 rank-10, P=12 x 30^3, S=10, decompose end to end (fp64)",
+           "seconds": float(np.median(walls)), "stage_seconds": met.stage_seconds,
+           "mode_rel_err": xt.evaluate(f, rec).mode_rel_err}
+    try:
+        from oracle.oracle import Reference
+        ref = Reference()
+        ref.L.xref_set_blas_threads(1)
+        threads = os.cpu_count() or 1
+        rw = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            rc, rrec, _ = ref.decompose(f, dims, red, R, P, S, 2, workers=threads)
+            rw.append(time.perf_counter() - t0)
+        out["reference_seconds"] = float(np.median(rw))
+        out["reference_cores"] = threads
+        out["reference_mode_rel_err"] = ref.evaluate(f, rrec)[0]
+    except Exception as e:  # reference build absent on this box
+        out["reference_seconds"] = None
+        out["reference_note"] = f"unavailable: {e}"
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -284,7 +323,7 @@ def main():
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": sustained, "unit": "TFLOP/s",
                 "frac": round(achieved / sustained, 4), "traffic": traffic,
-                "kernel": "ttm_fused_kernel (mode-1 + mode-2, tcgen05 kind::f16)",
+                "kernel": "ttm_pair_kernel (fused mode-1 + mode-2, tcgen05 kind::f16, cta_group::2)",
                 "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
                 "algorithmic_flops_per_launch": flops_per_launch,
                 "kernel_share_of_step": round(prof["fused_ms"] / ms, 4) if ms > 0 else None,
@@ -330,6 +369,13 @@ def main():
                "host_dtype": args.e2e_dtype, "ms_per_step": dt / args.e2e_steps * 1e3}
         del xh
 
+    cp = None
+    if rank == 0 and not args.no_cp_time:
+        try:
+            cp = cp_time_c1()
+        except Exception as e:
+            cp = {"error": str(e)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -352,6 +398,7 @@ def main():
                        "l2": "inputs (16 GB bf16 per rank) larger than L2; no flush",
                        "plan_create_s": round(t_plan, 3)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "cp_time": cp,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
