@@ -366,7 +366,10 @@ def main():
         e2e = {"value": elems_rank * world * args.e2e_steps / dt, "unit": "elements/s",
                "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                "d2h_bytes_per_step": int(yh.numel() * 4),
-               "host_dtype": args.e2e_dtype, "ms_per_step": dt / args.e2e_steps * 1e3}
+               "host_dtype": args.e2e_dtype, "ms_per_step": dt / args.e2e_steps * 1e3,
+               "pcie_h2d_bytes_per_step": int(xh.numel() * (2 if os.environ.get("XTSG_HOST_NARROW", "1") != "0"
+                                                            else xh.element_size())),
+               "note": "f32/f64 host input is narrowed to bf16 on the host (RNE, multi-threaded) before the DMA"}
         del xh
 
     cp = None

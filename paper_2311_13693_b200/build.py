@@ -48,7 +48,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             if src.suffix == ".cu":
                 cmd = [NVCC, *FLAGS, "-c", str(src), "-o", str(obj)]
             else:
-                cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off",
+                cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off",
                        "-I", str(ROOT / "include"), "-I", "/usr/local/cuda/include",
                        "-c", str(src), "-o", str(obj)]
             jobs.append(cmd)

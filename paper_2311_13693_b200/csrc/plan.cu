@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "comp_f64.cuh"
@@ -273,6 +275,8 @@ Plan::~Plan() {
   for (int b = 0; b < 2; ++b) {
     if (ev_copied[b]) cudaEventDestroy(ev_copied[b]);
     if (ev_consumed[b]) cudaEventDestroy(ev_consumed[b]);
+    if (ev_h2d[b]) cudaEventDestroy(ev_h2d[b]);
+    if (hpin[b]) cudaFreeHost(hpin[b]);
   }
 }
 
@@ -408,6 +412,89 @@ void Plan::ensure_z(int64_t floats, cudaStream_t s) {
   zbuf = DevBuf<float>(static_cast<size_t>(floats), s);
 }
 
+// host_narrow.cpp (host compiler, per-ISA clones)
+void narrow_rows_f32(const float* x, int64_t ni, int64_t nj, int64_t ld0, int64_t ld1, int64_t k0, int64_t row0,
+                     int64_t row1, int64_t ldi, uint16_t* out);
+void narrow_rows_f64(const double* x, int64_t ni, int64_t nj, int64_t ld0, int64_t ld1, int64_t k0, int64_t row0,
+                     int64_t row1, int64_t ldi, uint16_t* out);
+
+namespace {
+
+int host_threads() {
+  static const int n = [] {
+    const char* e = std::getenv("XTSG_HOST_THREADS");
+    if (e && std::atoi(e) > 0) return std::atoi(e);
+    const unsigned hc = std::thread::hardware_concurrency();
+    return static_cast<int>(std::max(1u, std::min(hc, 32u)));
+  }();
+  return n;
+}
+
+}  // namespace
+
+// Host f32/f64 input on a bf16 plan: the data is narrowed to bf16 ON THE HOST
+// (multi-threaded, round-to-nearest-even exactly like the device conversion)
+// into pinned slab buffers, so PCIe carries 2 bytes per element instead of 4
+// or 8. Three stages overlap: host threads narrow slab s + 1 while the copy
+// engine moves slab s and the tensor cores compress slab s - 1.
+void Plan::compress_host_narrow(const void* x, int32_t dtype, const int64_t ld[2], const int64_t off[3],
+                                const int64_t ext[3], float* ydst, bool acc_first, cudaStream_t s) {
+  const int64_t ldi = round_up(ext[0], 8);
+  const int64_t row_bytes = ldi * 2;
+  int64_t ks = std::max<int64_t>(1, (int64_t(256) << 20) / std::max<int64_t>(1, row_bytes * ext[1]));
+  ks = std::min(ks, ext[2]);
+  const size_t bytes = static_cast<size_t>(ks * ext[1] * row_bytes);
+  if (hpin_bytes < bytes) {
+    for (int b = 0; b < 2; ++b) {
+      if (hpin[b]) XCUDA(cudaFreeHost(hpin[b]));
+      hpin[b] = nullptr;
+    }
+    hpin_bytes = 0;
+    for (int b = 0; b < 2; ++b) XCUDA(cudaHostAlloc(&hpin[b], bytes, cudaHostAllocDefault));
+    hpin_bytes = bytes;
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (dstage[b].n < static_cast<size_t>(ks * ext[1] * ldi))
+      dstage[b] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * ext[1] * ldi), st);
+    if (!ev_h2d[b]) XCUDA(cudaEventCreateWithFlags(&ev_h2d[b], cudaEventDisableTiming));
+    if (!ev_consumed[b]) XCUDA(cudaEventCreateWithFlags(&ev_consumed[b], cudaEventDisableTiming));
+  }
+  XCUDA(cudaStreamSynchronize(st));  // device slab buffers exist before other streams use them
+  const int nthr = host_threads();
+  const int64_t nslabs = ceil_div(ext[2], ks);
+  bool acc = acc_first;
+  for (int64_t sl = 0; sl < nslabs; ++sl) {
+    const int b = static_cast<int>(sl & 1);
+    const int64_t k0 = sl * ks, kn = std::min(ks, ext[2] - k0);
+    // the pinned buffer is free once its previous copy has landed
+    if (sl >= 2) XCUDA(cudaEventSynchronize(ev_h2d[b]));
+    const int64_t rows = kn * ext[1];
+    uint16_t* hb = static_cast<uint16_t*>(hpin[b]);
+    std::vector<std::thread> pool;
+    const int nt = static_cast<int>(std::min<int64_t>(nthr, rows));
+    for (int t = 0; t < nt; ++t) {
+      const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
+      if (dtype == XTSG_DTYPE_F32)
+        pool.emplace_back(narrow_rows_f32, static_cast<const float*>(x), ext[0], ext[1], ld[0], ld[1], k0, r0, r1,
+                          ldi, hb);
+      else
+        pool.emplace_back(narrow_rows_f64, static_cast<const double*>(x), ext[0], ext[1], ld[0], ld[1], k0, r0,
+                          r1, ldi, hb);
+    }
+    for (auto& th : pool) th.join();
+    // the device buffer is free once the compression of slab sl - 2 is done
+    if (sl >= 2) XCUDA(cudaStreamWaitEvent(copy_st, ev_consumed[b], 0));
+    XCUDA(cudaMemcpyAsync(dstage[b].ptr, hb, static_cast<size_t>(rows * row_bytes), cudaMemcpyHostToDevice, copy_st));
+    XCUDA(cudaEventRecord(ev_h2d[b], copy_st));
+    XCUDA(cudaStreamWaitEvent(s, ev_h2d[b], 0));
+    const int64_t soff[3] = {off[0], off[1], off[2] + k0};
+    const int64_t sext[3] = {ext[0], ext[1], kn};
+    run_bf16_block(dstage[b].ptr, ldi, ldi * ext[1], soff, sext, ydst, acc, s);
+    XCUDA(cudaEventRecord(ev_consumed[b], s));
+    acc = true;
+  }
+}
+
 void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int64_t off[3],
                     const int64_t ext[3], void* y, bool accumulate, cudaStream_t s) {
   check_block(off, ext);
@@ -474,8 +561,14 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
   }
   const bool direct = x_dev && dtype == XTSG_DTYPE_BF16 && ld[0] % 8 == 0 && ld[1] % 8 == 0 &&
                       reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  static const bool narrow_on = [] {
+    const char* e = std::getenv("XTSG_HOST_NARROW");
+    return !(e && std::atoi(e) == 0);
+  }();
   if (direct) {
     run_bf16_block(static_cast<const __nv_bfloat16*>(x), ld[0], ld[1], off, ext, ydst, acc_first, s);
+  } else if (!x_dev && dtype != XTSG_DTYPE_BF16 && narrow_on) {
+    compress_host_narrow(x, dtype, ld, off, ext, ydst, acc_first, s);
   } else {
     // Slab pipeline: copy_st moves raw slab k-ranges H2D (host input) while s
     // converts the previous slab to bf16 and runs the tensor cores on it.

@@ -26,6 +26,14 @@ struct Plan {
   DevBuf<__nv_bfloat16> ut;   // i-major U copy for the sparse path (lazy)
   DevBuf<__nv_bfloat16> vtj;  // j-major V copy for the sparse path (lazy)
   int grid_limit = 0;  // testing knob: cap on persistent CTAs (0 = #SMs)
+  // host-narrowing pipeline (f32/f64 host input on a bf16 plan): pinned bf16
+  // slab buffers and their device twins, cached across calls
+  void* hpin[2] = {nullptr, nullptr};
+  size_t hpin_bytes = 0;
+  DevBuf<__nv_bfloat16> dstage[2];
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr};
+  void compress_host_narrow(const void* x, int32_t dtype, const int64_t ld[2], const int64_t off[3],
+                            const int64_t ext[3], float* ydst, bool acc_first, cudaStream_t s);
   // Live profiling (xtsg_plan_profile): CUDA events around every fused-TTM
   // and mode-3 launch on the launching stream, plus algorithmic flop counts.
   bool profiling = false;
