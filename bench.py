@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--e2e-dtype", default="f32", choices=["bf16", "f32", "f64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cp-time", action="store_true")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp16"],
+                    help="tensor-core operand type (fp16: 3 more mantissa bits, same speed)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--K", type=int, default=C2["K"], help="mode-3 extent per rank (testing)")
     return ap.parse_args()
@@ -128,7 +130,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_block(torch, xt, cfg, k0, K, device):
+def make_block(torch, xt, cfg, k0, K, device, dtype=None):
     """Rank's block X[:, :, k0:k0+K] of reconstruct(A, B, C) as bf16, (I, J, K) column-major.
 
     Factors follow generate({dims, R, dense, seed}) (pipeline.cpp:182-193): one
@@ -138,13 +140,14 @@ def make_block(torch, xt, cfg, k0, K, device):
     A = torch.from_numpy(xt.gen_gaussian(I, R, derive(cfg["factor_seed"], 1))).to(device, torch.float32)
     B = torch.from_numpy(xt.gen_gaussian(J, R, derive(cfg["factor_seed"], 2))).to(device, torch.float32)
     Cf = torch.from_numpy(xt.gen_gaussian(Ktot, R, derive(cfg["factor_seed"], 3))).to(device, torch.float32)
-    X = torch.empty((K, J, I), dtype=torch.bfloat16, device=device)
+    dtype = dtype or torch.bfloat16
+    X = torch.empty((K, J, I), dtype=dtype, device=device)
     step = 50
     for k in range(0, K, step):
         kk = min(step, K - k)
         ck = Cf[k0 + k:k0 + k + kk]                       # (kk, R)
         # X[k, j, i] = sum_r A[i, r] B[j, r] C[k, r]
-        X[k:k + kk] = torch.einsum("kr,jr,ir->kji", ck, B, A).to(torch.bfloat16)
+        X[k:k + kk] = torch.einsum("kr,jr,ir->kji", ck, B, A).to(dtype)
     return X.permute(2, 1, 0), (A, B, Cf)
 
 
@@ -261,9 +264,10 @@ def main():
     P = cfg["P"]
     k0 = rank * K
     t_plan = time.perf_counter()
-    plan = xt.Plan(dims, red, P, cfg["S"], derive(cfg["seed"], 11), precision=xt.PREC_BF16)
+    prec = xt.PREC_FP16 if args.precision == "fp16" else xt.PREC_BF16
+    plan = xt.Plan(dims, red, P, cfg["S"], derive(cfg["seed"], 11), precision=prec)
     t_plan = time.perf_counter() - t_plan
-    X, _ = make_block(torch, xt, cfg, k0, K, dev)
+    X, _ = make_block(torch, xt, cfg, k0, K, dev, torch.float16 if args.precision == "fp16" else torch.bfloat16)
     torch.cuda.synchronize()
     ysz = P * int(np.prod(red))
     y = torch.zeros(ysz, dtype=torch.float32, device=dev)
@@ -393,7 +397,7 @@ def main():
         line = {
             "metric": "input tensor elements compressed/sec", "value": value, "unit": "elements/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (rank-20 reconstruct(A,B,C) from the reference's generate() streams)",
             "config": {"workload": "C2: dense 2000^3 rank-20, streamed blocks, P=32 replicas of 64^3, S=40",
                        "dims_per_rank": [cfg["I"], cfg["J"], K], "reduced": list(red), "replicas": P,

@@ -163,10 +163,13 @@ int32_t xtsg_comp_naive_half(const double* t, int64_t n1, int64_t n2, int64_t n3
  * slabs/blocks of X with the fused tcgen05 TTM kernel. */
 #define XTSG_PREC_FP64 0   /* DFMA chain; reference-order arithmetic */
 #define XTSG_PREC_BF16 1   /* tcgen05 kind::f16, bf16 operands, fp32 accumulation */
+#define XTSG_PREC_FP16 2   /* tcgen05 kind::f16, fp16 operands (3 more mantissa bits, range 65504:
+                              U scaled by 2^-s / W by 2^s internally; overflow -> XTSG_E_HALFRANGE) */
 
 #define XTSG_DTYPE_BF16 0
 #define XTSG_DTYPE_F32 1
 #define XTSG_DTYPE_F64 2
+#define XTSG_DTYPE_F16 3
 
 typedef struct xtsg_plan_desc {
   int64_t dims[3];     /* I, J, K */

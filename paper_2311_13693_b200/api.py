@@ -15,7 +15,7 @@ import numpy as np
 
 from ._lib import (AlsConfig, EnsembleSpec, PlanDesc, PipelineConfigC, PipelineMetricsC, DTYPE_BF16,
                    DTYPE_F32, DTYPE_F64, KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE, LAW_DENSE, LAW_SPARSE,
-                   MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE, PREC_BF16, PREC_FP64, check, lib, ptr)
+                   MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE, PREC_BF16, PREC_FP64, DTYPE_F16, check, lib, ptr)
 
 _KINDS = {"gaussian": KIND_GAUSSIAN, "sparse": KIND_SPARSE, "two_stage": KIND_TWO_STAGE}
 
@@ -233,7 +233,8 @@ def comp_blocked(dims, block, source: Iterable, ensemble: Ensemble, deterministi
 
 def _torch_dtype_code(t):
     import torch
-    return {torch.bfloat16: DTYPE_BF16, torch.float32: DTYPE_F32, torch.float64: DTYPE_F64}[t.dtype]
+    return {torch.bfloat16: DTYPE_BF16, torch.float32: DTYPE_F32, torch.float64: DTYPE_F64,
+            torch.float16: DTYPE_F16}[t.dtype]
 
 
 class Plan:

@@ -17,6 +17,7 @@
 // space (10^6^3 in config C4), so the working set is the touched U columns.
 #include <cub/cub.cuh>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -83,6 +84,16 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ u, int64
   }
 }
 
+__device__ __forceinline__ void half8(const uint4& raw, float* f) {
+  const __half2* h = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 v = __half22float2(h[q]);
+    f[2 * q] = v.x;
+    f[2 * q + 1] = v.y;
+  }
+}
+
 __device__ __forceinline__ void bf16x8(const uint4& raw, float* f) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
@@ -95,14 +106,22 @@ __device__ __forceinline__ void bf16x8(const uint4& raw, float* f) {
 
 // y[q] += x * u[q] for the 8 bf16 of u: sm_100's mixed-precision FMA
 // (fma.rn.f32.bf16 -> FHFMA.BF16, half-select operands), no unpacking.
+template <bool F16>
 __device__ __forceinline__ void fma8(float* y, const uint4& u, uint16_t x) {
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n fma.rn.f32.bf16 %0, %3, lo, %0;\n"
-        " fma.rn.f32.bf16 %1, %3, hi, %1;\n}"
-        : "+f"(y[2 * q]), "+f"(y[2 * q + 1])
-        : "r"(w[q]), "h"(x));
+  for (int q = 0; q < 4; ++q) {
+    if constexpr (F16)
+      asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n fma.rn.f32.f16 %0, %3, lo, %0;\n"
+          " fma.rn.f32.f16 %1, %3, hi, %1;\n}"
+          : "+f"(y[2 * q]), "+f"(y[2 * q + 1])
+          : "r"(w[q]), "h"(x));
+    else
+      asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n fma.rn.f32.bf16 %0, %3, lo, %0;\n"
+          " fma.rn.f32.bf16 %1, %3, hi, %1;\n}"
+          : "+f"(y[2 * q]), "+f"(y[2 * q + 1])
+          : "r"(w[q]), "h"(x));
+  }
 }
 
 // Warp-level segmented accumulation over the (k, j)-sorted nonzeros of a
@@ -116,7 +135,7 @@ __device__ __forceinline__ void fma8(float* y, const uint4& u, uint16_t x) {
 // memory) with V_p[:, j] from the j-major copy: Z[m][r] += y1[r] * V_p[m, j],
 // shared-memory atomics (warps of the CTA share Z rows), rows skewed by r/8 so
 // the 32 lanes hit 32 banks.
-template <int C>
+template <int C, bool F16>
 __global__ void __launch_bounds__(NT) coo_fiber_kernel(
     const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, const float* __restrict__ cv,
     const int64_t* __restrict__ slice_off, const int32_t* __restrict__ slice_cnt, int64_t n_slices,
@@ -150,7 +169,8 @@ __global__ void __launch_bounds__(NT) coo_fiber_kernel(
               float* zr = zs + rl + rl / 8;
               for (int m0 = 0; m0 < mpad; m0 += 8) {
                 float v[8];
-                bf16x8(*reinterpret_cast<const uint4*>(vrow + m0), v);
+                if constexpr (F16) half8(*reinterpret_cast<const uint4*>(vrow + m0), v);
+                else bf16x8(*reinterpret_cast<const uint4*>(vrow + m0), v);
 #pragma unroll
                 for (int mm = 0; mm < 8; ++mm)
 #pragma unroll
@@ -173,7 +193,8 @@ __global__ void __launch_bounds__(NT) coo_fiber_kernel(
         if (lane < UNROLL && e0 + lane < w1) {
           li = __ldg(ci + e0 + lane);
           lj = __ldg(cj + e0 + lane);
-          lx = __bfloat16_as_ushort(__float2bfloat16_rn(__ldg(cv + e0 + lane)));
+          const float v = __ldg(cv + e0 + lane);
+          lx = F16 ? __half_as_ushort(__float2half_rn(v)) : __bfloat16_as_ushort(__float2bfloat16_rn(v));
         }
         uint4 u[UNROLL][C];
 #pragma unroll
@@ -190,7 +211,7 @@ __global__ void __launch_bounds__(NT) coo_fiber_kernel(
           for (int t = 0; t < UNROLL; ++t) {
             const uint16_t xt = static_cast<uint16_t>(__shfl_sync(0xffffffffu, lx, t));
 #pragma unroll
-            for (int c = 0; c < C; ++c) fma8(y1[c], u[t][c], xt);
+            for (int c = 0; c < C; ++c) fma8<F16>(y1[c], u[t][c], xt);
           }
         } else {
 #pragma unroll
@@ -203,7 +224,7 @@ __global__ void __launch_bounds__(NT) coo_fiber_kernel(
                 cur_j = jt;
               }
 #pragma unroll
-              for (int c = 0; c < C; ++c) fma8(y1[c], u[t][c], xt);
+              for (int c = 0; c < C; ++c) fma8<F16>(y1[c], u[t][c], xt);
             }
           }
         }
@@ -254,7 +275,7 @@ int gridn(int64_t work) { return static_cast<int>(std::max<int64_t>(1, std::min<
 
 void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, const float* val, int64_t nnz, float* y,
                         bool accumulate, cudaStream_t s) {
-  if (desc.precision != XTSG_PREC_BF16) usage("plan_compress_coo: needs a bf16 (tensor-core) plan");
+  if (!tensor_core()) usage("plan_compress_coo: needs a bf16/fp16 (tensor-core) plan");
   if (nnz < 0) usage("plan_compress_coo: negative nnz");
   if (nnz >= (int64_t(1) << 32)) usage("plan_compress_coo: at most 2^32-1 nonzeros per call");
   if (stage1) {
@@ -370,10 +391,13 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     kern<<<grid, NT, smem, s>>>(si, sj, sv, off.ptr, cnt.ptr, kd, ut.ptr, ld_ut, plrows, vtj.ptr, ld_vtj,
                                 static_cast<int>(mpad), static_cast<int>(lpad), P, z.ptr);
   };
-  if (cg == 2)
-    launch(coo_fiber_kernel<2>);
-  else
-    launch(coo_fiber_kernel<1>);
+  if (fp16()) {
+    if (cg == 2) launch(coo_fiber_kernel<2, true>);
+    else launch(coo_fiber_kernel<1, true>);
+  } else {
+    if (cg == 2) launch(coo_fiber_kernel<2, false>);
+    else launch(coo_fiber_kernel<1, false>);
+  }
   XLAUNCH_CHECK();
   // 4. mode 3 over the distinct slices
   DevBuf<float> wg(static_cast<size_t>(P * N * kd), s);
@@ -396,6 +420,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     compact_y2_kernel<<<gridn(ysz), 256, 0, s>>>(ypad.ptr, P, L, M, N, lpad, mpad, accumulate ? 1 : 0, yo.dev);
     XLAUNCH_CHECK();
   }
+  if (fp16()) check_finite16(yo.dev, ysz, s);
   if (yo.host) yo.finish();
 }
 

@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "plan.cuh"
+#include "sm100_ptx.cuh"
 
 namespace xtsg {
 
@@ -24,7 +25,7 @@ constexpr int TI = 128, TJ = 64, NT = 256;
 __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                       const float* __restrict__ Cm, int64_t I, int64_t J, int64_t K,
                                                       int R, int64_t k0, int64_t ldi,
-                                                      __nv_bfloat16* __restrict__ X) {
+                                                      __nv_bfloat16* __restrict__ X, bool f16) {
   extern __shared__ float sm[];
   float* As = sm;            // R x TI
   float* Bs = sm + R * TI;   // R x TJ (already scaled by c_k)
@@ -62,20 +63,17 @@ __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ 
     if (j >= J) continue;
     __nv_bfloat16* row = X + (kk * J + j) * ldi + i0 + tx * 8;
     if (i0 + tx * 8 + 8 <= I) {
-      uint4 pk;
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(acc[0][b], acc[1][b]);
-      __nv_bfloat162 h1 = __floats2bfloat162_rn(acc[2][b], acc[3][b]);
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[4][b], acc[5][b]);
-      __nv_bfloat162 h3 = __floats2bfloat162_rn(acc[6][b], acc[7][b]);
-      pk.x = *reinterpret_cast<uint32_t*>(&h0);
-      pk.y = *reinterpret_cast<uint32_t*>(&h1);
-      pk.z = *reinterpret_cast<uint32_t*>(&h2);
-      pk.w = *reinterpret_cast<uint32_t*>(&h3);
-      *reinterpret_cast<uint4*>(row) = pk;
+      float v8[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) v8[a] = acc[a][b];
+      *reinterpret_cast<uint4*>(row) = ptx::pack8(v8, f16);
     } else {
 #pragma unroll
       for (int a = 0; a < 8; ++a)
-        if (i0 + tx * 8 + a < ldi) row[a] = __float2bfloat16(i0 + tx * 8 + a < I ? acc[a][b] : 0.f);
+        if (i0 + tx * 8 + a < ldi) {
+          const float v = i0 + tx * 8 + a < I ? acc[a][b] : 0.f;
+          row[a] = f16 ? __ushort_as_bfloat16(__half_as_ushort(__float2half_rn(v))) : __float2bfloat16(v);
+        }
     }
   }
 }
@@ -104,7 +102,7 @@ int g1(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_
 
 void Plan::compress_factors(const double* a, const double* b, const double* c, int64_t rank, int64_t k0, int64_t k1,
                             float* y, bool accumulate, cudaStream_t s) {
-  if (desc.precision != XTSG_PREC_BF16) usage("plan_compress_factors: needs a bf16 (tensor-core) plan");
+  if (!tensor_core()) usage("plan_compress_factors: needs a bf16/fp16 (tensor-core) plan");
   if (stage1) {
     const int64_t ysz = desc.count * desc.reduced[0] * desc.reduced[1] * desc.reduced[2];
     OutView<float> yo(y, static_cast<size_t>(ysz), s);
@@ -155,7 +153,7 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
     dim3 grid(static_cast<unsigned>(ceil_div(I, TI)), static_cast<unsigned>(ceil_div(J, TJ)),
               static_cast<unsigned>(kn));
     gen_slab_kernel<<<grid, NT, smem, s>>>(fa.ptr, fb.ptr, fc.ptr, I, J, K, static_cast<int>(rank), kb, ldi,
-                                           stage.ptr);
+                                           stage.ptr, fp16());
     XLAUNCH_CHECK();
     const int64_t off[3] = {0, 0, kb}, ext[3] = {I, J, kn};
     run_bf16_block(stage.ptr, ldi, ldi * J, off, ext, ydst, acc, s);
@@ -165,6 +163,7 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
     compact_y3_kernel<<<g1(ysz), 256, 0, s>>>(ypad.ptr, P, L, M, N, lpad, mpad, accumulate ? 1 : 0, yo.dev);
     XLAUNCH_CHECK();
   }
+  if (fp16()) check_finite16(yo.dev, ysz, s);
   if (yo.host) yo.finish();
 }
 

@@ -10,6 +10,33 @@ namespace xtsg {
 
 namespace {
 
+// float -> binary16 bits, round to nearest even (== __float2half_rn): exact
+// for normals, subnormals, overflow to inf and NaN
+inline uint16_t f2h(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  const uint32_t sign = (u >> 16) & 0x8000u;
+  const uint32_t a = u & 0x7fffffffu;
+  if (a >= 0x7f800000u) return static_cast<uint16_t>(sign | 0x7c00u | (a > 0x7f800000u ? 0x200u : 0u));
+  if (a >= 0x477ff000u) return static_cast<uint16_t>(sign | 0x7c00u);  // rounds to >= 65520: inf
+  if (a < 0x38800000u) {  // half subnormal or zero: round a * 2^24 to an integer
+    if (a < 0x33000000u) return static_cast<uint16_t>(sign);  // below half of the smallest subnormal
+    const uint32_t m = (a & 0x7fffffu) | 0x800000u;
+    const int shift = 126 - static_cast<int>(a >> 23);  // 14..24
+    uint32_t r = m >> shift;
+    const uint32_t rem = m & ((1u << shift) - 1u), hp = 1u << (shift - 1);
+    if (rem > hp || (rem == hp && (r & 1u))) ++r;
+    return static_cast<uint16_t>(sign | r);
+  }
+  const uint32_t r = a + 0xfffu + ((a >> 13) & 1u);  // RNE at bit 13
+  return static_cast<uint16_t>(sign | ((r - 0x38000000u) >> 13));
+}
+
+template <class T>
+inline void narrow_row_h(const T* __restrict__ src, int64_t n, uint16_t* __restrict__ dst) {
+  for (int64_t i = 0; i < n; ++i) dst[i] = f2h(static_cast<float>(src[i]));
+}
+
 template <class T>
 inline void narrow_row(const T* __restrict__ src, int64_t n, uint16_t* __restrict__ dst) {
   for (int64_t i = 0; i < n; ++i) {
@@ -26,22 +53,24 @@ inline void narrow_row(const T* __restrict__ src, int64_t n, uint16_t* __restric
 
 __attribute__((target_clones("avx512f", "avx2", "default")))
 void narrow_rows_f32(const float* x, int64_t ni, int64_t nj, int64_t ld0, int64_t ld1, int64_t k0, int64_t row0,
-                     int64_t row1, int64_t ldi, uint16_t* out) {
+                     int64_t row1, int64_t ldi, uint16_t* out, bool f16) {
   for (int64_t row = row0; row < row1; ++row) {
     const int64_t j = row % nj, k = k0 + row / nj;
     uint16_t* dst = out + row * ldi;
-    narrow_row(x + j * ld0 + k * ld1, ni, dst);
+    if (f16) narrow_row_h(x + j * ld0 + k * ld1, ni, dst);
+    else narrow_row(x + j * ld0 + k * ld1, ni, dst);
     for (int64_t i = ni; i < ldi; ++i) dst[i] = 0;
   }
 }
 
 __attribute__((target_clones("avx512f", "avx2", "default")))
 void narrow_rows_f64(const double* x, int64_t ni, int64_t nj, int64_t ld0, int64_t ld1, int64_t k0, int64_t row0,
-                     int64_t row1, int64_t ldi, uint16_t* out) {
+                     int64_t row1, int64_t ldi, uint16_t* out, bool f16) {
   for (int64_t row = row0; row < row1; ++row) {
     const int64_t j = row % nj, k = k0 + row / nj;
     uint16_t* dst = out + row * ldi;
-    narrow_row(x + j * ld0 + k * ld1, ni, dst);
+    if (f16) narrow_row_h(x + j * ld0 + k * ld1, ni, dst);
+    else narrow_row(x + j * ld0 + k * ld1, ni, dst);
     for (int64_t i = ni; i < ldi; ++i) dst[i] = 0;
   }
 }

@@ -13,8 +13,10 @@
 // replicas. Non-bf16 or host-resident input is streamed slab by slab through
 // a double-buffered H2D + convert pipeline on a second stream.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -33,10 +35,11 @@ namespace xtsg {
 namespace {
 
 // P column-major (rows x cols) fp64 matrices -> row-major [p*rows_pad + r][c]
-// with leading dimension ld, converted to T. 32x32 smem transpose tiles.
+// with leading dimension ld, scaled by `scale` (a power of two: exact) and
+// converted to T. 32x32 smem transpose tiles.
 template <class T>
 __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t rows, int64_t cols, int64_t rows_pad,
-                                 int64_t ld, T* __restrict__ dst) {
+                                 int64_t ld, double scale, T* __restrict__ dst) {
   __shared__ double tile[32][33];
   const int64_t p = blockIdx.z;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
@@ -49,9 +52,10 @@ __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t rows, i
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const int64_t r = r0 + dy, c = c0 + threadIdx.x;
     if (r < rows && c < cols) {
-      const double v = tile[threadIdx.x][dy];
+      const double v = tile[threadIdx.x][dy] * scale;
       T* o = dst + (p * rows_pad + r) * ld + c;
       if constexpr (std::is_same<T, float>::value) *o = static_cast<float>(v);
+      else if constexpr (std::is_same<T, __half>::value) *o = __double2half(v);
       else *o = __double2bfloat16(v);
     }
   }
@@ -59,11 +63,20 @@ __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t rows, i
 
 template <class T>
 void pack_rows(const double* src, int64_t count, int64_t rows, int64_t cols, int64_t rows_pad, int64_t ld, T* dst,
-               cudaStream_t st) {
+               cudaStream_t st, double scale = 1.0) {
   dim3 grid(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(rows, 32)),
             static_cast<unsigned>(count));
-  pack_rows_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, rows_pad, ld, dst);
+  pack_rows_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, rows_pad, ld, scale, dst);
   XLAUNCH_CHECK();
+}
+
+// fp32 -> 16-bit operand storage: bf16 bits, or fp16 bits for XTSG_PREC_FP16
+__device__ __forceinline__ __nv_bfloat16 to_op16(float v, bool f16) {
+  if (f16) {
+    const __half h = __float2half_rn(v);
+    return __ushort_as_bfloat16(__half_as_ushort(h));
+  }
+  return __float2bfloat16(v);
 }
 
 template <class T>
@@ -74,19 +87,21 @@ template <>
 __device__ __forceinline__ float to_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <>
+__device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
 
 // X block (i, j, k) at src[i + ld0*j + ld1*k] -> bf16 dst[(k*nj + j)*ldi + i],
 // zero for ni <= i < ldi.
 template <class T>
 __global__ void stage_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj, int64_t nk, int64_t ld0,
-                               int64_t ld1, int64_t ldi, __nv_bfloat16* __restrict__ dst) {
+                               int64_t ld1, int64_t ldi, __nv_bfloat16* __restrict__ dst, bool f16) {
   const int64_t rows = nj * nk;
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const int64_t j = row % nj, k = row / nj;
     const T* s = src + j * ld0 + k * ld1;
     __nv_bfloat16* d = dst + row * ldi;
     for (int64_t i = threadIdx.x; i < ldi; i += blockDim.x)
-      d[i] = __float2bfloat16(i < ni ? to_f(s[i]) : 0.f);
+      d[i] = to_op16(i < ni ? to_f(s[i]) : 0.f, f16);
   }
 }
 
@@ -114,6 +129,12 @@ __global__ void compact_y_kernel(const float* __restrict__ ypad, int64_t count, 
     const float v = ypad[p * mpad * lpad * N + (m * lpad + l) + mpad * lpad * n];
     y[e] = accumulate ? y[e] + v : v;
   }
+}
+
+__global__ void finite_f32_kernel(const float* __restrict__ y, int64_t n, int* __restrict__ bad) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (!isfinite(y[e])) *bad = 1;
 }
 
 __global__ void f32_to_f64_kernel(const float* __restrict__ s, int64_t n, double* __restrict__ d) {
@@ -145,6 +166,7 @@ int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 size_t dtype_size(int32_t dt) {
   switch (dt) {
     case XTSG_DTYPE_BF16: return 2;
+    case XTSG_DTYPE_F16: return 2;
     case XTSG_DTYPE_F32: return 4;
     case XTSG_DTYPE_F64: return 8;
     default: usage("plan: unknown x dtype");
@@ -156,14 +178,15 @@ size_t dtype_size(int32_t dt) {
 Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
   const EnsembleShape sh =
       validate_ensemble(desc.dims, desc.reduced, desc.count, desc.shared_rows, desc.spec);
-  if (desc.precision != XTSG_PREC_FP64 && desc.precision != XTSG_PREC_BF16) usage("plan: unknown precision");
+  if (desc.precision != XTSG_PREC_FP64 && desc.precision != XTSG_PREC_BF16 && desc.precision != XTSG_PREC_FP16)
+    usage("plan: unknown precision");
   require_device();
   XCUDA(cudaGetDevice(&device));
   st = thread_stream();
   XCUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
   const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
-  const bool two = desc.spec.kind == XTSG_KIND_TWO_STAGE && desc.precision == XTSG_PREC_BF16;
+  const bool two = desc.spec.kind == XTSG_KIND_TWO_STAGE && tensor_core();
   // fp64 ensemble in the reference layout (make_ensemble, bit-exact)
   u64 = DevBuf<double>(static_cast<size_t>(P * L * I), st);
   v64 = DevBuf<double>(static_cast<size_t>(P * M * J), st);
@@ -198,7 +221,7 @@ Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
     u64.release();
     v64.release();
     w64.release();
-  } else if (desc.precision == XTSG_PREC_BF16) {
+  } else if (tensor_core()) {
     build_tc_operands();
   }
   XCUDA(cudaStreamSynchronize(st));
@@ -217,7 +240,7 @@ Plan::Plan(const xtsg_plan_desc& d, const double* u, const double* v, const doub
   XCUDA(cudaMemcpyAsync(u64.ptr, u, u64.n * sizeof(double), cudaMemcpyDefault, st));
   XCUDA(cudaMemcpyAsync(v64.ptr, v, v64.n * sizeof(double), cudaMemcpyDefault, st));
   XCUDA(cudaMemcpyAsync(w64.ptr, w, w64.n * sizeof(double), cudaMemcpyDefault, st));
-  if (desc.precision == XTSG_PREC_BF16) build_tc_operands();
+  if (tensor_core()) build_tc_operands();
   XCUDA(cudaStreamSynchronize(st));
 }
 
@@ -238,9 +261,21 @@ void Plan::build_tc_operands() {
   vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(P * mpad * ld_v), st);
   vt.zero();
   wf = DevBuf<float>(static_cast<size_t>(P * N * K), st);
-  pack_rows<__nv_bfloat16>(u64.ptr, P, L, I, lpad, ld_u, ustack.ptr, st);
-  pack_rows<__nv_bfloat16>(v64.ptr, P, M, J, mpad, ld_v, vt.ptr, st);
-  pack_rows<float>(w64.ptr, P, N, K, N, K, wf.ptr, st);
+  if (fp16()) {
+    // fp16 keeps 3 more mantissa bits than bf16 but tops out at 65504: the
+    // mode-1 partial sums (the mode-2 operand, |sum_i U X| ~ sqrt(I) |X|)
+    // are kept in range by scaling U by 2^-s and W by 2^s (exact powers of
+    // two, so Y is unchanged); non-finite replicas raise HalfRangeError.
+    int sexp = 0;
+    while ((int64_t(1) << (2 * (sexp + 2))) < I) ++sexp;
+    pack_rows<__half>(u64.ptr, P, L, I, lpad, ld_u, reinterpret_cast<__half*>(ustack.ptr), st, std::ldexp(1.0, -sexp));
+    pack_rows<__half>(v64.ptr, P, M, J, mpad, ld_v, reinterpret_cast<__half*>(vt.ptr), st);
+    pack_rows<float>(w64.ptr, P, N, K, N, K, wf.ptr, st, std::ldexp(1.0, sexp));
+  } else {
+    pack_rows<__nv_bfloat16>(u64.ptr, P, L, I, lpad, ld_u, ustack.ptr, st);
+    pack_rows<__nv_bfloat16>(v64.ptr, P, M, J, mpad, ld_v, vt.ptr, st);
+    pack_rows<float>(w64.ptr, P, N, K, N, K, wf.ptr, st);
+  }
   // the fp64 copies are not needed by the bf16 path any more
   u64.release();
   v64.release();
@@ -364,6 +399,7 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
       tl.prm.x_policy = hint_env == 2 ? pol[1] : pol[0];
     }
     tl.prm.z = zbuf.ptr;
+    tl.prm.f16 = fp16() ? 1 : 0;
     EvPair e1{}, e2{};
     if (profiling) {
       e1 = take_pair();
@@ -414,9 +450,9 @@ void Plan::ensure_z(int64_t floats, cudaStream_t s) {
 
 // host_narrow.cpp (host compiler, per-ISA clones)
 void narrow_rows_f32(const float* x, int64_t ni, int64_t nj, int64_t ld0, int64_t ld1, int64_t k0, int64_t row0,
-                     int64_t row1, int64_t ldi, uint16_t* out);
+                     int64_t row1, int64_t ldi, uint16_t* out, bool f16);
 void narrow_rows_f64(const double* x, int64_t ni, int64_t nj, int64_t ld0, int64_t ld1, int64_t k0, int64_t row0,
-                     int64_t row1, int64_t ldi, uint16_t* out);
+                     int64_t row1, int64_t ldi, uint16_t* out, bool f16);
 
 namespace {
 
@@ -476,10 +512,10 @@ void Plan::compress_host_narrow(const void* x, int32_t dtype, const int64_t ld[2
       const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
       if (dtype == XTSG_DTYPE_F32)
         pool.emplace_back(narrow_rows_f32, static_cast<const float*>(x), ext[0], ext[1], ld[0], ld[1], k0, r0, r1,
-                          ldi, hb);
+                          ldi, hb, fp16());
       else
         pool.emplace_back(narrow_rows_f64, static_cast<const double*>(x), ext[0], ext[1], ld[0], ld[1], k0, r0,
-                          r1, ldi, hb);
+                          r1, ldi, hb, fp16());
     }
     for (auto& th : pool) th.join();
     // the device buffer is free once the compression of slab sl - 2 is done
@@ -533,6 +569,9 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
     else if (dtype == XTSG_DTYPE_F32)
       stage_x64_kernel<float><<<grid_for(tot), 256, 0, s>>>(static_cast<const float*>(xd), ext[0], ext[1], ext[2],
                                                             ld[0], ld[1], x64.ptr);
+    else if (dtype == XTSG_DTYPE_F16)
+      stage_x64_kernel<__half><<<grid_for(tot), 256, 0, s>>>(static_cast<const __half*>(xd), ext[0], ext[1], ext[2],
+                                                             ld[0], ld[1], x64.ptr);
     else
       stage_x64_kernel<__nv_bfloat16><<<grid_for(tot), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(xd), ext[0],
                                                                     ext[1], ext[2], ld[0], ld[1], x64.ptr);
@@ -559,7 +598,8 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
     acc_first = false;
     if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
   }
-  const bool direct = x_dev && dtype == XTSG_DTYPE_BF16 && ld[0] % 8 == 0 && ld[1] % 8 == 0 &&
+  const int32_t op_dtype = fp16() ? XTSG_DTYPE_F16 : XTSG_DTYPE_BF16;
+  const bool direct = x_dev && dtype == op_dtype && ld[0] % 8 == 0 && ld[1] % 8 == 0 &&
                       reinterpret_cast<uintptr_t>(x) % 16 == 0;
   static const bool narrow_on = [] {
     const char* e = std::getenv("XTSG_HOST_NARROW");
@@ -567,7 +607,7 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
   }();
   if (direct) {
     run_bf16_block(static_cast<const __nv_bfloat16*>(x), ld[0], ld[1], off, ext, ydst, acc_first, s);
-  } else if (!x_dev && dtype != XTSG_DTYPE_BF16 && narrow_on) {
+  } else if (!x_dev && (dtype == XTSG_DTYPE_F32 || dtype == XTSG_DTYPE_F64) && narrow_on) {
     compress_host_narrow(x, dtype, ld, off, ext, ydst, acc_first, s);
   } else {
     // Slab pipeline: copy_st moves raw slab k-ranges H2D (host input) while s
@@ -615,15 +655,19 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
       }
       const int64_t rows = kn * ext[1];
       const int blocks = static_cast<int>(std::min<int64_t>(rows, 148 * 8));
+      const bool h = fp16();
       if (dtype == XTSG_DTYPE_F64)
         stage_x_kernel<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
-                                                       ld[0], ld[1], ldi, stage.ptr);
+                                                       ld[0], ld[1], ldi, stage.ptr, h);
       else if (dtype == XTSG_DTYPE_F32)
         stage_x_kernel<float><<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(src), ext[0], ext[1], kn,
-                                                      ld[0], ld[1], ldi, stage.ptr);
+                                                      ld[0], ld[1], ldi, stage.ptr, h);
+      else if (dtype == XTSG_DTYPE_F16)
+        stage_x_kernel<__half><<<blocks, 256, 0, s>>>(reinterpret_cast<const __half*>(src), ext[0], ext[1], kn,
+                                                       ld[0], ld[1], ldi, stage.ptr, h);
       else
         stage_x_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(src), ext[0],
-                                                              ext[1], kn, ld[0], ld[1], ldi, stage.ptr);
+                                                              ext[1], kn, ld[0], ld[1], ldi, stage.ptr, h);
       XLAUNCH_CHECK();
       if (!x_dev) XCUDA(cudaEventRecord(ev_consumed[b], s));
       const int64_t soff[3] = {off[0], off[1], off[2] + k0};
@@ -636,7 +680,22 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
     compact_y_kernel<<<grid_for(ysz), 256, 0, s>>>(ypad.ptr, P, L, M, N, lpad, mpad, accumulate ? 1 : 0, yo.dev);
     XLAUNCH_CHECK();
   }
+  if (fp16()) check_finite16(yo.dev, ysz, s);
   if (yo.host || !x_dev) yo.finish();
+}
+
+// fp16 plans: a binary16 overflow anywhere in the chain shows up as a
+// non-finite replica value -> HalfRangeError (the reference's exception for
+// values outside the binary16 range, errors.hpp).
+void Plan::check_finite16(const float* y, int64_t n, cudaStream_t s) {
+  DevBuf<int> flag(1, s);
+  flag.zero();
+  finite_f32_kernel<<<grid_for(n), 256, 0, s>>>(y, n, flag.ptr);
+  XLAUNCH_CHECK();
+  int h = 0;
+  XCUDA(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+  XCUDA(cudaStreamSynchronize(s));
+  if (h) throw Status(XTSG_E_HALFRANGE, "plan_compress: binary16 range exceeded in the fp16 tensor-core path");
 }
 
 }  // namespace xtsg

@@ -49,6 +49,9 @@ struct Plan {
   DevBuf<double> outer[3];
   int64_t inner_dims[3] = {0, 0, 0};
 
+  bool tensor_core() const { return desc.precision == XTSG_PREC_BF16 || desc.precision == XTSG_PREC_FP16; }
+  bool fp16() const { return desc.precision == XTSG_PREC_FP16; }
+  void check_finite16(const float* y, int64_t n, cudaStream_t s);
   explicit Plan(const xtsg_plan_desc& d);
   Plan(const xtsg_plan_desc& d, const double* u, const double* v, const double* w);
   void build_tc_operands();

@@ -4,6 +4,8 @@
 // tcgen05 (instruction descriptor for kind::f16, shared-memory matrix
 // descriptor with SWIZZLE_128B K-major canonical layout).
 #pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda.h>
 #include <cstdint>
 
@@ -245,6 +247,33 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   d |= static_cast<uint64_t>(1) << 46;              // descriptor version (sm_100)
   d |= static_cast<uint64_t>(2) << 61;              // SWIZZLE_128B
   return d;
+}
+
+// 8 fp32 -> 8 bf16 or fp16 (round to nearest even), packed for one 16-byte
+// shared-memory store of a mode-2 operand row segment.
+__device__ __forceinline__ uint4 pack8(const float* v, bool f16) {
+  uint32_t w[4];
+  if (f16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __half2 h = __floats2half2_rn(v[2 * q], v[2 * q + 1]);
+      w[q] = *reinterpret_cast<uint32_t*>(&h);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+      w[q] = *reinterpret_cast<uint32_t*>(&h);
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// kind::f16 A/B format fields (bits 7-9, 10-12): 1 = bf16, 0 = fp16. An
+// instruction descriptor built by idesc_bf16 is turned into its fp16 twin by
+// clearing them.
+__host__ __device__ constexpr uint32_t idesc_fmt_mask(bool f16) {
+  return f16 ? ~((7u << 7) | (7u << 10)) : ~0u;
 }
 
 // Instruction descriptor: kind::f16, A/B bf16, D fp32, both K-major, M x N.

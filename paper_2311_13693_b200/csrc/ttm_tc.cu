@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t d = tmem + b * 256;
           // ragged edges: the last j tile narrows N, the last i step issues
           // only the K=16 slices that hold data (TMA zero-fills the rest)
-          const uint32_t idesc1 = jt == j_tiles - 1 ? ptx::idesc_bf16(BM, p.n_last) : IDESC1;
+          const uint32_t idesc1 =
+              (jt == j_tiles - 1 ? ptx::idesc_bf16(BM, p.n_last) : IDESC1) & ptx::idesc_fmt_mask(p.f16 != 0);
           for (int ks = 0; ks < k_steps; ++ks) {
             ptx::mbar_wait(&bars->full1[s], ph);
             ptx::tc_fence_after();
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 3) {
     if (lane == 0) {
       // ---- mode-2 MMA issuer ----------------------------------------------
-      const uint32_t idesc2 = ptx::idesc_bf16(BM, p.n2);
+      const uint32_t idesc2 = ptx::idesc_bf16(BM, p.n2) & ptx::idesc_fmt_mask(p.f16 != 0);
       uint32_t t = 0, g = 0;
       for (int u = cid; u < n_units; u += n_clusters) {
         for (int jt = 0; jt < j_tiles; ++jt, ++t) {
@@ -269,15 +270,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
               const int q8 = h * 4 + q4;
-              uint4 pk;
-              __nv_bfloat162 h0 = __floats2bfloat162_rn(v[q4 * 8 + 0], v[q4 * 8 + 1]);
-              __nv_bfloat162 h1 = __floats2bfloat162_rn(v[q4 * 8 + 2], v[q4 * 8 + 3]);
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[q4 * 8 + 4], v[q4 * 8 + 5]);
-              __nv_bfloat162 h3 = __floats2bfloat162_rn(v[q4 * 8 + 6], v[q4 * 8 + 7]);
-              pk.x = *reinterpret_cast<uint32_t*>(&h0);
-              pk.y = *reinterpret_cast<uint32_t*>(&h1);
-              pk.z = *reinterpret_cast<uint32_t*>(&h2);
-              pk.w = *reinterpret_cast<uint32_t*>(&h3);
+              const uint4 pk = ptx::pack8(v + q4 * 8, p.f16 != 0);
               *reinterpret_cast<uint4*>(row + ((q8 ^ (r & 7)) << 4)) = pk;
             }
           }
@@ -336,7 +329,7 @@ EncodeFn encode_fn() {
 }
 
 void make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-              const uint32_t* box) {
+              const uint32_t* box, bool f16) {
   cuuint64_t d[3], s[2];
   cuuint32_t bx[3], es[3] = {1, 1, 1};
   for (int i = 0; i < rank; ++i) {
@@ -347,7 +340,7 @@ void make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
   if (reinterpret_cast<uintptr_t>(base) % 16) usage("tma: base address must be 16-byte aligned");
   for (int i = 0; i < rank - 1; ++i)
     if (s[i] % 16) usage("tma: strides must be multiples of 16 bytes");
-  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, bx, es,
+  CUresult r = encode_fn()(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, bx, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Status(XTSG_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
@@ -361,19 +354,19 @@ void launch_impl(const TtmLaunch& L, cudaStream_t st) {
     const uint64_t dims[2] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.rows_u)};
     const uint64_t str[1] = {static_cast<uint64_t>(L.ld_u) * 2};
     const uint32_t box[2] = {BK, BM};
-    make_map(&mu, L.u, 2, dims, str, box);
+    make_map(&mu, L.u, 2, dims, str, box, L.prm.f16 != 0);
   }
   {
     const uint64_t dims[3] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.nk)};
     const uint64_t str[2] = {static_cast<uint64_t>(L.ld_x0) * 2, static_cast<uint64_t>(L.ld_x1) * 2};
     const uint32_t box[3] = {BK, BN / CS, 1};
-    make_map(&mx, L.x, 3, dims, str, box);
+    make_map(&mx, L.x, 3, dims, str, box, L.prm.f16 != 0);
   }
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.rows_v)};
     const uint64_t str[1] = {static_cast<uint64_t>(L.ld_v) * 2};
     const uint32_t box[2] = {64, static_cast<uint32_t>(L.prm.n2)};
-    make_map(&mv, L.v, 2, dims, str, box);
+    make_map(&mv, L.v, 2, dims, str, box, L.prm.f16 != 0);
   }
   static bool attr_set = false;
   if (!attr_set) {

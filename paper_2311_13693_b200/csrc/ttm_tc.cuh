@@ -23,11 +23,12 @@ struct TtmParams {
   unsigned* sync;          // pair kernel: per-lane slot counters (null = no lane barrier)
   int32_t sync_j;          // pair kernel: lane barrier every sync_j j tiles
   uint64_t u_policy, x_policy;  // L2 cache-policy hints of the U / X tile loads
+  int32_t f16;             // operands are fp16 (XTSG_PREC_FP16) instead of bf16
   float* z;          // out: Z[p][kk][m][l], kk in [0, kc)
 };
 
 struct TtmLaunch {
-  const void* u;      // bf16 stacked U: rows_u x ld_u (row-major), columns [0, ni) used
+  const void* u;      // bf16/fp16 stacked U: rows_u x ld_u (row-major), columns [0, ni) used
   int64_t rows_u, ld_u;
   const void* x;      // bf16 X block: (i, j, k) at i + ld_x0*j + ld_x1*k
   int64_t ni, nj, nk, ld_x0, ld_x1;

@@ -207,8 +207,8 @@ int32_t xtsg_plan_compress_file(xtsg_plan* plan, const char* path, int64_t slab_
         read_exact(f.fd, v->data(), v->size() * 8, off, "read_tensor_file: truncated payload");
         off += static_cast<int64_t>(v->size() * 8);
       }
-      if (p->desc.precision != XTSG_PREC_BF16)
-        usage("plan_compress_file: factor files need a bf16 plan (xtsg_plan_compress_factors)");
+      if (!p->tensor_core())
+        usage("plan_compress_file: factor files need a bf16/fp16 plan (xtsg_plan_compress_factors)");
       p->compress_factors(a.data(), b.data(), c.data(), r, 0, p->desc.dims[2], static_cast<float*>(y),
                           accumulate != 0, s);
       return;
