@@ -338,9 +338,12 @@ def main():
     if not args.no_e2e:
         npdt = {"bf16": None, "f32": np.float32, "f64": np.float64}[args.e2e_dtype]
         tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[args.e2e_dtype]
-        xh = torch.empty((K, cfg["J"], cfg["I"]), dtype=tdt, pin_memory=True)
-        for k in range(0, K, 100):
-            xh[k:k + 100].copy_(X.permute(2, 1, 0)[k:k + 100].to(tdt))
+        # host memory is shared by the node's ranks: the e2e sample per rank
+        # shrinks with N (the metric is a rate; per-rank pinned input <= 32 GB)
+        Ke = max(100, K // world)
+        xh = torch.empty((Ke, cfg["J"], cfg["I"]), dtype=tdt, pin_memory=True)
+        for k in range(0, Ke, 100):
+            xh[k:k + 100].copy_(X.permute(2, 1, 0)[k:min(k + 100, Ke)].to(tdt))
         xh_v = xh.permute(2, 1, 0)
         yh = torch.zeros(ysz, dtype=torch.float32, pin_memory=True)
         del npdt
@@ -367,7 +370,8 @@ def main():
             t = torch.tensor([dt], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": elems_rank * world * args.e2e_steps / dt, "unit": "elements/s",
+        e2e = {"value": cfg["I"] * cfg["J"] * Ke * world * args.e2e_steps / dt, "unit": "elements/s",
+               "slices_per_rank": Ke,
                "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                "d2h_bytes_per_step": int(yh.numel() * 4),
                "host_dtype": args.e2e_dtype, "ms_per_step": dt / args.e2e_steps * 1e3,

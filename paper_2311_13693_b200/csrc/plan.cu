@@ -460,8 +460,12 @@ int host_threads() {
   static const int n = [] {
     const char* e = std::getenv("XTSG_HOST_THREADS");
     if (e && std::atoi(e) > 0) return std::atoi(e);
+    // one process per GPU shares the host: split the cores between the
+    // node's ranks (torchrun exports LOCAL_WORLD_SIZE)
     const unsigned hc = std::thread::hardware_concurrency();
-    return static_cast<int>(std::max(1u, std::min(hc, 32u)));
+    const char* lw = std::getenv("LOCAL_WORLD_SIZE");
+    const unsigned ranks = lw && std::atoi(lw) > 0 ? static_cast<unsigned>(std::atoi(lw)) : 1u;
+    return static_cast<int>(std::max(1u, std::min(hc / ranks, 32u)));
   }();
   return n;
 }

@@ -127,3 +127,21 @@ def test_two_stage_plan_matches_materialized_ensemble(gpu, restated):
     for p in range(P):
         want = restated.comp(t, ens.u[p], ens.v[p], ens.w[p])
         assert rel_diff(want, got[p]) <= BF16_TOL
+
+
+def test_host_narrowing_matches_device_staging_bitwise(gpu):
+    # f32/f64 HOST input is narrowed to bf16 on the host (round to nearest
+    # even, plan.cu compress_host_narrow); f32 DEVICE input is narrowed by the
+    # staging kernel. Same rounding, one slab each -> identical replicas.
+    import torch
+    dims, red, P = (200, 136, 30), (64, 32, 16), 6
+    rng = np.random.default_rng(9)
+    t = np.asfortranarray(rng.standard_normal(dims) * 3.0)
+    t[0, 0, 0], t[1, 0, 0], t[2, 0, 0] = 1e-40, -0.0, 3.0e38   # subnormal, signed zero, near overflow
+    plan = gpu.Plan(dims, red, P, 8, 17)
+    for dt in (np.float32, np.float64):
+        th = np.asfortranarray(t.astype(dt))
+        y_host = plan.compress(th)
+        xd = torch.from_numpy(th.ravel(order="F")).cuda().reshape(dims[2], dims[1], dims[0]).permute(2, 1, 0)
+        y_dev = plan.compress(xd).cpu().numpy()
+        assert np.array_equal(y_host, y_dev), dt
