@@ -135,13 +135,13 @@ __device__ __forceinline__ void fma8(float* y, const uint4& u, uint16_t x) {
 // memory) with V_p[:, j] from the j-major copy: Z[m][r] += y1[r] * V_p[m, j],
 // shared-memory atomics (warps of the CTA share Z rows), rows skewed by r/8 so
 // the 32 lanes hit 32 banks.
-template <int C, bool F16>
-__global__ void __launch_bounds__(NT) coo_fiber_kernel(
+template <int C, bool F16, int UNROLL>
+__global__ void __launch_bounds__(NT, (UNROLL <= 4 ? 3 : 2)) coo_fiber_kernel(
     const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, const float* __restrict__ cv,
     const int64_t* __restrict__ slice_off, const int32_t* __restrict__ slice_cnt, int64_t n_slices,
     const __nv_bfloat16* __restrict__ ut, int64_t ld_ut, int64_t plrows, const __nv_bfloat16* __restrict__ vtj,
     int64_t ld_vtj, int mpad, int lpad, int64_t count, float* __restrict__ z) {
-  constexpr int G = 256 * C, GS = G + G / 8, UNROLL = 8;
+  constexpr int G = 256 * C, GS = G + G / 8;
   extern __shared__ float zs[];  // [mpad][GS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t s = blockIdx.x; s < n_slices; s += gridDim.x) {
@@ -391,12 +391,18 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     kern<<<grid, NT, smem, s>>>(si, sj, sv, off.ptr, cnt.ptr, kd, ut.ptr, ld_ut, plrows, vtj.ptr, ld_vtj,
                                 static_cast<int>(mpad), static_cast<int>(lpad), P, z.ptr);
   };
+  // nonzeros in flight per warp: 4 keeps the kernel at <= 85 registers
+  // (3 CTAs per SM), 8 at 2 CTAs per SM (XTSG_COO_UNROLL)
+  static const int unroll = [] {
+    const char* e = std::getenv("XTSG_COO_UNROLL");
+    return e && std::atoi(e) == 8 ? 8 : 4;
+  }();
   if (fp16()) {
-    if (cg == 2) launch(coo_fiber_kernel<2, true>);
-    else launch(coo_fiber_kernel<1, true>);
+    if (cg == 2) unroll == 8 ? launch(coo_fiber_kernel<2, true, 8>) : launch(coo_fiber_kernel<2, true, 4>);
+    else unroll == 8 ? launch(coo_fiber_kernel<1, true, 8>) : launch(coo_fiber_kernel<1, true, 4>);
   } else {
-    if (cg == 2) launch(coo_fiber_kernel<2, false>);
-    else launch(coo_fiber_kernel<1, false>);
+    if (cg == 2) unroll == 8 ? launch(coo_fiber_kernel<2, false, 8>) : launch(coo_fiber_kernel<2, false, 4>);
+    else unroll == 8 ? launch(coo_fiber_kernel<1, false, 8>) : launch(coo_fiber_kernel<1, false, 4>);
   }
   XLAUNCH_CHECK();
   // 4. mode 3 over the distinct slices
