@@ -446,7 +446,9 @@ extern "C" int32_t xtsg_solve_stacked_ls(int64_t count, const int64_t* rows, int
       const char* e = std::getenv("XTSG_LS_CHOL");
       return !(e && std::atoi(e) == 0);
     }();
-    if (chol_on && cols >= 512 && m >= cols && lsq_chol_dev(A.ptr, m, cols, B.ptr, r, xo.dev, st)) {
+    // the normal-equations path replaces ~2*cols sequential QR launches by a
+    // few DMMA GEMMs and blocked Cholesky steps; below 32 columns QR is cheap
+    if (chol_on && cols >= 32 && m >= cols && lsq_chol_dev(A.ptr, m, cols, B.ptr, r, xo.dev, st)) {
       xo.finish();
       return;
     }
