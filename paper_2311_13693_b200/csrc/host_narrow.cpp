@@ -3,6 +3,8 @@
 // bit-identical to the device's __float2bfloat16 (and, for f64, to its
 // double -> float -> bf16 staging). Compiled by the host compiler with
 // per-ISA clones so the branchless loop vectorises on AVX-512 / AVX2 hosts.
+#include <immintrin.h>
+
 #include <cstdint>
 #include <cstring>
 
@@ -49,6 +51,40 @@ inline void narrow_row(const T* __restrict__ src, int64_t n, uint16_t* __restric
   }
 }
 
+// AVX2: 8 floats -> 8 bf16 per step, RNE + quiet NaN exactly like the scalar
+// rule, written with non-temporal 16-byte stores (no read-for-ownership of
+// the pinned destination: a third less host-memory traffic)
+__attribute__((target("avx2"))) void narrow_row_bf16_avx2(const float* __restrict__ src, int64_t n,
+                                                          uint16_t* __restrict__ dst) {
+  const __m256i bias = _mm256_set1_epi32(0x7fff), one = _mm256_set1_epi32(1);
+  const __m256i absm = _mm256_set1_epi32(0x7fffffff), inf = _mm256_set1_epi32(0x7f800000);
+  const __m256i qbit = _mm256_set1_epi32(0x40);
+  int64_t i = 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  for (; i + 8 <= n; i += 8) {
+    const __m256i u = _mm256_castps_si256(_mm256_loadu_ps(src + i));
+    const __m256i hi = _mm256_srli_epi32(u, 16);
+    __m256i r = _mm256_srli_epi32(_mm256_add_epi32(_mm256_add_epi32(u, bias), _mm256_and_si256(hi, one)), 16);
+    const __m256i nan = _mm256_cmpgt_epi32(_mm256_and_si256(u, absm), inf);
+    r = _mm256_blendv_epi8(r, _mm256_or_si256(hi, qbit), nan);
+    const __m256i pk = _mm256_permute4x64_epi64(_mm256_packus_epi32(r, r), 0x08);
+    const __m128i out = _mm256_castsi256_si128(pk);
+    if (aligned) _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), out);
+    else _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i), out);
+  }
+  for (; i < n; ++i) {
+    uint32_t u;
+    std::memcpy(&u, src + i, 4);
+    const uint32_t rne = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    dst[i] = static_cast<uint16_t>((u & 0x7fffffffu) > 0x7f800000u ? ((u >> 16) | 0x40u) : rne);
+  }
+}
+
+bool host_has_avx2() {
+  static const bool has = __builtin_cpu_supports("avx2");
+  return has;
+}
+
 }  // namespace
 
 __attribute__((target_clones("avx512f", "avx2", "default")))
@@ -58,9 +94,11 @@ void narrow_rows_f32(const float* x, int64_t ni, int64_t nj, int64_t ld0, int64_
     const int64_t j = row % nj, k = k0 + row / nj;
     uint16_t* dst = out + row * ldi;
     if (f16) narrow_row_h(x + j * ld0 + k * ld1, ni, dst);
+    else if (host_has_avx2()) narrow_row_bf16_avx2(x + j * ld0 + k * ld1, ni, dst);
     else narrow_row(x + j * ld0 + k * ld1, ni, dst);
     for (int64_t i = ni; i < ldi; ++i) dst[i] = 0;
   }
+  _mm_sfence();
 }
 
 __attribute__((target_clones("avx512f", "avx2", "default")))
