@@ -93,3 +93,20 @@ def test_fp16_pipeline_end_to_end(gpu):
         rec, met = gpu.decompose(cfg, factors=f)
         errs[name] = max(gpu.evaluate(f, rec).mode_rel_err)
     assert errs["fp16"] <= 2e-3 and errs["fp16"] < errs["bf16"], errs
+
+
+def test_fp16_host_narrowing_matches_device_staging_bitwise(gpu):
+    # host f32/f64 -> binary16 on the host (host_narrow.cpp f2h, RNE incl.
+    # subnormals) == the device staging kernel's __float2half_rn
+    import torch
+    dims, red, P = (160, 96, 20), (32, 32, 16), 4
+    rng = np.random.default_rng(12)
+    t = np.asfortranarray(rng.standard_normal(dims) * 30.0)
+    t[0, 0, 0], t[1, 0, 0], t[2, 0, 0], t[3, 0, 0] = 3e-6, -6.1e-5, 65500.0, 2.9802322387695312e-08
+    plan = gpu.Plan(dims, red, P, 8, 19, precision=gpu.PREC_FP16)
+    for dt in (np.float32, np.float64):
+        th = np.asfortranarray(t.astype(dt))
+        y_host = plan.compress(th)
+        xd = torch.from_numpy(th.ravel(order="F")).cuda().reshape(dims[2], dims[1], dims[0]).permute(2, 1, 0)
+        y_dev = plan.compress(xd).cpu().numpy()
+        assert np.array_equal(y_host, y_dev), dt
