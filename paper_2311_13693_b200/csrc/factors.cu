@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "plan.cuh"
@@ -143,7 +144,11 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
   // last wave's idle SMs amortized), within a quarter of the free HBM
   size_t free_b = 0, total_b = 0;
   XCUDA(cudaMemGetInfo(&free_b, &total_b));
-  const int64_t budget = std::min<int64_t>(int64_t(8) << 30, static_cast<int64_t>(free_b / 4));
+  static const int64_t slab_gb = [] {
+    const char* e = std::getenv("XTSG_SLAB_GB");
+    return e && std::atoi(e) > 0 ? static_cast<int64_t>(std::atoi(e)) : int64_t(8);
+  }();
+  const int64_t budget = std::min<int64_t>(slab_gb << 30, static_cast<int64_t>(free_b / 4));
   const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, budget / (ldi * J * 2)));
   DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * J * ldi), s);
   const size_t smem = static_cast<size_t>(rank) * (TI + TJ) * sizeof(float);
