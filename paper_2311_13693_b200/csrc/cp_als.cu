@@ -1166,29 +1166,39 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
   gram(s.B, n2, R, s.G2);
   gram(s.C, n3, R, s.G3);
   __syncthreads();
-  const int n12 = n1 * n2;
+  const int nf = n2 * nk;  // fibers (j, kk) of the slab
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int lr = lane >> 2, lc = lane & 3;  // DMMA m8n8k4 fragment coordinates
 
   int64_t it = 0;
   bool converged = false;
   double prev = 0.0;
   for (; it < in.cfg.max_iters; ++it) {
-    // ---- A update: slab partial of T(1) (C kr B), reduced over the cluster
-    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
-      const int i = e % n1, r = e / n1;
-      const double* Br = s.B + n2 * r;
-      double acc = 0.0;
-      for (int kk = 0; kk < nk; ++kk) {
-        const double* tk = Ts + i + n12 * kk;
-        double t0 = 0.0, t1 = 0.0;
-        int j = 0;
-        for (; j + 1 < n2; j += 2) {
-          t0 = fma(tk[n1 * j], Br[j], t0);
-          t1 = fma(tk[n1 * (j + 1)], Br[j + 1], t1);
+    // ---- A update: slab partial of T(1) (C kr B) on the fp64 tensor cores
+    // (DMMA m8n8k4: 8 i x 8 r tiles, K = the slab's (j, kk) fibers),
+    // reduced over the cluster
+    {
+      const int nti = (n1 + 7) / 8, ntr = (R + 7) / 8;
+      for (int tile = warp; tile < nti * ntr; tile += nwarps) {
+        const int i0 = (tile % nti) * 8, r0 = (tile / nti) * 8;
+        const int ia = i0 + lr, rb = r0 + lr;
+        double d0 = 0.0, d1 = 0.0;
+        for (int f0 = 0; f0 < nf; f0 += 4) {
+          const int f = f0 + lc;
+          const double a = (ia < n1 && f < nf) ? Ts[ia + static_cast<int64_t>(n1) * f] : 0.0;
+          double b = 0.0;
+          if (f < nf && rb < R) {
+            const int j = f % n2, kk = f / n2;
+            b = s.B[j + n2 * rb] * s.C[(k0 + kk) + n3 * rb];
+          }
+          ptx::dmma(d0, d1, a, b);
         }
-        if (j < n2) t0 = fma(tk[n1 * j], Br[j], t0);
-        acc = fma(s.C[(k0 + kk) + n3 * r], t0 + t1, acc);
+        const int rc = r0 + 2 * lc;
+        if (ia < n1) {
+          if (rc < R) MAp[ia + n1 * rc] = d0;
+          if (rc + 1 < R) MAp[ia + n1 * (rc + 1)] = d1;
+        }
       }
-      MAp[e] = acc;
     }
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
     cl.sync();
@@ -1203,19 +1213,25 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     __syncthreads();
     gram(s.A, n1, R, s.G1);
     __syncthreads();
-    // ---- P = T_c x1 A' on the slab (fibers (j, kk), r fastest), M_B partial
-    for (int e = threadIdx.x; e < R * n2 * nk; e += blockDim.x) {
-      const int r = e % R, f = e / R;  // f = j + n2 * kk
-      const double* col = Ts + static_cast<int64_t>(n1) * f;
-      const double* Ar = s.A + n1 * r;
-      double p0 = 0.0, p1 = 0.0;
-      int i = 0;
-      for (; i + 1 < n1; i += 2) {
-        p0 = fma(col[i], Ar[i], p0);
-        p1 = fma(col[i + 1], Ar[i + 1], p1);
+    // ---- P = A' T_c on the slab (DMMA: 8 r x 8 fibers tiles, K = i), M_B partial
+    {
+      const int ntr = (R + 7) / 8, ntf = (nf + 7) / 8;
+      for (int tile = warp; tile < ntr * ntf; tile += nwarps) {
+        const int r0 = (tile % ntr) * 8, f0 = (tile / ntr) * 8;
+        const int ra = r0 + lr, fb = f0 + lr;
+        double d0 = 0.0, d1 = 0.0;
+        for (int i0 = 0; i0 < n1; i0 += 4) {
+          const int i = i0 + lc;
+          const double a = (ra < R && i < n1) ? s.A[i + n1 * ra] : 0.0;
+          const double b = (fb < nf && i < n1) ? Ts[i + static_cast<int64_t>(n1) * fb] : 0.0;
+          ptx::dmma(d0, d1, a, b);
+        }
+        const int fc = f0 + 2 * lc;
+        if (ra < R) {
+          if (fc < nf) Pl[static_cast<int64_t>(ra) * n2 * kc + fc] = d0;
+          if (fc + 1 < nf) Pl[static_cast<int64_t>(ra) * n2 * kc + fc + 1] = d1;
+        }
       }
-      if (i < n1) p0 = fma(col[i], Ar[i], p0);
-      Pl[static_cast<int64_t>(r) * n2 * kc + f] = p0 + p1;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
@@ -1284,27 +1300,36 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     gram(s.A, n1, R, s.G1);
     gram(s.B, n2, R, s.G2);
     gram(s.C, n3, R, s.G3);
-    // ---- residual of the slab (lanes over i, warps over fibers)
+    // ---- residual of the slab: X^ = A (C kr B)' tile by tile on DMMA
+    // (8 i x 8 fibers, K = r), compared with the resident T
     {
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
       double acc = 0.0;
-      for (int i0 = 0; i0 < n1; i0 += 32) {
-        const int i = i0 + lane;
-        const bool on = i < n1;
-        const double* Ai = s.A + (on ? i : 0);
-        for (int f = warp; f < n2 * nk; f += nw) {
-          const int j = f % n2, kk = f / n2;
-          const double* Bj = s.B + j;
-          const double* Ck = s.C + k0 + kk;
-          double r0 = 0.0, r1 = 0.0;
-          int r = 0;
-          for (; r + 1 < R; r += 2) {
-            r0 = fma(Ai[n1 * r], Bj[n2 * r] * Ck[n3 * r], r0);
-            r1 = fma(Ai[n1 * (r + 1)], Bj[n2 * (r + 1)] * Ck[n3 * (r + 1)], r1);
+      const int nti = (n1 + 7) / 8, ntf = (nf + 7) / 8;
+      for (int tile = warp; tile < nti * ntf; tile += nwarps) {
+        const int i0 = (tile % nti) * 8, f0 = (tile / nti) * 8;
+        const int ia = i0 + lr, fb = f0 + lr;
+        int jb = 0, kb = 0;
+        if (fb < nf) {
+          jb = fb % n2;
+          kb = fb / n2;
+        }
+        double d0 = 0.0, d1 = 0.0;
+        for (int r0 = 0; r0 < R; r0 += 4) {
+          const int r = r0 + lc;
+          const double a = (ia < n1 && r < R) ? s.A[ia + n1 * r] : 0.0;
+          const double b = (fb < nf && r < R) ? s.B[jb + n2 * r] * s.C[(k0 + kb) + n3 * r] : 0.0;
+          ptx::dmma(d0, d1, a, b);
+        }
+        const int fc = f0 + 2 * lc;
+        if (ia < n1) {
+          if (fc < nf) {
+            const double dd = Ts[ia + static_cast<int64_t>(n1) * fc] - d0;
+            acc = fma(dd, dd, acc);
           }
-          if (r < R) r0 = fma(Ai[n1 * r], Bj[n2 * r] * Ck[n3 * r], r0);
-          const double d = on ? Ts[i + static_cast<int64_t>(n1) * f] - (r0 + r1) : 0.0;
-          acc = fma(d, d, acc);
+          if (fc + 1 < nf) {
+            const double dd = Ts[ia + static_cast<int64_t>(n1) * (fc + 1)] - d1;
+            acc = fma(dd, dd, acc);
+          }
         }
       }
       acc = block_sum(acc, s.red);
