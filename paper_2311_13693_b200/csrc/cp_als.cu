@@ -386,9 +386,14 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
         good = false;
         break;
       }
-      const double lkk = sqrt(d);
-      for (int i = k + 1 + lane; i < R; i += 32) Lm[i + R * k] /= lkk;
-      if (lane == 0) Lm[k + R * k] = lkk;
+      // one reciprocal square root per pivot (no divisions): L(k,k) = d * rsqrt(d),
+      // 1 / L(k,k) kept on the diagonal of s.V for the inverse below
+      const double rl = rsqrt(d);
+      for (int i = k + 1 + lane; i < R; i += 32) Lm[i + R * k] *= rl;
+      if (lane == 0) {
+        Lm[k + R * k] = d * rl;
+        s.V[k + R * k] = rl;
+      }
       __syncwarp();
       const int m = R - k - 1;
       for (int t = lane; t < m * m; t += 32) {
@@ -397,24 +402,21 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
       }
       __syncwarp();
     }
+    if (good) {
+      // L^-1 column by column (lane c), still inside warp 0: H^-1 = L^-T L^-1
+      for (int c = lane; c < R; c += 32)
+        for (int i = c + 1; i < R; ++i) {
+          double acc = 0.0;
+          for (int j = c; j < i; ++j) acc = fma(Lm[i + R * j], s.V[j + R * c], acc);
+          s.V[i + R * c] = -acc * s.V[i + R * i];
+        }
+    }
     if (lane == 0) *ok = good ? 1 : 0;
     }
   }
   __syncthreads();
   if (*ok) {
-    // H^-1 = L^-T L^-1: lane c of warp 0 forms column c of L^-1 (into s.V),
-    // then H^-1 (into s.H) and F = Mt H^-1 run over all threads
-    if (threadIdx.x < 32) {
-      for (int c = threadIdx.x; c < R; c += 32) {
-        s.V[c + R * c] = 1.0 / s.P[c + R * c];
-        for (int i = c + 1; i < R; ++i) {
-          double acc = 0.0;
-          for (int j = c; j < i; ++j) acc = fma(s.P[i + R * j], s.V[j + R * c], acc);
-          s.V[i + R * c] = -acc / s.P[i + R * i];
-        }
-      }
-    }
-    __syncthreads();
+    // H^-1 (into s.H) and F = Mt H^-1 over all threads
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
       const int a = e % R, b = e / R;
       double acc = 0.0;
