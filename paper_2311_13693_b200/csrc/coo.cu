@@ -255,18 +255,6 @@ __global__ void gather_w_kernel(const float* __restrict__ wf, int64_t count, int
   }
 }
 
-__global__ void compact_y2_kernel(const float* __restrict__ ypad, int64_t count, int64_t L, int64_t M, int64_t N,
-                                  int64_t lpad, int64_t mpad, int32_t accumulate, float* __restrict__ y) {
-  const int64_t per = L * M * N, total = count * per;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t p = e / per, r = e % per;
-    const int64_t l = r % L, mn = r / L, m = mn % M, n = mn / M;
-    const float v = ypad[p * mpad * lpad * N + (m * lpad + l) + mpad * lpad * n];
-    y[e] = accumulate ? y[e] + v : v;
-  }
-}
-
 int64_t round_up256(int64_t a) { return (a + 255) / 256 * 256; }
 
 int gridn(int64_t work) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * 16))); }
@@ -291,7 +279,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
   const int64_t ysz = P * L * M * N;
-  const bool padded = (lpad != L) || (mpad != M);
+  const bool padded = virt_padded();
   OutView<float> yo(y, static_cast<size_t>(ysz), s);
   if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
   if (nnz == 0) {
@@ -299,8 +287,8 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     if (yo.host) yo.finish();
     return;
   }
-  const int64_t plrows = P * lpad;
-  const int64_t ld_ut = round_up256(plrows), ld_vtj = P * mpad;
+  const int64_t plrows = vP * lpad;
+  const int64_t ld_ut = round_up256(plrows), ld_vtj = vP * mpad;
   if (!ut.ptr) {
     // i-major U (rows padded to 256 with zeros) and j-major V copies
     ut = DevBuf<__nv_bfloat16>(static_cast<size_t>(I * ld_ut), s);
@@ -374,7 +362,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     count_launch();
   }
   // 3. fibers -> Z[p][kd][m][l]
-  DevBuf<float> z(static_cast<size_t>(P * kd * mpad * lpad), s);
+  DevBuf<float> z(static_cast<size_t>(vP * kd * mpad * lpad), s);
   // C groups of 256 rows per pass, Z pass in shared memory (mpad x 1.125*G fp32)
   static const int cenv = [] {
     const char* e = std::getenv("XTSG_COO_C");
@@ -389,7 +377,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     XCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     const int grid = static_cast<int>(std::min<int64_t>(kd, static_cast<int64_t>(sm_count()) * std::max(1, per_sm)));
     kern<<<grid, NT, smem, s>>>(si, sj, sv, off.ptr, cnt.ptr, kd, ut.ptr, ld_ut, plrows, vtj.ptr, ld_vtj,
-                                static_cast<int>(mpad), static_cast<int>(lpad), P, z.ptr);
+                                static_cast<int>(mpad), static_cast<int>(lpad), vP, z.ptr);
   };
   // nonzeros in flight per warp: 4 keeps the kernel at <= 85 registers
   // (3 CTAs per SM), 8 at 2 CTAs per SM (XTSG_COO_UNROLL)
@@ -406,25 +394,24 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   }
   XLAUNCH_CHECK();
   // 4. mode 3 over the distinct slices
-  DevBuf<float> wg(static_cast<size_t>(P * N * kd), s);
-  gather_w_kernel<<<gridn(P * N * kd), 256, 0, s>>>(wf.ptr, P, N, K, uk.ptr, kd, wg.ptr);
+  DevBuf<float> wg(static_cast<size_t>(vP * N * kd), s);
+  gather_w_kernel<<<gridn(vP * N * kd), 256, 0, s>>>(wf.ptr, vP, N, K, uk.ptr, kd, wg.ptr);
   XLAUNCH_CHECK();
   DevBuf<float> ypad;
   float* ydst = yo.dev;
   if (padded) {
-    ypad = DevBuf<float>(static_cast<size_t>(P * mpad * lpad * N), s);
+    ypad = DevBuf<float>(static_cast<size_t>(vP * mpad * lpad * N), s);
     ydst = ypad.ptr;
   }
   GemmArgs<float> g;
-  g.m = mpad * lpad; g.n = N; g.k = kd; g.batch = P;
+  g.m = mpad * lpad; g.n = N; g.k = kd; g.batch = vP;
   g.a = z.ptr; g.lda = mpad * lpad; g.stride_a = kd * mpad * lpad;
   g.b = wg.ptr; g.ldb = kd; g.stride_b = N * kd;
   g.c = ydst; g.ldc = mpad * lpad; g.stride_c = mpad * lpad * N;
   g.beta = (accumulate && !padded) ? 1.f : 0.f;
   gemm_simt(g, s);
   if (padded) {
-    compact_y2_kernel<<<gridn(ysz), 256, 0, s>>>(ypad.ptr, P, L, M, N, lpad, mpad, accumulate ? 1 : 0, yo.dev);
-    XLAUNCH_CHECK();
+    compact(ypad.ptr, yo.dev, accumulate, s);
   }
   if (fp16()) check_finite16(yo.dev, ysz, s);
   if (yo.host) yo.finish();

@@ -85,18 +85,6 @@ __global__ void to_f32_kernel(const double* __restrict__ s, int64_t n, float* __
     d[e] = static_cast<float>(s[e]);
 }
 
-__global__ void compact_y3_kernel(const float* __restrict__ ypad, int64_t count, int64_t L, int64_t M, int64_t N,
-                                  int64_t lpad, int64_t mpad, int32_t accumulate, float* __restrict__ y) {
-  const int64_t per = L * M * N, total = count * per;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t p = e / per, r = e % per;
-    const int64_t l = r % L, mn = r / L, m = mn % M, n = mn / M;
-    const float v = ypad[p * mpad * lpad * N + (m * lpad + l) + mpad * lpad * n];
-    y[e] = accumulate ? y[e] + v : v;
-  }
-}
-
 int g1(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 16))); }
 
 }  // namespace
@@ -119,7 +107,7 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
   if (k0 < 0 || k1 > K || k0 >= k1) usage("plan_compress_factors: k range outside the tensor");
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
   const int64_t ysz = P * L * M * N;
-  const bool padded = (lpad != L) || (mpad != M);
+  const bool padded = virt_padded();
   OutView<float> yo(y, static_cast<size_t>(ysz), s);
   if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
   InView<double> da(a, static_cast<size_t>(I * rank), s), db(b, static_cast<size_t>(J * rank), s),
@@ -135,7 +123,7 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
   float* ydst = yo.dev;
   bool acc = accumulate;
   if (padded) {
-    ypad = DevBuf<float>(static_cast<size_t>(P * mpad * lpad * N), s);
+    ypad = DevBuf<float>(static_cast<size_t>(vP * mpad * lpad * N), s);
     ydst = ypad.ptr;
     acc = false;
   }
@@ -165,8 +153,7 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
     acc = true;
   }
   if (padded) {
-    compact_y3_kernel<<<g1(ysz), 256, 0, s>>>(ypad.ptr, P, L, M, N, lpad, mpad, accumulate ? 1 : 0, yo.dev);
-    XLAUNCH_CHECK();
+    compact(ypad.ptr, yo.dev, accumulate, s);
   }
   if (fp16()) check_finite16(yo.dev, ysz, s);
   if (yo.host) yo.finish();

@@ -34,26 +34,29 @@ namespace xtsg {
 
 namespace {
 
-// P column-major (rows x cols) fp64 matrices -> row-major [p*rows_pad + r][c]
-// with leading dimension ld, scaled by `scale` (a power of two: exact) and
-// converted to T. 32x32 smem transpose tiles.
+// P column-major (rows x cols) fp64 matrices -> the rows of virtual replica q
+// (p = q / per_p, split index (q / sdiv) % smod, rows [split * srows, +srows)
+// of matrix p) at dst[(q*rows_pad + r)*ld + c], scaled and converted to T.
 template <class T>
-__global__ void pack_rows_kernel(const double* __restrict__ src, int64_t rows, int64_t cols, int64_t rows_pad,
-                                 int64_t ld, double scale, T* __restrict__ dst) {
+__global__ void pack_virtual_kernel(const double* __restrict__ src, int64_t rows, int64_t cols, int64_t per_p,
+                                    int64_t sdiv, int64_t smod, int64_t srows, int64_t rows_pad, int64_t ld,
+                                    double scale, T* __restrict__ dst) {
   __shared__ double tile[32][33];
-  const int64_t p = blockIdx.z;
+  const int64_t q = blockIdx.z;
+  const int64_t p = q / per_p, split = (q / sdiv) % smod;
+  const int64_t rbase = split * srows;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
   const double* s = src + p * rows * cols;
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const int64_t c = c0 + dy, r = r0 + threadIdx.x;
-    tile[dy][threadIdx.x] = (r < rows && c < cols) ? s[r + rows * c] : 0.0;
+    tile[dy][threadIdx.x] = (r < srows && rbase + r < rows && c < cols) ? s[(rbase + r) + rows * c] : 0.0;
   }
   __syncthreads();
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const int64_t r = r0 + dy, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) {
+    if (r < srows && rbase + r < rows && c < cols) {
       const double v = tile[threadIdx.x][dy] * scale;
-      T* o = dst + (p * rows_pad + r) * ld + c;
+      T* o = dst + (q * rows_pad + r) * ld + c;
       if constexpr (std::is_same<T, float>::value) *o = static_cast<float>(v);
       else if constexpr (std::is_same<T, __half>::value) *o = __double2half(v);
       else *o = __double2bfloat16(v);
@@ -62,12 +65,31 @@ __global__ void pack_rows_kernel(const double* __restrict__ src, int64_t rows, i
 }
 
 template <class T>
-void pack_rows(const double* src, int64_t count, int64_t rows, int64_t cols, int64_t rows_pad, int64_t ld, T* dst,
-               cudaStream_t st, double scale = 1.0) {
-  dim3 grid(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(rows, 32)),
-            static_cast<unsigned>(count));
-  pack_rows_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, rows_pad, ld, scale, dst);
+void pack_virtual(const double* src, int64_t vcount, int64_t rows, int64_t cols, int64_t per_p, int64_t sdiv,
+                  int64_t smod, int64_t srows, int64_t rows_pad, int64_t ld, T* dst, cudaStream_t st,
+                  double scale = 1.0) {
+  dim3 grid(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(srows, 32)),
+            static_cast<unsigned>(vcount));
+  pack_virtual_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, per_p, sdiv, smod, srows, rows_pad, ld,
+                                                       scale, dst);
   XLAUNCH_CHECK();
+}
+
+// ypad[q][(m'*lpad + l')][n] of virtual replica q = (p*lsplit + a)*msplit + b
+// -> y(p, a*Lv + l', b*Mv + m', n)
+__global__ void compact_virtual_kernel(const float* __restrict__ ypad, int64_t count, int64_t L, int64_t M, int64_t N,
+                                       int64_t lpad, int64_t mpad, int64_t lsplit, int64_t msplit, int64_t Lv,
+                                       int64_t Mv, int32_t accumulate, float* __restrict__ y) {
+  const int64_t per = L * M * N, total = count * per;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t p = e / per, r = e % per;
+    const int64_t l = r % L, mn = r / L, m = mn % M, n = mn / M;
+    const int64_t a = l / Lv, b = m / Mv;
+    const int64_t q = (p * lsplit + a) * msplit + b;
+    const float v = ypad[q * mpad * lpad * N + ((m - b * Mv) * lpad + (l - a * Lv)) + mpad * lpad * n];
+    y[e] = accumulate ? y[e] + v : v;
+  }
 }
 
 // fp32 -> 16-bit operand storage: bf16 bits, or fp16 bits for XTSG_PREC_FP16
@@ -115,19 +137,6 @@ __global__ void stage_x64_kernel(const T* __restrict__ src, int64_t ni, int64_t 
     const T v = src[i + ld0 * j + ld1 * k];
     if constexpr (std::is_same<T, __nv_bfloat16>::value) dst[e] = static_cast<double>(__bfloat162float(v));
     else dst[e] = static_cast<double>(v);
-  }
-}
-
-// Ypad (per replica (m*Lpad + l) x N column-major) -> y (l + L*(m + M*n)).
-__global__ void compact_y_kernel(const float* __restrict__ ypad, int64_t count, int64_t L, int64_t M, int64_t N,
-                                 int64_t lpad, int64_t mpad, int32_t accumulate, float* __restrict__ y) {
-  const int64_t per = L * M * N, total = count * per;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t p = e / per, r = e % per;
-    const int64_t l = r % L, mn = r / L, m = mn % M, n = mn / M;
-    const float v = ypad[p * mpad * lpad * N + (m * lpad + l) + mpad * lpad * n];
-    y[e] = accumulate ? y[e] + v : v;
   }
 }
 
@@ -247,20 +256,26 @@ Plan::Plan(const xtsg_plan_desc& d, const double* u, const double* v, const doub
 void Plan::build_tc_operands() {
   const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
-  lpad = pad_reduced(L);
-  mpad = pad_reduced(M);
-  if (lpad < 0 || mpad < 0) usage("plan: the bf16 tensor-core path supports reduced dims <= 128");
+  lsplit = ceil_div(L, 128);
+  msplit = ceil_div(M, 128);
+  Lv = ceil_div(L, lsplit);
+  Mv = ceil_div(M, msplit);
+  vP = P * lsplit * msplit;
+  lpad = pad_reduced(Lv);
+  mpad = pad_reduced(Mv);
   rpb = 128 / lpad;
   n2 = rpb * mpad;
   if (n2 > 128) usage("plan: (128/Lpad)*Mpad must be <= 128 for the tensor-core path");
-  rows_u = round_up(P * lpad, 128);  // odd row-block counts run the kernel without clusters
+  rows_u = round_up(vP * lpad, 128);  // odd row-block counts run the kernel without clusters
   ld_u = round_up(I, 8);
   ld_v = round_up(J, 8);
   ustack = DevBuf<__nv_bfloat16>(static_cast<size_t>(rows_u * ld_u), st);
   ustack.zero();
-  vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(P * mpad * ld_v), st);
+  vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(vP * mpad * ld_v), st);
   vt.zero();
-  wf = DevBuf<float>(static_cast<size_t>(P * N * K), st);
+  wf = DevBuf<float>(static_cast<size_t>(vP * N * K), st);
+  const int64_t per_p = lsplit * msplit;
+  // U rows of virtual replica q: split a = (q / msplit) % lsplit; V rows: b = q % msplit
   if (fp16()) {
     // fp16 keeps 3 more mantissa bits than bf16 but tops out at 65504: the
     // mode-1 partial sums (the mode-2 operand, |sum_i U X| ~ sqrt(I) |X|)
@@ -268,13 +283,15 @@ void Plan::build_tc_operands() {
     // two, so Y is unchanged); non-finite replicas raise HalfRangeError.
     int sexp = 0;
     while ((int64_t(1) << (2 * (sexp + 2))) < I) ++sexp;
-    pack_rows<__half>(u64.ptr, P, L, I, lpad, ld_u, reinterpret_cast<__half*>(ustack.ptr), st, std::ldexp(1.0, -sexp));
-    pack_rows<__half>(v64.ptr, P, M, J, mpad, ld_v, reinterpret_cast<__half*>(vt.ptr), st);
-    pack_rows<float>(w64.ptr, P, N, K, N, K, wf.ptr, st, std::ldexp(1.0, sexp));
+    pack_virtual<__half>(u64.ptr, vP, L, I, per_p, msplit, lsplit, Lv, lpad, ld_u,
+                         reinterpret_cast<__half*>(ustack.ptr), st, std::ldexp(1.0, -sexp));
+    pack_virtual<__half>(v64.ptr, vP, M, J, per_p, 1, msplit, Mv, mpad, ld_v, reinterpret_cast<__half*>(vt.ptr),
+                         st);
+    pack_virtual<float>(w64.ptr, vP, N, K, per_p, 1, 1, N, N, K, wf.ptr, st, std::ldexp(1.0, sexp));
   } else {
-    pack_rows<__nv_bfloat16>(u64.ptr, P, L, I, lpad, ld_u, ustack.ptr, st);
-    pack_rows<__nv_bfloat16>(v64.ptr, P, M, J, mpad, ld_v, vt.ptr, st);
-    pack_rows<float>(w64.ptr, P, N, K, N, K, wf.ptr, st);
+    pack_virtual<__nv_bfloat16>(u64.ptr, vP, L, I, per_p, msplit, lsplit, Lv, lpad, ld_u, ustack.ptr, st);
+    pack_virtual<__nv_bfloat16>(v64.ptr, vP, M, J, per_p, 1, msplit, Mv, mpad, ld_v, vt.ptr, st);
+    pack_virtual<float>(w64.ptr, vP, N, K, per_p, 1, 1, N, N, K, wf.ptr, st);
   }
   // the fp64 copies are not needed by the bf16 path any more
   u64.release();
@@ -344,13 +361,13 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
   int64_t ldv = ld_v;
   if (off[1] % 8) {
     ldv = round_up(ext[1], 8);
-    vtmp = DevBuf<__nv_bfloat16>(static_cast<size_t>(P * mpad * ldv), s);
+    vtmp = DevBuf<__nv_bfloat16>(static_cast<size_t>(vP * mpad * ldv), s);
     vtmp.zero();
-    XCUDA(cudaMemcpy2DAsync(vtmp.ptr, ldv * 2, vt.ptr + off[1], ld_v * 2, ext[1] * 2, P * mpad,
+    XCUDA(cudaMemcpy2DAsync(vtmp.ptr, ldv * 2, vt.ptr + off[1], ld_v * 2, ext[1] * 2, vP * mpad,
                             cudaMemcpyDeviceToDevice, s));
     vop = vtmp.ptr;
   }
-  const int64_t per_k = P * mpad * lpad;  // Z floats per slice
+  const int64_t per_k = vP * mpad * lpad;  // Z floats per slice
   const int64_t kc_max = std::max<int64_t>(1, std::min<int64_t>(ext[2], (int64_t(1) << 28) / per_k));
   ensure_z(kc_max * per_k, s);
   bool acc = first_accumulate;
@@ -359,7 +376,7 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     TtmLaunch tl{};
     tl.u = uop; tl.rows_u = rows_u; tl.ld_u = ldu;
     tl.x = x; tl.ni = ext[0]; tl.nj = ext[1]; tl.nk = ext[2]; tl.ld_x0 = ld0; tl.ld_x1 = ld1;
-    tl.v = vop; tl.rows_v = P * mpad; tl.ld_v = ldv;
+    tl.v = vop; tl.rows_v = vP * mpad; tl.ld_v = ldv;
     tl.mpad = static_cast<int>(mpad);
     tl.grid_limit = grid_limit;
     if (!sync_ctr.ptr) sync_ctr = DevBuf<unsigned>(256, s);
@@ -372,7 +389,7 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     tl.prm.lpad = static_cast<int32_t>(lpad);
     tl.prm.rpb = static_cast<int32_t>(rpb);
     tl.prm.n2 = static_cast<int32_t>(n2);
-    tl.prm.count = static_cast<int32_t>(P);
+    tl.prm.count = static_cast<int32_t>(vP);
     const int64_t rem_i = ext[0] - 64 * (tl.prm.k_steps - 1);
     const int64_t rem_j = ext[1] - static_cast<int64_t>(ttm_block_n()) * (tl.prm.j_tiles - 1);
     tl.prm.k16_last = static_cast<int32_t>(ceil_div(rem_i, 16));
@@ -416,7 +433,7 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     }
     // mode 3: Y_p (Mpad*Lpad x N) (+)= Z_p (Mpad*Lpad x kc) * W_p[:, k0+kb : +kc]^T
     GemmArgs<float> g;
-    g.m = mpad * lpad; g.n = N; g.k = kc; g.batch = P;
+    g.m = mpad * lpad; g.n = N; g.k = kc; g.batch = vP;
     g.a = zbuf.ptr; g.lda = mpad * lpad; g.stride_a = kc * mpad * lpad;
     g.b = wf.ptr + off[2] + kb; g.ldb = K; g.stride_b = N * K;
     g.c = ydst; g.ldc = mpad * lpad; g.stride_c = mpad * lpad * N;
@@ -590,14 +607,14 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
   }
 
   // ---- bf16 tensor-core path ----
-  const bool padded = (lpad != L) || (mpad != M);
+  const bool padded = virt_padded();
   OutView<float> yo(static_cast<float*>(y), static_cast<size_t>(ysz), s);
   if (accumulate && yo.host && !padded) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
   DevBuf<float> ypad;
   float* ydst = yo.dev;
   bool acc_first = accumulate;
   if (padded) {
-    ypad = DevBuf<float>(static_cast<size_t>(P * mpad * lpad * N), s);
+    ypad = DevBuf<float>(static_cast<size_t>(vP * mpad * lpad * N), s);
     ydst = ypad.ptr;
     acc_first = false;
     if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
@@ -681,11 +698,18 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
     }
   }
   if (padded) {
-    compact_y_kernel<<<grid_for(ysz), 256, 0, s>>>(ypad.ptr, P, L, M, N, lpad, mpad, accumulate ? 1 : 0, yo.dev);
-    XLAUNCH_CHECK();
+    compact(ypad.ptr, yo.dev, accumulate, s);
   }
   if (fp16()) check_finite16(yo.dev, ysz, s);
   if (yo.host || !x_dev) yo.finish();
+}
+
+void Plan::compact(const float* ypad, float* y, bool accumulate, cudaStream_t s) {
+  const int64_t P = desc.count, L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2];
+  const int64_t ysz = P * L * M * N;
+  compact_virtual_kernel<<<grid_for(ysz), 256, 0, s>>>(ypad, P, L, M, N, lpad, mpad, lsplit, msplit, Lv, Mv,
+                                                       accumulate ? 1 : 0, y);
+  XLAUNCH_CHECK();
 }
 
 // fp16 plans: a binary16 overflow anywhere in the chain shows up as a

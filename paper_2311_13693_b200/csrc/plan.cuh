@@ -19,6 +19,11 @@ struct Plan {
   DevBuf<double> u64, v64, w64;
   // tensor-core operands
   int64_t lpad = 0, mpad = 0, rpb = 0, n2 = 0, rows_u = 0, ld_u = 0, ld_v = 0;
+  // virtual replicas: reduced dims above 128 are split into lsplit x msplit
+  // pieces of at most Lv x Mv rows (each a tensor-core replica of its own
+  // with the same W); vP = P * lsplit * msplit. M splits repeat the mode-1
+  // product of their rows (algorithmic flops stay P*L*...), L splits are free.
+  int64_t vP = 0, lsplit = 1, msplit = 1, Lv = 0, Mv = 0;
   DevBuf<__nv_bfloat16> ustack, vt;
   DevBuf<float> wf;
   DevBuf<float> zbuf;
@@ -52,6 +57,11 @@ struct Plan {
   bool tensor_core() const { return desc.precision == XTSG_PREC_BF16 || desc.precision == XTSG_PREC_FP16; }
   bool fp16() const { return desc.precision == XTSG_PREC_FP16; }
   void check_finite16(const float* y, int64_t n, cudaStream_t s);
+  bool virt_padded() const {
+    return lsplit > 1 || msplit > 1 || lpad != desc.reduced[0] || mpad != desc.reduced[1];
+  }
+  // ypad (vP x (Mpad*Lpad) x N, the tensor-core layout) -> y (P replicas L x M x N)
+  void compact(const float* ypad, float* y, bool accumulate, cudaStream_t s);
   explicit Plan(const xtsg_plan_desc& d);
   Plan(const xtsg_plan_desc& d, const double* u, const double* v, const double* w);
   void build_tc_operands();

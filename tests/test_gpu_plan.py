@@ -145,3 +145,33 @@ def test_host_narrowing_matches_device_staging_bitwise(gpu):
         xd = torch.from_numpy(th.ravel(order="F")).cuda().reshape(dims[2], dims[1], dims[0]).permute(2, 1, 0)
         y_dev = plan.compress(xd).cpu().numpy()
         assert np.array_equal(y_host, y_dev), dt
+
+
+@pytest.mark.parametrize("dims,red,P", [
+    ((300, 260, 40), (200, 64, 16), 2),     # L > 128: two free L splits
+    ((256, 300, 40), (96, 160, 32), 2),     # M > 128: M split (mode 1 repeated)
+    ((260, 270, 30), (256, 256, 24), 1),    # C5 L = M = 256
+])
+def test_reduced_dims_above_128_virtual_replicas(gpu, restated, dims, red, P):
+    # reduced dims beyond one 128-row block run as virtual replicas (L/M
+    # splits sharing W); dense, factored and sparse inputs
+    ens = restated.make_ensemble(dims, red, P, 8, seed=27)
+    t = _tensor(dims, 6, rank=4)
+    want = [restated.comp(t, ens[0][p], ens[1][p], ens[2][p]) for p in range(P)]
+    plan = gpu.Plan(dims, red, P, 8, 27)
+    got = gpu.Plan.replicas(plan.compress(t), P, red)
+    for p in range(P):
+        assert rel_diff(want[p], got[p]) <= BF16_TOL
+    # accumulate over two k blocks
+    y = plan.compress(np.asfortranarray(t[:, :, :10]), extent=(dims[0], dims[1], 10))
+    y = plan.compress(np.asfortranarray(t[:, :, 10:]), y=y, offset=(0, 0, 10), accumulate=True)
+    for p, g in enumerate(gpu.Plan.replicas(y, P, red)):
+        assert rel_diff(want[p], g) <= BF16_TOL
+    # sparse COO of the same tensor's nonzeros
+    i, j, k = np.nonzero(np.abs(t) > 2.0)
+    v = t[i, j, k].astype(np.float32)
+    ts = np.zeros(dims, order="F")
+    ts[i, j, k] = v
+    got = gpu.Plan.replicas(plan.compress_coo(i.astype(np.int32), j.astype(np.int32), k.astype(np.int32), v), P, red)
+    for p in range(P):
+        assert rel_diff(restated.comp(ts, ens[0][p], ens[1][p], ens[2][p]), got[p]) <= BF16_TOL
