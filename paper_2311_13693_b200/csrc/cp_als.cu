@@ -1363,18 +1363,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
   cl.sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
-// cluster size for the small-replica kernel: the smallest CL in {2, 4, 8}
-// whose per-CTA working set fits 110 KB (two clusters' CTAs per SM); 0 when
-// none does (or XTSG_ALS_CLUSTER=0)
+// cluster size for the small-replica kernel: the largest CL in {8, 4, 2}
+// (at most one slice per CTA) whose per-CTA working set fits 110 KB — more
+// CTAs per instance shorten every phase of the latency-bound sweep (30^3:
+// 61 -> 51 us per sweep from CL 4 to 8); 0 when none fits (or
+// XTSG_ALS_CLUSTER=0; XTSG_ALS_CLUSTER=1|2|4|8 forces a size)
 int als_cluster_size(int64_t n1, int64_t n2, int64_t n3, int64_t R) {
   static const int env = [] {
     const char* e = std::getenv("XTSG_ALS_CLUSTER");
     return e ? std::atoi(e) : -1;
   }();
   if (env == 0 || R > 32 || n1 > 64 || n2 > 64 || n3 > 64 || n3 < 2) return 0;
-  for (int cl : {2, 4, 8}) {
+  for (int cl : {16, 8, 4, 2, 1}) {
     if (env > 0 && cl != env) continue;
-    if (cl > n3) break;
+    if (env <= 0 && (cl == 1 || cl == 16)) continue;  // 1 and 16 (non-portable) only on request
+    if (cl > n3) continue;
     if (cluster_layout(int(n1), int(n2), int(n3), int(R), cl).doubles * 8 <= 110 * 1024) return cl;
   }
   return 0;
@@ -1390,9 +1393,12 @@ void launch_als_cluster(const AlsInst* din, int64_t count, int n1, int n2, int n
   const size_t smem = cluster_layout(n1, n2, n3, R, CL).doubles * 8;
   auto go = [&](auto kern) {
     XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (CL > 8) XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     kern<<<static_cast<unsigned>(count * CL), NT, smem, st>>>(din, n1, n2, n3, ia.ptr, ib.ptr, ic.ptr, tn.ptr);
   };
-  if (CL == 2) go(als_cluster_kernel<2>);
+  if (CL == 16) go(als_cluster_kernel<16>);
+  else if (CL == 1) go(als_cluster_kernel<1>);
+  else if (CL == 2) go(als_cluster_kernel<2>);
   else if (CL == 4) go(als_cluster_kernel<4>);
   else go(als_cluster_kernel<8>);
   XLAUNCH_CHECK();
