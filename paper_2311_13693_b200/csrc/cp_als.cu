@@ -877,7 +877,10 @@ __device__ void big_pass2(const double* __restrict__ T, int n1, int n2, int n3, 
         s.M[j + n2 * r] = fma(s.C[k + n3 * r], v, s.M[j + n2 * r]);
       }
     }
-    if (threadIdx.x == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, c + g.ns);
+    // pass 2: the group that just consumed chunk c refills that stage with
+    // chunk c + ns (its empty barrier only needs this group's arrivals), so
+    // the two groups pipeline independently instead of waiting on each other
+    if ((c & 1) == grp && gtid == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, c + g.ns);
   }
   __syncthreads();
 }
