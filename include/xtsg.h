@@ -214,6 +214,18 @@ int32_t xtsg_plan_compress_coo(xtsg_plan* plan, const int32_t* i, const int32_t*
                                const int32_t* k, const float* val, int64_t nnz, void* y,
                                int32_t accumulate, void* stream);
 
+/* Sparse input already in CSF form (new; mode order k -> j -> i): slice q
+ * has mode-3 index slice_k[q] and fibers [slice_ptr[q], slice_ptr[q+1]);
+ * fiber f has mode-2 index fiber_j[f] and nonzeros [fiber_ptr[f],
+ * fiber_ptr[f+1]) with mode-1 indices nz_i and values val. No sort or
+ * run-length pass: the fibers feed the fiber kernel directly. Duplicated
+ * slices/fibers/coordinates sum. XTSG_E_DATA for out-of-range indices or
+ * inconsistent pointers. */
+int32_t xtsg_plan_compress_csf(xtsg_plan* plan, int64_t n_slices, const int32_t* slice_k,
+                               const int64_t* slice_ptr, int64_t n_fibers, const int32_t* fiber_j,
+                               const int64_t* fiber_ptr, int64_t nnz, const int32_t* nz_i,
+                               const float* val, void* y, int32_t accumulate, void* stream);
+
 /* Out-of-core .xts source (io.hpp:9-12, io.cpp:55-125).
  * xts_header reads and validates a file's header: kind 0 dense tensor, 1
  * factor triple; dims; rank (factors). plan_compress_file compresses the

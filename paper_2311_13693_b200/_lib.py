@@ -140,6 +140,7 @@ _SIGS = {
     "xtsg_plan_compress_factors": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I32, _P]),
     "xtsg_plan_compress_coo": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _I32, _P]),
     "xtsg_xts_header": (_I32, [C.c_char_p, _P, _P, _P]),
+    "xtsg_plan_compress_csf": (_I32, [_P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I32, _P]),
     "xtsg_plan_compress_file": (_I32, [_P, C.c_char_p, _I64, _P, _I32, _P]),
     "xtsg_relative_error": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _I64, _P]),
     "xtsg_cp_als_batched": (_I32, [_I64, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),

@@ -347,6 +347,41 @@ class Plan:
                                          1 if accumulate else 0, st))
         return y
 
+    def compress_csf(self, slice_k, slice_ptr, fiber_j, fiber_ptr, nz_i, val, y=None, accumulate=False,
+                     stream=None, device=None):
+        """xtsg_plan_compress_csf: CSF input (slices k -> fibers j -> nonzeros i), no sort pass."""
+        def as_arr(v, dt):
+            if isinstance(v, np.ndarray) or not hasattr(v, "data_ptr"):
+                return np.ascontiguousarray(np.asarray(v, dt))
+            return v
+        slice_k, fiber_j, nz_i = (as_arr(v, np.int32) for v in (slice_k, fiber_j, nz_i))
+        slice_ptr, fiber_ptr = (as_arr(v, np.int64) for v in (slice_ptr, fiber_ptr))
+        val = as_arr(val, np.float32)
+        y = self._y(device, y)
+        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        check(lib.xtsg_plan_compress_csf(self._h, int(slice_k.shape[0]), ptr(slice_k), ptr(slice_ptr),
+                                         int(fiber_j.shape[0]), ptr(fiber_j), ptr(fiber_ptr), int(val.shape[0]),
+                                         ptr(nz_i), ptr(val), ptr(y), 1 if accumulate else 0, st))
+        return y
+
+    @staticmethod
+    def coo_to_csf(i, j, k, val):
+        """Host helper: COO -> CSF (stable sort by (k, j), slices and fibers of equal keys)."""
+        i, j, k = (np.asarray(a, np.int64) for a in (i, j, k))
+        order = np.lexsort((j, k))
+        i, j, k, v = i[order], j[order], k[order], np.asarray(val, np.float32)[order]
+        new_f = np.ones(len(k), bool)
+        new_f[1:] = (k[1:] != k[:-1]) | (j[1:] != j[:-1])
+        fstart = np.nonzero(new_f)[0]
+        fiber_ptr = np.append(fstart, len(k)).astype(np.int64)
+        fk = k[fstart]
+        new_s = np.ones(len(fstart), bool)
+        new_s[1:] = fk[1:] != fk[:-1]
+        sstart = np.nonzero(new_s)[0]
+        slice_ptr = np.append(sstart, len(fstart)).astype(np.int64)
+        return (fk[sstart].astype(np.int32), slice_ptr, j[fstart].astype(np.int32), fiber_ptr, i.astype(np.int32),
+                v)
+
     def compress_file(self, path, y=None, accumulate=False, stream=None, device=None, slab_bytes=0):
         """xtsg_plan_compress_file: compress a .xts file (dense or factor triple) straight from disk."""
         ydt = np.float64 if self.precision == PREC_FP64 else np.float32

@@ -255,6 +255,56 @@ __global__ void gather_w_kernel(const float* __restrict__ wf, int64_t count, int
   }
 }
 
+
+// CSF input (slices -> fibers -> nonzeros): per-nonzero fiber index j (one
+// warp per fiber), slice offsets/counts in nonzeros, and range/monotonicity
+// validation (bad[0]: coordinate outside the tensor, bad[1]: pointers not
+// monotone or not matching the array lengths)
+__global__ void csf_expand_kernel(const int64_t* __restrict__ fiber_ptr, const int32_t* __restrict__ fiber_j,
+                                  int64_t n_fibers, int64_t J, int64_t nnz, int32_t* __restrict__ sj,
+                                  int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t f = w0; f < n_fibers; f += nw) {
+    const int64_t b = fiber_ptr[f], e = fiber_ptr[f + 1];
+    const int32_t j = fiber_j[f];
+    if (lane == 0) {
+      if (j < 0 || j >= J) bad[0] = 1;
+      if (b > e || b < 0 || e > nnz) bad[1] = 1;
+    }
+    if (b > e || b < 0 || e > nnz) continue;
+    for (int64_t q = b + lane; q < e; q += 32) sj[q] = j;
+  }
+}
+
+__global__ void csf_slices_kernel(const int64_t* __restrict__ slice_ptr, const int64_t* __restrict__ fiber_ptr,
+                                  const int32_t* __restrict__ slice_k, int64_t n_slices, int64_t n_fibers,
+                                  int64_t K, int64_t* __restrict__ off, int32_t* __restrict__ cnt,
+                                  int* __restrict__ bad) {
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n_slices;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t f0 = slice_ptr[q], f1 = slice_ptr[q + 1];
+    if (f0 > f1 || f0 < 0 || f1 > n_fibers) {
+      bad[1] = 1;
+      off[q] = 0;
+      cnt[q] = 0;
+      continue;
+    }
+    if (slice_k[q] < 0 || slice_k[q] >= K) bad[0] = 1;
+    off[q] = fiber_ptr[f0];
+    const int64_t c = fiber_ptr[f1] - fiber_ptr[f0];
+    if (c < 0 || c > 0x7fffffff) bad[1] = 1;
+    cnt[q] = static_cast<int32_t>(c);
+  }
+}
+
+__global__ void range_i_kernel(const int32_t* __restrict__ ii, int64_t n, int64_t I, int* __restrict__ bad) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (ii[e] < 0 || ii[e] >= I) bad[0] = 1;
+}
+
 int64_t round_up256(int64_t a) { return (a + 255) / 256 * 256; }
 
 int gridn(int64_t work) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * 16))); }
@@ -287,20 +337,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     if (yo.host) yo.finish();
     return;
   }
-  const int64_t plrows = vP * lpad;
-  const int64_t ld_ut = round_up256(plrows), ld_vtj = vP * mpad;
-  if (!ut.ptr) {
-    // i-major U (rows padded to 256 with zeros) and j-major V copies
-    ut = DevBuf<__nv_bfloat16>(static_cast<size_t>(I * ld_ut), s);
-    ut.zero();
-    dim3 grid(static_cast<unsigned>(ceil_div(I, 32)), static_cast<unsigned>(ceil_div(plrows, 32)));
-    transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(ustack.ptr, plrows, ld_u, I, ld_ut, ut.ptr);
-    XLAUNCH_CHECK();
-    vtj = DevBuf<__nv_bfloat16>(static_cast<size_t>(J * ld_vtj), s);
-    dim3 gv(static_cast<unsigned>(ceil_div(J, 32)), static_cast<unsigned>(ceil_div(ld_vtj, 32)));
-    transpose_bf16_kernel<<<gv, dim3(32, 8), 0, s>>>(vt.ptr, ld_vtj, ld_v, J, ld_vtj, vtj.ptr);
-    XLAUNCH_CHECK();
-  }
+  ensure_sparse_operands(s);
   InView<int32_t> di(i, static_cast<size_t>(nnz), s), dj(j, static_cast<size_t>(nnz), s), dk(k, static_cast<size_t>(nnz), s);
   InView<float> dv(val, static_cast<size_t>(nnz), s);
   // 1. keys, validation, sortedness
@@ -361,6 +398,87 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     XCUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tb, cnt.ptr, off.ptr, kd, s));
     count_launch();
   }
+  coo_slices(si, sj, sv, off.ptr, cnt.ptr, uk.ptr, kd, yo.dev, accumulate, s);
+  if (fp16()) check_finite16(yo.dev, ysz, s);
+  if (yo.host) yo.finish();
+}
+
+
+// Sparse input already in CSF form (mode order k -> j -> i): no sort, no
+// run-length encoding — the fibers feed the warp-level fiber kernel directly.
+void Plan::compress_csf(int64_t n_slices, const int32_t* slice_k, const int64_t* slice_ptr, int64_t n_fibers,
+                        const int32_t* fiber_j, const int64_t* fiber_ptr, int64_t nnz, const int32_t* nz_i,
+                        const float* val, float* y, bool accumulate, cudaStream_t s) {
+  if (!tensor_core()) usage("plan_compress_csf: needs a bf16/fp16 (tensor-core) plan");
+  if (stage1) usage("plan_compress_csf: two-stage plans take COO input");
+  if (n_slices < 0 || n_fibers < 0 || nnz < 0) usage("plan_compress_csf: negative size");
+  const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
+  const int64_t ysz = desc.count * desc.reduced[0] * desc.reduced[1] * desc.reduced[2];
+  OutView<float> yo(y, static_cast<size_t>(ysz), s);
+  if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
+  if (nnz == 0 || n_slices == 0) {
+    if (!accumulate) XCUDA(cudaMemsetAsync(yo.dev, 0, ysz * 4, s));
+    if (yo.host) yo.finish();
+    return;
+  }
+  ensure_sparse_operands(s);
+  InView<int32_t> dk(slice_k, static_cast<size_t>(n_slices), s), dj(fiber_j, static_cast<size_t>(n_fibers), s),
+      di(nz_i, static_cast<size_t>(nnz), s);
+  InView<int64_t> dsp(slice_ptr, static_cast<size_t>(n_slices + 1), s),
+      dfp(fiber_ptr, static_cast<size_t>(n_fibers + 1), s);
+  InView<float> dv(val, static_cast<size_t>(nnz), s);
+  DevBuf<int32_t> sj(static_cast<size_t>(nnz), s), cnt(static_cast<size_t>(n_slices), s);
+  DevBuf<int64_t> off(static_cast<size_t>(n_slices), s);
+  DevBuf<int> bad(2, s);
+  bad.zero();
+  XCUDA(cudaMemsetAsync(sj.ptr, 0, sizeof(int32_t) * nnz, s));
+  csf_expand_kernel<<<gridn(n_fibers * 32), 256, 0, s>>>(dfp.dev, dj.dev, n_fibers, J, nnz, sj.ptr, bad.ptr);
+  XLAUNCH_CHECK();
+  csf_slices_kernel<<<gridn(n_slices), 256, 0, s>>>(dsp.dev, dfp.dev, dk.dev, n_slices, n_fibers, K, off.ptr, cnt.ptr,
+                                                    bad.ptr);
+  XLAUNCH_CHECK();
+  range_i_kernel<<<gridn(nnz), 256, 0, s>>>(di.dev, nnz, I, bad.ptr);
+  XLAUNCH_CHECK();
+  int hb[2] = {0, 0};
+  XCUDA(cudaMemcpyAsync(hb, bad.ptr, sizeof(hb), cudaMemcpyDeviceToHost, s));
+  XCUDA(cudaStreamSynchronize(s));
+  if (hb[0]) data_error("plan_compress_csf: coordinate outside the tensor");
+  if (hb[1]) data_error("plan_compress_csf: slice/fiber pointers not monotone or inconsistent with the sizes");
+  coo_slices(di.dev, sj.ptr, dv.dev, off.ptr, cnt.ptr, dk.dev, n_slices, yo.dev, accumulate, s);
+  if (fp16()) check_finite16(yo.dev, ysz, s);
+  if (yo.host) yo.finish();
+}
+
+// i-major U (rows padded to 256 with zeros) and j-major V copies of the
+// sparse path, built on first use
+void Plan::ensure_sparse_operands(cudaStream_t s) {
+  const int64_t I = desc.dims[0], J = desc.dims[1];
+  const int64_t plrows = vP * lpad;
+  const int64_t ld_ut = round_up256(plrows), ld_vtj = vP * mpad;
+  if (!ut.ptr) {
+    // i-major U (rows padded to 256 with zeros) and j-major V copies
+    ut = DevBuf<__nv_bfloat16>(static_cast<size_t>(I * ld_ut), s);
+    ut.zero();
+    dim3 grid(static_cast<unsigned>(ceil_div(I, 32)), static_cast<unsigned>(ceil_div(plrows, 32)));
+    transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(ustack.ptr, plrows, ld_u, I, ld_ut, ut.ptr);
+    XLAUNCH_CHECK();
+    vtj = DevBuf<__nv_bfloat16>(static_cast<size_t>(J * ld_vtj), s);
+    dim3 gv(static_cast<unsigned>(ceil_div(J, 32)), static_cast<unsigned>(ceil_div(ld_vtj, 32)));
+    transpose_bf16_kernel<<<gv, dim3(32, 8), 0, s>>>(vt.ptr, ld_vtj, ld_v, J, ld_vtj, vtj.ptr);
+    XLAUNCH_CHECK();
+  }
+}
+
+// Steps 3-5 of the sparse path on (k, j)-grouped nonzeros: kd slices, slice s
+// holding nonzeros [off[s], off[s] + cnt[s]) of mode-3 index uk[s], fibers
+// (runs of equal j) contiguous inside a slice -> y (+)= the replicas.
+void Plan::coo_slices(const int32_t* si, const int32_t* sj, const float* sv, const int64_t* off_p,
+                      const int32_t* cnt_p, const int32_t* uk_p, int64_t kd, float* ydev, bool accumulate,
+                      cudaStream_t s) {
+  const int64_t N = desc.reduced[2], K = desc.dims[2];
+  const bool padded = virt_padded();
+  const int64_t plrows = vP * lpad;
+  const int64_t ld_ut = round_up256(plrows), ld_vtj = vP * mpad;
   // 3. fibers -> Z[p][kd][m][l]
   DevBuf<float> z(static_cast<size_t>(vP * kd * mpad * lpad), s);
   // C groups of 256 rows per pass, Z pass in shared memory (mpad x 1.125*G fp32)
@@ -376,7 +494,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     int per_sm = 1;
     XCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     const int grid = static_cast<int>(std::min<int64_t>(kd, static_cast<int64_t>(sm_count()) * std::max(1, per_sm)));
-    kern<<<grid, NT, smem, s>>>(si, sj, sv, off.ptr, cnt.ptr, kd, ut.ptr, ld_ut, plrows, vtj.ptr, ld_vtj,
+    kern<<<grid, NT, smem, s>>>(si, sj, sv, off_p, cnt_p, kd, ut.ptr, ld_ut, plrows, vtj.ptr, ld_vtj,
                                 static_cast<int>(mpad), static_cast<int>(lpad), vP, z.ptr);
   };
   // nonzeros in flight per warp: 4 keeps the kernel at <= 85 registers
@@ -395,10 +513,10 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   XLAUNCH_CHECK();
   // 4. mode 3 over the distinct slices
   DevBuf<float> wg(static_cast<size_t>(vP * N * kd), s);
-  gather_w_kernel<<<gridn(vP * N * kd), 256, 0, s>>>(wf.ptr, vP, N, K, uk.ptr, kd, wg.ptr);
+  gather_w_kernel<<<gridn(vP * N * kd), 256, 0, s>>>(wf.ptr, vP, N, K, uk_p, kd, wg.ptr);
   XLAUNCH_CHECK();
   DevBuf<float> ypad;
-  float* ydst = yo.dev;
+  float* ydst = ydev;
   if (padded) {
     ypad = DevBuf<float>(static_cast<size_t>(vP * mpad * lpad * N), s);
     ydst = ypad.ptr;
@@ -411,10 +529,8 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   g.beta = (accumulate && !padded) ? 1.f : 0.f;
   gemm_simt(g, s);
   if (padded) {
-    compact(ypad.ptr, yo.dev, accumulate, s);
+    compact(ypad.ptr, ydev, accumulate, s);
   }
-  if (fp16()) check_finite16(yo.dev, ysz, s);
-  if (yo.host) yo.finish();
 }
 
 }  // namespace xtsg
@@ -427,5 +543,17 @@ extern "C" int32_t xtsg_plan_compress_coo(xtsg_plan* plan, const int32_t* i, con
     Plan* p = reinterpret_cast<Plan*>(plan);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
     p->compress_coo(i, j, k, val, nnz, static_cast<float*>(y), accumulate != 0, s);
+  });
+}
+
+extern "C" int32_t xtsg_plan_compress_csf(xtsg_plan* plan, int64_t n_slices, const int32_t* slice_k,
+                                          const int64_t* slice_ptr, int64_t n_fibers, const int32_t* fiber_j,
+                                          const int64_t* fiber_ptr, int64_t nnz, const int32_t* nz_i,
+                                          const float* val, void* y, int32_t accumulate, void* stream) {
+  return guard([&] {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
+    p->compress_csf(n_slices, slice_k, slice_ptr, n_fibers, fiber_j, fiber_ptr, nnz, nz_i, val,
+                    static_cast<float*>(y), accumulate != 0, s);
   });
 }

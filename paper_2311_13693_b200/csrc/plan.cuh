@@ -77,6 +77,12 @@ struct Plan {
                         float* y, bool accumulate, cudaStream_t s);
   void compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, const float* val, int64_t nnz, float* y,
                     bool accumulate, cudaStream_t s);
+  void compress_csf(int64_t n_slices, const int32_t* slice_k, const int64_t* slice_ptr, int64_t n_fibers,
+                    const int32_t* fiber_j, const int64_t* fiber_ptr, int64_t nnz, const int32_t* nz_i,
+                    const float* val, float* y, bool accumulate, cudaStream_t s);
+  void ensure_sparse_operands(cudaStream_t s);
+  void coo_slices(const int32_t* si, const int32_t* sj, const float* sv, const int64_t* off, const int32_t* cnt,
+                  const int32_t* uk, int64_t kd, float* ydev, bool accumulate, cudaStream_t s);
 };
 
 }  // namespace xtsg

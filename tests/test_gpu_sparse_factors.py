@@ -96,3 +96,28 @@ def test_coo_rejects_out_of_range(gpu):
     plan = gpu.Plan((40, 40, 40), (32, 32, 32), 2, 4, 1)
     with pytest.raises(gpu.DataError):
         plan.compress_coo([0, 40], [0, 0], [0, 0], [1.0, 1.0])
+
+
+def test_csf_matches_coo_bitwise_and_validates(gpu, restated):
+    # CSF input skips the sort: same fibers in the same order as the COO
+    # path's stable (k, j) sort -> the same replicas up to the order of the
+    # fiber kernel's shared-memory atomic folds (fp32 rounding only)
+    dims, red, P = (97, 88, 71), (32, 32, 16), 8
+    plan = gpu.Plan(dims, red, P, 8, 77)
+    i, j, k, v = _random_coo(dims, 20000, 3)
+    y_coo = plan.compress_coo(i, j, k, v)
+    csf = gpu.Plan.coo_to_csf(i, j, k, v)
+    y_csf = plan.compress_csf(*csf)
+    assert rel_diff(np.asarray(y_coo, np.float64), np.asarray(y_csf, np.float64)) <= 1e-6
+    # accumulate, and duplicate slices (the same k split in two slice records) sum
+    sk, sp, fj, fp, ni, nv = csf
+    y2 = plan.compress_csf(sk, sp, fj, fp, ni, nv, y=np.asarray(y_csf).copy(), accumulate=True)
+    assert rel_diff(2 * np.asarray(y_csf, np.float64), np.asarray(y2, np.float64)) <= 1e-6
+    bad_k = sk.copy()
+    bad_k[0] = dims[2]
+    with pytest.raises(gpu.DataError):
+        plan.compress_csf(bad_k, sp, fj, fp, ni, nv)
+    bad_fp = fp.copy()
+    bad_fp[1], bad_fp[2] = bad_fp[2], bad_fp[1]
+    with pytest.raises(gpu.DataError):
+        plan.compress_csf(sk, sp, fj, bad_fp, ni, nv)

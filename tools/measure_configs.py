@@ -96,6 +96,28 @@ def c4(args):
     ci, cj, ck, cv = (torch.cat([p[q] for p in parts]) for q in range(4))
     del parts
     nnz = int(cv.numel())
+    csf = None
+    if args.csf:
+        # the same nonzeros in CSF form (each rank-1 block is a dense 464^3
+        # sub-cube: slices = its k support, fibers = its j support)
+        sk, fj, ni, nv = [], [], [], []
+        for r in range(R):
+            sup = [torch.tensor(np.nonzero(f[m][:, r])[0], dtype=torch.int32, device=dev) for m in range(3)]
+            val = [torch.tensor(f[m][np.nonzero(f[m][:, r])[0], r], dtype=torch.float32, device=dev)
+                   for m in range(3)]
+            na, nb, nc = (len(x) for x in sup)
+            sk.append(sup[2])
+            fj.append(sup[1].repeat(nc))
+            ni.append(sup[0].repeat(nc * nb))
+            nv.append((val[2].view(nc, 1, 1) * val[1].view(1, nb, 1) * val[0].view(1, 1, na)).reshape(-1))
+        sk, fj, ni, nv = (torch.cat(x) for x in (sk, fj, ni, nv))
+        per_slice = int(fj.numel() // sk.numel())
+        per_fiber = int(ni.numel() // fj.numel())
+        sp = torch.arange(0, sk.numel() + 1, dtype=torch.int64, device=dev) * per_slice
+        fp = torch.arange(0, fj.numel() + 1, dtype=torch.int64, device=dev) * per_fiber
+        csf = (sk, sp, fj, fp, ni, nv)
+        del ci, cj, ck, cv
+        nnz = int(nv.numel())
     if args.presorted:
         order = torch.argsort(ck.long() * dims[1] + cj.long())
         ci, cj, ck, cv = ci[order], cj[order], ck[order], cv[order]
@@ -105,14 +127,20 @@ def c4(args):
     y = torch.zeros(P * int(np.prod(red)), dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
+    def step():
+        if csf is not None:
+            plan.compress_csf(*csf, y=y, stream=stream)
+        else:
+            plan.compress_coo(ci, cj, ck, cv, y=y, stream=stream)
+
     for _ in range(args.warmup):
-        plan.compress_coo(ci, cj, ck, cv, y=y, stream=stream)
+        step()
     torch.cuda.synchronize()
     l0 = xt.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        plan.compress_coo(ci, cj, ck, cv, y=y, stream=stream)
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -129,7 +157,7 @@ def c4(args):
     rate = nnz / (ms / 1e3)
     achieved = 16.0 * rate / 1e9
     emit({"config": f"C4: sparse COO 10^6^3 rank-{R}, {npc} nnz/col -> {nnz:.4g} nonzeros "
-                    f"({'pre-sorted by (k, j)' if args.presorted else 'unsorted: sort inside the step'}), "
+                    f"({'CSF input, no sort' if args.csf else 'pre-sorted by (k, j)' if args.presorted else 'unsorted: sort inside the step'}), "
                     f"P={P} replicas of 32^3",
           "metric": "nonzeros compressed/sec", "value": rate, "unit": "nnz/s", "ms_per_step": ms,
           "steps": args.steps, "warmup": args.warmup, "kernel_launches_per_step": launches,
@@ -248,6 +276,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--nnz-per-col", type=int, default=464)
     ap.add_argument("--presorted", action="store_true")
+    ap.add_argument("--csf", action="store_true")
     ap.add_argument("--n", type=int, default=4000)
     ap.add_argument("--L", type=int, nargs="+", default=[32, 64, 128])
     ap.add_argument("--P", type=int, nargs="+", default=[16, 32, 64, 128])
