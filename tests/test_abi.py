@@ -84,3 +84,35 @@ def test_usage_errors_precede_device_checks(xt):
         xt.make_ensemble([8, 8, 8], [4, 4, 4], 2, 5, 5)
     with pytest.raises(xt.UsageError):
         xt.make_ensemble([100] * 3, [50] * 3, 2, 2, 23, kind="two_stage", alpha=1.0)
+
+
+def test_header_is_plain_c_and_cpp():
+    # the drop-in boundary must compile as C (cgo/ctypes-style callers) and C++
+    import subprocess
+    import tempfile
+    src = '#include "xtsg.h"\nint main(void) { xtsg_plan_desc d; (void)d; return xtsg_version() > 0 ? 0 : 1; }\n'
+    with tempfile.TemporaryDirectory() as td:
+        for cc, ext in (("gcc", "c"), ("g++", "cpp")):
+            f = Path(td) / f"t.{ext}"
+            f.write_text(src)
+            r = subprocess.run([cc, "-std=c11" if ext == "c" else "-std=c++17", "-Wall", "-Werror", "-fsyntax-only",
+                                "-I", str(ROOT / "include"), str(f)], capture_output=True, text=True)
+            assert r.returncode == 0, (cc, r.stderr)
+
+
+def test_coo_to_csf_host_helper(xt):
+    rng = np.random.default_rng(5)
+    n = 500
+    i, j, k = (rng.integers(0, 9, n) for _ in range(3))
+    v = rng.standard_normal(n).astype(np.float32)
+    sk, sp, fj, fp, ni, nv = xt.Plan.coo_to_csf(i, j, k, v)
+    assert sp[0] == 0 and sp[-1] == len(fj) and fp[0] == 0 and fp[-1] == n
+    assert np.all(np.diff(sk) > 0)                      # one record per distinct k, sorted
+    dense = np.zeros((9, 9, 9))
+    np.add.at(dense, (i, j, k), v.astype(np.float64))
+    back = np.zeros((9, 9, 9))
+    for q, kk in enumerate(sk):
+        for f in range(sp[q], sp[q + 1]):
+            for e in range(fp[f], fp[f + 1]):
+                back[ni[e], fj[f], kk] += nv[e]
+    assert np.allclose(dense, back)
