@@ -80,6 +80,25 @@ __attribute__((target("avx2"))) void narrow_row_bf16_avx2(const float* __restric
   }
 }
 
+// F16C: 8 floats -> 8 binary16 per vcvtps2ph with round-to-nearest-even
+// (IEEE: subnormals, overflow to inf), non-temporal 16-byte stores
+__attribute__((target("avx2,f16c"))) void narrow_row_f16_f16c(const float* __restrict__ src, int64_t n,
+                                                             uint16_t* __restrict__ dst) {
+  int64_t i = 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  for (; i + 8 <= n; i += 8) {
+    const __m128i h = _mm256_cvtps_ph(_mm256_loadu_ps(src + i), _MM_FROUND_TO_NEAREST_INT);
+    if (aligned) _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), h);
+    else _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i), h);
+  }
+  for (; i < n; ++i) dst[i] = f2h(src[i]);
+}
+
+bool host_has_f16c() {
+  static const bool has = __builtin_cpu_supports("f16c") && __builtin_cpu_supports("avx2");
+  return has;
+}
+
 bool host_has_avx2() {
   static const bool has = __builtin_cpu_supports("avx2");
   return has;
@@ -93,7 +112,8 @@ void narrow_rows_f32(const float* x, int64_t ni, int64_t nj, int64_t ld0, int64_
   for (int64_t row = row0; row < row1; ++row) {
     const int64_t j = row % nj, k = k0 + row / nj;
     uint16_t* dst = out + row * ldi;
-    if (f16) narrow_row_h(x + j * ld0 + k * ld1, ni, dst);
+    if (f16 && host_has_f16c()) narrow_row_f16_f16c(x + j * ld0 + k * ld1, ni, dst);
+    else if (f16) narrow_row_h(x + j * ld0 + k * ld1, ni, dst);
     else if (host_has_avx2()) narrow_row_bf16_avx2(x + j * ld0 + k * ld1, ni, dst);
     else narrow_row(x + j * ld0 + k * ld1, ni, dst);
     for (int64_t i = ni; i < ldi; ++i) dst[i] = 0;
