@@ -99,6 +99,40 @@ bool host_has_f16c() {
   return has;
 }
 
+// AVX-512: 16 floats -> 16 bf16 per step (same integer RNE rule), 32-byte
+// non-temporal stores when aligned
+__attribute__((target("avx512f"))) void narrow_row_bf16_avx512(const float* __restrict__ src, int64_t n,
+                                                              uint16_t* __restrict__ dst) {
+  const __m512i bias = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1);
+  const __m512i absm = _mm512_set1_epi32(0x7fffffff), inf = _mm512_set1_epi32(0x7f800000);
+  const __m512i qbit = _mm512_set1_epi32(0x40);
+  int64_t i = 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 31) == 0;
+  for (; i + 16 <= n; i += 16) {
+    const __m512i u = _mm512_castps_si512(_mm512_loadu_ps(src + i));
+    const __m512i hi = _mm512_srli_epi32(u, 16);
+    __m512i r = _mm512_srli_epi32(_mm512_add_epi32(_mm512_add_epi32(u, bias), _mm512_and_si512(hi, one)), 16);
+    const __mmask16 nan = _mm512_cmpgt_epi32_mask(_mm512_and_si512(u, absm), inf);
+    r = _mm512_mask_blend_epi32(nan, r, _mm512_or_si512(hi, qbit));
+    const __m256i out = _mm512_cvtepi32_epi16(r);
+    if (aligned && ((reinterpret_cast<uintptr_t>(dst + i) & 31) == 0))
+      _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), out);
+    else
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), out);
+  }
+  for (; i < n; ++i) {
+    uint32_t u;
+    std::memcpy(&u, src + i, 4);
+    const uint32_t rne = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    dst[i] = static_cast<uint16_t>((u & 0x7fffffffu) > 0x7f800000u ? ((u >> 16) | 0x40u) : rne);
+  }
+}
+
+bool host_has_avx512() {
+  static const bool has = __builtin_cpu_supports("avx512f");
+  return has;
+}
+
 bool host_has_avx2() {
   static const bool has = __builtin_cpu_supports("avx2");
   return has;
@@ -114,6 +148,7 @@ void narrow_rows_f32(const float* x, int64_t ni, int64_t nj, int64_t ld0, int64_
     uint16_t* dst = out + row * ldi;
     if (f16 && host_has_f16c()) narrow_row_f16_f16c(x + j * ld0 + k * ld1, ni, dst);
     else if (f16) narrow_row_h(x + j * ld0 + k * ld1, ni, dst);
+    else if (host_has_avx512()) narrow_row_bf16_avx512(x + j * ld0 + k * ld1, ni, dst);
     else if (host_has_avx2()) narrow_row_bf16_avx2(x + j * ld0 + k * ld1, ni, dst);
     else narrow_row(x + j * ld0 + k * ld1, ni, dst);
     for (int64_t i = ni; i < ldi; ++i) dst[i] = 0;
