@@ -128,6 +128,51 @@ __attribute__((target("avx512f"))) void narrow_row_bf16_avx512(const float* __re
   }
 }
 
+// AVX512-BF16: vcvtneps2bf16 rounds to nearest even in hardware but treats
+// subnormal inputs as zero; vectors holding a float subnormal take the
+// integer rule instead, so the result stays bit-identical to the device's
+__attribute__((target("avx512f,avx512bf16"))) void narrow_row_bf16_hw(const float* __restrict__ src, int64_t n,
+                                                                     uint16_t* __restrict__ dst) {
+  const __m512i expm = _mm512_set1_epi32(0x7f800000), manm = _mm512_set1_epi32(0x007fffff);
+  const __m512i zero = _mm512_setzero_si512();
+  int64_t i = 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 31) == 0;
+  for (; i + 16 <= n; i += 16) {
+    const __m512 x = _mm512_loadu_ps(src + i);
+    const __m512i u = _mm512_castps_si512(x);
+    const __mmask16 sub = _mm512_cmpeq_epi32_mask(_mm512_and_si512(u, expm), zero) &
+                          _mm512_cmpneq_epi32_mask(_mm512_and_si512(u, manm), zero);
+    __m256i out;
+    if (sub == 0) {
+      out = reinterpret_cast<__m256i>(_mm512_cvtneps_pbh(x));
+    } else {
+      alignas(32) uint16_t tmp[16];
+      for (int q = 0; q < 16; ++q) {
+        uint32_t w;
+        std::memcpy(&w, src + i + q, 4);
+        const uint32_t rne = (w + 0x7fffu + ((w >> 16) & 1u)) >> 16;
+        tmp[q] = static_cast<uint16_t>((w & 0x7fffffffu) > 0x7f800000u ? ((w >> 16) | 0x40u) : rne);
+      }
+      out = _mm256_load_si256(reinterpret_cast<const __m256i*>(tmp));
+    }
+    if (aligned && ((reinterpret_cast<uintptr_t>(dst + i) & 31) == 0))
+      _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), out);
+    else
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), out);
+  }
+  for (; i < n; ++i) {
+    uint32_t u;
+    std::memcpy(&u, src + i, 4);
+    const uint32_t rne = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    dst[i] = static_cast<uint16_t>((u & 0x7fffffffu) > 0x7f800000u ? ((u >> 16) | 0x40u) : rne);
+  }
+}
+
+bool host_has_avx512bf16() {
+  static const bool has = __builtin_cpu_supports("avx512bf16");
+  return has;
+}
+
 bool host_has_avx512() {
   static const bool has = __builtin_cpu_supports("avx512f");
   return has;
@@ -148,6 +193,7 @@ void narrow_rows_f32(const float* x, int64_t ni, int64_t nj, int64_t ld0, int64_
     uint16_t* dst = out + row * ldi;
     if (f16 && host_has_f16c()) narrow_row_f16_f16c(x + j * ld0 + k * ld1, ni, dst);
     else if (f16) narrow_row_h(x + j * ld0 + k * ld1, ni, dst);
+    else if (host_has_avx512bf16()) narrow_row_bf16_hw(x + j * ld0 + k * ld1, ni, dst);
     else if (host_has_avx512()) narrow_row_bf16_avx512(x + j * ld0 + k * ld1, ni, dst);
     else if (host_has_avx2()) narrow_row_bf16_avx2(x + j * ld0 + k * ld1, ni, dst);
     else narrow_row(x + j * ld0 + k * ld1, ni, dst);
