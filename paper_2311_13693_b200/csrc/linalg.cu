@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -238,6 +239,216 @@ __global__ void omp_kernel(const double* __restrict__ y_all, const double* __res
   for (int a = threadIdx.x; a < na; a += blockDim.x) out[active[a] + ldo * col] = coef[a];
 }
 
+
+// ---- OMP for large dictionaries: the atom search spread over the GPU ------
+// The per-column CTA above scans every atom with one CTA per measured column
+// (10^6 atoms x 512 rows: seconds). Here every iteration is three launches
+// for all columns at once: (1) CTAs over atom chunks, one warp per atom,
+// lanes over rows, dot products against all (up to OMP_CB) residuals held in
+// shared memory -> per-CTA best (|d'r| / ||d||, lowest index on ties, active
+// atoms skipped through a byte mask); (2) per-column reduction of the CTA
+// candidates in CTA order (same tie rule: the reference's first maximum);
+// (3) one CTA per column grows the Cholesky factor, re-solves and recomputes
+// the residual exactly like omp_kernel. Finished columns are skipped.
+constexpr int OMP_CB = 16;  // columns per search pass (residuals in shared memory)
+
+__global__ void omp_search_kernel(const double* __restrict__ D, int64_t rows, int64_t atoms,
+                                  const double* __restrict__ atom_norm, const double* __restrict__ res_all,
+                                  const uint8_t* __restrict__ active_mask, const int* __restrict__ done,
+                                  int64_t c0, int nc, double* __restrict__ cand_v, int64_t* __restrict__ cand_i,
+                                  int64_t ncols) {
+  extern __shared__ double sres[];  // nc x rows
+  __shared__ double wbest[NT / 32][OMP_CB];
+  __shared__ int64_t wbi[NT / 32][OMP_CB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < nc * rows; e += blockDim.x) sres[e] = res_all[(c0 + e / rows) * rows + e % rows];
+  __syncthreads();
+  double best[OMP_CB];
+  int64_t bi[OMP_CB];
+#pragma unroll
+  for (int c = 0; c < OMP_CB; ++c) {
+    best[c] = 0.0;
+    bi[c] = -1;
+  }
+  const int64_t per = (atoms + gridDim.x - 1) / gridDim.x;
+  const int64_t a0 = blockIdx.x * per, a1 = min(atoms, a0 + per);
+  for (int64_t j = a0 + warp; j < a1; j += nw) {
+    const double* d = D + rows * j;
+    double dot[OMP_CB];
+#pragma unroll
+    for (int c = 0; c < OMP_CB; ++c) dot[c] = 0.0;
+    for (int64_t i = lane; i < rows; i += 32) {
+      const double dv = d[i];
+#pragma unroll
+      for (int c = 0; c < OMP_CB; ++c)
+        if (c < nc) dot[c] = fma(dv, sres[c * rows + i], dot[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < OMP_CB; ++c) {
+      if (c >= nc) continue;
+      double v = dot[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      const int64_t col = c0 + c;
+      if (lane == 0 && !done[col] && !active_mask[j * ncols + col]) {
+        const double corr = fabs(v) / atom_norm[j];
+        if (corr > best[c]) {  // ascending j within the warp: first maximum kept
+          best[c] = corr;
+          bi[c] = j;
+        }
+      }
+    }
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < OMP_CB; ++c) {
+      wbest[warp][c] = best[c];
+      wbi[warp][c] = bi[c];
+    }
+  __syncthreads();
+  if (threadIdx.x < nc) {
+    const int c = threadIdx.x;
+    double bv = 0.0;
+    int64_t bj = -1;
+    for (int w = 0; w < nw; ++w) {
+      const double v = wbest[w][c];
+      const int64_t i = wbi[w][c];
+      if (i >= 0 && (v > bv || (v == bv && (bj < 0 || i < bj)))) {
+        bv = v;
+        bj = i;
+      }
+    }
+    cand_v[(c0 + c) * gridDim.x + blockIdx.x] = bv;
+    cand_i[(c0 + c) * gridDim.x + blockIdx.x] = bj;
+  }
+}
+
+__global__ void omp_update_kernel(const double* __restrict__ y_all, const double* __restrict__ D, int64_t rows,
+                                  int64_t atoms, int sparsity, double tol, const double* __restrict__ cand_v,
+                                  const int64_t* __restrict__ cand_i, int ncand, uint8_t* __restrict__ active_mask,
+                                  int64_t ncols, int* __restrict__ done, int* __restrict__ na_all,
+                                  double* __restrict__ res_all, double* ws_all, int64_t ws_stride) {
+  __shared__ double red[32];
+  __shared__ int stop;
+  __shared__ int64_t s_sel;
+  __shared__ double s_corr;
+  const int64_t col = blockIdx.x;
+  if (done[col]) return;
+  const double* y = y_all + rows * col;
+  double* res = res_all + rows * col;
+  double* ws = ws_all + ws_stride * col;
+  double* chol = ws;
+  double* rhs = chol + sparsity * (sparsity + 1) / 2;
+  double* coef = rhs + sparsity;
+  double* g = coef + sparsity;
+  double* wv = g + sparsity;
+  int64_t* active = reinterpret_cast<int64_t*>(wv + sparsity);
+  const int na = na_all[col];
+  if (threadIdx.x == 0) {
+    double bv = 0.0;
+    int64_t bj = -1;
+    for (int q = 0; q < ncand; ++q) {  // CTA order = ascending atom chunks
+      const double v = cand_v[col * ncand + q];
+      const int64_t i = cand_i[col * ncand + q];
+      if (i >= 0 && (v > bv || (v == bv && (bj < 0 || i < bj)))) {
+        bv = v;
+        bj = i;
+      }
+    }
+    s_sel = bj;
+    s_corr = bv;
+  }
+  __syncthreads();
+  const int64_t sel = s_sel;
+  if (sel < 0 || s_corr == 0.0) {
+    if (threadIdx.x == 0) done[col] = 1;
+    return;
+  }
+  for (int a = 0; a < na; ++a) {
+    double dot = 0.0;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) dot = fma(D[i + rows * active[a]], D[i + rows * sel], dot);
+    dot = bsum2(dot, red);
+    if (threadIdx.x == 0) g[a] = dot;
+  }
+  double d2 = 0.0, yd = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    d2 = fma(D[i + rows * sel], D[i + rows * sel], d2);
+    yd = fma(D[i + rows * sel], y[i], yd);
+  }
+  d2 = bsum2(d2, red);
+  yd = bsum2(yd, red);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < na; ++i) {
+      double sacc = g[i];
+      for (int j = 0; j < i; ++j) sacc -= chol[i * (i + 1) / 2 + j] * wv[j];
+      wv[i] = sacc / chol[i * (i + 1) / 2 + i];
+    }
+    double diag2 = d2;
+    for (int i = 0; i < na; ++i) diag2 -= wv[i] * wv[i];
+    stop = diag2 <= 1e-28;
+    if (!stop) {
+      for (int i = 0; i < na; ++i) chol[na * (na + 1) / 2 + i] = wv[i];
+      chol[na * (na + 1) / 2 + na] = sqrt(diag2);
+      active[na] = sel;
+      rhs[na] = yd;
+      const int n = na + 1;
+      for (int i = 0; i < n; ++i) {
+        double sacc = rhs[i];
+        for (int j = 0; j < i; ++j) sacc -= chol[i * (i + 1) / 2 + j] * wv[j];
+        wv[i] = sacc / chol[i * (i + 1) / 2 + i];
+      }
+      for (int ii = n - 1; ii >= 0; --ii) {
+        double sacc = wv[ii];
+        for (int j = ii + 1; j < n; ++j) sacc -= chol[j * (j + 1) / 2 + ii] * coef[j];
+        coef[ii] = sacc / chol[ii * (ii + 1) / 2 + ii];
+      }
+      active_mask[sel * ncols + col] = 1;
+      na_all[col] = n;
+    } else {
+      done[col] = 1;
+    }
+  }
+  __syncthreads();
+  if (stop) return;
+  const int n = na + 1;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    double fit = 0.0;
+    for (int a = 0; a < n; ++a) fit = fma(D[i + rows * active[a]], coef[a], fit);
+    res[i] = y[i] - fit;
+  }
+  // the next iteration's residual-norm test (alignment.cpp:343-345)
+  double rn = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) rn = fma(res[i], res[i], rn);
+  rn = bsum2(rn, red);
+  if (threadIdx.x == 0 && (sqrt(rn) <= tol || n >= sparsity)) done[col] = 1;
+}
+
+__global__ void omp_init_kernel(const double* __restrict__ y_all, int64_t rows, int64_t ncols, double tol,
+                                double* __restrict__ res_all, int* __restrict__ done, int* __restrict__ na_all) {
+  __shared__ double red[32];
+  const int64_t col = blockIdx.x;
+  double rn = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double v = y_all[rows * col + i];
+    res_all[rows * col + i] = v;
+    rn = fma(v, v, rn);
+  }
+  rn = bsum2(rn, red);
+  if (threadIdx.x == 0) {
+    done[col] = sqrt(rn) <= tol ? 1 : 0;
+    na_all[col] = 0;
+  }
+}
+
+__global__ void omp_scatter_kernel(const double* __restrict__ ws_all, int64_t ws_stride, int sparsity,
+                                   const int* __restrict__ na_all, double* __restrict__ out, int64_t ldo) {
+  const int64_t col = blockIdx.x;
+  const double* ws = ws_all + ws_stride * col;
+  const double* coef = ws + sparsity * (sparsity + 1) / 2 + sparsity;
+  const int64_t* active = reinterpret_cast<const int64_t*>(coef + 3 * sparsity);
+  for (int a = threadIdx.x; a < na_all[col]; a += blockDim.x) out[active[a] + ldo * col] = coef[a];
+}
+
 __global__ void scale_cols_kernel(const double* v, int64_t rows, int64_t cols, const double* s, double* out) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < rows * cols;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -417,7 +628,41 @@ int32_t xtsg_omp_recover(const double* measured, int64_t rows, int64_t ncols, co
     XCUDA(cudaMemsetAsync(o.dev, 0, sizeof(double) * atoms * ncols, st));
     const int64_t ws_stride = rows + sparsity * (sparsity + 1) / 2 + 4 * sparsity + sparsity + 8;
     DevBuf<double> ws(static_cast<size_t>(std::max<int64_t>(1, ncols) * ws_stride), st);
-    if (ncols > 0) {
+    static const int64_t wide_from = [] {
+      const char* e = std::getenv("XTSG_OMP_WIDE_FROM");
+      return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(4096);
+    }();
+    if (ncols > 0 && atoms >= wide_from) {
+      // large dictionaries: the atom search over the whole GPU (omp_search_kernel)
+      const int nsearch = std::max(1, std::min(sm_count() * 4, static_cast<int>(ceil_div(atoms, 64))));
+      DevBuf<double> res(static_cast<size_t>(rows * ncols), st), cv(static_cast<size_t>(ncols * nsearch), st);
+      DevBuf<int64_t> ci(static_cast<size_t>(ncols * nsearch), st);
+      DevBuf<uint8_t> mask(static_cast<size_t>(atoms * ncols), st);
+      DevBuf<int> done(static_cast<size_t>(ncols), st), na(static_cast<size_t>(ncols), st);
+      mask.zero();
+      omp_init_kernel<<<static_cast<unsigned>(ncols), NT, 0, st>>>(y.dev, rows, ncols, residual_tol, res.ptr,
+                                                                   done.ptr, na.ptr);
+      XLAUNCH_CHECK();
+      const size_t smem = sizeof(double) * OMP_CB * rows;
+      if (smem > 48 * 1024)
+        XCUDA(cudaFuncSetAttribute(omp_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+      for (int64_t it = 0; it < sparsity; ++it) {
+        for (int64_t c0 = 0; c0 < ncols; c0 += OMP_CB) {
+          const int nc = static_cast<int>(std::min<int64_t>(OMP_CB, ncols - c0));
+          omp_search_kernel<<<nsearch, NT, sizeof(double) * nc * rows, st>>>(
+              d.dev, rows, atoms, nrm.ptr, res.ptr, mask.ptr, done.ptr, c0, nc, cv.ptr, ci.ptr, ncols);
+          XLAUNCH_CHECK();
+        }
+        omp_update_kernel<<<static_cast<unsigned>(ncols), NT, 0, st>>>(
+            y.dev, d.dev, rows, atoms, static_cast<int>(sparsity), residual_tol, cv.ptr, ci.ptr, nsearch, mask.ptr,
+            ncols, done.ptr, na.ptr, res.ptr, ws.ptr, ws_stride);
+        XLAUNCH_CHECK();
+      }
+      omp_scatter_kernel<<<static_cast<unsigned>(ncols), NT, 0, st>>>(ws.ptr, ws_stride, static_cast<int>(sparsity),
+                                                                      na.ptr, o.dev, atoms);
+      XLAUNCH_CHECK();
+    } else if (ncols > 0) {
       omp_kernel<<<static_cast<unsigned>(ncols), NT, 0, st>>>(y.dev, d.dev, rows, atoms, static_cast<int>(sparsity),
                                                               residual_tol, nrm.ptr, o.dev, atoms, ws.ptr, ws_stride);
       XLAUNCH_CHECK();

@@ -268,9 +268,47 @@ def twostage(args):
           "max_rel_err_vs_fp64_materialized_ensemble": err, "tolerance": 1e-2}, args.out)
 
 
+def omp(args):
+    """OMP recovery on the device at large dictionaries (sparse
+    factors at 10^6 atoms): rows = stacked compressed rows, R columns with s
+    nonzeros each, Gaussian dictionary (unit columns); time and support recovery."""
+    import torch
+    from paper_2311_13693_b200._lib import check, lib
+    dev = torch.device("cuda", 0)
+    rows, R, s = 512, 10, args.sparsity
+    for atoms in (10 ** 4, 10 ** 5, 10 ** 6):
+        g = torch.Generator(device=dev)
+        g.manual_seed(atoms)
+        D = torch.randn(atoms, rows, dtype=torch.float64, device=dev, generator=g).t().contiguous()  # column-major rows x atoms
+        D = D / D.norm(dim=0, keepdim=True)
+        Dcm = D.t().contiguous()          # (atoms, rows) row-major == rows x atoms column-major
+        X = torch.zeros(R, atoms, dtype=torch.float64, device=dev)
+        rng = np.random.default_rng(atoms)
+        supp = [np.sort(rng.choice(atoms, s, replace=False)) for _ in range(R)]
+        for c in range(R):
+            X[c, supp[c]] = torch.tensor(rng.choice([-1.0, 1.0], s) * (1 + rng.random(s)), dtype=torch.float64,
+                                         device=dev)
+        Y = (D @ X.t()).t().contiguous()  # (R, rows) row-major == rows x R column-major
+        out = torch.zeros(R, atoms, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        check(lib.xtsg_omp_recover(Y.data_ptr(), rows, R, Dcm.data_ptr(), atoms, s, 1e-9, out.data_ptr()))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        check(lib.xtsg_omp_recover(Y.data_ptr(), rows, R, Dcm.data_ptr(), atoms, s, 1e-9, out.data_ptr()))
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        got = out.cpu().numpy()
+        ok = sum(set(np.nonzero(np.abs(got[c]) > 1e-6)[0]) == set(supp[c]) for c in range(R))
+        err = float((out - X).norm() / X.norm())
+        emit({"config": f"OMP: {rows} measured rows x {atoms:.0e} atoms, {R} columns, sparsity {s}",
+              "seconds": dt, "supports_recovered": f"{ok}/{R}", "rel_err": err}, args.out)
+        del D, Dcm, X, Y, out
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c1", "c4", "c5", "twostage"])
+    ap.add_argument("which", choices=["c1", "c4", "c5", "twostage", "omp"])
+    ap.add_argument("--sparsity", type=int, default=16)
     ap.add_argument("--out", default=None)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
@@ -281,7 +319,7 @@ def main():
     ap.add_argument("--L", type=int, nargs="+", default=[32, 64, 128])
     ap.add_argument("--P", type=int, nargs="+", default=[16, 32, 64, 128])
     a = ap.parse_args()
-    {"c1": c1, "c4": c4, "c5": c5, "twostage": twostage}[a.which](a)
+    {"c1": c1, "c4": c4, "c5": c5, "twostage": twostage, "omp": omp}[a.which](a)
 
 
 if __name__ == "__main__":
