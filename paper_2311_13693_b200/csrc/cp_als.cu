@@ -688,7 +688,15 @@ struct BigSmem {
   double *Ts, *Bp, *red;
   uint64_t *full, *empty;
   int ldt, ldb, ns;
+  uint32_t ns_m, cpk_m;  // multiply-high reciprocals of ns and n2 / BJC
 };
+
+// x / d for d >= 2 and x < 2^32 / d: one IMAD.HI instead of the ~20-deep
+// dependent integer-division sequence, which (int64 `%`/`/` by the runtime
+// ring depth) was the per-chunk critical path of the ring (~1000 cycles per
+// chunk, measured: tools/micro/bulk_ring.cu)
+__host__ __device__ __forceinline__ uint32_t fdiv_magic(uint32_t d) { return 0xFFFFFFFFu / d + 1u; }
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint32_t m) { return __umulhi(x, m); }
 
 __device__ __forceinline__ int big_ld(int n) { return n + 4; }  // n % 16 == 0 -> ld % 16 == 4
 
@@ -698,11 +706,15 @@ __device__ void big_refresh(const Smem& s, const BigSmem& g, int n2, int R) {
 }
 
 // thread 0: stage global chunk number `gnum` (local chunk c of the pass)
-__device__ __forceinline__ void big_issue(const BigSmem& g, const double* T, int n1, int n2, int64_t gnum, int c) {
-  const int stage = static_cast<int>(gnum % g.ns);
-  if (gnum >= g.ns) ptx::mbar_wait(&g.empty[stage], static_cast<uint32_t>(((gnum / g.ns) - 1) & 1));
+// (gnum: the chunk's global number, only compared with ns; x: the same number
+// reduced by a multiple of 2 * ns, small enough for fdiv)
+__device__ __forceinline__ void big_issue(const BigSmem& g, const double* T, int n1, int n2, int64_t gnum, uint32_t x,
+                                          int c) {
+  const uint32_t gq = fdiv(x, g.ns_m);
+  const int stage = static_cast<int>(x - gq * g.ns);
+  if (gnum >= g.ns) ptx::mbar_wait(&g.empty[stage], (gq - 1u) & 1u);
   const int cpk = n2 / BJC;
-  const int k = c / cpk, jb = (c % cpk) * BJC;
+  const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb = (c - k * cpk) * BJC;
   const uint32_t col_bytes = static_cast<uint32_t>(n1) * 8u;
   ptx::mbar_arrive_expect_tx(&g.full[stage], col_bytes * BJC);
   double* dst = g.Ts + stage * BJC * g.ldt;
@@ -738,10 +750,11 @@ __device__ double big_pass1(const double* __restrict__ T, int n1, int n2, int n3
       areg[m][kr] = r < R ? s.A[((warp * MTPW + m) * 8 + lr) + n1 * r] : 0.0;
     }
   double res = 0.0;
+  const uint32_t gb = static_cast<uint32_t>(gcn % (2 * g.ns));  // ring position, once per pass
   for (int c = 0; c < nch; ++c, ++gcn) {
     if (threadIdx.x == 0 && c == 0)
-      for (int q0 = 0; q0 < g.ns && q0 < nch; ++q0) big_issue(g, T, n1, n2, gcn + q0, q0);
-    const int k = c / cpk, jb = (c % cpk) * BJC;
+      for (int q0 = 0; q0 < g.ns && q0 < nch; ++q0) big_issue(g, T, n1, n2, gcn + q0, gb + q0, q0);
+    const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb = (c - k * cpk) * BJC;
     if (jb == 0) {
 #pragma unroll
       for (int kr = 0; kr < 2 * NTR; ++kr) {
@@ -751,8 +764,9 @@ __device__ double big_pass1(const double* __restrict__ T, int n1, int n2, int n3
         for (int m = 0; m < MTPW; ++m) ahat[m][kr] = areg[m][kr] * ck;
       }
     }
-    const int stage = static_cast<int>(gcn % g.ns);
-    ptx::mbar_wait(&g.full[stage], static_cast<uint32_t>((gcn / g.ns) & 1));
+    const uint32_t gq = fdiv(gb + c, g.ns_m);
+    const int stage = static_cast<int>(gb + c - gq * g.ns);
+    ptx::mbar_wait(&g.full[stage], gq & 1u);
     const double* ts = g.Ts + stage * BJC * g.ldt;
     // GEMM 1: q[i, r] += sum_j T[i, j] B[j, r]
 #pragma unroll
@@ -785,7 +799,7 @@ __device__ double big_pass1(const double* __restrict__ T, int n1, int n2, int n3
     }
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&g.empty[stage]);
-    if (threadIdx.x == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, c + g.ns);
+    if (threadIdx.x == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, gb + c + g.ns, c + g.ns);
     if (jb + BJC == n2) {  // slice k complete: macc += c_k .* q
 #pragma unroll
       for (int t = 0; t < NTR; ++t)
@@ -839,13 +853,15 @@ __device__ void big_pass2(const double* __restrict__ T, int n1, int n2, int n3, 
   __syncthreads();
   const int rp = NTR * 8;
   int use = 0;
+  const uint32_t gb = static_cast<uint32_t>(gcn % (2 * g.ns));  // ring position, once per pass
   for (int c = 0; c < nch; ++c, ++gcn) {
     if (threadIdx.x == 0 && c == 0)
-      for (int q0 = 0; q0 < g.ns && q0 < nch; ++q0) big_issue(g, T, n1, n2, gcn + q0, q0);
-    const int stage = static_cast<int>(gcn % g.ns);
+      for (int q0 = 0; q0 < g.ns && q0 < nch; ++q0) big_issue(g, T, n1, n2, gcn + q0, gb + q0, q0);
     if ((c & 1) == grp) {
-      const int k = c / cpk, jb = (c % cpk) * BJC;
-      ptx::mbar_wait(&g.full[stage], static_cast<uint32_t>((gcn / g.ns) & 1));
+      const uint32_t gq = fdiv(gb + c, g.ns_m);
+      const int stage = static_cast<int>(gb + c - gq * g.ns);
+      const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb = (c - k * cpk) * BJC;
+      ptx::mbar_wait(&g.full[stage], gq & 1u);
       const double* ts = g.Ts + stage * BJC * g.ldt;
       double acc[NTR][2];
 #pragma unroll
@@ -880,7 +896,7 @@ __device__ void big_pass2(const double* __restrict__ T, int n1, int n2, int n3, 
     // pass 2: the group that just consumed chunk c refills that stage with
     // chunk c + ns (its empty barrier only needs this group's arrivals), so
     // the two groups pipeline independently instead of waiting on each other
-    if ((c & 1) == grp && gtid == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, c + g.ns);
+    if ((c & 1) == grp && gtid == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, gb + c + g.ns, c + g.ns);
   }
   __syncthreads();
 }
@@ -903,7 +919,7 @@ int big_stages(int n1, int n2, int n3, int R) {
 
 template <int MTPW, int NTR>
 __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3,
-                                                        int ns) {
+                                                        int ns, int dbg) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_ok;
   __shared__ __align__(8) uint64_t bars[2 * BNS_MAX];
@@ -916,6 +932,8 @@ __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restric
   g.ldt = big_ld(n1);
   g.ldb = big_ld(n2);
   g.ns = ns;
+  g.ns_m = fdiv_magic(static_cast<uint32_t>(ns));
+  g.cpk_m = fdiv_magic(static_cast<uint32_t>(n2 / BJC));
   double* q = sm;
   g.Ts = q; q += ns * BJC * g.ldt;
   g.Bp = q; q += g.ldb * rp;
@@ -969,9 +987,12 @@ __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restric
   int64_t gcn = 0, it = 0, iters = 0;
   bool converged = false, stopped = false;
   double prev = 0.0;
+  long long tp1 = 0, tp2 = 0, tc = 0, t00 = clock64();
   for (; it < in.cfg.max_iters; ++it) {
     // pass 1: M_A for sweep it, residual of sweep it - 1
+    long long t0 = clock64();
     const double part = big_pass1<MTPW, NTR>(T, n1, n2, n3, R, s, g, gcn, it >= 1);
+    tp1 += clock64() - t0;
     if (it >= 1) {
       const double res = sqrt(block_sum(part, s.red));
       const double err = tn > 0.0 ? res / tn : res;
@@ -993,7 +1014,10 @@ __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restric
     gram(s.A, n1, R, s.G1);
     __syncthreads();
     // pass 2 + B update
+    t0 = clock64();
     big_pass2<NTR>(T, n1, n2, n3, R, s, g, gcn, in.pbuf);
+    tp2 += clock64() - t0;
+    t0 = clock64();
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G1[e];
     __syncthreads();
     solve_gram(s.M, n2, R, s, s.B, &s_ok);
@@ -1002,6 +1026,7 @@ __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restric
     __syncthreads();
     // C update
     mttkrp2_from_p(in.pbuf, n2, n3, R, s, s.M);
+    tc += clock64() - t0;
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G2[e] * s.G1[e];
     __syncthreads();
     solve_gram(s.M, n3, R, s, s.C, &s_ok);
@@ -1033,6 +1058,16 @@ __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restric
     gram(s.C, n3, R, s.G3);
     big_refresh(s, g, n2, R);
     __syncthreads();
+  }
+  if (dbg & 8) {
+    if (threadIdx.x == 0) {
+      in.hist[0] = double(tp1);
+      in.hist[1] = double(tp2);
+      in.hist[2] = double(tc);
+      in.hist[3] = double(clock64() - t00);
+      in.hist[4] = double(it);
+    }
+    return;
   }
   if (!stopped) {
     // residual of the last sweep (no next pass 1 to carry it)
@@ -1424,7 +1459,11 @@ void launch_als_big(const AlsInst* din, int64_t count, int n1, int n2, int n3, i
   const int mtpw = n1 / 64, ntr = (R + 7) / 8;
   auto go = [&](auto kern) {
     XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<static_cast<unsigned>(count), NT, smem, st>>>(din, n1, n2, n3, ns);
+    static const int dbg = [] {
+      const char* e = std::getenv("XTSG_ALS_BIG_DBG");  // 8: per-phase cycle counts (tools/als_big_cycles.py)
+      return e ? std::atoi(e) : 0;
+    }();
+    kern<<<static_cast<unsigned>(count), NT, smem, st>>>(din, n1, n2, n3, ns, dbg);
   };
   if (mtpw == 1) {
     if (ntr == 1) go(als_big_kernel<1, 1>); else if (ntr == 2) go(als_big_kernel<1, 2>); else go(als_big_kernel<1, 3>);

@@ -34,7 +34,10 @@ def run(cnt, its):
     t0 = time.perf_counter()
     check(lib.xtsg_cp_als_batched(cnt, ptr(td), n, n, n, cfgs, ptr(fa), ptr(fb), ptr(fc), ptr(it), ptr(cv), ptr(h)))
     torch.cuda.synchronize()
-    return time.perf_counter() - t0, h[its - 1].item()
+    dt = time.perf_counter() - t0
+    if "--abs" in sys.argv:
+        print(f"  batch={cnt} its={its}: {dt * 1e3:.2f} ms total, iters {sorted(set(it.cpu().tolist()))}")
+    return dt, h[its - 1].item()
 
 
 run(1, 2)
