@@ -688,7 +688,8 @@ struct BigSmem {
   double *Ts, *Bp, *red;
   uint64_t *full, *empty;
   int ldt, ldb, ns;
-  uint32_t ns_m, cpk_m;  // multiply-high reciprocals of ns and n2 / BJC
+  int sub;               // BJC-column sub-chunks per ring stage (1 or 2)
+  uint32_t ns_m, cpk_m;  // multiply-high reciprocals of ns and n2 / (sub * BJC)
 };
 
 // x / d for d >= 2 and x < 2^32 / d: one IMAD.HI instead of the ~20-deep
@@ -713,14 +714,13 @@ __device__ __forceinline__ void big_issue(const BigSmem& g, const double* T, int
   const uint32_t gq = fdiv(x, g.ns_m);
   const int stage = static_cast<int>(x - gq * g.ns);
   if (gnum >= g.ns) ptx::mbar_wait(&g.empty[stage], (gq - 1u) & 1u);
-  const int cpk = n2 / BJC;
-  const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb = (c - k * cpk) * BJC;
+  const int w = g.sub * BJC, cpk = n2 / w;
+  const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb = (c - k * cpk) * w;
   const uint32_t col_bytes = static_cast<uint32_t>(n1) * 8u;
-  ptx::mbar_arrive_expect_tx(&g.full[stage], col_bytes * BJC);
-  double* dst = g.Ts + stage * BJC * g.ldt;
+  ptx::mbar_arrive_expect_tx(&g.full[stage], col_bytes * w);
+  double* dst = g.Ts + stage * w * g.ldt;
   const double* src = T + static_cast<int64_t>(n1) * (jb + static_cast<int64_t>(n2) * k);
-#pragma unroll
-  for (int jj = 0; jj < BJC; ++jj)
+  for (int jj = 0; jj < w; ++jj)
     ptx::bulk_g2s(dst + jj * g.ldt, src + static_cast<int64_t>(n1) * jj, col_bytes, &g.full[stage]);
 }
 
@@ -735,7 +735,7 @@ __device__ double big_pass1(const double* __restrict__ T, int n1, int n2, int n3
                             const BigSmem& g, int64_t& gcn, bool want_res) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lr = lane >> 2, lc = lane & 3;
-  const int cpk = n2 / BJC, nch = n3 * cpk;
+  const int cpk = n2 / (g.sub * BJC), nch = n3 * cpk;
   double q[MTPW][NTR][2], macc[MTPW][NTR][2], areg[MTPW][2 * NTR], ahat[MTPW][2 * NTR];
 #pragma unroll
   for (int m = 0; m < MTPW; ++m)
@@ -754,65 +754,70 @@ __device__ double big_pass1(const double* __restrict__ T, int n1, int n2, int n3
   for (int c = 0; c < nch; ++c, ++gcn) {
     if (threadIdx.x == 0 && c == 0)
       for (int q0 = 0; q0 < g.ns && q0 < nch; ++q0) big_issue(g, T, n1, n2, gcn + q0, gb + q0, q0);
-    const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb = (c - k * cpk) * BJC;
-    if (jb == 0) {
-#pragma unroll
-      for (int kr = 0; kr < 2 * NTR; ++kr) {
-        const int r = kr * 4 + lc;
-        const double ck = r < R ? s.C[k + n3 * r] : 0.0;
-#pragma unroll
-        for (int m = 0; m < MTPW; ++m) ahat[m][kr] = areg[m][kr] * ck;
-      }
-    }
+    const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb0 = (c - k * cpk) * (g.sub * BJC);
     const uint32_t gq = fdiv(gb + c, g.ns_m);
     const int stage = static_cast<int>(gb + c - gq * g.ns);
     ptx::mbar_wait(&g.full[stage], gq & 1u);
-    const double* ts = g.Ts + stage * BJC * g.ldt;
-    // GEMM 1: q[i, r] += sum_j T[i, j] B[j, r]
+    for (int sb = 0; sb < g.sub; ++sb) {
+      const int jb = jb0 + sb * BJC;
+      const double* ts = g.Ts + (stage * g.sub + sb) * BJC * g.ldt;
+      if (jb == 0) {
 #pragma unroll
-    for (int ks = 0; ks < BJC / 4; ++ks) {
-      double b[NTR];
-#pragma unroll
-      for (int t = 0; t < NTR; ++t) b[t] = g.Bp[(jb + ks * 4 + lc) + g.ldb * (t * 8 + lr)];
-#pragma unroll
-      for (int m = 0; m < MTPW; ++m) {
-        const double a = ts[((warp * MTPW + m) * 8 + lr) + g.ldt * (ks * 4 + lc)];
-#pragma unroll
-        for (int t = 0; t < NTR; ++t) ptx::dmma(q[m][t][0], q[m][t][1], a, b[t]);
-      }
-    }
-    // GEMM 2 + residual: X^[i, j] = sum_r (A[i, r] C[k, r]) B[j, r]
-    if (want_res) {
-      double bb[2 * NTR];
-#pragma unroll
-      for (int kr = 0; kr < 2 * NTR; ++kr) bb[kr] = g.Bp[(jb + lr) + g.ldb * (kr * 4 + lc)];
-#pragma unroll
-      for (int m = 0; m < MTPW; ++m) {
-        double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-        for (int kr = 0; kr < 2 * NTR; ++kr) ptx::dmma(d0, d1, ahat[m][kr], bb[kr]);
-        const int i = (warp * MTPW + m) * 8 + lr;
-        const double t0 = ts[i + g.ldt * (2 * lc)], t1 = ts[i + g.ldt * (2 * lc + 1)];
-        res = fma(t0 - d0, t0 - d0, res);
-        res = fma(t1 - d1, t1 - d1, res);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&g.empty[stage]);
-    if (threadIdx.x == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, gb + c + g.ns, c + g.ns);
-    if (jb + BJC == n2) {  // slice k complete: macc += c_k .* q
-#pragma unroll
-      for (int t = 0; t < NTR; ++t)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = t * 8 + 2 * lc + e;
+        for (int kr = 0; kr < 2 * NTR; ++kr) {
+          const int r = kr * 4 + lc;
           const double ck = r < R ? s.C[k + n3 * r] : 0.0;
 #pragma unroll
-          for (int m = 0; m < MTPW; ++m) {
-            macc[m][t][e] = fma(ck, q[m][t][e], macc[m][t][e]);
-            q[m][t][e] = 0.0;
-          }
+          for (int m = 0; m < MTPW; ++m) ahat[m][kr] = areg[m][kr] * ck;
         }
+      }
+      // GEMM 1: q[i, r] += sum_j T[i, j] B[j, r]
+#pragma unroll
+      for (int ks = 0; ks < BJC / 4; ++ks) {
+        double b[NTR];
+#pragma unroll
+        for (int t = 0; t < NTR; ++t) b[t] = g.Bp[(jb + ks * 4 + lc) + g.ldb * (t * 8 + lr)];
+#pragma unroll
+        for (int m = 0; m < MTPW; ++m) {
+          const double a = ts[((warp * MTPW + m) * 8 + lr) + g.ldt * (ks * 4 + lc)];
+#pragma unroll
+          for (int t = 0; t < NTR; ++t) ptx::dmma(q[m][t][0], q[m][t][1], a, b[t]);
+        }
+      }
+      // GEMM 2 + residual: X^[i, j] = sum_r (A[i, r] C[k, r]) B[j, r]
+      if (want_res) {
+        double bb[2 * NTR];
+#pragma unroll
+        for (int kr = 0; kr < 2 * NTR; ++kr) bb[kr] = g.Bp[(jb + lr) + g.ldb * (kr * 4 + lc)];
+#pragma unroll
+        for (int m = 0; m < MTPW; ++m) {
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int kr = 0; kr < 2 * NTR; ++kr) ptx::dmma(d0, d1, ahat[m][kr], bb[kr]);
+          const int i = (warp * MTPW + m) * 8 + lr;
+          const double t0 = ts[i + g.ldt * (2 * lc)], t1 = ts[i + g.ldt * (2 * lc + 1)];
+          res = fma(t0 - d0, t0 - d0, res);
+          res = fma(t1 - d1, t1 - d1, res);
+        }
+      }
+      if (sb == g.sub - 1) {  // stage fully read: release it, refill
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&g.empty[stage]);
+        if (threadIdx.x == 0 && c + g.ns < nch) big_issue(g, T, n1, n2, gcn + g.ns, gb + c + g.ns, c + g.ns);
+      }
+      if (jb + BJC == n2) {  // slice k complete: macc += c_k .* q
+#pragma unroll
+        for (int t = 0; t < NTR; ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = t * 8 + 2 * lc + e;
+            const double ck = r < R ? s.C[k + n3 * r] : 0.0;
+#pragma unroll
+            for (int m = 0; m < MTPW; ++m) {
+              macc[m][t][e] = fma(ck, q[m][t][e], macc[m][t][e]);
+              q[m][t][e] = 0.0;
+            }
+          }
+      }
     }
   }
 #pragma unroll
@@ -830,8 +835,9 @@ __device__ double big_pass1(const double* __restrict__ T, int n1, int n2, int n3
 // Pass 2: P[r][k][j] = sum_i T[i, j, k] A[i, r] into global P, and
 // M_B[j, r] = sum_k C[k, r] P[r][k][j] into s.M (n2 x R). Two groups of four
 // warps take alternate chunks (K = i split over a group's warps, partials
-// reduced in a fixed order behind a group barrier); n2 % 16 == 0 keeps every
-// j column's slices in one group, so M_B accumulates over k in order.
+// reduced in a fixed order behind a group barrier); an even number of ring
+// chunks per slice keeps every j column's slices in one group, so M_B
+// accumulates over k in order.
 template <int NTR>
 __device__ void big_pass2(const double* __restrict__ T, int n1, int n2, int n3, int R, const Smem& s,
                           const BigSmem& g, int64_t& gcn, double* __restrict__ P) {
@@ -839,7 +845,7 @@ __device__ void big_pass2(const double* __restrict__ T, int n1, int n2, int n3, 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = warp >> 2, wq = warp & 3, gtid = threadIdx.x & 127;
   const int lr = lane >> 2, lc = lane & 3;
-  const int cpk = n2 / BJC, nch = n3 * cpk;
+  const int cpk = n2 / (g.sub * BJC), nch = n3 * cpk;  // cpk even: see big_sub()
   const int iw = n1 / 4, ks2 = iw / 4;  // i rows per warp, K steps
   double areg[NTR][KS_MAX];
 #pragma unroll
@@ -860,37 +866,42 @@ __device__ void big_pass2(const double* __restrict__ T, int n1, int n2, int n3, 
     if ((c & 1) == grp) {
       const uint32_t gq = fdiv(gb + c, g.ns_m);
       const int stage = static_cast<int>(gb + c - gq * g.ns);
-      const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb = (c - k * cpk) * BJC;
+      const int k = static_cast<int>(fdiv(c, g.cpk_m)), jb0 = (c - k * cpk) * (g.sub * BJC);
       ptx::mbar_wait(&g.full[stage], gq & 1u);
-      const double* ts = g.Ts + stage * BJC * g.ldt;
-      double acc[NTR][2];
+      for (int sb = 0; sb < g.sub; ++sb) {
+        const int jb = jb0 + sb * BJC;
+        const double* ts = g.Ts + (stage * g.sub + sb) * BJC * g.ldt;
+        double acc[NTR][2];
 #pragma unroll
-      for (int t = 0; t < NTR; ++t) acc[t][0] = acc[t][1] = 0.0;
+        for (int t = 0; t < NTR; ++t) acc[t][0] = acc[t][1] = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < KS_MAX; ++ks) {
-        if (ks < ks2) {
-          const double b = ts[(wq * iw + ks * 4 + lc) + g.ldt * lr];
+        for (int ks = 0; ks < KS_MAX; ++ks) {
+          if (ks < ks2) {
+            const double b = ts[(wq * iw + ks * 4 + lc) + g.ldt * lr];
 #pragma unroll
-          for (int t = 0; t < NTR; ++t) ptx::dmma(acc[t][0], acc[t][1], areg[t][ks], b);
+            for (int t = 0; t < NTR; ++t) ptx::dmma(acc[t][0], acc[t][1], areg[t][ks], b);
+          }
         }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&g.empty[stage], 2);
-      double* red = g.red + (grp * 2 + (use & 1)) * 4 * rp * BJC;
-      ++use;
+        if (sb == g.sub - 1) {  // stage fully read by this warp
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cnt(&g.empty[stage], 2);
+        }
+        double* red = g.red + (grp * 2 + (use & 1)) * 4 * rp * BJC;
+        ++use;
 #pragma unroll
-      for (int t = 0; t < NTR; ++t)
+        for (int t = 0; t < NTR; ++t)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) red[(wq * rp + t * 8 + lr) * BJC + 2 * lc + e] = acc[t][e];
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-      for (int e = gtid; e < R * BJC; e += 128) {
-        const int r = e / BJC, jj = e % BJC;
-        double v = 0.0;
+          for (int e = 0; e < 2; ++e) red[(wq * rp + t * 8 + lr) * BJC + 2 * lc + e] = acc[t][e];
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+        for (int e = gtid; e < R * BJC; e += 128) {
+          const int r = e / BJC, jj = e % BJC;
+          double v = 0.0;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) v += red[(w * rp + r) * BJC + jj];
-        const int j = jb + jj;
-        P[static_cast<int64_t>(r) * n2 * n3 + static_cast<int64_t>(n2) * k + j] = v;
-        s.M[j + n2 * r] = fma(s.C[k + n3 * r], v, s.M[j + n2 * r]);
+          for (int w = 0; w < 4; ++w) v += red[(w * rp + r) * BJC + jj];
+          const int j = jb + jj;
+          P[static_cast<int64_t>(r) * n2 * n3 + static_cast<int64_t>(n2) * k + j] = v;
+          s.M[j + n2 * r] = fma(s.C[k + n3 * r], v, s.M[j + n2 * r]);
+        }
       }
     }
     // pass 2: the group that just consumed chunk c refills that stage with
@@ -909,17 +920,18 @@ size_t big_fixed_doubles(int n1, int n2, int n3, int R) {
 }
 constexpr size_t BIG_SMEM_CAP = 225 * 1024;
 
-// stages that fit next to the fixed working set (0 when not even 3 do)
-int big_stages(int n1, int n2, int n3, int R) {
+// stages of `sub` sub-chunks that fit next to the fixed working set (0 when
+// not even 3 do)
+int big_stages(int n1, int n2, int n3, int R, int sub = 1) {
   const size_t fixed = big_fixed_doubles(n1, n2, n3, R) * 8;
-  const size_t per = static_cast<size_t>(BJC) * (n1 + 4) * 8;
+  const size_t per = static_cast<size_t>(sub) * BJC * (n1 + 4) * 8;
   if (fixed + 3 * per > BIG_SMEM_CAP) return 0;
   return static_cast<int>(std::min<size_t>(BNS_MAX, (BIG_SMEM_CAP - fixed) / per));
 }
 
 template <int MTPW, int NTR>
 __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3,
-                                                        int ns, int dbg) {
+                                                        int ns, int sub, int dbg) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_ok;
   __shared__ __align__(8) uint64_t bars[2 * BNS_MAX];
@@ -932,10 +944,11 @@ __global__ void __launch_bounds__(NT, 1) als_big_kernel(const AlsInst* __restric
   g.ldt = big_ld(n1);
   g.ldb = big_ld(n2);
   g.ns = ns;
+  g.sub = sub;
   g.ns_m = fdiv_magic(static_cast<uint32_t>(ns));
-  g.cpk_m = fdiv_magic(static_cast<uint32_t>(n2 / BJC));
+  g.cpk_m = fdiv_magic(static_cast<uint32_t>(n2 / (sub * BJC)));
   double* q = sm;
-  g.Ts = q; q += ns * BJC * g.ldt;
+  g.Ts = q; q += ns * sub * BJC * g.ldt;
   g.Bp = q; q += g.ldb * rp;
   g.red = q; q += 4 * 4 * rp * BJC;
   s.A = q; q += n1 * R;
@@ -1453,9 +1466,19 @@ bool als_big_eligible(int64_t n1, int64_t n2, int64_t n3, int64_t R) {
   return big_stages(int(n1), int(n2), int(n3), int(R)) >= 3;
 }
 
+// sub-chunks per ring stage: two (16 columns: half the per-stage ring
+// bookkeeping, barrier waits and refills) when n2 % 32 == 0 keeps an even
+// number of stages per slice and at least 3 such stages fit, else one
+int big_sub(int n1, int n2, int n3, int R) {
+  if (const char* e = std::getenv("XTSG_ALS_BIG_SUB"))  // "1": 8-column stages (A/B runs)
+    if (std::atoi(e) == 1) return 1;
+  return (n2 % 32 == 0 && big_stages(n1, n2, n3, R, 2) >= 3) ? 2 : 1;
+}
+
 void launch_als_big(const AlsInst* din, int64_t count, int n1, int n2, int n3, int R, cudaStream_t st) {
-  const int ns = big_stages(n1, n2, n3, R);
-  const size_t smem = 8 * (big_fixed_doubles(n1, n2, n3, R) + static_cast<size_t>(ns) * BJC * (n1 + 4));
+  const int sub = big_sub(n1, n2, n3, R);
+  const int ns = big_stages(n1, n2, n3, R, sub);
+  const size_t smem = 8 * (big_fixed_doubles(n1, n2, n3, R) + static_cast<size_t>(ns) * sub * BJC * (n1 + 4));
   const int mtpw = n1 / 64, ntr = (R + 7) / 8;
   auto go = [&](auto kern) {
     XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1463,7 +1486,7 @@ void launch_als_big(const AlsInst* din, int64_t count, int n1, int n2, int n3, i
       const char* e = std::getenv("XTSG_ALS_BIG_DBG");  // 8: per-phase cycle counts (tools/als_big_cycles.py)
       return e ? std::atoi(e) : 0;
     }();
-    kern<<<static_cast<unsigned>(count), NT, smem, st>>>(din, n1, n2, n3, ns, dbg);
+    kern<<<static_cast<unsigned>(count), NT, smem, st>>>(din, n1, n2, n3, ns, sub, dbg);
   };
   if (mtpw == 1) {
     if (ntr == 1) go(als_big_kernel<1, 1>); else if (ntr == 2) go(als_big_kernel<1, 2>); else go(als_big_kernel<1, 3>);
