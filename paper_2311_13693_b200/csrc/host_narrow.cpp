@@ -5,8 +5,13 @@
 // per-ISA clones so the branchless loop vectorises on AVX-512 / AVX2 hosts.
 #include <immintrin.h>
 
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 namespace xtsg {
 
@@ -212,6 +217,68 @@ void narrow_rows_f64(const double* x, int64_t ni, int64_t nj, int64_t ld0, int64
     else narrow_row(x + j * ld0 + k * ld1, ni, dst);
     for (int64_t i = ni; i < ldi; ++i) dst[i] = 0;
   }
+}
+
+// Persistent fork-join workers for the narrowing slabs: spawning and joining
+// a fresh std::thread per worker per 256 MB slab cost ~0.3 ms of a ~6 ms
+// slab. One run at a time (callers serialise on run_mu); the pool is leaked
+// on purpose so no joinable thread is destroyed at process exit.
+namespace {
+class WorkerPool {
+ public:
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> rg(run_mu_);
+    while (static_cast<int>(th_.size()) < n - 1) {
+      const int id = static_cast<int>(th_.size()) + 1;
+      th_.emplace_back([this, id] { worker(id); });
+    }
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &fn;
+      njob_ = n;
+      remaining_ = n - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [&] { return remaining_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void worker(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f = nullptr;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (id >= njob_) continue;
+        f = job_;
+      }
+      (*f)(id);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--remaining_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> th_;
+  const std::function<void(int)>* job_ = nullptr;
+  int njob_ = 0, remaining_ = 0;
+  uint64_t gen_ = 0;
+};
+}  // namespace
+
+void run_workers(int n, const std::function<void(int)>& fn) {
+  static WorkerPool* pool = new WorkerPool;
+  if (n <= 1) {
+    fn(0);
+    return;
+  }
+  pool->run(n, fn);
 }
 
 }  // namespace xtsg

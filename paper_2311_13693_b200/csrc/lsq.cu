@@ -309,11 +309,8 @@ bool lsq_chol_dev(const double* A, int64_t m, int64_t n, const double* B, int64_
   if (!(mx > 0.0)) return false;
   const double tau = 1e-6 * mx;
   const size_t smem = sizeof(double) * 2 * CNB * (CNB + 1);
-  static bool attr = false;
-  if (!attr) {
-    XCUDA(cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = true;
-  }
+  // per call (the attribute is per device; no unsynchronised static flag)
+  XCUDA(cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   for (int64_t b = 0; b < nblk; ++b) {
     const int64_t j0 = b * CNB, nb = std::min<int64_t>(CNB, n - j0), n2 = n - j0 - nb;
     potrf_block_kernel<<<1, 256, smem, st>>>(G.ptr, n, j0, static_cast<int>(nb), Linv.ptr + b * CNB * CNB, fail.ptr,

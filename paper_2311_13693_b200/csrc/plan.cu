@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -470,6 +471,7 @@ void narrow_rows_f32(const float* x, int64_t ni, int64_t nj, int64_t ld0, int64_
                      int64_t row1, int64_t ldi, uint16_t* out, bool f16);
 void narrow_rows_f64(const double* x, int64_t ni, int64_t nj, int64_t ld0, int64_t ld1, int64_t k0, int64_t row0,
                      int64_t row1, int64_t ldi, uint16_t* out, bool f16);
+void run_workers(int n, const std::function<void(int)>& fn);
 
 namespace {
 
@@ -527,18 +529,14 @@ void Plan::compress_host_narrow(const void* x, int32_t dtype, const int64_t ld[2
     if (sl >= 2) XCUDA(cudaEventSynchronize(ev_h2d[b]));
     const int64_t rows = kn * ext[1];
     uint16_t* hb = static_cast<uint16_t*>(hpin[b]);
-    std::vector<std::thread> pool;
     const int nt = static_cast<int>(std::min<int64_t>(nthr, rows));
-    for (int t = 0; t < nt; ++t) {
+    run_workers(nt, [&](int t) {
       const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
       if (dtype == XTSG_DTYPE_F32)
-        pool.emplace_back(narrow_rows_f32, static_cast<const float*>(x), ext[0], ext[1], ld[0], ld[1], k0, r0, r1,
-                          ldi, hb, fp16());
+        narrow_rows_f32(static_cast<const float*>(x), ext[0], ext[1], ld[0], ld[1], k0, r0, r1, ldi, hb, fp16());
       else
-        pool.emplace_back(narrow_rows_f64, static_cast<const double*>(x), ext[0], ext[1], ld[0], ld[1], k0, r0,
-                          r1, ldi, hb, fp16());
-    }
-    for (auto& th : pool) th.join();
+        narrow_rows_f64(static_cast<const double*>(x), ext[0], ext[1], ld[0], ld[1], k0, r0, r1, ldi, hb, fp16());
+    });
     // the device buffer is free once the compression of slab sl - 2 is done
     if (sl >= 2) XCUDA(cudaStreamWaitEvent(copy_st, ev_consumed[b], 0));
     XCUDA(cudaMemcpyAsync(dstage[b].ptr, hb, static_cast<size_t>(rows * row_bytes), cudaMemcpyHostToDevice, copy_st));

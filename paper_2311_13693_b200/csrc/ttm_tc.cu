@@ -368,12 +368,9 @@ void launch_impl(const TtmLaunch& L, cudaStream_t st) {
     const uint32_t box[2] = {64, static_cast<uint32_t>(L.prm.n2)};
     make_map(&mv, L.v, 2, dims, str, box, L.prm.f16 != 0);
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    XCUDA(cudaFuncSetAttribute(ttm_fused_kernel<MPAD, Cfg, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               Cfg::SMEM_TOTAL));
-    attr_set = true;
-  }
+  // per launch: the attribute is per device, and a static flag would race
+  XCUDA(cudaFuncSetAttribute(ttm_fused_kernel<MPAD, Cfg, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::SMEM_TOTAL));
   if (L.prm.n_rb % CS) usage("ttm_fused: row blocks must be a multiple of the cluster size");
   const int clusters = (L.prm.n_rb / CS) * L.prm.kc;
   const int cap = (L.grid_limit > 0 ? L.grid_limit : sm_count()) / CS;

@@ -458,11 +458,9 @@ void launch_pair(const TtmLaunch& L, cudaStream_t st) {
     map_bf16(&mv, L.v, 2, dims, str, box, L.prm.f16 != 0);
   }
   constexpr int SMEM_TOTAL = smem_total(S, A2_SLOTS);
-  static bool attr_set = false;
-  if (!attr_set) {
-    XCUDA(cudaFuncSetAttribute(ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
-    attr_set = true;
-  }
+  // per launch: the attribute is per device, and a static flag would race
+  XCUDA(cudaFuncSetAttribute(ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_TOTAL));
   const int clusters = (L.prm.n_rb / 2) * L.prm.kc;
   const int cap = (L.grid_limit > 0 ? L.grid_limit : sm_count()) / 2;
   const int ncl = std::max(1, std::min(clusters, cap));
