@@ -1236,15 +1236,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
         const int i0 = (tile % nti) * 8, r0 = (tile / nti) * 8;
         const int ia = i0 + lr, rb = r0 + lr;
         double d0 = 0.0, d1 = 0.0;
+        // fiber f = f0 + lc -> (j, kk) = (f % n2, f / n2), stepped by 4
+        // without a runtime division per DMMA (it sat on the chain's critical path)
+        int j = lc % n2, kk = lc / n2;
         for (int f0 = 0; f0 < nf; f0 += 4) {
           const int f = f0 + lc;
           const double a = (ia < n1 && f < nf) ? Ts[ia + static_cast<int64_t>(n1) * f] : 0.0;
-          double b = 0.0;
-          if (f < nf && rb < R) {
-            const int j = f % n2, kk = f / n2;
-            b = s.B[j + n2 * rb] * s.C[(k0 + kk) + n3 * rb];
-          }
+          const double b = (f < nf && rb < R) ? s.B[j + n2 * rb] * s.C[(k0 + kk) + n3 * rb] : 0.0;
           ptx::dmma(d0, d1, a, b);
+          j += 4;
+          while (j >= n2) {
+            j -= n2;
+            ++kk;
+          }
         }
         const int rc = r0 + 2 * lc;
         if (ia < n1) {
