@@ -497,10 +497,12 @@ bool ttm_pair_supported(const TtmLaunch& L) {
 void launch_ttm_pair(const TtmLaunch& L, cudaStream_t st) {
   if (!ttm_pair_supported(L)) usage("ttm_pair: unsupported shape for the CTA-pair kernel");
   // 0: mode 2 on the pair (M = 256); 1: mode 2 per CTA (cta_group::1, M = 128,
-  // half the wasted columns), 4 stages; 2: per-CTA mode 2, 5 stages / 2 A2 slots
+  // half the wasted columns), 4 stages; 2 (default): per-CTA mode 2, 5 stages /
+  // 2 A2 slots — measured back to back on one box: C2 29.2 -> 28.4 ms/step,
+  // every C5 (L, P) point +1-5 %, C3 within 2 % (profiles/r1_pair_variants.json)
   static const int variant = [] {
     const char* e = std::getenv("XTSG_TTM_PAIR_CFG");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   auto go = [&](auto mpad_tag) {
     constexpr int MP = decltype(mpad_tag)::value;
