@@ -499,7 +499,7 @@ void launch_ttm_pair(const TtmLaunch& L, cudaStream_t st) {
   // 0: mode 2 on the pair (M = 256); 1: mode 2 per CTA (cta_group::1, M = 128,
   // half the wasted columns), 4 stages; 2 (default): per-CTA mode 2, 5 stages /
   // 2 A2 slots — measured back to back on one box: C2 29.2 -> 28.4 ms/step,
-  // every C5 (L, P) point +1-5 %, C3 within 2 % (profiles/r1_pair_variants.json)
+  // every C5 (L, P) point +1-5 %, C3 equal (profiles/r1_pair_variants.json)
   static const int variant = [] {
     const char* e = std::getenv("XTSG_TTM_PAIR_CFG");
     return e ? std::atoi(e) : 2;
