@@ -132,6 +132,7 @@ def _noisy(shape, rank, seed, noise):
     ((64, 64, 64), 5, 0.0, 300),      # exact low rank (this seed swamps in both)
     ((128, 96, 40), 20, 3e-3, 60),    # config-3-like noisy replica, capped sweeps
     ((64, 128, 24), 12, 1e-2, 7),     # max_iters path (final residual pass)
+    ((128, 48, 30), 10, 1e-3, 40),    # n2 % 32 == 16: 8-column ring stages (one sub-chunk per stage)
 ])
 def test_large_replica_trajectory_matches_reference(gpu, reference, shape, rank, noise, max_iters):
     t = _noisy(shape, rank, 17, noise)
