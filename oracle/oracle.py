@@ -56,6 +56,7 @@ class Restated:
             "or_gen_gaussian": (None, [_I64, _I64, _U64, _P]),
             "or_gen_sparse": (None, [_I64, _I64, _D, _U64, _P]),
             "or_make_ensemble": (None, [_P, _P, _I64, _I64, C.c_int, _D, C.c_int, _D, _P, _U64, _P, _P, _P]),
+            "or_gen_replica_cols": (None, [_I64, _I64, _I64, C.c_int, _D, _U64, _U64, _U64, _I64, _P, _P]),
             "or_comp": (None, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
             "or_reconstruct": (None, [_P, _P, _P, _I64, _I64, _I64, _I64, _P]),
             "or_comp_from_factors": (None, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
@@ -109,6 +110,26 @@ class Restated:
         per = [int(red[m] * dims[m]) for m in range(3)]
         return [[bufs[m][p * per[m]:(p + 1) * per[m]].reshape(int(red[m]), int(dims[m]), order="F")
                  for p in range(count)] for m in range(3)]
+
+    def ensemble_cols(self, dims, red, count, shared, seed, cols=None, kind=0, s=1.0, threads=None):
+        """make_ensemble (gaussian/sparse kinds, compression.cpp:115-155)
+        restricted to the columns cols[m] (sorted int64 indices; None = all)
+        of each mode; the (mode, replica) matrices are generated on a thread
+        pool (ctypes releases the GIL). Returns [mode][p] -> red[m] x len(cols[m])."""
+        from concurrent.futures import ThreadPoolExecutor
+        import os
+        cols = [np.arange(int(dims[m]), dtype=np.int64) if cols is None or cols[m] is None
+                else np.ascontiguousarray(cols[m], dtype=np.int64) for m in range(3)]
+        out = [[np.zeros((int(red[m]), len(cols[m])), order="F") for _ in range(count)] for m in range(3)]
+
+        def one(mp):
+            m, p = mp
+            self.L.or_gen_replica_cols(int(red[m]), p, shared, kind, s, self.derive(seed, 101 + m), seed, m,
+                                       len(cols[m]), _ptr(cols[m]), _ptr(out[m][p]))
+
+        with ThreadPoolExecutor(threads or os.cpu_count() or 4) as ex:
+            list(ex.map(one, [(m, p) for m in range(3) for p in range(count)]))
+        return out
 
     def comp(self, t, u, v, w):
         t, u, v, w = _f(t), _f(u), _f(v), _f(w)
@@ -250,6 +271,26 @@ class Reference:
         per = [int(red[m] * dims[m]) for m in range(3)]
         return [[bufs[m][p * per[m]:(p + 1) * per[m]].reshape(int(red[m]), int(dims[m]), order="F")
                  for p in range(count)] for m in range(3)]
+
+    def ensemble_cols(self, dims, red, count, shared, seed, cols=None, kind=0, s=1.0, threads=None):
+        """make_ensemble (gaussian/sparse kinds, compression.cpp:115-155)
+        restricted to the columns cols[m] (sorted int64 indices; None = all)
+        of each mode; the (mode, replica) matrices are generated on a thread
+        pool (ctypes releases the GIL). Returns [mode][p] -> red[m] x len(cols[m])."""
+        from concurrent.futures import ThreadPoolExecutor
+        import os
+        cols = [np.arange(int(dims[m]), dtype=np.int64) if cols is None or cols[m] is None
+                else np.ascontiguousarray(cols[m], dtype=np.int64) for m in range(3)]
+        out = [[np.zeros((int(red[m]), len(cols[m])), order="F") for _ in range(count)] for m in range(3)]
+
+        def one(mp):
+            m, p = mp
+            self.L.or_gen_replica_cols(int(red[m]), p, shared, kind, s, self.derive(seed, 101 + m), seed, m,
+                                       len(cols[m]), _ptr(cols[m]), _ptr(out[m][p]))
+
+        with ThreadPoolExecutor(threads or os.cpu_count() or 4) as ex:
+            list(ex.map(one, [(m, p) for m in range(3) for p in range(count)]))
+        return out
 
     def comp(self, t, u, v, w):
         t, u, v, w = _f(t), _f(u), _f(v), _f(w)

@@ -117,6 +117,26 @@ void or_gen_mode(int64_t rows, int64_t cols, int64_t count, int64_t shared, int 
   }
 }
 
+/* compression.cpp:51-72 for ONE replica p of one mode, keeping only the
+ * columns idx[0..nidx) (ascending): each row's stream is drawn up to the last
+ * kept column, exactly as fill_row draws it. out is rows x nidx column-major.
+ * Lets the tests check index spaces (10^6 columns) without materialising the
+ * whole ensemble, and lets callers spread replicas over threads. */
+void or_gen_replica_cols(int64_t rows, int64_t p, int64_t shared, int kind, double s, uint64_t shared_seed,
+                         uint64_t seed, uint64_t tag, int64_t nidx, const int64_t* idx, double* out) {
+  const uint64_t rep = or_derive(seed, 1000 + 8 * (uint64_t)p + tag);
+  const int64_t last = nidx ? idx[nidx - 1] : -1;
+  for (int64_t r = 0; r < rows; ++r) {
+    const int sh = r < shared;
+    orng g = mk(or_derive(sh ? shared_seed : rep, (uint64_t)r));
+    int64_t q = 0;
+    for (int64_t j = 0; j <= last; ++j) {
+      const double x = (sh || kind == 0) ? normal(&g) : three_point(&g, s);
+      while (q < nidx && idx[q] == j) out[r + rows * q++] = x;
+    }
+  }
+}
+
 /* naive column-major gemm C = A * B (fixed k order) */
 static void gemm_nn(int64_t m, int64_t n, int64_t k, const double* a, const double* b, double* c) {
   for (int64_t j = 0; j < n; ++j)

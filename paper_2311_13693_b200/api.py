@@ -82,8 +82,6 @@ def make_ensemble(dims, reduced, count: int, shared_rows: int, seed: int, kind="
     dims, reduced = _arr3(dims), _arr3(reduced)
     sp = _spec(kind, **spec)
     P = max(int(count), 0)
-    bufs = [np.zeros((P, int(reduced[m]), int(dims[m])), np.float64) for m in range(3)]
-    mats = [np.zeros((P, int(reduced[m]), int(dims[m])), np.float64).transpose(0, 2, 1) for m in range(3)]
     inner = outer = None
     if sp.kind == KIND_TWO_STAGE:
         ratio = [sp.alpha, sp.beta, sp.gamma]
@@ -94,7 +92,6 @@ def make_ensemble(dims, reduced, count: int, shared_rows: int, seed: int, kind="
     args = raw + (inner if inner else [None] * 3) + (outer if outer else [None] * 3)
     check(lib.xtsg_make_ensemble(ptr(dims), ptr(reduced), int(count), int(shared_rows),
                                  C.byref(sp), C.c_uint64(seed), *[ptr(a) for a in args]))
-    del bufs, mats
     per = [int(reduced[m] * dims[m]) for m in range(3)]
     lists = [[raw[m][p * per[m]:(p + 1) * per[m]].reshape(int(reduced[m]), int(dims[m]), order="F")
               for p in range(P)] for m in range(3)]
@@ -429,12 +426,23 @@ class AlsResult:
 
 
 def cp_als_batched(tensors: Sequence, rank: int, max_iters: int = 500, tol: float = 1e-10,
-                   seeds: Sequence[int] = (0,), init: Sequence[int] | int = 0):
+                   seeds: Sequence[int] | int = 0, init: Sequence[int] | int = 0):
+    """cp_als over a batch of same-shape tensors; ``seeds``/``init`` are one
+    value for every tensor or one per tensor."""
     ts = [_f64(t) for t in tensors]
     n = len(ts)
+    if n == 0:
+        return []
     n1, n2, n3 = ts[0].shape
+    if any(t.shape != ts[0].shape for t in ts):
+        from ._lib import UsageError
+        raise UsageError("cp_als_batched: every tensor must have the same shape")
+    seeds = [int(seeds)] * n if isinstance(seeds, (int, np.integer)) else list(seeds)
+    inits = [int(init)] * n if isinstance(init, (int, np.integer)) else list(init)
+    if len(seeds) != n or len(inits) != n:
+        from ._lib import UsageError
+        raise UsageError("cp_als_batched: seeds/init must be a scalar or one per tensor")
     cfgs = (AlsConfig * n)()
-    inits = [init] * n if isinstance(init, int) else list(init)
     for q in range(n):
         cfgs[q] = AlsConfig(int(rank), int(max_iters), float(tol), C.c_uint64(seeds[q]).value,
                             int(inits[q]), 0)

@@ -542,6 +542,7 @@ extern "C" int32_t xtsg_plan_compress_coo(xtsg_plan* plan, const int32_t* i, con
   return guard([&] {
     Plan* p = reinterpret_cast<Plan*>(plan);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
+    PlanUse use(p, s);
     p->compress_coo(i, j, k, val, nnz, static_cast<float*>(y), accumulate != 0, s);
   });
 }
@@ -553,6 +554,7 @@ extern "C" int32_t xtsg_plan_compress_csf(xtsg_plan* plan, int64_t n_slices, con
   return guard([&] {
     Plan* p = reinterpret_cast<Plan*>(plan);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
+    PlanUse use(p, s);
     p->compress_csf(n_slices, slice_k, slice_ptr, n_fibers, fiber_j, fiber_ptr, nnz, nz_i, val,
                     static_cast<float*>(y), accumulate != 0, s);
   });

@@ -169,6 +169,7 @@ extern "C" int32_t xtsg_plan_compress_factors(xtsg_plan* plan, const double* a, 
   return guard([&] {
     Plan* p = reinterpret_cast<Plan*>(plan);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
+    PlanUse use(p, s);
     p->compress_factors(a, b, c, rank, k0, k1, static_cast<float*>(y), accumulate != 0, s);
   });
 }

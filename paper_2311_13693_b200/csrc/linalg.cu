@@ -632,7 +632,15 @@ int32_t xtsg_omp_recover(const double* measured, int64_t rows, int64_t ncols, co
       const char* e = std::getenv("XTSG_OMP_WIDE_FROM");
       return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(4096);
     }();
-    if (ncols > 0 && atoms >= wide_from) {
+    // residuals of `cb` columns must fit the opt-in shared memory next to the
+    // kernel's static arrays; with not even one column (rows > ~28k) the
+    // per-column omp_kernel (no rows limit) runs instead
+    int dev = 0, optin = 0;
+    XCUDA(cudaGetDevice(&dev));
+    XCUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const int64_t static_smem = (NT / 32) * OMP_CB * (sizeof(double) + sizeof(int64_t)) + 1024;
+    const int64_t cb = std::min<int64_t>(OMP_CB, (optin - static_smem) / (sizeof(double) * std::max<int64_t>(1, rows)));
+    if (ncols > 0 && atoms >= wide_from && cb >= 1) {
       // large dictionaries: the atom search over the whole GPU (omp_search_kernel)
       const int nsearch = std::max(1, std::min(sm_count() * 4, static_cast<int>(ceil_div(atoms, 64))));
       DevBuf<double> res(static_cast<size_t>(rows * ncols), st), cv(static_cast<size_t>(ncols * nsearch), st);
@@ -643,13 +651,13 @@ int32_t xtsg_omp_recover(const double* measured, int64_t rows, int64_t ncols, co
       omp_init_kernel<<<static_cast<unsigned>(ncols), NT, 0, st>>>(y.dev, rows, ncols, residual_tol, res.ptr,
                                                                    done.ptr, na.ptr);
       XLAUNCH_CHECK();
-      const size_t smem = sizeof(double) * OMP_CB * rows;
+      const size_t smem = sizeof(double) * cb * rows;
       if (smem > 48 * 1024)
         XCUDA(cudaFuncSetAttribute(omp_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
       for (int64_t it = 0; it < sparsity; ++it) {
-        for (int64_t c0 = 0; c0 < ncols; c0 += OMP_CB) {
-          const int nc = static_cast<int>(std::min<int64_t>(OMP_CB, ncols - c0));
+        for (int64_t c0 = 0; c0 < ncols; c0 += cb) {
+          const int nc = static_cast<int>(std::min<int64_t>(cb, ncols - c0));
           omp_search_kernel<<<nsearch, NT, sizeof(double) * nc * rows, st>>>(
               d.dev, rows, atoms, nrm.ptr, res.ptr, mask.ptr, done.ptr, c0, nc, cv.ptr, ci.ptr, ncols);
           XLAUNCH_CHECK();

@@ -194,6 +194,7 @@ Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
   XCUDA(cudaGetDevice(&device));
   st = thread_stream();
   XCUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
+  XCUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
   const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
   const bool two = desc.spec.kind == XTSG_KIND_TWO_STAGE && tensor_core();
@@ -243,6 +244,7 @@ Plan::Plan(const xtsg_plan_desc& d, const double* u, const double* v, const doub
   XCUDA(cudaGetDevice(&device));
   st = thread_stream();
   XCUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
+  XCUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
   const int64_t P = desc.count;
   u64 = DevBuf<double>(static_cast<size_t>(P * desc.reduced[0] * desc.dims[0]), st);
   v64 = DevBuf<double>(static_cast<size_t>(P * desc.reduced[1] * desc.dims[1]), st);
@@ -315,6 +317,10 @@ void Plan::stage2(const float* zin, float* y, bool accumulate, cudaStream_t s) {
 }
 
 Plan::~Plan() {
+  if (ev_done) {
+    cudaEventSynchronize(ev_done);
+    cudaEventDestroy(ev_done);
+  }
   cudaStreamSynchronize(st);
   for (auto* v : {&ev_pool, &ev_fused, &ev_mode3})
     for (auto& e : *v) {
@@ -741,12 +747,17 @@ int32_t xtsg_plan_create(const xtsg_plan_desc* desc, xtsg_plan** out) {
 void xtsg_plan_destroy(xtsg_plan* plan) { delete reinterpret_cast<Plan*>(plan); }
 
 int32_t xtsg_plan_set_profiling(xtsg_plan* plan, int32_t on) {
-  return guard([&] { reinterpret_cast<Plan*>(plan)->profiling = on != 0; });
+  return guard([&] {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->profiling = on != 0;
+  });
 }
 
 int32_t xtsg_plan_profile(xtsg_plan* plan, int32_t reset, double out[6]) {
   return guard([&] {
     Plan* p = reinterpret_cast<Plan*>(plan);
+    std::lock_guard<std::mutex> lk(p->mu);
     double fused = 0.0, m3 = 0.0;
     for (auto& e : p->ev_fused) {
       float ms = 0.f;
@@ -782,6 +793,7 @@ int32_t xtsg_plan_compress(xtsg_plan* plan, const void* x, int32_t x_dtype, cons
   return guard([&] {
     Plan* p = reinterpret_cast<Plan*>(plan);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
+    PlanUse use(p, s);
     p->compress(x, x_dtype, ld, offset, extent, y, accumulate != 0, s);
   });
 }

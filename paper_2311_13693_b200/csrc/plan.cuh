@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -11,6 +12,12 @@ namespace xtsg {
 
 struct Plan {
   xtsg_plan_desc desc;
+  // Calls on one plan serialise: the host side under `mu`, the device side
+  // through `ev_done` (each call's stream waits for the previous call's work,
+  // on whatever stream it ran), because Z, the lane counters and the pinned
+  // ring are per plan. Concurrent compressions use one plan each.
+  std::mutex mu;
+  cudaEvent_t ev_done = nullptr;
   int device = 0;
   cudaStream_t st = nullptr;       // creation stream
   cudaStream_t copy_st = nullptr;  // H2D slab stream
@@ -83,6 +90,17 @@ struct Plan {
   void ensure_sparse_operands(cudaStream_t s);
   void coo_slices(const int32_t* si, const int32_t* sj, const float* sv, const int64_t* off, const int32_t* cnt,
                   const int32_t* uk, int64_t kd, float* ydev, bool accumulate, cudaStream_t s);
+};
+
+// RAII use of a plan by one C-ABI call on stream s (see Plan::mu).
+struct PlanUse {
+  Plan* p;
+  cudaStream_t s;
+  std::lock_guard<std::mutex> lk;
+  PlanUse(Plan* p_, cudaStream_t s_) : p(p_), s(s_), lk(p_->mu) { XCUDA(cudaStreamWaitEvent(s, p->ev_done, 0)); }
+  ~PlanUse() { cudaEventRecord(p->ev_done, s); }
+  PlanUse(const PlanUse&) = delete;
+  PlanUse& operator=(const PlanUse&) = delete;
 };
 
 }  // namespace xtsg

@@ -191,6 +191,7 @@ int32_t xtsg_plan_compress_file(xtsg_plan* plan, const char* path, int64_t slab_
     if (!path) usage("plan_compress_file: null path");
     Plan* p = reinterpret_cast<Plan*>(plan);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : thread_stream();
+    PlanUse use(p, s);
     Fd f;
     f.fd = ::open(path, O_RDONLY);
     if (f.fd < 0) data_error(std::string("cannot open: ") + path);

@@ -18,6 +18,39 @@ def slab_range(K: int, rank: int, world: int) -> tuple[int, int]:
     return k0, k0 + base + (1 if rank < extra else 0)
 
 
+class RemoteStageError(RuntimeError):
+    """A stage failed on another rank; every rank raises this (or the
+    original exception on the failing rank) instead of blocking in the next
+    collective."""
+
+
+def _broadcast_outcome(rank, dst, group, shapes=None, error=None):
+    """dst tells every rank whether its stage succeeded (and the factor
+    shapes) before any tensor collective; returns the shapes or raises."""
+    import torch.distributed as dist
+
+    box = [(shapes, error)] if rank == dst else [None]
+    dist.broadcast_object_list(box, src=dst, group=group)
+    shapes, error = box[0]
+    if error is not None:
+        raise RemoteStageError(error)
+    return shapes
+
+
+def _broadcast_factors(factors, shapes, rank, dst, group, device):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    out = []
+    for m, shp in enumerate(shapes):
+        t = (torch.from_numpy(np.asfortranarray(factors[m]).ravel(order="F")).to(device) if rank == dst
+             else torch.zeros(shp[0] * shp[1], dtype=torch.float64, device=device))
+        dist.broadcast(t, src=dst, group=group)
+        out.append(t.cpu().numpy().reshape(shp, order="F"))
+    return tuple(out)
+
+
 def compress_sharded(local_compress, K: int, y, dst: int = 0, group=None):
     """Run ``local_compress(k0, k1, y)`` on this rank's slab, then sum-reduce y to ``dst``.
 
@@ -47,26 +80,27 @@ def decompose_sharded(compress_slab, K: int, y, decompose_replicas, dst: int = 0
     The recovered factor triple (three small fp64 matrices) is broadcast back,
     so every rank returns the same factors; metrics only on ``dst``.
     """
-    import torch
     import torch.distributed as dist
 
     compress_sharded(compress_slab, K, y, dst=dst, group=group)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    factors, metrics = (None, None)
+    if world == 1:
+        return decompose_replicas(y)
+    factors, metrics, err = None, None, None
     if rank == dst:
-        factors, metrics = decompose_replicas(y)
-    if world > 1:
-        shapes = [list(f.shape) for f in factors] if rank == dst else None
-        box = [shapes]
-        dist.broadcast_object_list(box, src=dst, group=group)
-        out = []
-        for m, shp in enumerate(box[0]):
-            t = (torch.from_numpy(factors[m].ravel(order="F")).to(y.device) if rank == dst
-                 else torch.zeros(shp[0] * shp[1], dtype=torch.float64, device=y.device))
-            dist.broadcast(t, src=dst, group=group)
-            out.append(t.cpu().numpy().reshape(shp, order="F"))
-        factors = tuple(out)
+        try:
+            factors, metrics = decompose_replicas(y)
+        except Exception as e:  # tell the other ranks before anyone blocks
+            err = e
+    try:
+        shapes = _broadcast_outcome(rank, dst, group, [list(f.shape) for f in factors] if factors else None,
+                                    f"rank {dst}: {type(err).__name__}: {err}" if err is not None else None)
+    except RemoteStageError:
+        if err is not None:
+            raise err
+        raise
+    factors = _broadcast_factors(factors, shapes, rank, dst, group, y.device)
     return factors, metrics
 
 
@@ -114,29 +148,42 @@ def decompose_distributed(compress_slab, K: int, P: int, lmn: int, y, stage1, fi
             mine = y.narrow(0, rank * per * lmn, per * lmn)
     p0, p1 = replica_range(P, rank, world)
     t0 = time.perf_counter()
-    res = stage1(mine.narrow(0, 0, (p1 - p0) * lmn), np.arange(p0, p1, dtype=np.int64)) if p1 > p0 else None
+    res, s1_err = None, None
+    try:
+        res = stage1(mine.narrow(0, 0, (p1 - p0) * lmn), np.arange(p0, p1, dtype=np.int64)) if p1 > p0 else None
+    except Exception as e:  # reported through the gather, re-raised below
+        if world == 1:
+            raise
+        s1_err = e
     t_s1 = time.perf_counter() - t0
     if world > 1:
         parts = [None] * world if rank == dst else None
-        dist.gather_object(res, parts, dst=dst, group=group)
+        dist.gather_object((res, f"rank {rank}: {type(s1_err).__name__}: {s1_err}" if s1_err else None), parts,
+                           dst=dst, group=group)
     else:
-        parts = [res]
-    factors, metrics = (None, None)
+        parts = [(res, None)]
+    factors, metrics, err = None, None, None
     if rank == dst:
         from .api import Stage1Result
-        parts = [r for r in parts if r is not None]
-        merged = Stage1Result(*(np.concatenate([getattr(r, f) for r in parts])
-                                for f in ("ids", "factors", "fit_err", "converged", "sweeps")))
-        factors, metrics = finish(merged)
+        errs = [e for _, e in parts if e is not None]
+        if errs:
+            err = "; ".join(errs)
+        else:
+            try:
+                rs = [r for r, _ in parts if r is not None]
+                merged = Stage1Result(*(np.concatenate([getattr(r, f) for r in rs])
+                                        for f in ("ids", "factors", "fit_err", "converged", "sweeps")))
+                factors, metrics = finish(merged)
+            except Exception as e:
+                if world == 1:
+                    raise
+                err = f"rank {dst}: {type(e).__name__}: {e}"
     if world > 1:
-        box = [[list(f.shape) for f in factors] if rank == dst else None]
-        dist.broadcast_object_list(box, src=dst, group=group)
-        dev = y.device
-        out = []
-        for m, shp in enumerate(box[0]):
-            t = (torch.from_numpy(np.asfortranarray(factors[m]).ravel(order="F")).to(dev) if rank == dst
-                 else torch.zeros(shp[0] * shp[1], dtype=torch.float64, device=dev))
-            dist.broadcast(t, src=dst, group=group)
-            out.append(t.cpu().numpy().reshape(shp, order="F"))
-        factors = tuple(out)
+        try:
+            shapes = _broadcast_outcome(rank, dst, group, [list(f.shape) for f in factors] if factors else None, err)
+        except RemoteStageError:
+            if s1_err is not None:
+                raise s1_err
+            raise
+        factors = _broadcast_factors(factors, shapes, rank, dst, group, y.device)
     return factors, metrics, t_s1

@@ -163,3 +163,50 @@ def test_gloo_world2_als_sharded_pipeline():
     assert out[0][1] == [0, 1, 2] and out[1][1] == [3, 4]   # ceil(5 / 2) replicas per rank
     assert out[0][2] <= 1e-12 and out[1][2] <= 1e-12   # slab sums vs one-shot: rounding only
     assert out[0][3] and not out[1][3]
+
+
+def _failing_worker(rank, world, port, out, where):
+    # a stage that raises on one rank must surface on every rank instead of
+    # leaving the others blocked in the next collective
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=__import__("datetime").timedelta(seconds=60))
+    from paper_2311_13693_b200.api import Stage1Result
+    from paper_2311_13693_b200.dist import decompose_distributed, decompose_sharded
+    P, lmn = 4, 8
+    y = torch.zeros(P * lmn, dtype=torch.float64)
+
+    def local(k0, k1, yy):
+        yy.fill_(1.0)
+
+    def stage1(reps, ids):
+        if where == "stage1" and rank == 1:
+            raise ValueError("every replica failed to fit")
+        return Stage1Result(ids, np.zeros((len(ids), 3)), ids * 0.0, np.ones(len(ids), np.int32), ids)
+
+    def finish(merged):
+        if where == "finish":
+            raise ValueError("ill-posed stack")
+        return (np.zeros((2, 1)),) * 3, {}
+
+    def decompose(yy):
+        raise ValueError("no survivors")
+
+    try:
+        if where == "sharded":
+            decompose_sharded(local, 10, y, decompose)
+        else:
+            decompose_distributed(local, 10, P, lmn, y, stage1, finish)
+        out[rank] = "returned"
+    except Exception as e:  # noqa: BLE001
+        out[rank] = f"{type(e).__name__}: {e}"
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("where", ["sharded", "stage1", "finish"])
+def test_gloo_world2_stage_failure_raises_everywhere(where):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_failing_worker, args=(2, _free_port(), out, where), nprocs=2, join=True)
+    assert "returned" not in (out[0], out[1])
+    msg = {"sharded": "no survivors", "stage1": "every replica failed", "finish": "ill-posed"}[where]
+    assert msg in out[0] and msg in out[1]

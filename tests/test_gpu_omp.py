@@ -42,7 +42,10 @@ def _omp_ref(Y, D, s, tol):
     return out
 
 
-@pytest.mark.parametrize("rows,atoms,ncols,s", [(128, 6000, 3, 8), (96, 20000, 18, 5)])
+# the last two: stacked systems taller than the 16-column residual batch fits
+# in shared memory (batch shrinks to 14 / 7 columns)
+@pytest.mark.parametrize("rows,atoms,ncols,s", [(128, 6000, 3, 8), (96, 20000, 18, 5),
+                                                (2048, 5000, 20, 6), (4096, 4100, 9, 4)])
 def test_wide_omp_matches_reference_loop(gpu, rows, atoms, ncols, s):
     rng = np.random.default_rng(atoms)
     D = np.asfortranarray(rng.standard_normal((rows, atoms)))

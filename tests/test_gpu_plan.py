@@ -175,3 +175,44 @@ def test_reduced_dims_above_128_virtual_replicas(gpu, restated, dims, red, P):
     got = gpu.Plan.replicas(plan.compress_coo(i.astype(np.int32), j.astype(np.int32), k.astype(np.int32), v), P, red)
     for p in range(P):
         assert rel_diff(restated.comp(ts, ens[0][p], ens[1][p], ens[2][p]), got[p]) <= BF16_TOL
+
+
+def test_one_plan_two_threads_two_streams(gpu, restated):
+    """A plan shared by two host threads compressing on their own streams
+    (the reference calls comp from parallel_for workers, pipeline.cpp:386-390):
+    calls serialise on the plan (host mutex + device event), both results match
+    the oracle."""
+    import threading
+    import torch
+    dims, red, P, S, seed = (320, 256, 48), (64, 64, 32), 6, 8, 17
+    plan = gpu.Plan(dims, red, P, S, seed, precision=gpu.PREC_BF16)
+    ens = gpu.make_ensemble(dims, red, P, S, seed)
+    ts = [_tensor(dims, 40 + q, rank=4) for q in range(2)]
+    wants = [_oracle_replicas(restated, t, ens) for t in ts]
+    xs = []
+    for t in ts:
+        xd = torch.from_numpy(np.asarray(t, np.float32).ravel(order="F")).cuda().to(torch.bfloat16)
+        xs.append(xd.reshape(dims[2], dims[1], dims[0]).permute(2, 1, 0))
+    ys = [torch.zeros(P * int(np.prod(red)), dtype=torch.float32, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    errors = []
+
+    def worker(q):
+        try:
+            for _ in range(25):
+                plan.compress(xs[q], y=ys[q], stream=streams[q])
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(q,)) for q in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for q in range(2):
+        got = gpu.Plan.replicas(ys[q].cpu().numpy(), P, red)
+        errs = [rel_diff(w, g) for w, g in zip(wants[q], got)]
+        assert max(errs) <= BF16_TOL, (q, errs)
+    plan.close()

@@ -156,3 +156,17 @@ def test_comp_mixed_restatement_bitexact(restated, reference):
         assert np.array_equal(restated.comp_mixed(*parts), reference.comp_mixed(t, u, v, w, stored))
     rounded = [restated.split(a, 0)[0] for a in (t, u, v, w)]
     assert np.array_equal(restated.comp_half(*rounded), reference.comp_naive_half(t, u, v, w))
+
+
+def test_ensemble_cols_matches_make_ensemble(restated):
+    """or_gen_replica_cols (column subsets, threaded) == or_make_ensemble."""
+    for kind, s in ((0, 1.0), (1, 3.0)):
+        dims, red, P, S, seed = (50, 40, 30), (6, 5, 4), 3, 2, 7
+        full = restated.make_ensemble(dims, red, P, S, seed, kind=kind, s=s)
+        sub = restated.ensemble_cols(dims, red, P, S, seed, kind=kind, s=s)
+        assert all(np.array_equal(full[m][p], sub[m][p]) for m in range(3) for p in range(P))
+        idx = [np.array([0, 3, 17, 49]), None, np.array([29])]
+        sub2 = restated.ensemble_cols(dims, red, P, S, seed, cols=idx, kind=kind, s=s)
+        assert np.array_equal(sub2[0][1], full[0][1][:, idx[0]])
+        assert np.array_equal(sub2[1][2], full[1][2])
+        assert np.array_equal(sub2[2][2], full[2][2][:, [29]])
