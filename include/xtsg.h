@@ -4,8 +4,10 @@
  * This is the drop-in boundary for the reference's hot path
  * (/root/reference/proj/include/xts/{compression,cp_als,alignment}.hpp).
  * Every entry point below names the reference function it replaces
- * (file:line); the C++ facade in include/xts/xts_b200.hpp re-exposes them
- * with the reference's exact C++ signatures and exception types.
+ * (file:line); the C++ facade paper_2311_13693_b200/facade/xts_facade.cpp
+ * implements the reference's own declarations (the unmodified
+ * /root/reference/proj/include/xts/*.hpp) on top of them, with the exact C++
+ * signatures and exception types.
  *
  * Conventions (shared by every function):
  *  - Plain pointers and sizes only. Matrices are column-major
@@ -22,8 +24,11 @@
  *    Both are thread-local.
  *  - Thread-safe and re-entrant: each host thread gets its own CUDA stream
  *    (the reference calls comp/cp_als concurrently from parallel_for,
- *    pipeline.cpp:386-434). There is no CPU fallback: without a usable
- *    sm_100 device every compute entry point returns XTSG_E_CUDA.
+ *    pipeline.cpp:386-434). Calls that share one xtsg_plan serialise on it
+ *    (host mutex, and each call's stream waits for the previous call's device
+ *    work), because a plan owns its scratch; use one plan per concurrent
+ *    stream for overlap. There is no CPU fallback: without a usable sm_100
+ *    device every compute entry point returns XTSG_E_CUDA.
  */
 #ifndef XTSG_H_
 #define XTSG_H_
@@ -165,6 +170,12 @@ int32_t xtsg_comp_naive_half(const double* t, int64_t n1, int64_t n2, int64_t n3
 #define XTSG_PREC_BF16 1   /* tcgen05 kind::f16, bf16 operands, fp32 accumulation */
 #define XTSG_PREC_FP16 2   /* tcgen05 kind::f16, fp16 operands (3 more mantissa bits, range 65504:
                               U scaled by 2^-s / W by 2^s internally; overflow -> XTSG_E_HALFRANGE) */
+#define XTSG_PREC_FP16X3 3 /* compensated tensor-core mode (the reference's Eq. 5 split, mixed.cpp:18-24,
+                              done on tcgen05): every operand is an fp16 pair (hi, lo' = (x - hi) * 2^11)
+                              and each mode product is hi*hi + hi*lo + lo*hi (3 MMAs; lo*lo dropped,
+                              2^-22 relative), the mode-1 sum over i in chunks, the mode-3 sum over k in
+                              fp64; replicas ~1e-7 relative vs fp64. |x| must fit binary16
+                              (else XTSG_E_HALFRANGE); output fp32 like the other tensor-core modes */
 
 #define XTSG_DTYPE_BF16 0
 #define XTSG_DTYPE_F32 1
@@ -188,8 +199,8 @@ void xtsg_plan_destroy(xtsg_plan* plan);
 
 /* Compress the block of X that starts at offset[3] with extent[3] (a cell of
  * a BlockGrid, a mode-3 slab, or the whole tensor) into the P replicas y
- * (P x L x M x N, column-major per replica; fp32 for XTSG_PREC_BF16, fp64 for
- * XTSG_PREC_FP64), accumulating when accumulate != 0. x points at the block's first element; ld[0] is the
+ * (P x L x M x N, column-major per replica; fp32 for the tensor-core
+ * precisions XTSG_PREC_BF16/FP16/FP16X3, fp64 for XTSG_PREC_FP64), accumulating when accumulate != 0. x points at the block's first element; ld[0] is the
  * distance between consecutive j (>= extent[0]), ld[1] between consecutive k
  * (>= ld[0]*extent[1]), in elements. x may be host or device memory, any
  * XTSG_DTYPE_*; host or non-bf16 input is streamed slab by slab through a
@@ -294,8 +305,11 @@ int32_t xtsg_solve_stacked_ls(int64_t count, const int64_t* rows, int64_t r, int
 int32_t xtsg_recover_perm_scale(const double* global_head, const double* sampled,
                                 int64_t rows, int64_t cols, int64_t* perm, double* scale);
 
-/* omp_recover (alignment.cpp:306-419): column-wise greedy sparse recovery,
- * one CTA per measured column. out: atoms x ncols. */
+/* omp_recover (alignment.cpp:306-419): column-wise greedy sparse recovery.
+ * Below 4096 atoms one CTA per measured column; from 4096 atoms the atom
+ * search of each iteration spreads over the GPU (warp per atom, a batch of
+ * the columns' residuals in shared memory), then a per-column Cholesky
+ * update. out: atoms x ncols. */
 int32_t xtsg_omp_recover(const double* measured, int64_t rows, int64_t ncols, const double* dictionary,
                          int64_t atoms, int64_t sparsity, double residual_tol, double* out);
 

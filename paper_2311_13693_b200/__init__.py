@@ -17,7 +17,7 @@ import numpy as np
 from ._lib import (  # noqa: F401
     CudaError, DataError, DegenerateColumnError, HalfRangeError, IllPosedError,
     InsufficientReplicasError, StageError, UsageError, XtsError, lib, check, ptr,
-    KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE, PREC_FP64, PREC_BF16, PREC_FP16,
+    KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE, PREC_FP64, PREC_BF16, PREC_FP16, PREC_FP16X3,
     DTYPE_BF16, DTYPE_F32, DTYPE_F64, DTYPE_F16, EnsembleSpec, PlanDesc, AlsConfig,
     LAW_DENSE, LAW_SPARSE, MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE,
 )

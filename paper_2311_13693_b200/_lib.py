@@ -13,7 +13,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libxtsg.so"
 
 KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE = 0, 1, 2
-PREC_FP64, PREC_BF16, PREC_FP16 = 0, 1, 2
+PREC_FP64, PREC_BF16, PREC_FP16, PREC_FP16X3 = 0, 1, 2, 3
 DTYPE_BF16, DTYPE_F32, DTYPE_F64, DTYPE_F16 = 0, 1, 2, 3
 LAW_DENSE, LAW_SPARSE = 0, 1
 MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE = 0, 1, 2

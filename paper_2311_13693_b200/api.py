@@ -234,6 +234,27 @@ def _torch_dtype_code(t):
             torch.float16: DTYPE_F16}[t.dtype]
 
 
+_CUDA_STREAM_LEGACY = 0x1   # cudaStreamLegacy: the explicit handle of the legacy default stream
+
+
+def _stream_arg(stream, *arrays):
+    """The CUDA stream a plan call runs on. An explicit ``stream`` (torch
+    stream or raw handle) wins; otherwise, when any argument is a torch CUDA
+    tensor, the call joins torch's current stream (the legacy default stream
+    by its explicit handle, since 0 means "the library's own per-thread
+    stream" in the C ABI) so the results are ordered with later torch work;
+    host-only calls run on the library's stream and return synchronised."""
+    if stream is not None:
+        h = getattr(stream, "cuda_stream", stream)
+        return C.c_void_p(h if h else _CUDA_STREAM_LEGACY)
+    for a in arrays:
+        if getattr(a, "is_cuda", False):
+            import torch
+            h = torch.cuda.current_stream(a.device).cuda_stream
+            return C.c_void_p(h if h else _CUDA_STREAM_LEGACY)
+    return None
+
+
 class Plan:
     """Device-resident compression plan (include/xtsg.h, xtsg_plan_*)."""
 
@@ -304,7 +325,7 @@ class Plan:
                 y = torch.zeros(self.count * int(np.prod(self.reduced)),
                                 dtype=torch.float64 if ydt == np.float64 else torch.float32,
                                 device=x.device)
-        st = None if stream is None else C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else stream)
+        st = _stream_arg(stream, x, y)
         check(lib.xtsg_plan_compress(self._h, ptr(xa), code, ptr(np.asarray(ld, np.int64)),
                                      ptr(_arr3(offset)), ptr(_arr3(extent)), ptr(y),
                                      1 if accumulate else 0, st))
@@ -324,7 +345,7 @@ class Plan:
         a, b, c = (_f64(x) for x in factors)
         k1 = self.dims[2] if k1 is None else k1
         y = self._y(device, y)
-        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        st = _stream_arg(stream, y)
         check(lib.xtsg_plan_compress_factors(self._h, ptr(a), ptr(b), ptr(c), a.shape[1], int(k0), int(k1), ptr(y),
                                              1 if accumulate else 0, st))
         return y
@@ -339,7 +360,7 @@ class Plan:
         val = as_arr(val, np.float32)
         nnz = int(val.shape[0])
         y = self._y(device, y)
-        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        st = _stream_arg(stream, y, i, val)
         check(lib.xtsg_plan_compress_coo(self._h, ptr(i), ptr(j), ptr(k), ptr(val), nnz, ptr(y),
                                          1 if accumulate else 0, st))
         return y
@@ -355,7 +376,7 @@ class Plan:
         slice_ptr, fiber_ptr = (as_arr(v, np.int64) for v in (slice_ptr, fiber_ptr))
         val = as_arr(val, np.float32)
         y = self._y(device, y)
-        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        st = _stream_arg(stream, y, nz_i, val)
         check(lib.xtsg_plan_compress_csf(self._h, int(slice_k.shape[0]), ptr(slice_k), ptr(slice_ptr),
                                          int(fiber_j.shape[0]), ptr(fiber_j), ptr(fiber_ptr), int(val.shape[0]),
                                          ptr(nz_i), ptr(val), ptr(y), 1 if accumulate else 0, st))
@@ -389,7 +410,7 @@ class Plan:
             else:
                 import torch
                 y = torch.zeros(n, dtype=torch.float64 if ydt == np.float64 else torch.float32, device=device)
-        st = None if stream is None else C.c_void_p(getattr(stream, "cuda_stream", stream))
+        st = _stream_arg(stream, y)
         check(lib.xtsg_plan_compress_file(self._h, str(path).encode(), int(slab_bytes), ptr(y),
                                           1 if accumulate else 0, st))
         return y

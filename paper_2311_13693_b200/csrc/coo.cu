@@ -314,6 +314,7 @@ int gridn(int64_t work) { return static_cast<int>(std::max<int64_t>(1, std::min<
 void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, const float* val, int64_t nnz, float* y,
                         bool accumulate, cudaStream_t s) {
   if (!tensor_core()) usage("plan_compress_coo: needs a bf16/fp16 (tensor-core) plan");
+  if (comp()) usage("plan_compress_coo: the compensated mode covers dense input only (use a bf16/fp16 plan)");
   if (nnz < 0) usage("plan_compress_coo: negative nnz");
   if (nnz >= (int64_t(1) << 32)) usage("plan_compress_coo: at most 2^32-1 nonzeros per call");
   if (stage1) {
@@ -410,6 +411,7 @@ void Plan::compress_csf(int64_t n_slices, const int32_t* slice_k, const int64_t*
                         const int32_t* fiber_j, const int64_t* fiber_ptr, int64_t nnz, const int32_t* nz_i,
                         const float* val, float* y, bool accumulate, cudaStream_t s) {
   if (!tensor_core()) usage("plan_compress_csf: needs a bf16/fp16 (tensor-core) plan");
+  if (comp()) usage("plan_compress_csf: the compensated mode covers dense input only (use a bf16/fp16 plan)");
   if (stage1) usage("plan_compress_csf: two-stage plans take COO input");
   if (n_slices < 0 || n_fibers < 0 || nnz < 0) usage("plan_compress_csf: negative size");
   const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];

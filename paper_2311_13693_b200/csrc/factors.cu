@@ -23,10 +23,13 @@ namespace {
 constexpr int TI = 128, TJ = 64, NT = 256;
 
 // X[kk][j][i] (ld_i) = sum_r A[i,r] B[j,r] C[k0+kk,r]; A/B/C fp32 column-major.
+// Compensated plans (X_lo != null): fp16 hi into X, lo' = (x - hi) * 2^11
+// into X_lo, and the slab's max |x| into *amax (float bits).
 __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                       const float* __restrict__ Cm, int64_t I, int64_t J, int64_t K,
                                                       int R, int64_t k0, int64_t ldi,
-                                                      __nv_bfloat16* __restrict__ X, bool f16) {
+                                                      __nv_bfloat16* __restrict__ X, bool f16,
+                                                      __nv_bfloat16* __restrict__ X_lo, unsigned* __restrict__ amax) {
   extern __shared__ float sm[];
   float* As = sm;            // R x TI
   float* Bs = sm + R * TI;   // R x TJ (already scaled by c_k)
@@ -57,6 +60,47 @@ __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ 
     for (int a = 0; a < 8; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(av[a], bv[b], acc[a][b]);
+  }
+  if (X_lo) {
+    float m = 0.f;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t j = j0 + ty + 16 * b;
+      if (j >= J) continue;
+      const int64_t o = (kk * J + j) * ldi + i0 + tx * 8;
+      float v8[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        v8[a] = i0 + tx * 8 + a < I ? acc[a][b] : 0.f;
+        m = fmaxf(m, fabsf(v8[a]));
+      }
+      if (i0 + tx * 8 + 8 <= ldi) {
+        uint32_t wh[4], wl[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const __half2 h = __floats2half2_rn(v8[2 * q], v8[2 * q + 1]);
+          const float2 hf = __half22float2(h);
+          const __half2 l = __floats2half2_rn((v8[2 * q] - hf.x) * 2048.f, (v8[2 * q + 1] - hf.y) * 2048.f);
+          wh[q] = *reinterpret_cast<const uint32_t*>(&h);
+          wl[q] = *reinterpret_cast<const uint32_t*>(&l);
+        }
+        *reinterpret_cast<uint4*>(X + o) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+        *reinterpret_cast<uint4*>(X_lo + o) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          if (i0 + tx * 8 + a >= ldi) continue;
+          const __half h = __float2half_rn(v8[a]);
+          const __half l = __float2half_rn((v8[a] - __half2float(h)) * 2048.f);
+          X[o + a] = __ushort_as_bfloat16(__half_as_ushort(h));
+          X_lo[o + a] = __ushort_as_bfloat16(__half_as_ushort(l));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
+    return;
   }
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
@@ -120,9 +164,14 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
   count_launch(2);
   XLAUNCH_CHECK();
   DevBuf<float> ypad;
+  DevBuf<double> y64;
   float* ydst = yo.dev;
   bool acc = accumulate;
-  if (padded) {
+  if (comp()) {
+    y64 = DevBuf<double>(static_cast<size_t>(vP * mpad * lpad * N), s);
+    comp_y = y64.ptr;
+    acc = false;
+  } else if (padded) {
     ypad = DevBuf<float>(static_cast<size_t>(vP * mpad * lpad * N), s);
     ydst = ypad.ptr;
     acc = false;
@@ -137,25 +186,32 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
     return e && std::atoi(e) > 0 ? static_cast<int64_t>(std::atoi(e)) : int64_t(8);
   }();
   const int64_t budget = std::min<int64_t>(slab_gb << 30, static_cast<int64_t>(free_b / 4));
-  const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, budget / (ldi * J * 2)));
-  DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * J * ldi), s);
+  const int64_t planes = comp() ? 2 : 1;
+  const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, budget / (planes * ldi * J * 2)));
+  DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * J * ldi), s), stage_lo;
+  if (comp()) stage_lo = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
   const size_t smem = static_cast<size_t>(rank) * (TI + TJ) * sizeof(float);
   XCUDA(cudaFuncSetAttribute(gen_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   for (int64_t kb = k0; kb < k1; kb += ks) {
     const int64_t kn = std::min(ks, k1 - kb);
     dim3 grid(static_cast<unsigned>(ceil_div(I, TI)), static_cast<unsigned>(ceil_div(J, TJ)),
               static_cast<unsigned>(kn));
+    if (comp()) XCUDA(cudaMemsetAsync(amax.ptr, 0, sizeof(unsigned), s));
     gen_slab_kernel<<<grid, NT, smem, s>>>(fa.ptr, fb.ptr, fc.ptr, I, J, K, static_cast<int>(rank), kb, ldi,
-                                           stage.ptr, fp16());
+                                           stage.ptr, fp16(), comp() ? stage_lo.ptr : nullptr,
+                                           comp() ? amax.ptr : nullptr);
     XLAUNCH_CHECK();
     const int64_t off[3] = {0, 0, kb}, ext[3] = {I, J, kn};
-    run_bf16_block(stage.ptr, ldi, ldi * J, off, ext, ydst, acc, s);
+    run_bf16_block(stage.ptr, ldi, ldi * J, off, ext, ydst, acc, s, comp() ? stage_lo.ptr : nullptr);
     acc = true;
   }
-  if (padded) {
+  if (comp()) {
+    comp_finish(y64.ptr, yo.dev, accumulate, s);
+    comp_y = nullptr;
+  } else if (padded) {
     compact(ypad.ptr, yo.dev, accumulate, s);
   }
-  if (fp16()) check_finite16(yo.dev, ysz, s);
+  if (fp16() || comp()) check_finite16(yo.dev, ysz, s);
   if (yo.host) yo.finish();
 }
 

@@ -831,8 +831,9 @@ int32_t xtsg_decompose(const xtsg_pipeline_config* cfg, const int64_t dims[3], c
   return guard([&] {
     if (metrics) *metrics = xtsg_pipeline_metrics{};
     const Resolved rs = resolve(*cfg, dims);
-    if (cfg->precision != XTSG_PREC_FP64 && cfg->precision != XTSG_PREC_BF16 && cfg->precision != XTSG_PREC_FP16)
-      usage("decompose: precision must be XTSG_PREC_FP64, XTSG_PREC_BF16 or XTSG_PREC_FP16");
+    if (cfg->precision != XTSG_PREC_FP64 && cfg->precision != XTSG_PREC_BF16 && cfg->precision != XTSG_PREC_FP16 &&
+        cfg->precision != XTSG_PREC_FP16X3)
+      usage("decompose: precision must be XTSG_PREC_FP64, XTSG_PREC_BF16, XTSG_PREC_FP16 or XTSG_PREC_FP16X3");
     require_device();
     cudaStream_t st = thread_stream();
     const Source src = make_source(dims, tensor, fa, fb, fc, factor_rank, st);

@@ -76,9 +76,54 @@ void pack_virtual(const double* src, int64_t vcount, int64_t rows, int64_t cols,
   XLAUNCH_CHECK();
 }
 
+// Compensated operands: like pack_virtual_kernel, but each value v (scaled
+// by 2^-b so |v| < 16) becomes three fp16 planes, plane_stride elements
+// apart: (hi * 2^11, hi, lo' = (v - hi) * 2^11) for U (hi_first = true:
+// products (Uh*2^11, Xh), (Uh, Xl'), (Ul', Xh)), and (hi * 2^11, lo', hi) for
+// V (products (Th, Vh*2^11), (Th, Vl'), (Tl', Vh)).
+__global__ void pack_split_kernel(const double* __restrict__ src, int64_t rows, int64_t cols, int64_t per_p,
+                                  int64_t sdiv, int64_t smod, int64_t srows, int64_t rows_pad, int64_t ld,
+                                  double scale, int64_t plane_stride, int32_t v_order, __half* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int64_t q = blockIdx.z;
+  const int64_t p = q / per_p, split = (q / sdiv) % smod;
+  const int64_t rbase = split * srows;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const double* s = src + p * rows * cols;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t c = c0 + dy, r = r0 + threadIdx.x;
+    tile[dy][threadIdx.x] = (r < srows && rbase + r < rows && c < cols) ? s[(rbase + r) + rows * c] : 0.0;
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < srows && rbase + r < rows && c < cols) {
+      const double v = tile[threadIdx.x][dy] * scale;
+      const __half hi = __double2half(v);
+      const __half lo = __double2half((v - static_cast<double>(__half2float(hi))) * 2048.0);
+      const __half hi2 = __float2half_rn(__half2float(hi) * 2048.f);  // exact: |hi| < 16
+      __half* o = dst + (q * rows_pad + r) * ld + c;
+      o[0] = hi2;
+      o[plane_stride] = v_order ? lo : hi;
+      o[2 * plane_stride] = v_order ? hi : lo;
+    }
+  }
+}
+
+__global__ void amax_f64_kernel(const double* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = fmax(m, fabs(x[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
 // ypad[q][(m'*lpad + l')][n] of virtual replica q = (p*lsplit + a)*msplit + b
 // -> y(p, a*Lv + l', b*Mv + m', n)
-__global__ void compact_virtual_kernel(const float* __restrict__ ypad, int64_t count, int64_t L, int64_t M, int64_t N,
+template <class TIN>
+__global__ void compact_virtual_kernel(const TIN* __restrict__ ypad, int64_t count, int64_t L, int64_t M, int64_t N,
                                        int64_t lpad, int64_t mpad, int64_t lsplit, int64_t msplit, int64_t Lv,
                                        int64_t Mv, int32_t accumulate, float* __restrict__ y) {
   const int64_t per = L * M * N, total = count * per;
@@ -88,8 +133,8 @@ __global__ void compact_virtual_kernel(const float* __restrict__ ypad, int64_t c
     const int64_t l = r % L, mn = r / L, m = mn % M, n = mn / M;
     const int64_t a = l / Lv, b = m / Mv;
     const int64_t q = (p * lsplit + a) * msplit + b;
-    const float v = ypad[q * mpad * lpad * N + ((m - b * Mv) * lpad + (l - a * Lv)) + mpad * lpad * n];
-    y[e] = accumulate ? y[e] + v : v;
+    const TIN v = ypad[q * mpad * lpad * N + ((m - b * Mv) * lpad + (l - a * Lv)) + mpad * lpad * n];
+    y[e] = accumulate ? static_cast<float>(y[e] + v) : static_cast<float>(v);
   }
 }
 
@@ -125,6 +170,102 @@ __global__ void stage_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj
     __nv_bfloat16* d = dst + row * ldi;
     for (int64_t i = threadIdx.x; i < ldi; i += blockDim.x)
       d[i] = to_op16(i < ni ? to_f(s[i]) : 0.f, f16);
+  }
+}
+
+// Compensated staging: X block -> fp16 planes hi = fp16(x), lo' =
+// fp16((x - hi) * 2^11) in the TMA layout, plus max |x| of the block
+// (float bits; atomicMax on non-negative floats orders like their bits).
+template <class T>
+__global__ void split_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj, int64_t nk, int64_t ld0,
+                               int64_t ld1, int64_t ldi, __half* __restrict__ hi, __half* __restrict__ lo,
+                               unsigned* __restrict__ amax) {
+  const int64_t rows = nj * nk;
+  float m = 0.f;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t j = row % nj, k = row / nj;
+    const T* s = src + j * ld0 + k * ld1;
+    for (int64_t i = threadIdx.x; i < ldi; i += blockDim.x) {
+      float v = 0.f, r = 0.f;
+      if (i < ni) {
+        if constexpr (std::is_same<T, double>::value) {
+          const double d = s[i];
+          const __half h = __double2half(d);
+          v = __half2float(h);
+          r = static_cast<float>((d - static_cast<double>(v)) * 2048.0);
+          m = fmaxf(m, static_cast<float>(fabs(d)));
+        } else {
+          const float f = to_f(s[i]);
+          v = __half2float(__float2half_rn(f));
+          r = (f - v) * 2048.f;
+          m = fmaxf(m, fabsf(f));
+        }
+      }
+      hi[row * ldi + i] = __float2half_rn(v);
+      lo[row * ldi + i] = __float2half_rn(r);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
+}
+
+// Compensated mode 3: Y64[q] (mrows x N) (+)= 2^e * Z[q] (mrows x kc, fp32)
+// * W[q][:, k0:k0+kc]^T (fp32, row n at W + n*ldw), fp64 accumulation. e =
+// e0 + exponent(max |x| of the launch) undoes the power-of-two operand
+// scales (U, V pre-scales, the 2^11 of the hi*2^11 products, the split
+// scale of the mode-1 result).
+constexpr int M3_TM = 64, M3_TN = 32, M3_TK = 32;
+__global__ void __launch_bounds__(256) mode3_comp_kernel(const float* __restrict__ Z, int64_t mrows, int64_t kc,
+                                                         const float* __restrict__ W, int64_t ldw, int64_t wstride,
+                                                         int64_t N, const unsigned* __restrict__ amax, int e0,
+                                                         int32_t beta, double* __restrict__ Y) {
+  __shared__ float As[M3_TK][M3_TM];
+  __shared__ float Bs[M3_TK][M3_TN + 1];
+  const int64_t q = blockIdx.z;
+  const float* Zq = Z + q * kc * mrows;
+  const float* Wq = W + q * wstride;
+  double* Yq = Y + q * mrows * N;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * M3_TM, n0 = static_cast<int64_t>(blockIdx.y) * M3_TN;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 4 m x 2 n outputs per thread
+  double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  for (int64_t k0 = 0; k0 < kc; k0 += M3_TK) {
+    for (int e = threadIdx.x; e < M3_TK * M3_TM; e += 256) {
+      const int kk = e / M3_TM, mm = e % M3_TM;
+      As[kk][mm] = (k0 + kk < kc && m0 + mm < mrows) ? Zq[(k0 + kk) * mrows + m0 + mm] : 0.f;
+    }
+    for (int e = threadIdx.x; e < M3_TK * M3_TN; e += 256) {
+      const int nn = e / M3_TK, kk = e % M3_TK;
+      Bs[kk][nn] = (k0 + kk < kc && n0 + nn < N) ? Wq[(n0 + nn) * ldw + k0 + kk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < M3_TK; ++kk) {
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][tx + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bs[kk][ty + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const int ex = ilogbf(fmaxf(__uint_as_float(*amax), 1e-30f)) + 1;
+  const double sc = ldexp(1.0, e0 + ex);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int64_t n = n0 + ty + 16 * j;
+    if (n >= N) continue;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t m = m0 + tx + 16 * i;
+      if (m >= mrows) continue;
+      double* d = Yq + m + mrows * n;
+      *d = beta ? *d + acc[i][j] * sc : acc[i][j] * sc;
+    }
   }
 }
 
@@ -188,7 +329,8 @@ size_t dtype_size(int32_t dt) {
 Plan::Plan(const xtsg_plan_desc& d) : desc(d) {
   const EnsembleShape sh =
       validate_ensemble(desc.dims, desc.reduced, desc.count, desc.shared_rows, desc.spec);
-  if (desc.precision != XTSG_PREC_FP64 && desc.precision != XTSG_PREC_BF16 && desc.precision != XTSG_PREC_FP16)
+  if (desc.precision != XTSG_PREC_FP64 && desc.precision != XTSG_PREC_BF16 && desc.precision != XTSG_PREC_FP16 &&
+      desc.precision != XTSG_PREC_FP16X3)
     usage("plan: unknown precision");
   require_device();
   XCUDA(cudaGetDevice(&device));
@@ -269,17 +411,49 @@ void Plan::build_tc_operands() {
   rpb = 128 / lpad;
   n2 = rpb * mpad;
   if (n2 > 128) usage("plan: (128/Lpad)*Mpad must be <= 128 for the tensor-core path");
-  rows_u = round_up(vP * lpad, 128);  // odd row-block counts run the kernel without clusters
+  // odd row-block counts run the single-CTA kernel; the compensated mode
+  // exists only as the CTA-pair kernel, so it pads to whole pairs
+  rows_u = round_up(vP * lpad, comp() ? 256 : 128);
   ld_u = round_up(I, 8);
   ld_v = round_up(J, 8);
-  ustack = DevBuf<__nv_bfloat16>(static_cast<size_t>(rows_u * ld_u), st);
+  const int planes = comp() ? 3 : 1;
+  ustack = DevBuf<__nv_bfloat16>(static_cast<size_t>(planes * rows_u * ld_u), st);
   ustack.zero();
-  vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(vP * mpad * ld_v), st);
+  vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(planes * vP * mpad * ld_v), st);
   vt.zero();
   wf = DevBuf<float>(static_cast<size_t>(vP * N * K), st);
   const int64_t per_p = lsplit * msplit;
   // U rows of virtual replica q: split a = (q / msplit) % lsplit; V rows: b = q % msplit
-  if (fp16()) {
+  if (comp()) {
+    // pre-scales 2^-b with max |u| * 2^-b < 16 (so hi * 2^11 < 2^15 fits binary16)
+    auto prescale = [&](const double* m, int64_t n) {
+      DevBuf<unsigned long long> mx(1, st);
+      mx.zero();
+      amax_f64_kernel<<<grid_for(n), 256, 0, st>>>(m, n, mx.ptr);
+      XLAUNCH_CHECK();
+      unsigned long long bits = 0;
+      XCUDA(cudaMemcpyAsync(&bits, mx.ptr, sizeof(bits), cudaMemcpyDeviceToHost, st));
+      XCUDA(cudaStreamSynchronize(st));
+      double v;
+      std::memcpy(&v, &bits, sizeof(v));
+      return v > 0.0 ? std::max(0, std::ilogb(v) - 3) : 0;
+    };
+    comp_bu = prescale(u64.ptr, P * L * I);
+    comp_bv = prescale(v64.ptr, P * M * J);
+    auto pack3 = [&](const double* src, int64_t rows, int64_t cols, int64_t sdiv, int64_t smod, int64_t srows,
+                     int64_t rows_pad, int64_t ld, int64_t plane, int b, int v_order, __nv_bfloat16* dst) {
+      dim3 grid(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(srows, 32)),
+                static_cast<unsigned>(vP));
+      pack_split_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, per_p, sdiv, smod, srows, rows_pad, ld,
+                                                      std::ldexp(1.0, -b), plane, v_order,
+                                                      reinterpret_cast<__half*>(dst));
+      XLAUNCH_CHECK();
+    };
+    pack3(u64.ptr, L, I, msplit, lsplit, Lv, lpad, ld_u, rows_u * ld_u, comp_bu, 0, ustack.ptr);
+    pack3(v64.ptr, M, J, 1, msplit, Mv, mpad, ld_v, vP * mpad * ld_v, comp_bv, 1, vt.ptr);
+    pack_virtual<float>(w64.ptr, vP, N, K, per_p, 1, 1, N, N, K, wf.ptr, st);
+    amax = DevBuf<unsigned>(1, st);
+  } else if (fp16()) {
     // fp16 keeps 3 more mantissa bits than bf16 but tops out at 65504: the
     // mode-1 partial sums (the mode-2 operand, |sum_i U X| ~ sqrt(I) |X|)
     // are kept in range by scaling U by 2^-s and W by 2^s (exact powers of
@@ -348,19 +522,22 @@ void Plan::check_block(const int64_t off[3], const int64_t ext[3]) const {
 
 // Z = ttm(X block), Y(+)= Z W^T for k in [kb, kb + nk) of a bf16 device block.
 void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, const int64_t off[3],
-                          const int64_t ext[3], float* ydst, bool first_accumulate, cudaStream_t s) {
+                          const int64_t ext[3], float* ydst, bool first_accumulate, cudaStream_t s,
+                          const __nv_bfloat16* x_lo) {
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
   const int64_t K = desc.dims[2];
+  if (comp() && !x_lo) usage("plan: the compensated mode needs the X lo plane");
+  const int planes = comp() ? 3 : 1;
   // Operand slices; TMA needs 16-byte aligned bases, so unaligned offsets get
-  // an aligned copy of the slice.
+  // an aligned copy of the slice (every plane).
   const __nv_bfloat16* uop = ustack.ptr + off[0];
   int64_t ldu = ld_u;
   DevBuf<__nv_bfloat16> utmp, vtmp;
   if (off[0] % 8) {
     ldu = round_up(ext[0], 8);
-    utmp = DevBuf<__nv_bfloat16>(static_cast<size_t>(rows_u * ldu), s);
+    utmp = DevBuf<__nv_bfloat16>(static_cast<size_t>(planes * rows_u * ldu), s);
     utmp.zero();
-    XCUDA(cudaMemcpy2DAsync(utmp.ptr, ldu * 2, ustack.ptr + off[0], ld_u * 2, ext[0] * 2, rows_u,
+    XCUDA(cudaMemcpy2DAsync(utmp.ptr, ldu * 2, ustack.ptr + off[0], ld_u * 2, ext[0] * 2, planes * rows_u,
                             cudaMemcpyDeviceToDevice, s));
     uop = utmp.ptr;
   }
@@ -368,9 +545,9 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
   int64_t ldv = ld_v;
   if (off[1] % 8) {
     ldv = round_up(ext[1], 8);
-    vtmp = DevBuf<__nv_bfloat16>(static_cast<size_t>(vP * mpad * ldv), s);
+    vtmp = DevBuf<__nv_bfloat16>(static_cast<size_t>(planes * vP * mpad * ldv), s);
     vtmp.zero();
-    XCUDA(cudaMemcpy2DAsync(vtmp.ptr, ldv * 2, vt.ptr + off[1], ld_v * 2, ext[1] * 2, vP * mpad,
+    XCUDA(cudaMemcpy2DAsync(vtmp.ptr, ldv * 2, vt.ptr + off[1], ld_v * 2, ext[1] * 2, planes * vP * mpad,
                             cudaMemcpyDeviceToDevice, s));
     vop = vtmp.ptr;
   }
@@ -423,7 +600,15 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
       tl.prm.x_policy = hint_env == 2 ? pol[1] : pol[0];
     }
     tl.prm.z = zbuf.ptr;
-    tl.prm.f16 = fp16() ? 1 : 0;
+    tl.prm.f16 = f16_operands() ? 1 : 0;
+    if (comp()) {
+      tl.x_lo = x_lo;
+      tl.prm.comp = 1;
+      tl.prm.kpc = comp_kpc();
+      tl.prm.i_chunks = static_cast<int32_t>(ceil_div(tl.prm.k_steps, tl.prm.kpc));
+      tl.prm.amax = amax.ptr;
+      tl.prm.comp_c0 = comp_c0(ext[0]);
+    }
     EvPair e1{}, e2{};
     if (profiling) {
       e1 = take_pair();
@@ -433,12 +618,22 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     if (profiling) {
       XCUDA(cudaEventRecord(e1.b, s));
       ev_fused.push_back(e1);
+      // useful (algorithmic) flops; the compensated mode issues 3x these
       flops_fused += 2.0 * P * L * static_cast<double>(ext[0]) * ext[1] * kc +
                      2.0 * P * L * static_cast<double>(M) * ext[1] * kc;
       e2 = take_pair();
       XCUDA(cudaEventRecord(e2.a, s));
     }
     // mode 3: Y_p (Mpad*Lpad x N) (+)= Z_p (Mpad*Lpad x kc) * W_p[:, k0+kb : +kc]^T
+    if (comp()) {
+      // fp64 accumulation; 2^(c0 + e_x + bu + bv - 22) undoes the operand scales
+      const int64_t mrows = mpad * lpad;
+      dim3 grid(static_cast<unsigned>(ceil_div(mrows, M3_TM)), static_cast<unsigned>(ceil_div(N, M3_TN)),
+                static_cast<unsigned>(vP));
+      mode3_comp_kernel<<<grid, 256, 0, s>>>(zbuf.ptr, mrows, kc, wf.ptr + off[2] + kb, K, N * K, N, amax.ptr,
+                                             comp_c0(ext[0]) + comp_bu + comp_bv - 22, acc ? 1 : 0, comp_y);
+      XLAUNCH_CHECK();
+    } else {
     GemmArgs<float> g;
     g.m = mpad * lpad; g.n = N; g.k = kc; g.batch = vP;
     g.a = zbuf.ptr; g.lda = mpad * lpad; g.stride_a = kc * mpad * lpad;
@@ -446,6 +641,7 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
     g.c = ydst; g.ldc = mpad * lpad; g.stride_c = mpad * lpad * N;
     g.beta = acc ? 1.f : 0.f;
     gemm_simt(g, s);
+    }
     if (profiling) {
       XCUDA(cudaEventRecord(e2.b, s));
       ev_mode3.push_back(e2);
@@ -624,15 +820,22 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
     if (accumulate && yo.host) XCUDA(cudaMemcpyAsync(yo.dev, y, ysz * 4, cudaMemcpyHostToDevice, s));
   }
   const int32_t op_dtype = fp16() ? XTSG_DTYPE_F16 : XTSG_DTYPE_BF16;
-  const bool direct = x_dev && dtype == op_dtype && ld[0] % 8 == 0 && ld[1] % 8 == 0 &&
+  // the compensated mode always stages (X split into its fp16 hi/lo' planes)
+  const bool direct = !comp() && x_dev && dtype == op_dtype && ld[0] % 8 == 0 && ld[1] % 8 == 0 &&
                       reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  DevBuf<double> y64;
+  if (comp()) {
+    y64 = DevBuf<double>(static_cast<size_t>(vP * mpad * lpad * N), s);
+    comp_y = y64.ptr;
+    acc_first = false;
+  }
   static const bool narrow_on = [] {
     const char* e = std::getenv("XTSG_HOST_NARROW");
     return !(e && std::atoi(e) == 0);
   }();
   if (direct) {
     run_bf16_block(static_cast<const __nv_bfloat16*>(x), ld[0], ld[1], off, ext, ydst, acc_first, s);
-  } else if (!x_dev && (dtype == XTSG_DTYPE_F32 || dtype == XTSG_DTYPE_F64) && narrow_on) {
+  } else if (!comp() && !x_dev && (dtype == XTSG_DTYPE_F32 || dtype == XTSG_DTYPE_F64) && narrow_on) {
     compress_host_narrow(x, dtype, ld, off, ext, ydst, acc_first, s);
   } else {
     // Slab pipeline: copy_st moves raw slab k-ranges H2D (host input) while s
@@ -642,7 +845,8 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
     const int64_t target = int64_t(1) << 30;  // ~1 GiB of bf16 per slab
     int64_t ks = std::max<int64_t>(1, target / std::max<int64_t>(1, ldi * ext[1] * 2));
     ks = std::min(ks, ext[2]);
-    DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * ext[1] * ldi), s);
+    DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * ext[1] * ldi), s), stage_lo;
+    if (comp()) stage_lo = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * ext[1] * ldi), s);
     DevBuf<uint8_t> raw[2];
     if (!x_dev) {
       for (int b = 0; b < 2; ++b) {
@@ -681,7 +885,23 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
       const int64_t rows = kn * ext[1];
       const int blocks = static_cast<int>(std::min<int64_t>(rows, 148 * 8));
       const bool h = fp16();
-      if (dtype == XTSG_DTYPE_F64)
+      if (comp()) {
+        XCUDA(cudaMemsetAsync(amax.ptr, 0, sizeof(unsigned), s));
+        auto* hi = reinterpret_cast<__half*>(stage.ptr);
+        auto* lo = reinterpret_cast<__half*>(stage_lo.ptr);
+        if (dtype == XTSG_DTYPE_F64)
+          split_x_kernel<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
+                                                         ld[0], ld[1], ldi, hi, lo, amax.ptr);
+        else if (dtype == XTSG_DTYPE_F32)
+          split_x_kernel<float><<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(src), ext[0], ext[1], kn,
+                                                        ld[0], ld[1], ldi, hi, lo, amax.ptr);
+        else if (dtype == XTSG_DTYPE_F16)
+          split_x_kernel<__half><<<blocks, 256, 0, s>>>(reinterpret_cast<const __half*>(src), ext[0], ext[1], kn,
+                                                         ld[0], ld[1], ldi, hi, lo, amax.ptr);
+        else
+          split_x_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(src), ext[0],
+                                                                ext[1], kn, ld[0], ld[1], ldi, hi, lo, amax.ptr);
+      } else if (dtype == XTSG_DTYPE_F64)
         stage_x_kernel<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
                                                        ld[0], ld[1], ldi, stage.ptr, h);
       else if (dtype == XTSG_DTYPE_F32)
@@ -697,23 +917,54 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
       if (!x_dev) XCUDA(cudaEventRecord(ev_consumed[b], s));
       const int64_t soff[3] = {off[0], off[1], off[2] + k0};
       const int64_t sext[3] = {ext[0], ext[1], kn};
-      run_bf16_block(stage.ptr, ldi, ldi * ext[1], soff, sext, ydst, acc, s);
+      run_bf16_block(stage.ptr, ldi, ldi * ext[1], soff, sext, ydst, acc, s, comp() ? stage_lo.ptr : nullptr);
       acc = true;
     }
   }
-  if (padded) {
+  if (comp()) {
+    comp_finish(y64.ptr, yo.dev, accumulate, s);
+    comp_y = nullptr;
+  } else if (padded) {
     compact(ypad.ptr, yo.dev, accumulate, s);
   }
-  if (fp16()) check_finite16(yo.dev, ysz, s);
+  if (fp16() || comp()) check_finite16(yo.dev, ysz, s);
   if (yo.host || !x_dev) yo.finish();
 }
 
 void Plan::compact(const float* ypad, float* y, bool accumulate, cudaStream_t s) {
   const int64_t P = desc.count, L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2];
   const int64_t ysz = P * L * M * N;
-  compact_virtual_kernel<<<grid_for(ysz), 256, 0, s>>>(ypad, P, L, M, N, lpad, mpad, lsplit, msplit, Lv, Mv,
-                                                       accumulate ? 1 : 0, y);
+  compact_virtual_kernel<float><<<grid_for(ysz), 256, 0, s>>>(ypad, P, L, M, N, lpad, mpad, lsplit, msplit, Lv, Mv,
+                                                              accumulate ? 1 : 0, y);
   XLAUNCH_CHECK();
+}
+
+// compensated mode: the fp64 padded accumulator -> the caller's fp32 replicas
+void Plan::comp_finish(const double* y64, float* y, bool accumulate, cudaStream_t s) {
+  const int64_t P = desc.count, L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2];
+  const int64_t ysz = P * L * M * N;
+  compact_virtual_kernel<double><<<grid_for(ysz), 256, 0, s>>>(y64, P, L, M, N, lpad, mpad, lsplit, msplit, Lv, Mv,
+                                                               accumulate ? 1 : 0, y);
+  XLAUNCH_CHECK();
+}
+
+int Plan::comp_kpc() const {
+  // 8 steps = 512 i per fp32 TMEM accumulation (XTSG_COMP_KPC overrides):
+  // the chain error grows ~linearly with its MMA count (C2: 4 -> 1.6e-6 at
+  // 4.1x the bf16 time, 8 -> 2.5e-6 at 3.1x, 16 -> 4.2e-6 at 2.9x)
+  static const int v = [] {
+    const char* e = std::getenv("XTSG_COMP_KPC");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 8;
+  }();
+  return v;
+}
+
+// the split of the mode-1 result (~2^11 * 2^-bu * sqrt(ni) * max|x| at most
+// in rms) is scaled by 2^-(c0 + e_x), e_x = exponent of max |x|, to ~2^10
+int Plan::comp_c0(int64_t ni) const {
+  int c = 0;
+  while ((int64_t(1) << (2 * c)) < ni) ++c;  // 2^c >= sqrt(ni)
+  return 1 - comp_bu + c;
 }
 
 // fp16 plans: a binary16 overflow anywhere in the chain shows up as a

@@ -61,8 +61,25 @@ struct Plan {
   DevBuf<double> outer[3];
   int64_t inner_dims[3] = {0, 0, 0};
 
-  bool tensor_core() const { return desc.precision == XTSG_PREC_BF16 || desc.precision == XTSG_PREC_FP16; }
+  // compensated fp16 hi/lo mode (XTSG_PREC_FP16X3): U and V as three fp16
+  // planes each, X staged as two; `amax` holds the current launch's max |x|
+  // (float bits) that scales the split of the mode-1 result; comp_bu/bv are
+  // the power-of-two pre-scales of U/V (kept < 16 in magnitude so hi*2^11
+  // fits binary16); mode 3 accumulates in fp64 into comp_y (padded layout)
+  DevBuf<unsigned> amax;
+  int comp_bu = 0, comp_bv = 0;
+  double* comp_y = nullptr;
+  bool comp() const { return desc.precision == XTSG_PREC_FP16X3; }
+  // fp32 mode-1 accumulation per chunk of comp_kpc 64-wide i steps
+  int comp_kpc() const;
+  int comp_c0(int64_t ni) const;
+  void comp_finish(const double* y64, float* y, bool accumulate, cudaStream_t s);
+
+  bool tensor_core() const {
+    return desc.precision == XTSG_PREC_BF16 || desc.precision == XTSG_PREC_FP16 || comp();
+  }
   bool fp16() const { return desc.precision == XTSG_PREC_FP16; }
+  bool f16_operands() const { return fp16() || comp(); }
   void check_finite16(const float* y, int64_t n, cudaStream_t s);
   bool virt_padded() const {
     return lsplit > 1 || msplit > 1 || lpad != desc.reduced[0] || mpad != desc.reduced[1];
@@ -78,7 +95,8 @@ struct Plan {
   void compress(const void* x, int32_t dtype, const int64_t ld[2], const int64_t off[3], const int64_t ext[3],
                 void* y, bool accumulate, cudaStream_t s);
   void run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, const int64_t off[3],
-                      const int64_t ext[3], float* ydst, bool first_accumulate, cudaStream_t s);
+                      const int64_t ext[3], float* ydst, bool first_accumulate, cudaStream_t s,
+                      const __nv_bfloat16* x_lo = nullptr);
   void ensure_z(int64_t floats, cudaStream_t s);
   void compress_factors(const double* a, const double* b, const double* c, int64_t rank, int64_t k0, int64_t k1,
                         float* y, bool accumulate, cudaStream_t s);

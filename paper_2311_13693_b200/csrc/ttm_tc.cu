@@ -396,6 +396,13 @@ void launch_impl(const TtmLaunch& L, cudaStream_t st) {
 void launch_ttm_fused(const TtmLaunch& L, cudaStream_t st) {
   if (L.prm.n2 > 128 || L.prm.n2 % 16 || L.prm.lpad * L.prm.rpb != BM)
     usage("ttm_fused: unsupported reduced dims for the tensor-core path");
+  if (L.prm.comp) {
+    // the compensated mode exists only as the CTA-pair kernel (plans round
+    // their stacked rows up to whole pairs of row blocks)
+    if (!ttm_pair_supported(L)) usage("ttm_fused: compensated mode needs the CTA-pair kernel shape");
+    launch_ttm_pair(L, st);
+    return;
+  }
   if (ttm_pair_enabled() && ttm_pair_supported(L)) {
     launch_ttm_pair(L, st);  // cta_group::2 kernel (ttm_tc2.cu)
     return;

@@ -24,6 +24,13 @@ struct TtmParams {
   int32_t sync_j;          // pair kernel: lane barrier every sync_j j tiles
   uint64_t u_policy, x_policy;  // L2 cache-policy hints of the U / X tile loads
   int32_t f16;             // operands are fp16 (XTSG_PREC_FP16) instead of bf16
+  // compensated fp16 hi/lo mode (XTSG_PREC_FP16X3, pair kernel only)
+  int32_t comp;            // 1: three products per mode, planes below
+  int32_t u_plane_rows;    // rows between the U planes (Uh*2^11, Uh, Ul')
+  int32_t v_plane_rows;    // rows between the V planes (Vh*2^11, Vl', Vh)
+  int32_t i_chunks, kpc;   // i steps split into i_chunks chunks of kpc (0: one chunk)
+  const unsigned* amax;    // max |x| of this launch's X (float bits), sets the mode-2 operand scale
+  int32_t comp_c0;         // 2^-(comp_c0 + exponent(max|x|)) scales the mode-1 result before its split
   float* z;          // out: Z[p][kk][m][l], kk in [0, kc)
 };
 
@@ -31,6 +38,7 @@ struct TtmLaunch {
   const void* u;      // bf16/fp16 stacked U: rows_u x ld_u (row-major), columns [0, ni) used
   int64_t rows_u, ld_u;
   const void* x;      // bf16 X block: (i, j, k) at i + ld_x0*j + ld_x1*k
+  const void* x_lo;   // compensated: the lo' plane of X, same layout (else null)
   int64_t ni, nj, nk, ld_x0, ld_x1;
   const void* v;      // bf16 Vt: rows_v x ld_v (row (p,m), j contiguous)
   int64_t rows_v, ld_v;

@@ -42,9 +42,19 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int A2_BYTES = BM * 64 * 2;   // 16 KB
 constexpr int B2_BYTES = 128 * 64 * 2;  // 16 KB (n2 <= 128 rows per CTA)
 constexpr int CHUNKS = BN / 64;
-// S TMA stages, A2_SLOTS bf16 mode-1 chunks in flight to mode 2
-constexpr int smem_total(int S, int A2_SLOTS) { return S * STAGE_BYTES + A2_SLOTS * A2_BYTES + 2 * B2_BYTES + 1024 + 512; }
+// Compensated mode (XTSG_PREC_FP16X3): every operand is an fp16 pair
+// (hi, lo' = (x - hi) * 2^11) and each product is hi*hi*2^11 + hi*lo' + lo'*hi
+// (the dropped lo*lo term is 2^-22 relative). Mode 1 streams three (U plane,
+// X plane) stages per 64-wide i step — (Uh*2^11, Xh), (Uh, Xl'), (Ul', Xh) —
+// into the same accumulator; the epilogue splits the fp32 mode-1 result into
+// an A2 (hi, lo') pair and mode 2 issues (Th, Vh*2^11), (Th, Vl'), (Tl', Vh).
+// S TMA stages, A2_SLOTS mode-1 chunks in flight to mode 2 (a pair of tiles
+// each when compensated), B2_SLOTS V chunks (three planes when compensated).
+constexpr int smem_total(int S, int A2_SLOTS, bool COMP = false, int B2_SLOTS = 2) {
+  return S * STAGE_BYTES + A2_SLOTS * A2_BYTES * (COMP ? 2 : 1) + B2_SLOTS * B2_BYTES * (COMP ? 3 : 1) + 1024 + 512;
+}
 static_assert(smem_total(4, 4) <= 232448 && smem_total(5, 2) <= 232448, "shared memory budget");
+static_assert(smem_total(3, 2, true, 1) <= 232448, "shared memory budget (compensated)");
 constexpr uint32_t IDESC1 = ptx::idesc_bf16(2 * BM, BN);
 constexpr uint16_t PAIR = 0x3;
 
@@ -114,25 +124,45 @@ __device__ __forceinline__ void lane_barrier(unsigned* ctr, unsigned target) {
   }
 }
 
-template <int S, int A2_SLOTS>
+template <int S, int A2_SLOTS, int B2_SLOTS>
 struct Bars2 {
   uint64_t full1[S], empty1[S];
   uint64_t tmem_full[2], tmem_empty[2], d2_full[2];
   uint64_t a2_full[A2_SLOTS], a2_empty[A2_SLOTS];
-  uint64_t b2_full[2], b2_empty[2];
+  uint64_t b2_full[B2_SLOTS], b2_empty[B2_SLOTS];
   uint32_t tmem_base;
 };
 
-template <int MPAD, bool LOCAL2, int S, int A2_SLOTS>
+// split of an fp32 value into the fp16 pair (hi, lo' = (v - hi) * 2^11)
+__device__ __forceinline__ void split16x2(const float* v, uint4& hi, uint4& lo) {
+  uint32_t wh[4], wl[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const __half2 h = __floats2half2_rn(v[2 * q], v[2 * q + 1]);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn((v[2 * q] - hf.x) * 2048.f, (v[2 * q + 1] - hf.y) * 2048.f);
+    wh[q] = *reinterpret_cast<const uint32_t*>(&h);
+    wl[q] = *reinterpret_cast<const uint32_t*>(&l);
+  }
+  hi = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+  lo = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+}
+
+template <int MPAD, bool LOCAL2, int S, int A2_SLOTS, bool COMP = false, int B2_SLOTS = 2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     ttm_pair_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_x,
-                    const __grid_constant__ CUtensorMap tm_v, const TtmParams p) {
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_xl,
+                    const TtmParams p) {
+  static_assert(!COMP || LOCAL2, "the compensated mode runs mode 2 per CTA");
+  constexpr int NC = COMP ? 3 : 1;                      // mode-1 products per i step
+  constexpr int A2_SLOT = A2_BYTES * (COMP ? 2 : 1);    // (hi[, lo']) mode-2 A tiles
+  constexpr int B2_SLOT = B2_BYTES * (COMP ? 3 : 1);    // (Vh*2^11, Vl', Vh) planes
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
   uint8_t* a2_base = smem + S * STAGE_BYTES;
-  uint8_t* b2_base = a2_base + A2_SLOTS * A2_BYTES;
-  auto* bars = reinterpret_cast<Bars2<S, A2_SLOTS>*>(b2_base + 2 * B2_BYTES);
+  uint8_t* b2_base = a2_base + A2_SLOTS * A2_SLOT;
+  auto* bars = reinterpret_cast<Bars2<S, A2_SLOTS, B2_SLOTS>*>(b2_base + B2_SLOTS * B2_SLOT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = ptx::cluster_ctarank();
@@ -146,6 +176,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       ptx::mbar_init(&bars->tmem_full[b], 1);
       ptx::mbar_init(&bars->tmem_empty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy)
       ptx::mbar_init(&bars->d2_full[b], 1);
+    }
+    for (int b = 0; b < B2_SLOTS; ++b) {
       ptx::mbar_init(&bars->b2_full[b], 1);
       ptx::mbar_init(&bars->b2_empty[b], 1);
     }
@@ -159,6 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     ptx::tma_prefetch(&tm_u);
     ptx::tma_prefetch(&tm_x);
     ptx::tma_prefetch(&tm_v);
+    if (COMP) ptx::tma_prefetch(&tm_xl);
   }
   if (warp == 1) ptx::tmem_alloc_pair(&bars->tmem_base, 512);
   ptx::tc_fence_before();
@@ -170,6 +203,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int cid = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int n_rb2 = p.n_rb >> 1;
   const int j_tiles = p.j_tiles, k_steps = p.k_steps;
+  // a tile is (j tile, i chunk): each i chunk of kpc steps gets its own
+  // mode-1 accumulator and mode-2 pass (shorter fp32 TMEM sums), the mode-2
+  // results of all chunks fold into the same register accumulators
+  const int i_chunks = p.i_chunks > 0 ? p.i_chunks : 1, kpc = p.i_chunks > 0 ? p.kpc : k_steps;
+  const int n_tiles = j_tiles * i_chunks;
   const int n2c = p.n2;            // mode-2 columns contributed by this CTA
   const int n2 = LOCAL2 ? n2c : 2 * n2c;  // mode-2 MMA N
   const int need = (n2 + 63) / 64;        // D1 chunks D2 overlaps
@@ -185,22 +223,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       unsigned sync_no = 0;
       while (us.next(act, kk, rb2)) {
         const int urow = rb2 * 2 * BM + crank * BM;
-        for (int jt = 0; jt < j_tiles; ++jt) {
+        for (int t2 = 0; t2 < n_tiles; ++t2) {
+          const int jt = t2 / i_chunks, ic = t2 - jt * i_chunks;
           // lane barrier every sync_j tiles (idle clusters of a partial group
           // keep arriving so the counts stay aligned)
-          if (p.sync && jt % p.sync_j == 0) lane_barrier(p.sync + us.lane, 2u * us.group * ++sync_no);
+          if (p.sync && ic == 0 && jt % p.sync_j == 0) lane_barrier(p.sync + us.lane, 2u * us.group * ++sync_no);
           if (!act) continue;
-          for (int ks = 0; ks < k_steps; ++ks) {
-            ptx::mbar_wait(&bars->empty1[s], ph ^ 1);
-            uint8_t* st = stage_base + s * STAGE_BYTES;
-            if (leader) ptx::mbar_arrive_expect_tx(&bars->full1[s], 2 * STAGE_BYTES);
-            const uint32_t fb = ptx::mapa_shared(&bars->full1[s], 0);
-            ptx::tma_load_2d_pair_hint(st, &tm_u, fb, ks * BK, urow, p.u_policy);
-            // the last j tile runs with N = n_last: each CTA holds n_last / 2 of its j
-            const int half = jt == j_tiles - 1 ? (p.n_last >> 1) : BNC;
-            ptx::tma_load_3d_pair_hint(st + A_BYTES, &tm_x, fb, ks * BK, jt * BN + crank * half, p.k_first + kk,
-                                       p.x_policy);
-            if (++s == S) { s = 0; ph ^= 1; }
+          const int ks1 = min(k_steps, (ic + 1) * kpc);
+          for (int ks = ic * kpc; ks < ks1; ++ks) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              ptx::mbar_wait(&bars->empty1[s], ph ^ 1);
+              uint8_t* st = stage_base + s * STAGE_BYTES;
+              if (leader) ptx::mbar_arrive_expect_tx(&bars->full1[s], 2 * STAGE_BYTES);
+              const uint32_t fb = ptx::mapa_shared(&bars->full1[s], 0);
+              ptx::tma_load_2d_pair_hint(st, &tm_u, fb, ks * BK, urow + c * p.u_plane_rows, p.u_policy);
+              // the last j tile runs with N = n_last: each CTA holds n_last / 2 of its j
+              const int half = jt == j_tiles - 1 ? (p.n_last >> 1) : BNC;
+              ptx::tma_load_3d_pair_hint(st + A_BYTES, (COMP && c == 1) ? &tm_xl : &tm_x, fb, ks * BK,
+                                         jt * BN + crank * half, p.k_first + kk, p.x_policy);
+              if (++s == S) { s = 0; ph ^= 1; }
+            }
           }
         }
       }
@@ -215,26 +258,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       bool act;
       while (us.next(act, kk, rb2)) {
         if (!act) continue;
-        for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+        for (int t2 = 0; t2 < n_tiles; ++t2, ++t) {
+          const int jt = t2 / i_chunks, ic = t2 - jt * i_chunks;
           const uint32_t b = t & 1, use = t >> 1;
           ptx::mbar_wait(&bars->tmem_empty[b], (use & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t d = tmem + b * 256;
           const uint32_t idesc1 =
               (jt == j_tiles - 1 ? ptx::idesc_bf16(2 * BM, p.n_last) : IDESC1) & ptx::idesc_fmt_mask(p.f16 != 0);
-          for (int ks = 0; ks < k_steps; ++ks) {
-            ptx::mbar_wait(&bars->full1[s], ph);
-            ptx::tc_fence_after();
-            const uint32_t a0 = ptx::smem_u32(stage_base + s * STAGE_BYTES);
-            const uint32_t b0 = a0 + A_BYTES;
+          const int ks0 = ic * kpc, ks1 = min(k_steps, ks0 + kpc);
+          for (int ks = ks0; ks < ks1; ++ks) {
             const int nk16 = ks == k_steps - 1 ? p.k16_last : BK / 16;
 #pragma unroll
-            for (int k4 = 0; k4 < BK / 16; ++k4)
-              if (k4 < nk16)
-                ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc1,
-                                   (ks | k4) != 0);
-            ptx::mma_commit_pair(&bars->empty1[s], PAIR);
-            if (++s == S) { s = 0; ph ^= 1; }
+            for (int c = 0; c < NC; ++c) {
+              ptx::mbar_wait(&bars->full1[s], ph);
+              ptx::tc_fence_after();
+              const uint32_t a0 = ptx::smem_u32(stage_base + s * STAGE_BYTES);
+              const uint32_t b0 = a0 + A_BYTES;
+#pragma unroll
+              for (int k4 = 0; k4 < BK / 16; ++k4)
+                if (k4 < nk16)
+                  ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc1,
+                                     (ks != ks0 || c != 0 || k4 != 0));
+              ptx::mma_commit_pair(&bars->empty1[s], PAIR);
+              if (++s == S) { s = 0; ph ^= 1; }
+            }
           }
           ptx::mma_commit_pair(&bars->tmem_full[b], PAIR);
         }
@@ -251,17 +299,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       while (us.next(act, kk, rb2)) {
         if (!act) continue;
         const int vrow = (rb2 * 2 + static_cast<int>(crank)) * n2c;
-        for (int jt = 0; jt < j_tiles; ++jt) {
+        for (int t2 = 0; t2 < n_tiles; ++t2) {
+          const int jt = t2 / i_chunks;
           const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
           for (int c = 0; c < nch; ++c, ++g) {
-            const int slot = g & 1;
-            ptx::mbar_wait(&bars->b2_empty[slot], ((g >> 1) & 1) ^ 1);
+            const int slot = g % B2_SLOTS;
+            ptx::mbar_wait(&bars->b2_empty[slot], ((g / B2_SLOTS) & 1) ^ 1);
             if (LOCAL2) {
-              ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], bytes);
-              ptx::tma_load_2d(b2_base + slot * B2_BYTES, &tm_v, &bars->b2_full[slot], jt * BN + c * 64, vrow);
+              ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], bytes * NC);
+#pragma unroll
+              for (int pl = 0; pl < NC; ++pl)
+                ptx::tma_load_2d(b2_base + slot * B2_SLOT + pl * B2_BYTES, &tm_v, &bars->b2_full[slot],
+                                 jt * BN + c * 64, vrow + pl * p.v_plane_rows);
             } else {
               if (leader) ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], 2 * bytes);
-              ptx::tma_load_2d_pair(b2_base + slot * B2_BYTES, &tm_v, ptx::mapa_shared(&bars->b2_full[slot], 0),
+              ptx::tma_load_2d_pair(b2_base + slot * B2_SLOT, &tm_v, ptx::mapa_shared(&bars->b2_full[slot], 0),
                                     jt * BN + c * 64, vrow);
             }
           }
@@ -278,28 +330,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       bool act;
       while (us.next(act, kk, rb2)) {
         if (!act) continue;
-        for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+        for (int t2 = 0; t2 < n_tiles; ++t2, ++t) {
+          const int jt = t2 / i_chunks;
           const uint32_t b = t & 1;
           const uint32_t d = tmem + b * 256;
           const bool last = jt == j_tiles - 1;
           const int nch = last ? p.chunks_last : CHUNKS;
-          const int pre = nch < need ? nch : need;
-          for (int c = 0; c < pre; ++c)
-            ptx::mbar_wait(&bars->a2_full[(g + c) % A2_SLOTS], ((g + c) / A2_SLOTS) & 1);
+          // D2 overwrites drained D1 columns: a region's first MMA waits until
+          // the `need` chunks it overlaps are drained. Compensated tiles use
+          // two D2 regions (chunks 0-1 -> columns [0, n2), chunks 2-3 ->
+          // [128, 128 + n2)) so each fp32 mode-2 chain spans 24 MMAs, not 48.
+          const uint32_t g0 = g;
+          int waited = 0;
           for (int c = 0; c < nch; ++c, ++g) {
-            const int slot = g % A2_SLOTS, bslot = g & 1;
-            if (c >= pre) ptx::mbar_wait(&bars->a2_full[slot], (g / A2_SLOTS) & 1);
-            ptx::mbar_wait(&bars->b2_full[bslot], (g >> 1) & 1);
+            const int rs = (COMP && c >= 2) ? 2 : 0;
+            const int upto = c == rs ? (nch < rs + need ? nch : rs + need) : c + 1;
+            for (; waited < upto; ++waited)
+              ptx::mbar_wait(&bars->a2_full[(g0 + waited) % A2_SLOTS], ((g0 + waited) / A2_SLOTS) & 1);
+            const uint32_t dr = d + (rs ? 128u : 0u);
+            const int slot = g % A2_SLOTS, bslot = g % B2_SLOTS;
+            ptx::mbar_wait(&bars->b2_full[bslot], (g / B2_SLOTS) & 1);
             ptx::tc_fence_after();
-            const uint32_t a0 = ptx::smem_u32(a2_base + slot * A2_BYTES);
-            const uint32_t b0 = ptx::smem_u32(b2_base + bslot * B2_BYTES);
+            const uint32_t a0 = ptx::smem_u32(a2_base + slot * A2_SLOT);
+            const uint32_t b0 = ptx::smem_u32(b2_base + bslot * B2_SLOT);
             const int nk16 = (last && c == nch - 1) ? p.k16_chunk_last : 4;
             if (LOCAL2) {
+              // (A2 tile, V plane) per product: (Th, Vh*2^11), (Th, Vl'), (Tl', Vh)
 #pragma unroll
-              for (int k4 = 0; k4 < 4; ++k4)
-                if (k4 < nk16)
-                  ptx::mma_bf16(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc2,
-                                (c | k4) != 0);
+              for (int q = 0; q < NC; ++q) {
+                const uint32_t aq = a0 + (q == 2 ? A2_BYTES : 0), bq = b0 + q * B2_BYTES;
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4)
+                  if (k4 < nk16)
+                    ptx::mma_bf16(dr, ptx::sw128_desc(aq + k4 * 32), ptx::sw128_desc(bq + k4 * 32), idesc2,
+                                  (c != rs || k4 != 0 || q != 0));
+              }
               ptx::mma_commit(&bars->a2_empty[slot]);
               ptx::mma_commit(&bars->b2_empty[bslot]);
             } else {
@@ -331,12 +396,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     UnitSched us(cid, n_clusters, n_rb2, p);
     int kk, rb2;
     bool act;
+    // compensated: the mode-1 result (2^11 * 2^-bu * U X) is scaled by 2^-a
+    // into the fp16 range before the split, a from this launch's max |x|
+    float t_scale = 1.f;
+    if (COMP) {
+      const int ex = p.amax ? ilogbf(fmaxf(__uint_as_float(*p.amax), 1e-30f)) + 1 : 0;
+      t_scale = exp2f(static_cast<float>(-(p.comp_c0 + ex)));
+    }
     while (us.next(act, kk, rb2)) {
       if (!act) continue;
       float zacc[MPAD];
 #pragma unroll
       for (int m = 0; m < MPAD; ++m) zacc[m] = 0.f;
-      for (int jt = 0; jt < j_tiles; ++jt, ++t) {
+      for (int t2 = 0; t2 < n_tiles; ++t2, ++t) {
+        const int jt = t2 / i_chunks;
         const uint32_t b = t & 1, use = t >> 1;
         const int nch = jt == j_tiles - 1 ? p.chunks_last : CHUNKS;
         ptx::mbar_wait(&bars->tmem_full[b], use & 1);
@@ -344,7 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         for (int c = 0; c < nch; ++c, ++g) {
           const int slot = g % A2_SLOTS;
           ptx::mbar_wait(&bars->a2_empty[slot], ((g / A2_SLOTS) & 1) ^ 1);
-          uint8_t* row = a2_base + slot * A2_BYTES + r * 128;
+          uint8_t* row = a2_base + slot * A2_SLOT + r * 128;
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
             float v[32];
@@ -353,8 +426,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
               const int q8 = h * 4 + q4;
-              const uint4 pk = ptx::pack8(v + q4 * 8, p.f16 != 0);
-              *reinterpret_cast<uint4*>(row + ((q8 ^ (r & 7)) << 4)) = pk;
+              if (COMP) {
+                float w8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) w8[e] = v[q4 * 8 + e] * t_scale;
+                uint4 hi, lo;
+                split16x2(w8, hi, lo);
+                *reinterpret_cast<uint4*>(row + ((q8 ^ (r & 7)) << 4)) = hi;
+                *reinterpret_cast<uint4*>(row + A2_BYTES + ((q8 ^ (r & 7)) << 4)) = lo;
+              } else {
+                const uint4 pk = ptx::pack8(v + q4 * 8, p.f16 != 0);
+                *reinterpret_cast<uint4*>(row + ((q8 ^ (r & 7)) << 4)) = pk;
+              }
             }
           }
           ptx::fence_proxy_async_smem();
@@ -376,6 +459,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e) zacc[mc * 32 + e] += v[e];
+        }
+        if (COMP && nch > 2) {
+#pragma unroll
+          for (int mc = 0; mc < MPAD / 32; ++mc) {
+            float v[32];
+            ptx::tmem_ld32(lane_addr + b * 256 + 128 + d2col + mc * 32, v);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) zacc[mc * 32 + e] += v[e];
+          }
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -436,11 +529,12 @@ void map_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
   if (r != CUDA_SUCCESS) throw Status(XTSG_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
-template <int MPAD, bool LOCAL2, int S, int A2_SLOTS>
+template <int MPAD, bool LOCAL2, int S, int A2_SLOTS, bool COMP = false, int B2_SLOTS = 2>
 void launch_pair(const TtmLaunch& L, cudaStream_t st) {
-  CUtensorMap mu, mx, mv;
+  CUtensorMap mu, mx, mv, mxl;
   {
-    const uint64_t dims[2] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.rows_u)};
+    // compensated: three U planes of rows_u rows each, stacked
+    const uint64_t dims[2] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.rows_u * (COMP ? 3 : 1))};
     const uint64_t str[1] = {static_cast<uint64_t>(L.ld_u) * 2};
     const uint32_t box[2] = {BK, BM};
     map_bf16(&mu, L.u, 2, dims, str, box, L.prm.f16 != 0);
@@ -450,17 +544,19 @@ void launch_pair(const TtmLaunch& L, cudaStream_t st) {
     const uint64_t str[2] = {static_cast<uint64_t>(L.ld_x0) * 2, static_cast<uint64_t>(L.ld_x1) * 2};
     const uint32_t box[3] = {BK, BNC, 1};
     map_bf16(&mx, L.x, 3, dims, str, box, L.prm.f16 != 0);
+    if (COMP) map_bf16(&mxl, L.x_lo, 3, dims, str, box, true);
+    else mxl = mx;
   }
   {
-    const uint64_t dims[2] = {static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.rows_v)};
+    const uint64_t dims[2] = {static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.rows_v * (COMP ? 3 : 1))};
     const uint64_t str[1] = {static_cast<uint64_t>(L.ld_v) * 2};
     const uint32_t box[2] = {64, static_cast<uint32_t>(L.prm.n2)};
     map_bf16(&mv, L.v, 2, dims, str, box, L.prm.f16 != 0);
   }
-  constexpr int SMEM_TOTAL = smem_total(S, A2_SLOTS);
+  constexpr int SMEM_TOTAL = smem_total(S, A2_SLOTS, COMP, B2_SLOTS);
   // per launch: the attribute is per device, and a static flag would race
-  XCUDA(cudaFuncSetAttribute(ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_TOTAL));
+  XCUDA(cudaFuncSetAttribute(ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS, COMP, B2_SLOTS>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
   const int clusters = (L.prm.n_rb / 2) * L.prm.kc;
   const int cap = (L.grid_limit > 0 ? L.grid_limit : sm_count()) / 2;
   const int ncl = std::max(1, std::min(clusters, cap));
@@ -484,14 +580,16 @@ void launch_pair(const TtmLaunch& L, cudaStream_t st) {
     XCUDA(cudaMemsetAsync(L.sync, 0, sizeof(unsigned) * prm.lanes, st));
     prm.sync = L.sync;
   }
-  ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, prm);
+  prm.u_plane_rows = static_cast<int32_t>(L.rows_u);
+  prm.v_plane_rows = static_cast<int32_t>(L.rows_v);
+  ttm_pair_kernel<MPAD, LOCAL2, S, A2_SLOTS, COMP, B2_SLOTS><<<grid, 256, SMEM_TOTAL, st>>>(mu, mx, mv, mxl, prm);
   XLAUNCH_CHECK();
 }
 
 }  // namespace
 
 bool ttm_pair_supported(const TtmLaunch& L) {
-  return L.prm.n_rb % 2 == 0 && L.prm.n2 <= 128 && L.prm.lpad * L.prm.rpb == BM;
+  return L.prm.n_rb % 2 == 0 && L.prm.n2 <= 128 && L.prm.lpad * L.prm.rpb == BM && (!L.prm.comp || L.x_lo);
 }
 
 void launch_ttm_pair(const TtmLaunch& L, cudaStream_t st) {
@@ -506,7 +604,9 @@ void launch_ttm_pair(const TtmLaunch& L, cudaStream_t st) {
   }();
   auto go = [&](auto mpad_tag) {
     constexpr int MP = decltype(mpad_tag)::value;
-    if (variant == 0)
+    if (L.prm.comp)
+      launch_pair<MP, true, 3, 2, true, 1>(L, st);
+    else if (variant == 0)
       launch_pair<MP, false, 4, 4>(L, st);
     else if (variant == 1)
       launch_pair<MP, true, 4, 4>(L, st);
