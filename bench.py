@@ -17,6 +17,15 @@ replicas back D2H.
 `--impl reference` times the reference's own CPU implementation (compiled in
 place into oracle/_ref) on the box's host cores: comp_blocked fast mode on a
 bounded mode-3 slab sample of the same workload.
+
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU); NCCL_DEBUG=INFO is set so
+the communicator's rank count is in the log. `--cpu-smoke` runs the same rank
+plumbing (spawn, slab split, reduce, max-over-ranks timing, JSON line) on CPU
+with gloo and a torch einsum per rank, for the CPU test suite; it is never a
+bench number. After the timed region rank 0 checks two replicas of the timed
+output against the CPU oracle (comp_from_factors of the generating factors)
+and reports `parity.max_rel_err`.
 """
 from __future__ import annotations
 
@@ -55,6 +64,9 @@ def derive(seed, tag):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--cpu-smoke", action="store_true",
+                    help="rank plumbing on CPU (gloo, torch einsum per rank): for the CPU test suite, not a bench")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="xtsg", choices=["xtsg", "reference"])
@@ -63,8 +75,9 @@ def parse():
     ap.add_argument("--e2e-dtype", default="f32", choices=["bf16", "f32", "f64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cp-time", action="store_true")
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp16"],
-                    help="tensor-core operand type (fp16: 3 more mantissa bits, same speed)")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp16", "fp16x3"],
+                    help="tensor-core operand type (fp16: 3 more mantissa bits, same speed; fp16x3: the "
+                         "compensated hi/lo mode, ~1e-6 replicas at ~3x the tensor-core work)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--K", type=int, default=C2["K"], help="mode-3 extent per rank (testing)")
     return ap.parse_args()
@@ -218,6 +231,90 @@ def cp_time_c1():
     return out
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def maybe_spawn(args):
+    """--gpus N outside torchrun: re-launch under torch.distributed.run, one rank per GPU."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd, env=env))
+
+
+def run_cpu_smoke(args):
+    """The multi-rank plumbing on CPU: gloo, mode-3 slabs, one reduce, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2311_13693_b200.dist import slab_range
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    I, J, K, P, L = 64, 48, 16 * world, 4, 8
+    g = torch.Generator().manual_seed(0)
+    X = torch.randn(I, J, K, generator=g, dtype=torch.float64)
+    U, V, W = (torch.randn(P, L, n, generator=g, dtype=torch.float64) for n in (I, J, K))
+    k0, k1 = slab_range(K, rank, world)
+    y = torch.zeros(P, L, L, L, dtype=torch.float64)
+
+    def step():
+        y.copy_(torch.einsum("ijk,pai,pbj,pck->pabc", X[:, :, k0:k1], U, V, W[:, :, k0:k1]))
+        if world > 1:
+            dist.reduce(y, dst=0)
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    if world > 1:
+        dist.barrier()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        full = torch.einsum("ijk,pai,pbj,pck->pabc", X, U, V, W)
+        err = float((y - full).abs().max() / full.abs().max())
+        print(json.dumps({"impl": "cpu-smoke", "metric": "input tensor elements compressed/sec",
+                          "value": I * J * K * args.steps / float(dt.item()), "unit": "elements/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "config": {"workload": f"cpu smoke {I}x{J}x{K}", "parallelism": f"mode-3 slabs x{world}"},
+                          "check_max_rel_err": err}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def parity_check(y, cfg, dims, red, P, reps):
+    """Outside the timed region: replicas `reps` of the timed output vs the
+    CPU oracle's comp_from_factors (compression.cpp:215-220) of the
+    generating factors (pipeline.cpp:182-193) with the reference ensemble."""
+    from oracle.oracle import Restated, rel_diff
+    o = Restated()
+    f = o.generate_dense(dims, cfg["R"], cfg["factor_seed"])
+    ens = o.ensemble_cols(dims, red, P, cfg["S"], derive(cfg["seed"], 11))
+    yh = y.detach().cpu().numpy()
+    n = int(np.prod(red))
+    errs = {}
+    for p in reps:
+        want = o.comp_from_factors(*f, ens[0][p], ens[1][p], ens[2][p])
+        errs[int(p)] = rel_diff(want, yh[p * n:(p + 1) * n].reshape(red, order="F"))
+    return {"oracle": "comp_from_factors (oracle/xts_oracle.c)", "replicas": sorted(errs),
+            "max_rel_err": max(errs.values())}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -241,6 +338,10 @@ def run_reference(args):
 
 def main():
     args = parse()
+    maybe_spawn(args)
+    if args.cpu_smoke:
+        run_cpu_smoke(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
@@ -253,6 +354,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     import paper_2311_13693_b200 as xt
 
@@ -264,10 +367,13 @@ def main():
     P = cfg["P"]
     k0 = rank * K
     t_plan = time.perf_counter()
-    prec = xt.PREC_FP16 if args.precision == "fp16" else xt.PREC_BF16
+    prec = {"bf16": xt.PREC_BF16, "fp16": xt.PREC_FP16, "fp16x3": xt.PREC_FP16X3}[args.precision]
+    comp3 = prec == xt.PREC_FP16X3
     plan = xt.Plan(dims, red, P, cfg["S"], derive(cfg["seed"], 11), precision=prec)
     t_plan = time.perf_counter() - t_plan
-    X, _ = make_block(torch, xt, cfg, k0, K, dev, torch.float16 if args.precision == "fp16" else torch.bfloat16)
+    # the compensated mode splits fp32 X into its fp16 (hi, lo') planes on the device
+    X, _ = make_block(torch, xt, cfg, k0, K, dev, {"fp16": torch.float16, "bf16": torch.bfloat16,
+                                                     "fp16x3": torch.float32}[args.precision])
     torch.cuda.synchronize()
     ysz = P * int(np.prod(red))
     y = torch.zeros(ysz, dtype=torch.float32, device=dev)
@@ -326,27 +432,27 @@ def main():
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": sustained, "unit": "TFLOP/s",
-                "frac": round(achieved / sustained, 4), "traffic": traffic,
+                "frac": round(achieved / sustained, 4), "traffic": traffic if args.precision == "bf16" else None,
                 "kernel": "ttm_pair_kernel (fused mode-1 + mode-2, tcgen05 kind::f16, cta_group::2)",
                 "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
                 "algorithmic_flops_per_launch": flops_per_launch,
                 "kernel_share_of_step": round(prof["fused_ms"] / ms, 4) if ms > 0 else None,
                 "mode3_ms_per_step": prof["mode3_ms"] / args.steps}
+    if comp3:
+        # three products per mode: the tensor cores execute 3x the useful flops
+        roofline["flops"] = "useful (algorithmic); issued = 3x"
+        roofline["issued_achieved"] = round(3 * achieved, 2)
+        roofline["issued_frac"] = round(3 * achieved / sustained, 4)
+        roofline["kernel"] = "ttm_pair_kernel compensated (fp16 hi/lo x3, tcgen05 kind::f16, cta_group::2)"
 
     # ---- e2e through the C ABI with host buffers ----
-    e2e = None
-    if not args.no_e2e:
-        npdt = {"bf16": None, "f32": np.float32, "f64": np.float64}[args.e2e_dtype]
-        tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[args.e2e_dtype]
-        # host memory is shared by the node's ranks: the e2e sample per rank
-        # shrinks with N (the metric is a rate; per-rank pinned input <= 32 GB)
-        Ke = max(100, K // world)
+    def run_e2e(host_dtype, Ke, steps):
+        tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[host_dtype]
         xh = torch.empty((Ke, cfg["J"], cfg["I"]), dtype=tdt, pin_memory=True)
         for k in range(0, Ke, 100):
             xh[k:k + 100].copy_(X.permute(2, 1, 0)[k:min(k + 100, Ke)].to(tdt))
         xh_v = xh.permute(2, 1, 0)
         yh = torch.zeros(ysz, dtype=torch.float32, pin_memory=True)
-        del npdt
 
         def e2e_step():
             plan.compress(xh_v, y=yh, offset=(0, 0, k0))
@@ -360,7 +466,7 @@ def main():
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
+        for _ in range(steps):
             e2e_step()
         torch.cuda.synchronize()
         if world > 1:
@@ -370,15 +476,34 @@ def main():
             t = torch.tensor([dt], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": cfg["I"] * cfg["J"] * Ke * world * args.e2e_steps / dt, "unit": "elements/s",
-               "slices_per_rank": Ke,
+        narrow = os.environ.get("XTSG_HOST_NARROW", "1") != "0" and not comp3 and host_dtype != "bf16"
+        out = {"value": cfg["I"] * cfg["J"] * Ke * world * steps / dt, "unit": "elements/s",
+               "slices_per_rank": Ke, "steps": steps,
                "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                "d2h_bytes_per_step": int(yh.numel() * 4),
-               "host_dtype": args.e2e_dtype, "ms_per_step": dt / args.e2e_steps * 1e3,
-               "pcie_h2d_bytes_per_step": int(xh.numel() * (2 if os.environ.get("XTSG_HOST_NARROW", "1") != "0"
-                                                            else xh.element_size())),
-               "note": "f32/f64 host input is narrowed to bf16 on the host (RNE, multi-threaded) before the DMA"}
+               "host_dtype": host_dtype, "ms_per_step": dt / steps * 1e3,
+               "pcie_h2d_bytes_per_step": int(xh.numel() * (2 if narrow else xh.element_size())),
+               "note": ("f32/f64 host input is narrowed to bf16 on the host (RNE, multi-threaded) before the DMA"
+                        if narrow else "host input copied as is; converted/split on the device")}
         del xh
+        return out
+
+    e2e = e2e_f64 = None
+    if not args.no_e2e:
+        # host memory is shared by the node's ranks: the e2e sample per rank
+        # shrinks with N (the metric is a rate; per-rank pinned input <= 32 GB)
+        e2e = run_e2e(args.e2e_dtype, max(100, K // world), args.e2e_steps)
+        # the drop-in's own boundary type (Tensor3::values is fp64,
+        # tensor.hpp:30-44): a quarter-size sample (8 GB pinned per rank)
+        if args.e2e_dtype != "f64":
+            e2e_f64 = run_e2e("f64", max(100, K // (4 * world)), max(2, args.e2e_steps // 2))
+
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            parity = parity_check(y, cfg, dims, red, P, (0, P - 1))
+        except Exception as e:  # oracle build absent
+            parity = {"error": str(e)}
 
     cp = None
     if rank == 0 and not args.no_cp_time:
@@ -388,7 +513,7 @@ def main():
             cp = {"error": str(e)}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
             v, sample = cpu_reference_rate(cfg, args.cpu_seconds, threads)
@@ -408,8 +533,9 @@ def main():
                        "shared_rows": cfg["S"], "parallelism": f"mode-3 slabs x{world}",
                        "l2": "inputs (16 GB bf16 per rank) larger than L2; no flush",
                        "plan_create_s": round(t_plan, 3)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "cp_time": cp,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_f64_host": e2e_f64,
+            "gpu_launches": int(launches),
+            "cp_time": cp, "parity": parity,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -6,7 +6,7 @@
  * Every entry point below names the reference function it replaces
  * (file:line); the C++ facade paper_2311_13693_b200/facade/xts_facade.cpp
  * implements the reference's own declarations (the unmodified
- * /root/reference/proj/include/xts/*.hpp) on top of them, with the exact C++
+ * headers under /root/reference/proj/include/xts) on top of them, with the exact C++
  * signatures and exception types.
  *
  * Conventions (shared by every function):
@@ -217,6 +217,30 @@ int32_t xtsg_plan_compress(xtsg_plan* plan, const void* x, int32_t x_dtype, cons
 int32_t xtsg_plan_compress_factors(xtsg_plan* plan, const double* a, const double* b,
                                    const double* c, int64_t rank, int64_t k0, int64_t k1,
                                    void* y, int32_t accumulate, void* stream);
+
+/* ---- multi-GPU compression (SURVEY §8 e; no reference counterpart: the
+ * reference compresses on one host, pipeline.cpp:386-405) ------------------
+ * One plan per GPU of the node (the same ensemble regenerated on each from
+ * the seed), one persistent host thread per GPU, contiguous mode-3 slabs
+ * k in [K*g/G, K*(g+1)/G) per GPU, and one NCCL reduce (sum, fp32) of the
+ * P*L*M*N partial replicas onto gpus[0] (ncclCommInitAll clique; NCCL is
+ * dlopen'ed, "libnccl.so.2"). y: host memory or device memory on gpus[0].
+ * gpus may be NULL (devices 0..ngpus-1). Calls on one xtsg_multi serialise. */
+typedef struct xtsg_multi xtsg_multi;
+int32_t xtsg_multi_create(const xtsg_plan_desc* desc, int32_t ngpus, const int32_t* gpus, xtsg_multi** out);
+void xtsg_multi_destroy(xtsg_multi* multi);
+/* X = reconstruct(a, b, c) (host fp64 factors I x R, J x R, K x R), every GPU
+ * generating its own slab on the device */
+int32_t xtsg_multi_compress_factors(xtsg_multi* multi, const double* a, const double* b, const double* c,
+                                    int64_t rank, void* y, int32_t accumulate);
+/* dense X (whole tensor, column-major with leading dimensions ld like
+ * xtsg_plan_compress; host memory is streamed to each GPU slab by slab) */
+int32_t xtsg_multi_compress(xtsg_multi* multi, const void* x, int32_t x_dtype, const int64_t ld[2], void* y,
+                            int32_t accumulate);
+/* device time of the last call: max over the GPUs of compress + reduce (ms) */
+int32_t xtsg_multi_last_ms(xtsg_multi* multi, double* ms);
+/* the NCCL version the multi-GPU path resolved (e.g. 22809), or XTSG_E_CUDA */
+int32_t xtsg_nccl_version(int32_t* version);
 
 /* Sparse COO input (new, no reference counterpart; Eq. 3 restricted to the
  * nonzeros, duplicates sum): coordinates int32 SoA (i[nnz], j[nnz], k[nnz]),

@@ -24,7 +24,7 @@ from ._lib import (  # noqa: F401
 from .api import (  # noqa: F401
     compute_replica_count, gen_gaussian, gen_sparse_projection, make_ensemble, comp,
     comp_from_factors, reconstruct, round_to_half, split_half, half_gemm, comp_half, comp_mixed,
-    comp_naive_half, comp_blocked, Plan, launch_count, device_ready,
+    comp_naive_half, comp_blocked, Plan, MultiPlan, nccl_version, launch_count, device_ready,
     cp_als, cp_als_batched, relative_error, normalize_shared, max_trace_assignment,
     align_replicas, solve_stacked_ls, recover_perm_scale, apply_forward, apply_recovery,
     generate_factors, xts_header, PipelineConfig, RunMetrics, decompose, decompose_replicas, decompose_stage1,

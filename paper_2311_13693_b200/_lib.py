@@ -138,6 +138,12 @@ _SIGS = {
     "xtsg_plan_set_profiling": (_I32, [_P, _I32]),
     "xtsg_plan_profile": (_I32, [_P, _I32, _P]),
     "xtsg_plan_compress_factors": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I32, _P]),
+    "xtsg_multi_create": (_I32, [_P, _I32, _P, _P]),
+    "xtsg_multi_destroy": (None, [_P]),
+    "xtsg_multi_compress_factors": (_I32, [_P, _P, _P, _P, _I64, _P, _I32]),
+    "xtsg_multi_compress": (_I32, [_P, _P, _I32, _P, _P, _I32]),
+    "xtsg_multi_last_ms": (_I32, [_P, _P]),
+    "xtsg_nccl_version": (_I32, [_P]),
     "xtsg_plan_compress_coo": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _I32, _P]),
     "xtsg_xts_header": (_I32, [C.c_char_p, _P, _P, _P]),
     "xtsg_plan_compress_csf": (_I32, [_P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I32, _P]),

@@ -432,6 +432,72 @@ class Plan:
         return [y[p * n:(p + 1) * n].reshape(tuple(reduced), order="F") for p in range(count)]
 
 
+class MultiPlan:
+    """xtsg_multi_*: one plan per GPU of the node, mode-3 slabs per GPU and one
+    NCCL reduce of the replicas onto the first GPU (SURVEY §8 e), driven from
+    one process through the C ABI (no torch.distributed)."""
+
+    def __init__(self, dims, reduced, count: int, shared_rows: int, seed: int, gpus=(0,),
+                 precision: int = PREC_BF16, kind="gaussian", **spec):
+        d = PlanDesc()
+        for m in range(3):
+            d.dims[m] = int(dims[m])
+            d.reduced[m] = int(reduced[m])
+        d.count, d.shared_rows = int(count), int(shared_rows)
+        d.spec = _spec(kind, **spec)
+        d.seed = C.c_uint64(seed).value
+        d.precision = int(precision)
+        self.desc, self.count, self.reduced = d, int(count), tuple(int(x) for x in reduced)
+        self.gpus = np.asarray(gpus, np.int32)
+        # load torch (and with it torch's NCCL) first: the library dlopens
+        # whatever libnccl.so.2 the process already has, and a different
+        # system NCCL loaded first would break a later `import torch`
+        import torch  # noqa: F401
+        self._h = C.c_void_p()
+        check(lib.xtsg_multi_create(C.byref(d), len(self.gpus), ptr(self.gpus), C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib.xtsg_multi_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _y(self, y):
+        return np.zeros(self.count * int(np.prod(self.reduced)), np.float32) if y is None else y
+
+    def compress_factors(self, factors, y=None, accumulate=False):
+        a, b, c = (_f64(x) for x in factors)
+        y = self._y(y)
+        check(lib.xtsg_multi_compress_factors(self._h, ptr(a), ptr(b), ptr(c), a.shape[1], ptr(y),
+                                              1 if accumulate else 0))
+        return y
+
+    def compress(self, x, y=None, accumulate=False):
+        xa = np.asfortranarray(x)
+        code = {np.dtype(np.float64): DTYPE_F64, np.dtype(np.float32): DTYPE_F32}[xa.dtype]
+        ld = np.asarray([xa.shape[0], xa.shape[0] * xa.shape[1]], np.int64)
+        y = self._y(y)
+        check(lib.xtsg_multi_compress(self._h, ptr(xa), code, ptr(ld), ptr(y), 1 if accumulate else 0))
+        return y
+
+    def last_ms(self) -> float:
+        out = np.zeros(1)
+        check(lib.xtsg_multi_last_ms(self._h, ptr(out)))
+        return float(out[0])
+
+
+def nccl_version() -> int:
+    import torch  # noqa: F401  (see MultiPlan)
+    v = np.zeros(1, np.int32)
+    check(lib.xtsg_nccl_version(ptr(v)))
+    return int(v[0])
+
+
 # ---------------------------------------------------------------------------
 # CP-ALS (cp_als.hpp:10-40)
 
