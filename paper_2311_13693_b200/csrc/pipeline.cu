@@ -125,23 +125,46 @@ std::vector<double> reconstruct_rows(const std::vector<double>* f, const int64_t
   return t;
 }
 
-// gather_block (pipeline.cpp:36-44) from a host or device column-major tensor.
+// device side of gather_block: out[i + n1*(j + n2*k)] = t[si[i] + d0*(sj[j] + d1*sk[k])]
+__global__ void gather_block_kernel(const double* __restrict__ t, int64_t d0, int64_t d1,
+                                    const int64_t* __restrict__ sel, int64_t n1, int64_t n2, int64_t n3,
+                                    double* __restrict__ out) {
+  const int64_t total = n1 * n2 * n3;
+  const int64_t *si = sel, *sj = sel + n1, *sk = sel + n1 + n2;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % n1, jk = e / n1, j = jk % n2, k = jk / n2;
+    out[e] = t[si[i] + d0 * (sj[j] + d1 * sk[k])];
+  }
+}
+
+// gather_block (pipeline.cpp:36-44) from a host or device column-major tensor
+// (device tensors: one gather kernel and one D2H copy of the block).
 std::vector<double> gather_block(const double* t, const int64_t* dims, const std::vector<int64_t>* sel,
                                  cudaStream_t st) {
   const size_t n1 = sel[0].size(), n2 = sel[1].size(), n3 = sel[2].size();
   std::vector<double> out(n1 * n2 * n3);
-  const bool dev = is_device_ptr(t);
+  if (out.empty()) return out;
+  if (is_device_ptr(t)) {
+    std::vector<int64_t> idx;
+    idx.reserve(n1 + n2 + n3);
+    for (int m = 0; m < 3; ++m) idx.insert(idx.end(), sel[m].begin(), sel[m].end());
+    DevBuf<int64_t> dsel(idx.size(), st);
+    DevBuf<double> dout(out.size(), st);
+    XCUDA(cudaMemcpyAsync(dsel.ptr, idx.data(), idx.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    const int64_t total = static_cast<int64_t>(out.size());
+    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    gather_block_kernel<<<grid, 256, 0, st>>>(t, dims[0], dims[1], dsel.ptr, static_cast<int64_t>(n1),
+                                              static_cast<int64_t>(n2), static_cast<int64_t>(n3), dout.ptr);
+    XLAUNCH_CHECK();
+    XCUDA(cudaMemcpyAsync(out.data(), dout.ptr, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    XCUDA(cudaStreamSynchronize(st));
+    return out;
+  }
   for (size_t k = 0; k < n3; ++k)
     for (size_t j = 0; j < n2; ++j)
-      for (size_t i = 0; i < n1; ++i) {
-        const int64_t off = sel[0][i] + dims[0] * (sel[1][j] + dims[1] * sel[2][k]);
-        double* dst = &out[i + n1 * (j + n2 * k)];
-        if (dev)
-          XCUDA(cudaMemcpyAsync(dst, t + off, sizeof(double), cudaMemcpyDeviceToHost, st));
-        else
-          *dst = t[off];
-      }
-  if (dev) XCUDA(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < n1; ++i)
+        out[i + n1 * (j + n2 * k)] = t[sel[0][i] + dims[0] * (sel[1][j] + dims[1] * sel[2][k])];
   return out;
 }
 
