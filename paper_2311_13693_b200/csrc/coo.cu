@@ -273,7 +273,7 @@ __global__ void csf_expand_kernel(const int64_t* __restrict__ fiber_ptr, const i
       if (j < 0 || j >= J) bad[0] = 1;
       if (b > e || b < 0 || e > nnz) bad[1] = 1;
     }
-    if (b > e || b < 0 || e > nnz) continue;
+    if (b > e || b < 0 || e > nnz || !sj) continue;
     for (int64_t q = b + lane; q < e; q += 32) sj[q] = j;
   }
 }
@@ -369,6 +369,14 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     DevBuf<uint8_t> tmp(tmp_bytes, s);
     XCUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tmp_bytes, keys.ptr, keys2.ptr, idx.ptr, idx2.ptr, nnz, 0, end_bit, s));
     count_launch();
+    if (sparse_tc_ok()) {
+      keys.release();
+      idx.release();
+      sparse_tc_sorted(keys2.ptr, idx2.ptr, nullptr, nullptr, nnz, yo.dev, accumulate, s);
+      if (fp16()) check_finite16(yo.dev, ysz, s);
+      if (yo.host) yo.finish();
+      return;
+    }
     bi = DevBuf<int32_t>(static_cast<size_t>(nnz), s);
     bj = DevBuf<int32_t>(static_cast<size_t>(nnz), s);
     bk = DevBuf<int32_t>(static_cast<size_t>(nnz), s);
@@ -376,6 +384,13 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     coo_unpack_kernel<<<gridn(nnz), 256, 0, s>>>(keys2.ptr, idx2.ptr, nnz, J, bi.ptr, bj.ptr, bk.ptr, bv.ptr);
     XLAUNCH_CHECK();
     si = bi.ptr; sj = bj.ptr; sk = bk.ptr; sv = bv.ptr;
+  }
+  if (!hf[1] && sparse_tc_ok()) {
+    idx.release();
+    sparse_tc_sorted(keys.ptr, nullptr, di.dev, dv.dev, nnz, yo.dev, accumulate, s);
+    if (fp16()) check_finite16(yo.dev, ysz, s);
+    if (yo.host) yo.finish();
+    return;
   }
   keys.release();
   idx.release();
@@ -429,11 +444,12 @@ void Plan::compress_csf(int64_t n_slices, const int32_t* slice_k, const int64_t*
   InView<int64_t> dsp(slice_ptr, static_cast<size_t>(n_slices + 1), s),
       dfp(fiber_ptr, static_cast<size_t>(n_fibers + 1), s);
   InView<float> dv(val, static_cast<size_t>(nnz), s);
-  DevBuf<int32_t> sj(static_cast<size_t>(nnz), s), cnt(static_cast<size_t>(n_slices), s);
+  const bool tc = sparse_tc_ok();
+  DevBuf<int32_t> sj(tc ? 0 : static_cast<size_t>(nnz), s), cnt(static_cast<size_t>(n_slices), s);
   DevBuf<int64_t> off(static_cast<size_t>(n_slices), s);
   DevBuf<int> bad(2, s);
   bad.zero();
-  XCUDA(cudaMemsetAsync(sj.ptr, 0, sizeof(int32_t) * nnz, s));
+  if (!tc) XCUDA(cudaMemsetAsync(sj.ptr, 0, sizeof(int32_t) * nnz, s));
   csf_expand_kernel<<<gridn(n_fibers * 32), 256, 0, s>>>(dfp.dev, dj.dev, n_fibers, J, nnz, sj.ptr, bad.ptr);
   XLAUNCH_CHECK();
   csf_slices_kernel<<<gridn(n_slices), 256, 0, s>>>(dsp.dev, dfp.dev, dk.dev, n_slices, n_fibers, K, off.ptr, cnt.ptr,
@@ -446,6 +462,12 @@ void Plan::compress_csf(int64_t n_slices, const int32_t* slice_k, const int64_t*
   XCUDA(cudaStreamSynchronize(s));
   if (hb[0]) data_error("plan_compress_csf: coordinate outside the tensor");
   if (hb[1]) data_error("plan_compress_csf: slice/fiber pointers not monotone or inconsistent with the sizes");
+  if (tc) {
+    sparse_tc(n_slices, dk.dev, dsp.dev, dfp.dev, dj.dev, di.dev, dv.dev, yo.dev, accumulate, s);
+    if (fp16()) check_finite16(yo.dev, ysz, s);
+    if (yo.host) yo.finish();
+    return;
+  }
   coo_slices(di.dev, sj.ptr, dv.dev, off.ptr, cnt.ptr, dk.dev, n_slices, yo.dev, accumulate, s);
   if (fp16()) check_finite16(yo.dev, ysz, s);
   if (yo.host) yo.finish();
@@ -477,8 +499,6 @@ void Plan::ensure_sparse_operands(cudaStream_t s) {
 void Plan::coo_slices(const int32_t* si, const int32_t* sj, const float* sv, const int64_t* off_p,
                       const int32_t* cnt_p, const int32_t* uk_p, int64_t kd, float* ydev, bool accumulate,
                       cudaStream_t s) {
-  const int64_t N = desc.reduced[2], K = desc.dims[2];
-  const bool padded = virt_padded();
   const int64_t plrows = vP * lpad;
   const int64_t ld_ut = round_up256(plrows), ld_vtj = vP * mpad;
   // 3. fibers -> Z[p][kd][m][l]
@@ -513,7 +533,14 @@ void Plan::coo_slices(const int32_t* si, const int32_t* sj, const float* sv, con
     else unroll == 8 ? launch(coo_fiber_kernel<1, false, 8>) : launch(coo_fiber_kernel<1, false, 4>);
   }
   XLAUNCH_CHECK();
-  // 4. mode 3 over the distinct slices
+  sparse_mode3(z.ptr, uk_p, kd, ydev, accumulate, s);
+}
+
+// 4-5. mode 3 over the distinct slices: y (+)= Z_p W_p[:, uk]^T
+void Plan::sparse_mode3(const float* z, const int32_t* uk_p, int64_t kd, float* ydev, bool accumulate,
+                        cudaStream_t s) {
+  const int64_t N = desc.reduced[2], K = desc.dims[2];
+  const bool padded = virt_padded();
   DevBuf<float> wg(static_cast<size_t>(vP * N * kd), s);
   gather_w_kernel<<<gridn(vP * N * kd), 256, 0, s>>>(wf.ptr, vP, N, K, uk_p, kd, wg.ptr);
   XLAUNCH_CHECK();
@@ -525,7 +552,7 @@ void Plan::coo_slices(const int32_t* si, const int32_t* sj, const float* sv, con
   }
   GemmArgs<float> g;
   g.m = mpad * lpad; g.n = N; g.k = kd; g.batch = vP;
-  g.a = z.ptr; g.lda = mpad * lpad; g.stride_a = kd * mpad * lpad;
+  g.a = z; g.lda = mpad * lpad; g.stride_a = kd * mpad * lpad;
   g.b = wg.ptr; g.ldb = kd; g.stride_b = N * kd;
   g.c = ydst; g.ldc = mpad * lpad; g.stride_c = mpad * lpad * N;
   g.beta = (accumulate && !padded) ? 1.f : 0.f;
