@@ -463,7 +463,7 @@ void Plan::compress_csf(int64_t n_slices, const int32_t* slice_k, const int64_t*
   if (hb[0]) data_error("plan_compress_csf: coordinate outside the tensor");
   if (hb[1]) data_error("plan_compress_csf: slice/fiber pointers not monotone or inconsistent with the sizes");
   if (tc) {
-    sparse_tc(n_slices, dk.dev, dsp.dev, dfp.dev, dj.dev, di.dev, dv.dev, yo.dev, accumulate, s);
+    sparse_tc(n_slices, dk.dev, dsp.dev, n_fibers, dfp.dev, dj.dev, nnz, di.dev, dv.dev, yo.dev, accumulate, s);
     if (fp16()) check_finite16(yo.dev, ysz, s);
     if (yo.host) yo.finish();
     return;

@@ -112,9 +112,9 @@ struct Plan {
   void sparse_mode3(const float* z, const int32_t* uk, int64_t kd, float* ydev, bool accumulate, cudaStream_t s);
   // tensor-core sparse path (sparse_tc.cu): dense tiles of a slice
   bool sparse_tc_ok() const;
-  void sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* slice_ptr, const int64_t* fiber_ptr,
-                 const int32_t* fiber_j, const int32_t* nz_i, const float* val, float* ydev, bool accumulate,
-                 cudaStream_t s);
+  void sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* slice_ptr, int64_t n_fibers,
+                 const int64_t* fiber_ptr, const int32_t* fiber_j, int64_t nnz, const int32_t* nz_i,
+                 const float* val, float* ydev, bool accumulate, cudaStream_t s);
   void sparse_tc_sorted(const uint64_t* skeys, const uint64_t* spay, const int32_t* si, const float* sv,
                         int64_t nnz, float* ydev, bool accumulate, cudaStream_t s);
 };

@@ -40,51 +40,75 @@
 #include "gemm_simt.cuh"
 #include "plan.cuh"
 #include "sm100_ptx.cuh"
+#include "ttm_tc.cuh"
 
 namespace xtsg {
 
 namespace {
 
-constexpr int SP_NT = 512;  // 16 warps: the densify passes are latency-bound
-constexpr int SP_SPT = 2048 / SP_NT;  // hash slots per thread in the id compaction
+constexpr int SP_NT = 512;   // tensor kernel: 16 warps
+constexpr int PL_NT = 256;   // planner: 8 warps, several CTAs per SM
 constexpr int SP_NF = 64;    // fibers per tile (mode-1 UMMA N, mode-2 K)
 constexpr int SP_NI = 512;   // distinct i per tile (mode-1 K)
-constexpr int SP_HS = 2048;  // hash slots (load <= 0.25 + in-flight claims)
+constexpr int SP_HS = 2048;  // planner hash slots (<= SP_NI + PL_NT claims)
 constexpr int SP_NS = 4;     // U gather ring slots
-constexpr int SP_AHEAD = 3;  // chunks issued ahead of the MMA
+constexpr int SP_AHEAD = 3;  // cp.async groups in flight per producer
 constexpr int XD_CHUNK = SP_NF * 128;              // 64 fibers x 64 i, 8 KB
 constexpr int XD_BYTES = (SP_NI / 64) * XD_CHUNK;  // 64 KB
 constexpr int UC_BYTES = 128 * 64 * 2;             // 128 rows x 64 i, 16 KB
 constexpr int A2_BYTES = 128 * 128;                // 128 rows x 64 fibers
-constexpr int VG_BYTES = 128 * 64 * 2;             // 128 (p, m) x 64 fibers
+constexpr int VG_BYTES = 128 * 64 * 2;             // 128 (p, m) x 64 fibers (x2 buffers)
+
+// one planned tile: fibers [f0, f0 + nf) of slice s, nonzeros [e0, e0 + n)
+// (a piece of one fiber when nf == 1 and the fiber is longer), local ids
+// 0..ni-1 standing for si_g[si0 ..), each nonzero's id at li_g[e]
+struct SpTile {
+  int64_t e0, f0, si0;  // first nonzero, first fiber, id -> i list at si_g[si0 ..)
+  int32_t s, n, nf, ni, dup, pad;
+};
 
 struct SpMisc {
-  uint64_t mma_done[SP_NS];
-  uint64_t d1_full, d2_full;
+  uint64_t full[SP_NS], empty[SP_NS];  // U gather ring
+  uint64_t vg_full[2], vg_empty[2];    // V rows (mode-2 B), double-buffered
+  uint64_t d1_full[2], d1_empty[2];    // mode-1 accumulator (TMEM, double-buffered)
+  uint64_t a2_full, d2_full, d2_empty;
   uint32_t tmem_base;
-  int count, ovf;
-  int64_t slice;
-  int wsum[SP_NT / 32];
+  int64_t tile;
+  SpTile t;
 };
 
 constexpr int OFF_RING = XD_BYTES;
 constexpr int OFF_A2 = OFF_RING + SP_NS * UC_BYTES;
 constexpr int OFF_VG = OFF_A2 + A2_BYTES;
-constexpr int OFF_KEYS = OFF_VG + VG_BYTES;
-constexpr int OFF_LIS = OFF_KEYS + SP_HS * 4;
-constexpr int OFF_SI = OFF_LIS + SP_HS * 2;
+constexpr int OFF_SI = OFF_VG + 2 * VG_BYTES;
 constexpr int OFF_TFP = OFF_SI + SP_NI * 4;
-constexpr int OFF_TFJ = OFF_TFP + (SP_NF + 2) * 8;
+constexpr int OFF_TFJ = OFF_TFP + (SP_NF + 2) * 4;
 constexpr int OFF_MISC = OFF_TFJ + SP_NF * 4;
 constexpr int SP_SMEM = OFF_MISC + static_cast<int>(sizeof(SpMisc)) + 1024;
 static_assert(SP_SMEM <= 232448, "shared memory budget");
 
-struct SpTcParams {
+struct SpPlanParams {
   const int64_t* slice_ptr;  // n_slices + 1 fiber offsets
   const int64_t* fiber_ptr;  // nonzero offsets per fiber
-  const int32_t* fiber_j;
   const int32_t* nz_i;
+  int64_t n_slices;
+  int32_t* si_g;    // nnz: a tile's distinct i at [e0, e0 + ni)
+  uint16_t* li_g;   // nnz: local id of each nonzero
+  SpTile* tiles;
+  int64_t max_tiles;
+  unsigned long long* counters;  // [0] slice counter, [1] tile count
+};
+
+struct SpTcParams {
+  const int64_t* fiber_ptr;
+  const int32_t* fiber_j;
   const float* val;
+  const int32_t* si_g;
+  const uint16_t* li_g;
+  const SpTile* tiles;
+  const unsigned long long* n_tiles;
+  int64_t max_tiles;
+  unsigned long long* counter;
   int64_t n_slices;
   const __nv_bfloat16* ut;  // [I][ld_ut], row (p, l) contiguous
   int64_t ld_ut;
@@ -93,7 +117,6 @@ struct SpTcParams {
   int lpad, mpad, nrb, n2;
   int64_t vp;
   float* z;  // [vp][n_slices][mpad][lpad]
-  unsigned long long* counter;
 };
 
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -109,10 +132,16 @@ __device__ __forceinline__ int atoms_add(int* p, int v) {
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(ptx::smem_u32(p)), "r"(v) : "memory");
   return old;
 }
-// x += v on a 16-bit float in shared memory (bf16 or fp16): CAS on its 32-bit word
+__device__ __forceinline__ uint32_t atoms_or(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(ptx::smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+
+// x += v on a 16-bit float at shared address a (bf16 or fp16): CAS on its
+// 32-bit word (sm_100 has no native shared-memory float reduction)
 template <bool F16>
-__device__ __forceinline__ void atoms_add16(uint8_t* dst, float v) {
-  const uint32_t a = ptx::smem_u32(dst);
+__device__ __forceinline__ void atoms_add16(uint32_t a, float v) {
   const uint32_t w = a & ~3u, sh = (a & 2u) * 8u;
   uint32_t old;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(old) : "r"(w) : "memory");
@@ -129,298 +158,119 @@ __device__ __forceinline__ void atoms_add16(uint8_t* dst, float v) {
   }
 }
 
+// volatile shared-memory loads (a generic volatile pointer becomes a slow system-scope load)
+__device__ __forceinline__ int lds_volatile(const int* p) {
+  int v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(ptx::smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ uint16_t lds_volatile16(const uint16_t* p) {
+  uint16_t v;
+  asm volatile("ld.volatile.shared.u16 %0, [%1];" : "=h"(v) : "r"(ptx::smem_u32(p)));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t sp_hash(int32_t key) {
   return (static_cast<uint32_t>(key) * 2654435761u) >> (32 - 11);
 }
 
-// f(x, i) over the tile's nonzeros, x = e - e0 the local offset (< 2^30):
-// head scalars, 16-byte vector body (U loads in flight per thread), tail
-// scalars, so each thread sees increasing x. f returns false to stop early.
-template <int U, class F>
-__device__ __forceinline__ void for_each_i(const int32_t* __restrict__ nz_i, int64_t e0, int64_t e1,
-                                           volatile int* stop, F&& f) {
+// Batched visitor over nonzeros [e0, e1) (e1 - e0 < 2^30) with NT threads:
+// f(n, xs, ks) with n <= 4*U valid entries (xs = e - e0, ascending per
+// thread; ks the i), 16-byte loads, U in flight per thread; the batch lets f
+// keep its shared-memory round trips in flight together.
+template <int NT, int U, class F>
+__device__ __forceinline__ void for_each_i(const int32_t* __restrict__ nz_i, int64_t e0, int64_t e1, F&& f) {
+  constexpr int B = 4 * U;
   const int tid = threadIdx.x;
   const int64_t a0 = min(e1, (e0 + 3) & ~int64_t(3));
   const int64_t a1 = max(a0, e1 & ~int64_t(3));
-  for (int64_t e = e0 + tid; e < a0; e += SP_NT) f(static_cast<int>(e - e0), __ldg(nz_i + e));
-  const int4* v = reinterpret_cast<const int4*>(nz_i + a0);
-  const int nv = static_cast<int>((a1 - a0) >> 2), xa = static_cast<int>(a0 - e0);
-  for (int b = 0; b < nv; b += SP_NT * U) {
-    if (*stop) return;
-    int4 x[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = b + u * SP_NT + tid;
-      if (idx < nv) x[u] = __ldg(v + idx);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = b + u * SP_NT + tid;
-      if (idx < nv) {
-        const int xl = xa + idx * 4;
-        f(xl, x[u].x);
-        f(xl + 1, x[u].y);
-        f(xl + 2, x[u].z);
-        f(xl + 3, x[u].w);
-      }
-    }
+  int xs[B];
+  int32_t ks[B];
+  if (e0 + tid < a0) {  // head: fewer than 4 entries
+    xs[0] = tid;
+    ks[0] = __ldg(nz_i + e0 + tid);
+    f(1, xs, ks);
   }
-  for (int64_t e = a1 + tid; e < e1; e += SP_NT) f(static_cast<int>(e - e0), __ldg(nz_i + e));
-}
-
-// f(x, i, value) over the tile's nonzeros, same order as for_each_i
-template <int U, class F>
-__device__ __forceinline__ void for_each_ix(const int32_t* __restrict__ nz_i, const float* __restrict__ val,
-                                            int64_t e0, int64_t e1, volatile int* stop, F&& f) {
-  const int tid = threadIdx.x;
-  const int64_t a0 = min(e1, (e0 + 3) & ~int64_t(3));
-  const int64_t a1 = max(a0, e1 & ~int64_t(3));
-  for (int64_t e = e0 + tid; e < a0; e += SP_NT) f(static_cast<int>(e - e0), __ldg(nz_i + e), __ldg(val + e));
   const int4* vi = reinterpret_cast<const int4*>(nz_i + a0);
-  const float4* vv = reinterpret_cast<const float4*>(val + a0);
   const int nv = static_cast<int>((a1 - a0) >> 2), xa = static_cast<int>(a0 - e0);
-  for (int b = 0; b < nv; b += SP_NT * U) {
-    if (*stop) return;
-    int4 x[U];
-    float4 w[U];
+  for (int b = 0; b < nv; b += NT * U) {
+    int n = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int idx = b + u * SP_NT + tid;
+      const int idx = b + u * NT + tid;
       if (idx < nv) {
-        x[u] = __ldg(vi + idx);
-        w[u] = __ldg(vv + idx);
-      }
-    }
+        const int4 x = __ldg(vi + idx);
+        ks[4 * u] = x.x;
+        ks[4 * u + 1] = x.y;
+        ks[4 * u + 2] = x.z;
+        ks[4 * u + 3] = x.w;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = b + u * SP_NT + tid;
-      if (idx < nv) {
-        const int xl = xa + idx * 4;
-        f(xl, x[u].x, w[u].x);
-        f(xl + 1, x[u].y, w[u].y);
-        f(xl + 2, x[u].z, w[u].z);
-        f(xl + 3, x[u].w, w[u].w);
+        for (int q = 0; q < 4; ++q) xs[4 * u + q] = xa + idx * 4 + q;
+        n = 4 * (u + 1);
       }
     }
+    if (n) f(n, xs, ks);
   }
-  for (int64_t e = a1 + tid; e < e1; e += SP_NT)
-    f(static_cast<int>(e - e0), __ldg(nz_i + e), __ldg(val + e));
+  if (a1 + tid < e1) {  // tail: fewer than 4 entries
+    xs[0] = static_cast<int>(a1 + tid - e0);
+    ks[0] = __ldg(nz_i + a1 + tid);
+    f(1, xs, ks);
+  }
 }
 
-template <bool F16>
-__global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* xd = sm;
-  uint8_t* ring = sm + OFF_RING;
-  uint8_t* a2 = sm + OFF_A2;
-  uint8_t* vg = sm + OFF_VG;
-  int32_t* keys = reinterpret_cast<int32_t*>(sm + OFF_KEYS);
-  uint16_t* lis = reinterpret_cast<uint16_t*>(sm + OFF_LIS);
-  int32_t* si = reinterpret_cast<int32_t*>(sm + OFF_SI);
-  int32_t* tfp = reinterpret_cast<int32_t*>(sm + OFF_TFP);  // fiber starts, local offsets
-  int32_t* tfj = reinterpret_cast<int32_t*>(sm + OFF_TFJ);
-  SpMisc* ms = reinterpret_cast<SpMisc*>(sm + OFF_MISC);
-  volatile int* vflag = &ms->ovf;  // overflow (insert) or miss (lookup) of the current pass
-  volatile int* vcount = &ms->count;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    for (int s = 0; s < SP_NS; ++s) ptx::mbar_init(&ms->mma_done[s], 1);
-    ptx::mbar_init(&ms->d1_full, 1);
-    ptx::mbar_init(&ms->d2_full, 1);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 0) ptx::tmem_alloc(&ms->tmem_base, 256);
-  // stale operand bytes beyond a partial chunk must be finite (they multiply zeros)
-  for (int e = tid; e < (SP_NS * UC_BYTES + A2_BYTES + VG_BYTES) / 16; e += SP_NT)
-    reinterpret_cast<uint4*>(ring)[e] = make_uint4(0, 0, 0, 0);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = ms->tmem_base;
-  const uint32_t d1 = tmem, d2 = tmem + 128;
-  const uint32_t idesc1 = (ptx::idesc_bf16(128, SP_NF) | ptx::IDESC_A_MN) & ptx::idesc_fmt_mask(F16);
-  const uint32_t idesc2 = (ptx::idesc_bf16(128, p.n2) | ptx::IDESC_B_MN) & ptx::idesc_fmt_mask(F16);
-  const int q = warp & 3, hh = warp >> 2;
-  const int r = q * 32 + lane;  // row of the 128-row block == TMEM lane
-  const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
-  const int p_local = r / p.lpad, l = r % p.lpad;
-  const int rpb = 128 / p.lpad;
-  const int half = p.mpad >> 1;
-  const uint32_t ring_u = ptx::smem_u32(ring), xd_u = ptx::smem_u32(xd);
-  uint32_t g = 0, n1 = 0, n2c = 0;  // U chunk sequence number, D1 / D2 commit counts
-
-  // the i -> local id table persists across the tiles of a slice (their i
-  // supports usually coincide); lis = 0xFFFF marks a key without an id yet
+// ---------------------------------------------------------------------------
+// Planner: one CTA per slice (dynamic), cuts it into tiles of <= 64 fibers
+// with <= 512 distinct i and writes, per tile, a descriptor and the local id
+// of every nonzero (li_g). One pass per nonzero: the i -> id table persists
+// across the tiles of a slice (their i supports usually coincide) and a new i
+// gets the next id when it is first claimed. A table epoch (the tiles between
+// two clears) writes its id -> i list once, at si_g[first nonzero of the
+// epoch ...) (an epoch holds at least as many nonzeros as committed ids), and
+// its tiles use a prefix of it. When a tile pushes the table past 512 ids the
+// epoch is closed, the table cleared and the tile redone; if it overflows a
+// fresh table it is retried with half the fibers (a long fiber is cut into
+// 512-nonzero pieces). Duplicate coordinates inside a tile are flagged (the
+// tensor kernel then sums them with atomics; otherwise it stores).
+__global__ void __launch_bounds__(PL_NT, 4) sparse_plan_kernel(const SpPlanParams p) {
+  __shared__ int keys[SP_HS];
+  __shared__ uint16_t lis[SP_HS];
+  __shared__ uint32_t seen[SP_NF * SP_NI / 32];  // (fiber, id) occupancy bits
+  __shared__ int32_t tfp[SP_NF + 1];            // fiber starts relative to the tile
+  __shared__ int32_t idkey[SP_NI];              // id -> i of the current epoch
+  __shared__ int count, ovf, dup, wsum[PL_NT / 32];
+  __shared__ int64_t slice;
+  const int tid = threadIdx.x;
+  // empty table: no keys, no ids (a claimed slot shows 0xFFFF until its id is published)
   auto clear_table = [&]() {
-    for (int t = tid; t < SP_HS; t += SP_NT) {
+    for (int t = tid; t < SP_HS; t += PL_NT) {
       keys[t] = -1;
       lis[t] = 0xFFFF;
     }
-    if (tid == 0) ms->count = 0;
+    if (tid == 0) count = 0;
   };
   clear_table();
-  __syncthreads();
-
   for (;;) {
-    if (tid == 0) ms->slice = static_cast<int64_t>(atomicAdd(p.counter, 1ull));
+    if (tid == 0) slice = static_cast<int64_t>(atomicAdd(p.counters, 1ull));
     __syncthreads();
-    const int64_t s = ms->slice;
-    __syncthreads();
+    const int64_t s = slice;
     if (s >= p.n_slices) break;
     const int64_t fs0 = p.slice_ptr[s], fs1 = p.slice_ptr[s + 1];
-    const int64_t es0 = fs1 > fs0 ? p.fiber_ptr[fs0] : 0, es1 = fs1 > fs0 ? p.fiber_ptr[fs1] : 0;
-    if (es1 <= es0) continue;  // no nonzeros: Z of the slice stays zero
-    if (*vcount) {
-      clear_table();
-      __syncthreads();
-    }
-    int64_t f = fs0, e_in = es0;
+    int64_t f = fs0, e_in = fs1 > fs0 ? p.fiber_ptr[fs0] : 0;
+    int64_t epoch0 = e_in;  // first nonzero of the current table epoch
+    int committed = 0;      // ids used by the epoch's finished tiles
     int nt = SP_NF;
+    // close the epoch: its committed ids -> si_g, then an empty table
+    auto close_epoch = [&]() {
+      for (int t = tid; t < committed; t += PL_NT) p.si_g[epoch0 + t] = idkey[t];
+      clear_table();
+      committed = 0;
+      __syncthreads();
+    };
     while (f < fs1) {
       int nf = static_cast<int>(imin64(nt, fs1 - f));
       const int64_t fend0 = p.fiber_ptr[f + 1];
-      if (nt > 1 && p.fiber_ptr[f + nf] - e_in > (int64_t(1) << 30)) nt = nf = 1;  // local offsets stay 32-bit
+      if (nt > 1 && p.fiber_ptr[f + nf] - e_in > (int64_t(1) << 30)) nt = nf = 1;
       const int64_t e_end = nt == 1 ? imin64(fend0, e_in + SP_NI) : p.fiber_ptr[f + nf];
-      for (int t = tid; t <= nf; t += SP_NT)
-        tfp[t] = t == 0 ? 0 : static_cast<int32_t>((t == nf ? e_end : p.fiber_ptr[f + t]) - e_in);
-      for (int t = tid; t < nf; t += SP_NT) tfj[t] = p.fiber_j[f + t];
-      for (int e = tid; e < XD_BYTES / 16; e += SP_NT) reinterpret_cast<uint4*>(xd)[e] = make_uint4(0, 0, 0, 0);
-      if (tid == 0) {
-        ms->ovf = 0;
-        // the next tile's nonzeros (about as many as this one) into L2
-        const int64_t n = e_end - e_in;
-        const int64_t pa = (e_end + 3) & ~int64_t(3), pb = imin64(es1, e_end + n) & ~int64_t(3);
-        if (pb > pa) {
-          const uint32_t bytes = static_cast<uint32_t>(imin64((pb - pa) * 4, 1 << 20));
-          ptx::bulk_prefetch_l2(p.nz_i + pa, bytes);
-          ptx::bulk_prefetch_l2(p.val + pa, bytes);
-        }
-      }
-      __syncthreads();
-      // scatter pass: look each i up, add the value into Xd[fiber][id]; a key
-      // without an id raises the flag (and the pass stops early)
-      auto scatter = [&]() {
-        int fl = 0;  // fiber cursor: x only grows per thread
-        for_each_ix<2>(p.nz_i, p.val, e_in, e_end, vflag, [&](int x, int32_t key, float v) {
-          uint32_t h = sp_hash(key);
-          int li;
-          for (;;) {
-            const int k2 = keys[h];
-            if (k2 == key) {
-              li = lis[h];
-              break;
-            }
-            if (k2 == -1) {
-              li = 0xFFFF;
-              break;
-            }
-            h = (h + 1) & (SP_HS - 1);
-          }
-          if (li == 0xFFFF) {
-            *vflag = 1;
-            return;
-          }
-          while (tfp[fl + 1] <= x) ++fl;
-          uint8_t* dst = xd + (li >> 6) * XD_CHUNK + (fl >> 3) * 1024 + (fl & 7) * 128 +
-                         ((((li & 63) >> 3) ^ (fl & 7)) << 4) + (li & 7) * 2;
-          atoms_add16<F16>(dst, v);
-        });
-      };
-      // insert pass: claim a slot for every new i (ids assigned afterwards)
-      auto insert = [&]() {
-        for_each_i<4>(p.nz_i, e_in, e_end, vflag, [&](int, int32_t key) {
-          uint32_t h = sp_hash(key);
-          for (;;) {
-            int old = keys[h];
-            if (old == key) return;
-            if (old == -1) {
-              if (*vcount >= SP_NI) {  // bounds the claims: <= SP_NI + SP_NT < SP_HS slots
-                *vflag = 1;
-                return;
-              }
-              old = atoms_cas(&keys[h], -1, key);
-              if (old == -1) {
-                if (atoms_add(&ms->count, 1) >= SP_NI) *vflag = 1;
-                return;
-              }
-              if (old == key) return;
-            }
-            h = (h + 1) & (SP_HS - 1);
-          }
-        });
-      };
-      bool fresh = *vcount == 0;
-      bool ok = false;
-      if (!fresh) {
-        scatter();
-        __syncthreads();
-        ok = *vflag == 0;
-        __syncthreads();
-        if (!ok) {  // new keys: extend the table, else start it over for this tile
-          for (int e = tid; e < XD_BYTES / 16; e += SP_NT) reinterpret_cast<uint4*>(xd)[e] = make_uint4(0, 0, 0, 0);
-          if (tid == 0) ms->ovf = 0;
-          __syncthreads();
-          insert();
-          __syncthreads();
-          const bool ovf = *vflag != 0;
-          __syncthreads();
-          if (ovf) {
-            clear_table();
-            if (tid == 0) ms->ovf = 0;
-            __syncthreads();
-            fresh = true;
-          }
-        }
-      }
-      if (fresh) {
-        insert();
-        __syncthreads();
-        const bool ovf = *vflag != 0;
-        __syncthreads();
-        if (ovf) {  // more than SP_NI distinct i: fewer fibers
-          clear_table();
-          __syncthreads();
-          nt = max(1, nt >> 1);
-          continue;
-        }
-      }
-      if (!ok) {
-        // ids for the keys without one, in slot order: thread t owns SP_SPT slots
-        const int base0 = *vcount;
-        int c = 0;
-#pragma unroll
-        for (int k = 0; k < SP_SPT; ++k) c += keys[tid * SP_SPT + k] != -1 && lis[tid * SP_SPT + k] == 0xFFFF;
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        if (lane == 31) ms->wsum[warp] = incl;
-        __syncthreads();
-        int base = incl - c;
-        for (int w = 0; w < warp; ++w) base += ms->wsum[w];
-        int nassigned = 0;
-        for (int w = 0; w < SP_NT / 32; ++w) nassigned += ms->wsum[w];
-        base = base0 - nassigned + base;  // count already includes the new keys
-#pragma unroll
-        for (int k = 0; k < SP_SPT; ++k) {
-          const int key = keys[tid * SP_SPT + k];
-          if (key != -1 && lis[tid * SP_SPT + k] == 0xFFFF) {
-            lis[tid * SP_SPT + k] = static_cast<uint16_t>(base);
-            si[base] = key;
-            ++base;
-          }
-        }
-        __syncthreads();
-        scatter();
-      }
-      const int ni = *vcount;
-      ptx::fence_proxy_async_smem();
-      __syncthreads();
-      // next cursor (every thread computes the same)
       int64_t f_next = f + nf, e_next;
       if (nt == 1 && e_end < fend0) {
         f_next = f;
@@ -429,119 +279,451 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
         if (nt == 1) f_next = f + 1;
         e_next = f_next < fs1 ? p.fiber_ptr[f_next] : 0;
       }
-      {
-        const int nch = (ni + 63) >> 6;
-        const int k16_last = (ni - (nch - 1) * 64 + 15) >> 4;
-        // 2-3. row blocks: gathered-U mode 1, then mode 2 into Z
-        const int total = p.nrb * nch;
-        auto issue = [&](int t) {
-          const int rb = t / nch, c = t - rb * nch;
-          const uint32_t gg = g + static_cast<uint32_t>(t);
-          const int slot = static_cast<int>(gg % SP_NS);
-          if (gg >= SP_NS) ptx::mbar_wait(&ms->mma_done[slot], ((gg / SP_NS) + 1) & 1);
-          uint8_t* dst = ring + slot * UC_BYTES;
-          const int kcnt = min(64, ni - c * 64);
-          for (int x = tid; x < kcnt * 16; x += SP_NT) {
-            const int k = x >> 4, qq = x & 15;
-            const __nv_bfloat16* src = p.ut + static_cast<int64_t>(si[c * 64 + k]) * p.ld_ut + rb * 128 + qq * 8;
-            ptx::cp_async16(dst + ((k >> 3) * 2 + (qq >> 3)) * 1024 + (k & 7) * 128 + (((qq & 7) ^ (k & 7)) << 4),
-                            src);
-          }
-          ptx::cp_async_commit();
-        };
-        const int pre = min(SP_AHEAD, total);
-        for (int t = 0; t < pre; ++t) issue(t);
-        int t = 0;
-        for (int rb = 0; rb < p.nrb; ++rb) {
-          // V rows of this block's replicas for the tile's fibers (MN-major B of mode 2)
-          constexpr int VU = 1024 / SP_NT;
-          uint4 vreg[VU];
+      if (e_end == e_in) {  // empty fibers only
+        f = f_next;
+        e_in = e_next;
+        continue;
+      }
+      for (int t = tid; t <= nf; t += PL_NT)
+        tfp[t] = t == 0 ? 0 : static_cast<int32_t>((t == nf ? e_end : p.fiber_ptr[f + t]) - e_in);
+      // lookup pass: id of every nonzero -> li_g, (fiber, id) occupancy ->
+      // dup; an i without an id sets `miss` (and the pass stops early)
+      auto lookup = [&]() {
+        int fl = 0;
+        for_each_i<PL_NT, 2>(p.nz_i, e_in, e_end, [&](int n, const int* xs, const int32_t* ks) {
+          constexpr int B = 8;
+          uint32_t h[B];
+          int li[B];
 #pragma unroll
-          for (int u = 0; u < VU; ++u) {
-            const int x = tid + u * SP_NT, fl = x >> 4, qq = x & 15;
-            const int64_t col = static_cast<int64_t>(rb) * p.n2 + qq * 8;
-            vreg[u] = make_uint4(0, 0, 0, 0);
-            if (fl < nf && qq * 8 < p.n2 && col < p.ld_vtj)
-              vreg[u] = __ldg(reinterpret_cast<const uint4*>(p.vtj + static_cast<int64_t>(tfj[fl]) * p.ld_vtj + col));
+          for (int e = 0; e < B; ++e) {  // first probes in flight together
+            h[e] = sp_hash(ks[e]);
+            li[e] = e < n ? keys[h[e]] : 0;
           }
-          for (int c = 0; c < nch; ++c, ++t) {
-            const int allow = min(SP_AHEAD - 1, total - t - 1);
-            if (allow >= 2) ptx::cp_async_wait<2>();
-            else if (allow == 1) ptx::cp_async_wait<1>();
-            else ptx::cp_async_wait<0>();
-            ptx::fence_proxy_async_smem();
-            __syncthreads();
-            if (tid == 0) {
-              ptx::tc_fence_after();
-              const int slot = static_cast<int>((g + static_cast<uint32_t>(t)) % SP_NS);
-              const uint32_t a0 = ring_u + slot * UC_BYTES, b0 = xd_u + c * XD_CHUNK;
-              const int nk = c == nch - 1 ? k16_last : 4;
+          if (lds_volatile(&ovf)) return;
+          bool m = false;
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                if (kk < nk)
-                  ptx::mma_bf16(d1, ptx::sw128_mn_desc(a0 + kk * 4096, 1024, 2048), ptx::sw128_desc(b0 + kk * 32),
-                                idesc1, (c | kk) != 0);
-              ptx::mma_commit(&ms->mma_done[slot]);
-              if (c == nch - 1) ptx::mma_commit(&ms->d1_full);
+          for (int e = 0; e < B; ++e) {
+            if (e >= n) continue;
+            uint32_t hp = h[e];
+            int k2 = li[e];
+            while (k2 != ks[e] && k2 != -1) {
+              hp = (hp + 1) & (SP_HS - 1);
+              k2 = keys[hp];
             }
-            if (t + SP_AHEAD < total) issue(t + SP_AHEAD);
+            li[e] = k2 == -1 ? 0xFFFF : lis[hp];
+            m |= li[e] == 0xFFFF;
           }
-          // D1 -> bf16 A operand of mode 2 (row r, fibers contiguous)
-          ptx::mbar_wait(&ms->d1_full, n1 & 1);
-          ++n1;
-          ptx::tc_fence_after();
-          if (warp < 8) {
-            float v[32];
-            ptx::tmem_ld32(d1 + lane_addr + hh * 32, v);
-            ptx::tmem_wait_ld();
-            uint8_t* row = a2 + r * 128;
+          if (m) {
+            ovf = 1;  // here: a miss
+            return;
+          }
+          bool d = false;
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              const int q8 = hh * 4 + q4;
-              *reinterpret_cast<uint4*>(row + ((q8 ^ (r & 7)) << 4)) = ptx::pack8(v + q4 * 8, F16);
-            }
+          for (int e = 0; e < B; ++e) {
+            if (e >= n) continue;
+            while (tfp[fl + 1] <= xs[e]) ++fl;
+            p.li_g[e_in + xs[e]] = static_cast<uint16_t>(li[e]);
+            const int bit = fl * SP_NI + li[e];
+            d |= (atoms_or(&seen[bit >> 5], 1u << (bit & 31)) >> (bit & 31)) & 1u;
           }
-#pragma unroll
-          for (int u = 0; u < VU; ++u) {
-            const int x = tid + u * SP_NT, fl = x >> 4, qq = x & 15;
-            *reinterpret_cast<uint4*>(vg + ((fl >> 3) * 2 + (qq >> 3)) * 1024 + (fl & 7) * 128 +
-                                      (((qq & 7) ^ (fl & 7)) << 4)) = vreg[u];
-          }
-          ptx::fence_proxy_async_smem();
-          ptx::tc_fence_before();
-          __syncthreads();
-          if (tid == 0) {
-            ptx::tc_fence_after();
-            const int nk2 = (nf + 15) >> 4;
-            const uint32_t a0 = ptx::smem_u32(a2), b0 = ptx::smem_u32(vg);
-            for (int kk = 0; kk < nk2; ++kk)
-              ptx::mma_bf16(d2, ptx::sw128_desc(a0 + kk * 32), ptx::sw128_mn_desc(b0 + kk * 4096, 1024, 2048),
-                            idesc2, kk != 0);
-            ptx::mma_commit(&ms->d2_full);
-          }
-          ptx::mbar_wait(&ms->d2_full, n2c & 1);
-          ++n2c;
-          ptx::tc_fence_after();
-          // diagonal replica block of D2 -> Z (zeroed by the host; fire-and-forget reductions)
-          const int64_t prep = static_cast<int64_t>(rb) * rpb + p_local;
-          for (int cb = 0; cb < (warp < 8 ? half : 0); cb += 16) {
-            float v[16];
-            ptx::tmem_ld16(d2 + lane_addr + p_local * p.mpad + hh * half + cb, v);
-            ptx::tmem_wait_ld();
-            if (prep < p.vp) {
-              float* zp = p.z + ((prep * p.n_slices + s) * p.mpad + hh * half + cb) * p.lpad + l;
-#pragma unroll
-              for (int e = 0; e < 16; ++e) atomicAdd(zp + static_cast<int64_t>(e) * p.lpad, v[e]);
-            }
-          }
-          ptx::tc_fence_before();
-          __syncthreads();
+          if (d) dup = 1;
+        });
+      };
+      bool hit = false;
+      if (committed > 0) {  // a warm table usually holds all of the tile's i
+        for (int t = tid; t < SP_NF * SP_NI / 32; t += PL_NT) seen[t] = 0;
+        if (tid == 0) {
+          ovf = 0;
+          dup = 0;
         }
-        g += static_cast<uint32_t>(total);
+        __syncthreads();
+        lookup();
+        __syncthreads();
+        hit = lds_volatile(&ovf) == 0;
+        __syncthreads();
+      }
+      if (!hit) {
+        // claim slots for the new i (ids afterwards, in slot order)
+        if (tid == 0) ovf = 0;
+        __syncthreads();
+        for_each_i<PL_NT, 2>(p.nz_i, e_in, e_end, [&](int n, const int*, const int32_t* ks) {
+          constexpr int B = 8;
+          uint32_t h[B];
+          int k2[B];
+#pragma unroll
+          for (int e = 0; e < B; ++e) {
+            h[e] = sp_hash(ks[e]);
+            k2[e] = e < n ? keys[h[e]] : 0;
+          }
+          if (lds_volatile(&ovf)) return;
+#pragma unroll
+          for (int e = 0; e < B; ++e) {
+            if (e >= n || k2[e] == ks[e]) continue;
+            const int32_t key = ks[e];
+            uint32_t hp = h[e];
+            int old = k2[e];
+            for (;;) {
+              if (old == key) break;
+              if (old == -1) {
+                if (lds_volatile(&count) >= SP_NI) {  // bounds the claims: <= SP_NI + PL_NT < SP_HS slots
+                  ovf = 1;
+                  break;
+                }
+                old = atoms_cas(&keys[hp], -1, key);
+                if (old == -1) {
+                  if (atoms_add(&count, 1) >= SP_NI) ovf = 1;
+                  break;
+                }
+                continue;  // lost the race for this slot: look at what landed there
+              }
+              hp = (hp + 1) & (SP_HS - 1);
+              old = keys[hp];
+            }
+          }
+        });
+        __syncthreads();
+        if (lds_volatile(&ovf)) {
+          const bool fresh = committed == 0;
+          __syncthreads();
+          if (fresh) {  // too many distinct i even alone: fewer fibers
+            clear_table();
+            __syncthreads();
+            nt = max(1, nt >> 1);
+          } else {      // close the epoch and redo this tile on an empty table
+            close_epoch();
+            epoch0 = e_in;
+          }
+          continue;
+        }
+        // ids for the new keys, in slot order (thread t owns SP_HS / PL_NT slots)
+        {
+          constexpr int SPT = SP_HS / PL_NT;
+          const int lane = tid & 31, warp = tid >> 5;
+          int c = 0;
+#pragma unroll
+          for (int k = 0; k < SPT; ++k) c += keys[tid * SPT + k] != -1 && lis[tid * SPT + k] == 0xFFFF;
+          int incl = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          if (lane == 31) wsum[warp] = incl;
+          __syncthreads();
+          int base = incl - c + committed;
+          for (int w = 0; w < warp; ++w) base += wsum[w];
+#pragma unroll
+          for (int k = 0; k < SPT; ++k) {
+            const int key = keys[tid * SPT + k];
+            if (key != -1 && lis[tid * SPT + k] == 0xFFFF) {
+              lis[tid * SPT + k] = static_cast<uint16_t>(base);
+              idkey[base] = key;
+              ++base;
+            }
+          }
+        }
+        for (int t = tid; t < SP_NF * SP_NI / 32; t += PL_NT) seen[t] = 0;
+        if (tid == 0) {
+          ovf = 0;
+          dup = 0;
+        }
+        __syncthreads();
+        lookup();
+        __syncthreads();
+      }
+      committed = lds_volatile(&count);
+      if (tid == 0) {
+        const unsigned long long t = atomicAdd(p.counters + 1, 1ull);
+        if (static_cast<int64_t>(t) < p.max_tiles) {
+          SpTile d;
+          d.e0 = e_in;
+          d.f0 = f;
+          d.si0 = epoch0;
+          d.s = static_cast<int32_t>(s);
+          d.n = static_cast<int32_t>(e_end - e_in);
+          d.nf = nf;
+          d.ni = committed;
+          d.dup = dup;
+          p.tiles[t] = d;
+        }
       }
       f = f_next;
       e_in = e_next;
       nt = (f < fs1 && e_in != p.fiber_ptr[f]) ? 1 : min(SP_NF, nt * 2);
+    }
+    close_epoch();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor kernel: one CTA per SM takes planned tiles off a counter (any order:
+// the Z contributions are reductions). Per tile all warps scatter the values
+// into the dense tile Xd (plain stores; shared-memory CAS adds when the
+// planner saw duplicates), then the row blocks run on the roles below.
+template <bool F16>
+__global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* xd = sm;
+  uint8_t* ring = sm + OFF_RING;
+  uint8_t* a2 = sm + OFF_A2;
+  uint8_t* vg = sm + OFF_VG;
+  int32_t* si = reinterpret_cast<int32_t*>(sm + OFF_SI);
+  int32_t* tfp = reinterpret_cast<int32_t*>(sm + OFF_TFP);  // fiber starts, local offsets
+  int32_t* tfj = reinterpret_cast<int32_t*>(sm + OFF_TFJ);
+  SpMisc* ms = reinterpret_cast<SpMisc*>(sm + OFF_MISC);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < SP_NS; ++s) {
+      ptx::mbar_init(&ms->full[s], 192);
+      ptx::mbar_init(&ms->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&ms->vg_full[b], 192);
+      ptx::mbar_init(&ms->vg_empty[b], 1);
+      ptx::mbar_init(&ms->d1_full[b], 1);
+      ptx::mbar_init(&ms->d1_empty[b], 256);
+    }
+    ptx::mbar_init(&ms->a2_full, 256);
+    ptx::mbar_init(&ms->d2_full, 1);
+    ptx::mbar_init(&ms->d2_empty, 256);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 0) ptx::tmem_alloc(&ms->tmem_base, 256);
+  // stale operand bytes beyond a partial chunk must be finite (they multiply zeros)
+  for (int e = tid; e < (SP_NS * UC_BYTES + A2_BYTES + 2 * VG_BYTES) / 16; e += SP_NT)
+    reinterpret_cast<uint4*>(ring)[e] = make_uint4(0, 0, 0, 0);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = ms->tmem_base;
+  const uint32_t d1 = tmem, d2 = tmem + 128;
+  const uint32_t idesc1 = (ptx::idesc_bf16(128, SP_NF) | ptx::IDESC_A_MN) & ptx::idesc_fmt_mask(F16);
+  const uint32_t idesc2 = (ptx::idesc_bf16(128, p.n2) | ptx::IDESC_B_MN) & ptx::idesc_fmt_mask(F16);
+  const int q = warp & 3;
+  const int r = q * 32 + lane;  // row of the 128-row block == TMEM lane
+  const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+  const int p_local = r / p.lpad, l = r % p.lpad;
+  const int rpb = 128 / p.lpad;
+  const int half = p.mpad >> 1;
+  const uint32_t ring_u = ptx::smem_u32(ring), xd_u = ptx::smem_u32(xd);
+  const int64_t n_tiles = imin64(static_cast<int64_t>(*p.n_tiles), p.max_tiles);
+  uint32_t g = 0, rbs = 0;  // U chunk and row-block sequence numbers (barrier phases)
+
+  for (;;) {
+    if (tid == 0) ms->tile = static_cast<int64_t>(atomicAdd(p.counter, 1ull));
+    __syncthreads();
+    const int64_t tile = ms->tile;
+    if (tile >= n_tiles) break;
+    const SpTile T = p.tiles[tile];
+    const int64_t s = T.s, e0 = T.e0;
+    const int nf = T.nf, ni = T.ni, nnz = T.n;
+    for (int t = tid; t <= nf; t += SP_NT)
+      tfp[t] = t == 0 ? 0 : (t == nf ? nnz : static_cast<int32_t>(p.fiber_ptr[T.f0 + t] - e0));
+    for (int t = tid; t < nf; t += SP_NT) tfj[t] = p.fiber_j[T.f0 + t];
+    for (int t = tid; t < ni; t += SP_NT) si[t] = p.si_g[T.si0 + t];
+    const int nch = (ni + 63) >> 6;
+    for (int e = tid; e < nch * (XD_CHUNK / 16); e += SP_NT) reinterpret_cast<uint4*>(xd)[e] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    // 1. scatter: Xd[fiber][id] = value (K-major SWIZZLE_128B, 64-id chunks)
+    {
+      int fl = 0;  // fiber cursor: x only grows per thread
+      auto put = [&](int x, uint32_t li, float v) {
+        while (tfp[fl + 1] <= x) ++fl;
+        const uint32_t a = xd_u + (li >> 6) * XD_CHUNK + (fl >> 3) * 1024 + (fl & 7) * 128 +
+                           ((((li & 63) >> 3) ^ (fl & 7)) << 4) + (li & 7) * 2;
+        if (T.dup) {
+          atoms_add16<F16>(a, v);
+        } else {
+          const uint16_t b = F16 ? __half_as_ushort(__float2half_rn(v)) : __bfloat16_as_ushort(__float2bfloat16_rn(v));
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(b) : "memory");
+        }
+      };
+      const int64_t a0 = imin64(e0 + nnz, (e0 + 3) & ~int64_t(3));
+      const int64_t a1 = max(a0, (e0 + nnz) & ~int64_t(3));
+      if (e0 + tid < a0) put(tid, p.li_g[e0 + tid], __ldg(p.val + e0 + tid));
+      const uint2* vl = reinterpret_cast<const uint2*>(p.li_g + a0);
+      const float4* vv = reinterpret_cast<const float4*>(p.val + a0);
+      const int nv = static_cast<int>((a1 - a0) >> 2), xa = static_cast<int>(a0 - e0);
+      constexpr int U = 4;
+      for (int b = 0; b < nv; b += SP_NT * U) {
+        uint2 li4[U];
+        float4 v4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = b + u * SP_NT + tid;
+          if (idx < nv) {
+            li4[u] = __ldg(vl + idx);
+            v4[u] = __ldg(vv + idx);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = b + u * SP_NT + tid;
+          if (idx < nv) {
+            const int x = xa + idx * 4;
+            put(x, li4[u].x & 0xFFFF, v4[u].x);
+            put(x + 1, li4[u].x >> 16, v4[u].y);
+            put(x + 2, li4[u].y & 0xFFFF, v4[u].z);
+            put(x + 3, li4[u].y >> 16, v4[u].w);
+          }
+        }
+      }
+      if (a1 + tid < e0 + nnz) put(static_cast<int>(a1 + tid - e0), p.li_g[a1 + tid], __ldg(p.val + a1 + tid));
+    }
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+    // 2-3. row blocks: roles inside the CTA, hand-offs on mbarriers only
+    //   warps 2-7   : producers (cp.async gathers of U columns and V rows)
+    //   warp 0 lane 0: MMA issuer (mode 1 of rb, then mode 2 of rb - 1)
+    //   warps 8-15  : epilogue (D1 -> bf16 A2, D2 diagonal -> Z)
+    {
+        const int k16_last = (ni - (nch - 1) * 64 + 15) >> 4;
+        const int nk2 = (nf + 15) >> 4;
+        const int nmg2 = (p.n2 + 63) >> 6;
+        if (warp >= 2 && warp < 8) {
+          // producers (192 threads): 16-byte cp.async gathers of the U chunks
+          // (and, with each row block's first chunk, its V rows) into the
+          // MN-major SW128 stages, SP_AHEAD commit groups in flight; each
+          // thread arrives on a stage's barrier once its own copies landed
+          constexpr int NPT = 192;
+          const int pt = tid - 64;
+          uint32_t gs = g;
+          int pending = 0;  // committed groups whose barriers are not arrived yet
+          uint32_t q_slot[SP_AHEAD + 1];
+          int q_vs[SP_AHEAD + 1];
+          auto retire = [&]() {  // oldest pending group has landed: publish it
+            ptx::fence_proxy_async_smem();
+            ptx::mbar_arrive(&ms->full[q_slot[0]]);
+            if (q_vs[0] >= 0) ptx::mbar_arrive(&ms->vg_full[q_vs[0]]);
+#pragma unroll
+            for (int e = 0; e < SP_AHEAD; ++e) {
+              q_slot[e] = q_slot[e + 1];
+              q_vs[e] = q_vs[e + 1];
+            }
+            --pending;
+          };
+          for (int rb = 0; rb < p.nrb; ++rb) {
+            const uint32_t rs = rbs + rb, vs = rs & 1, vuse = rs >> 1;
+            for (int c = 0; c < nch; ++c, ++gs) {
+              const int slot = static_cast<int>(gs % SP_NS);
+              ptx::mbar_wait(&ms->empty[slot], ((gs / SP_NS) & 1) ^ 1);
+              uint8_t* udst = ring + slot * UC_BYTES;
+              const int kcnt = min(64, ni - c * 64);
+              for (int x = pt; x < kcnt * 16; x += NPT) {
+                const int k = x >> 4, qq = x & 15;
+                ptx::cp_async16(udst + ((k >> 3) * 2 + (qq >> 3)) * 1024 + (k & 7) * 128 + (((qq & 7) ^ (k & 7)) << 4),
+                                p.ut + static_cast<int64_t>(si[c * 64 + k]) * p.ld_ut + rb * 128 + qq * 8);
+              }
+              int vflag_slot = -1;
+              if (c == 0) {
+                // the MMA may need our unpublished chunks before it frees this V buffer
+                if (!ptx::mbar_test(&ms->vg_empty[vs], (vuse & 1) ^ 1)) {
+                  ptx::cp_async_wait<0>();
+                  while (pending > 0) retire();
+                  ptx::mbar_wait(&ms->vg_empty[vs], (vuse & 1) ^ 1);
+                }
+                uint8_t* vdst = vg + vs * VG_BYTES;
+                for (int x = pt; x < nf * 16; x += NPT) {
+                  const int fl = x >> 4, qq = x & 15;
+                  const int64_t col = static_cast<int64_t>(rb) * p.n2 + qq * 8;
+                  uint8_t* d = vdst + ((fl >> 3) * 2 + (qq >> 3)) * 1024 + (fl & 7) * 128 + (((qq & 7) ^ (fl & 7)) << 4);
+                  if (qq * 8 < p.n2 && col < p.ld_vtj)
+                    ptx::cp_async16(d, p.vtj + static_cast<int64_t>(tfj[fl]) * p.ld_vtj + col);
+                  else
+                    *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
+                }
+                vflag_slot = static_cast<int>(vs);
+              }
+              ptx::cp_async_commit();
+              q_slot[pending] = static_cast<uint32_t>(slot);
+              q_vs[pending] = vflag_slot;
+              ++pending;
+              if (pending == SP_AHEAD) {
+                ptx::cp_async_wait<SP_AHEAD - 1>();
+                retire();
+              }
+            }
+          }
+          ptx::cp_async_wait<0>();
+          while (pending > 0) retire();
+        } else if (warp == 0 && lane == 0) {
+          uint32_t gs = g;
+          auto mode2 = [&](int rb) {
+            const uint32_t rs = rbs + rb, vs = rs & 1;
+            ptx::mbar_wait(&ms->a2_full, rs & 1);
+            ptx::mbar_wait(&ms->vg_full[vs], (rs >> 1) & 1);
+            ptx::mbar_wait(&ms->d2_empty, (rs & 1) ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t a0 = ptx::smem_u32(a2), b0 = ptx::smem_u32(vg + vs * VG_BYTES);
+            for (int kk = 0; kk < nk2; ++kk)
+              ptx::mma_bf16(d2, ptx::sw128_desc(a0 + kk * 32), ptx::sw128_mn_desc(b0 + kk * 4096, 1024, 2048),
+                            idesc2, kk != 0);
+            ptx::mma_commit(&ms->d2_full);
+            ptx::mma_commit(&ms->vg_empty[vs]);
+          };
+          for (int rb = 0; rb < p.nrb; ++rb) {
+            const uint32_t rs = rbs + rb, b = rs & 1, use = rs >> 1;
+            ptx::mbar_wait(&ms->d1_empty[b], (use & 1) ^ 1);
+            ptx::tc_fence_after();
+            for (int c = 0; c < nch; ++c, ++gs) {
+              const int slot = static_cast<int>(gs % SP_NS);
+              ptx::mbar_wait(&ms->full[slot], (gs / SP_NS) & 1);
+              ptx::tc_fence_after();
+              const uint32_t a0 = ring_u + slot * UC_BYTES, b0 = xd_u + c * XD_CHUNK;
+              const int nk = c == nch - 1 ? k16_last : 4;
+              for (int kk = 0; kk < nk; ++kk)
+                ptx::mma_bf16(d1 + b * 64, ptx::sw128_mn_desc(a0 + kk * 4096, 1024, 2048),
+                              ptx::sw128_desc(b0 + kk * 32), idesc1, (c | kk) != 0);
+              ptx::mma_commit(&ms->empty[slot]);
+            }
+            ptx::mma_commit(&ms->d1_full[b]);
+            if (rb > 0) mode2(rb - 1);
+          }
+          mode2(p.nrb - 1);
+        } else if (warp >= 8) {
+          const int hh = (warp - 8) >> 2;
+          for (int rb = 0; rb < p.nrb; ++rb) {
+            const uint32_t rs = rbs + rb, b = rs & 1;
+            ptx::mbar_wait_sleep(&ms->d1_full[b], (rs >> 1) & 1);
+            ptx::tc_fence_after();
+            {
+              float v[32];
+              ptx::tmem_ld32(d1 + b * 64 + lane_addr + hh * 32, v);
+              ptx::tmem_wait_ld();
+              uint8_t* row = a2 + r * 128;
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                const int q8 = hh * 4 + q4;
+                *reinterpret_cast<uint4*>(row + ((q8 ^ (r & 7)) << 4)) = ptx::pack8(v + q4 * 8, F16);
+              }
+            }
+            ptx::fence_proxy_async_smem();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&ms->a2_full);
+            ptx::mbar_arrive(&ms->d1_empty[b]);
+            ptx::mbar_wait_sleep(&ms->d2_full, rs & 1);
+            ptx::tc_fence_after();
+            // diagonal replica block of D2 -> Z (zeroed by the host; fire-and-forget reductions)
+            const int64_t prep = static_cast<int64_t>(rb) * rpb + p_local;
+            for (int cb = 0; cb < half; cb += 16) {
+              float v[16];
+              ptx::tmem_ld16(d2 + lane_addr + p_local * p.mpad + hh * half + cb, v);
+              ptx::tmem_wait_ld();
+              if (prep < p.vp) {
+                float* zp = p.z + ((prep * p.n_slices + s) * p.mpad + hh * half + cb) * p.lpad + l;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) atomicAdd(zp + static_cast<int64_t>(e) * p.lpad, v[e]);
+              }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&ms->d2_empty);
+          }
+        }
+        g += static_cast<uint32_t>(p.nrb * nch);
+        rbs += static_cast<uint32_t>(p.nrb);
+        __syncthreads();
     }
   }
   ptx::tc_fence_before();
@@ -596,20 +778,48 @@ bool Plan::sparse_tc_ok() const {
 
 // CSF (slices -> fibers -> nonzeros, already validated, on the device) -> Z
 // through the tensor-core tile kernel, then mode 3 over the slices.
-void Plan::sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* slice_ptr, const int64_t* fiber_ptr,
-                     const int32_t* fiber_j, const int32_t* nz_i, const float* val, float* ydev, bool accumulate,
-                     cudaStream_t s) {
+void Plan::sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* slice_ptr, int64_t n_fibers,
+                     const int64_t* fiber_ptr, const int32_t* fiber_j, int64_t nnz, const int32_t* nz_i,
+                     const float* val, float* ydev, bool accumulate, cudaStream_t s) {
   const int64_t plrows = vP * lpad;
   DevBuf<float> z(static_cast<size_t>(vP * n_slices * mpad * lpad), s);
-  z.zero();  // the kernel adds every tile's contribution (and skips empty slices)
-  DevBuf<unsigned long long> ctr(1, s);
+  z.zero();  // the tensor kernel adds every tile's contribution (empty slices stay zero)
+  // 1. plan the tiles (every tile holds >= 1 nonzero and is either whole
+  //    fibers or a piece of <= 512 nonzeros of one fiber)
+  const int64_t max_tiles = n_fibers + nnz / SP_NI + 1;
+  DevBuf<int32_t> si_g(static_cast<size_t>(nnz), s);
+  DevBuf<uint16_t> li_g(static_cast<size_t>(nnz) + 8, s);
+  DevBuf<SpTile> tiles(static_cast<size_t>(max_tiles), s);
+  DevBuf<unsigned long long> ctr(3, s);
   ctr.zero();
+  SpPlanParams pp{};
+  pp.slice_ptr = slice_ptr;
+  pp.fiber_ptr = fiber_ptr;
+  pp.nz_i = nz_i;
+  pp.n_slices = n_slices;
+  pp.si_g = si_g.ptr;
+  pp.li_g = li_g.ptr;
+  pp.tiles = tiles.ptr;
+  pp.max_tiles = max_tiles;
+  pp.counters = ctr.ptr;
+  {
+    int per_sm = 1;
+    XCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sparse_plan_kernel, PL_NT, 0));
+    const int grid = static_cast<int>(std::min<int64_t>(n_slices, static_cast<int64_t>(sm_count()) * std::max(1, per_sm)));
+    sparse_plan_kernel<<<grid, PL_NT, 0, s>>>(pp);
+    XLAUNCH_CHECK();
+  }
+  // 2. tensor-core tiles
   SpTcParams prm{};
-  prm.slice_ptr = slice_ptr;
   prm.fiber_ptr = fiber_ptr;
   prm.fiber_j = fiber_j;
-  prm.nz_i = nz_i;
   prm.val = val;
+  prm.si_g = si_g.ptr;
+  prm.li_g = li_g.ptr;
+  prm.tiles = tiles.ptr;
+  prm.n_tiles = ctr.ptr + 1;
+  prm.max_tiles = max_tiles;
+  prm.counter = ctr.ptr + 2;
   prm.n_slices = n_slices;
   prm.ut = ut.ptr;
   prm.ld_ut = (plrows + 255) / 256 * 256;
@@ -621,11 +831,9 @@ void Plan::sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* sl
   prm.n2 = static_cast<int>((128 / lpad) * mpad);
   prm.vp = vP;
   prm.z = z.ptr;
-  prm.counter = ctr.ptr;
   auto launch = [&](auto kern) {
     XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP_SMEM));
-    const int grid = static_cast<int>(std::min<int64_t>(n_slices, sm_count()));
-    kern<<<grid, SP_NT, SP_SMEM, s>>>(prm);
+    kern<<<sm_count(), SP_NT, SP_SMEM, s>>>(prm);
   };
   if (fp16()) launch(sparse_tc_kernel<true>);
   else launch(sparse_tc_kernel<false>);
@@ -687,7 +895,7 @@ void Plan::sparse_tc_sorted(const uint64_t* skeys, const uint64_t* spay, const i
     ni = bi.ptr;
     nv = bv.ptr;
   }
-  sparse_tc(kd, uk.ptr, sptr.ptr, fptr.ptr, fj.ptr, ni, nv, ydev, accumulate, s);
+  sparse_tc(kd, uk.ptr, sptr.ptr, nf, fptr.ptr, fj.ptr, nnz, ni, nv, ydev, accumulate, s);
 }
 
 }  // namespace xtsg
