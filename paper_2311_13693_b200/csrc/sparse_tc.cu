@@ -51,13 +51,15 @@ constexpr int PL_NT = 256;   // planner: 8 warps, several CTAs per SM
 constexpr int SP_NF = 64;    // fibers per tile (mode-1 UMMA N, mode-2 K)
 constexpr int SP_NI = 512;   // distinct i per tile (mode-1 K)
 constexpr int SP_HS = 2048;  // planner hash slots (<= SP_NI + PL_NT claims)
-constexpr int SP_NS = 4;     // U gather ring slots
-constexpr int SP_AHEAD = 3;  // cp.async groups in flight per producer
+constexpr int SP_NS = 5;     // U gather ring slots
+constexpr int SP_AHEAD = 4;  // cp.async groups in flight per producer
+constexpr int SP_NV = 3;     // V-row buffers: the producer never waits on the mode-2 MMA it feeds
+constexpr int SC_NT = 320;   // scatter team: warps 0, 1, 8-15 (the producers gather meanwhile)
 constexpr int XD_CHUNK = SP_NF * 128;              // 64 fibers x 64 i, 8 KB
 constexpr int XD_BYTES = (SP_NI / 64) * XD_CHUNK;  // 64 KB
 constexpr int UC_BYTES = 128 * 64 * 2;             // 128 rows x 64 i, 16 KB
 constexpr int A2_BYTES = 128 * 128;                // 128 rows x 64 fibers
-constexpr int VG_BYTES = 128 * 64 * 2;             // 128 (p, m) x 64 fibers (x2 buffers)
+constexpr int VG_BYTES = 128 * 64 * 2;             // 128 (p, m) x 64 fibers (x SP_NV buffers)
 
 // one planned tile: fibers [f0, f0 + nf) of slice s, nonzeros [e0, e0 + n)
 // (a piece of one fiber when nf == 1 and the fiber is longer), local ids
@@ -69,9 +71,10 @@ struct SpTile {
 
 struct SpMisc {
   uint64_t full[SP_NS], empty[SP_NS];  // U gather ring
-  uint64_t vg_full[2], vg_empty[2];    // V rows (mode-2 B), double-buffered
+  uint64_t vg_full[SP_NV], vg_empty[SP_NV];  // V rows (mode-2 B)
   uint64_t d1_full[2], d1_empty[2];    // mode-1 accumulator (TMEM, double-buffered)
   uint64_t a2_full, d2_full, d2_empty;
+  uint64_t xd_full;                    // the tile's dense X is in shared memory
   uint32_t tmem_base;
   int64_t tile;
   SpTile t;
@@ -80,7 +83,7 @@ struct SpMisc {
 constexpr int OFF_RING = XD_BYTES;
 constexpr int OFF_A2 = OFF_RING + SP_NS * UC_BYTES;
 constexpr int OFF_VG = OFF_A2 + A2_BYTES;
-constexpr int OFF_SI = OFF_VG + 2 * VG_BYTES;
+constexpr int OFF_SI = OFF_VG + SP_NV * VG_BYTES;
 constexpr int OFF_TFP = OFF_SI + SP_NI * 4;
 constexpr int OFF_TFJ = OFF_TFP + (SP_NF + 2) * 4;
 constexpr int OFF_MISC = OFF_TFJ + SP_NF * 4;
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(PL_NT, 4) sparse_plan_kernel(const SpPlanParam
           for (int e = 0; e < B; ++e) {
             if (e >= n) continue;
             while (tfp[fl + 1] <= xs[e]) ++fl;
-            p.li_g[e_in + xs[e]] = static_cast<uint16_t>(li[e]);
+            p.li_g[e_in + xs[e]] = static_cast<uint16_t>((fl << 9) | li[e]);  // fiber (6 bits) | id (9 bits)
             const int bit = fl * SP_NI + li[e];
             d |= (atoms_or(&seen[bit >> 5], 1u << (bit & 31)) >> (bit & 31)) & 1u;
           }
@@ -479,20 +482,23 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
       ptx::mbar_init(&ms->full[s], 192);
       ptx::mbar_init(&ms->empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < SP_NV; ++b) {
       ptx::mbar_init(&ms->vg_full[b], 192);
       ptx::mbar_init(&ms->vg_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&ms->d1_full[b], 1);
       ptx::mbar_init(&ms->d1_empty[b], 256);
     }
     ptx::mbar_init(&ms->a2_full, 256);
     ptx::mbar_init(&ms->d2_full, 1);
     ptx::mbar_init(&ms->d2_empty, 256);
+    ptx::mbar_init(&ms->xd_full, SC_NT);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc(&ms->tmem_base, 256);
   // stale operand bytes beyond a partial chunk must be finite (they multiply zeros)
-  for (int e = tid; e < (SP_NS * UC_BYTES + A2_BYTES + 2 * VG_BYTES) / 16; e += SP_NT)
+  for (int e = tid; e < (SP_NS * UC_BYTES + A2_BYTES + SP_NV * VG_BYTES) / 16; e += SP_NT)
     reinterpret_cast<uint4*>(ring)[e] = make_uint4(0, 0, 0, 0);
   ptx::tc_fence_before();
   __syncthreads();
@@ -511,12 +517,20 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
   const int64_t n_tiles = imin64(static_cast<int64_t>(*p.n_tiles), p.max_tiles);
   uint32_t g = 0, rbs = 0;  // U chunk and row-block sequence numbers (barrier phases)
 
-  for (;;) {
-    if (tid == 0) ms->tile = static_cast<int64_t>(atomicAdd(p.counter, 1ull));
-    __syncthreads();
-    const int64_t tile = ms->tile;
+  const bool scatterer = warp < 2 || warp >= 8;
+  const int st = warp < 2 ? tid : tid - 192;  // rank in the scatter team
+  for (int64_t it = 0;; ++it) {
+    // static tile order (the planner's tiles are alike in size): the next
+    // tile of this CTA is known, so its nonzeros are pulled into L2 now
+    const int64_t tile = blockIdx.x + it * gridDim.x;
     if (tile >= n_tiles) break;
     const SpTile T = p.tiles[tile];
+    if (tid == 0 && tile + gridDim.x < n_tiles) {
+      const SpTile Tn = p.tiles[tile + gridDim.x];
+      const int64_t a = Tn.e0 & ~int64_t(7), b = (Tn.e0 + Tn.n + 7) & ~int64_t(7);
+      ptx::bulk_prefetch_l2(p.li_g + a, static_cast<uint32_t>(imin64((b - a) * 2, 1 << 20)));
+      ptx::bulk_prefetch_l2(p.val + a, static_cast<uint32_t>(imin64((b - a) * 4, 1 << 20)));
+    }
     const int64_t s = T.s, e0 = T.e0;
     const int nf = T.nf, ni = T.ni, nnz = T.n;
     for (int t = tid; t <= nf; t += SP_NT)
@@ -526,33 +540,34 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
     const int nch = (ni + 63) >> 6;
     for (int e = tid; e < nch * (XD_CHUNK / 16); e += SP_NT) reinterpret_cast<uint4*>(xd)[e] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    // 1. scatter: Xd[fiber][id] = value (K-major SWIZZLE_128B, 64-id chunks)
-    {
-      int fl = 0;  // fiber cursor: x only grows per thread
-      auto put = [&](int x, uint32_t li, float v) {
-        while (tfp[fl + 1] <= x) ++fl;
+    // 1. scatter (warps 0, 1, 8-15; the producers start gathering U meanwhile):
+    //    Xd[fiber][id] = value (K-major SWIZZLE_128B, 64-id chunks)
+    if (scatterer) {
+      // li_g packs the nonzero's tile fiber (bits 9-14) and local id (bits 0-8)
+      auto put = [&](int, uint32_t code, float v) {
+        const uint32_t fl = code >> 9, li = code & 511u;
         const uint32_t a = xd_u + (li >> 6) * XD_CHUNK + (fl >> 3) * 1024 + (fl & 7) * 128 +
                            ((((li & 63) >> 3) ^ (fl & 7)) << 4) + (li & 7) * 2;
         if (T.dup) {
           atoms_add16<F16>(a, v);
         } else {
           const uint16_t b = F16 ? __half_as_ushort(__float2half_rn(v)) : __bfloat16_as_ushort(__float2bfloat16_rn(v));
-          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(b) : "memory");
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(b));
         }
       };
       const int64_t a0 = imin64(e0 + nnz, (e0 + 3) & ~int64_t(3));
       const int64_t a1 = max(a0, (e0 + nnz) & ~int64_t(3));
-      if (e0 + tid < a0) put(tid, p.li_g[e0 + tid], __ldg(p.val + e0 + tid));
+      if (e0 + st < a0) put(st, p.li_g[e0 + st], __ldg(p.val + e0 + st));
       const uint2* vl = reinterpret_cast<const uint2*>(p.li_g + a0);
       const float4* vv = reinterpret_cast<const float4*>(p.val + a0);
       const int nv = static_cast<int>((a1 - a0) >> 2), xa = static_cast<int>(a0 - e0);
-      constexpr int U = 4;
-      for (int b = 0; b < nv; b += SP_NT * U) {
+      constexpr int U = 8;
+      for (int b = 0; b < nv; b += SC_NT * U) {
         uint2 li4[U];
         float4 v4[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int idx = b + u * SP_NT + tid;
+          const int idx = b + u * SC_NT + st;
           if (idx < nv) {
             li4[u] = __ldg(vl + idx);
             v4[u] = __ldg(vv + idx);
@@ -560,7 +575,7 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int idx = b + u * SP_NT + tid;
+          const int idx = b + u * SC_NT + st;
           if (idx < nv) {
             const int x = xa + idx * 4;
             put(x, li4[u].x & 0xFFFF, v4[u].x);
@@ -570,10 +585,10 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
           }
         }
       }
-      if (a1 + tid < e0 + nnz) put(static_cast<int>(a1 + tid - e0), p.li_g[a1 + tid], __ldg(p.val + a1 + tid));
+      if (a1 + st < e0 + nnz) put(static_cast<int>(a1 + st - e0), p.li_g[a1 + st], __ldg(p.val + a1 + st));
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(&ms->xd_full);
     }
-    ptx::fence_proxy_async_smem();
-    __syncthreads();
     // 2-3. row blocks: roles inside the CTA, hand-offs on mbarriers only
     //   warps 2-7   : producers (cp.async gathers of U columns and V rows)
     //   warp 0 lane 0: MMA issuer (mode 1 of rb, then mode 2 of rb - 1)
@@ -605,16 +620,20 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
             --pending;
           };
           for (int rb = 0; rb < p.nrb; ++rb) {
-            const uint32_t rs = rbs + rb, vs = rs & 1, vuse = rs >> 1;
+            const uint32_t rs = rbs + rb, vs = rs % SP_NV, vuse = rs / SP_NV;
             for (int c = 0; c < nch; ++c, ++gs) {
               const int slot = static_cast<int>(gs % SP_NS);
               ptx::mbar_wait(&ms->empty[slot], ((gs / SP_NS) & 1) ^ 1);
               uint8_t* udst = ring + slot * UC_BYTES;
               const int kcnt = min(64, ni - c * 64);
-              for (int x = pt; x < kcnt * 16; x += NPT) {
-                const int k = x >> 4, qq = x & 15;
-                ptx::cp_async16(udst + ((k >> 3) * 2 + (qq >> 3)) * 1024 + (k & 7) * 128 + (((qq & 7) ^ (k & 7)) << 4),
-                                p.ut + static_cast<int64_t>(si[c * 64 + k]) * p.ld_ut + rb * 128 + qq * 8);
+              // one task = 64 contiguous bytes (32 rows) of one gathered column
+              for (int x = pt; x < kcnt * 4; x += NPT) {
+                const int k = x >> 2, q4 = x & 3;
+                const __nv_bfloat16* src = p.ut + static_cast<int64_t>(si[c * 64 + k]) * p.ld_ut + rb * 128 + q4 * 32;
+                uint8_t* drow = udst + ((k >> 3) * 2 + (q4 >> 1)) * 1024 + (k & 7) * 128;
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  ptx::cp_async16(drow + ((((q4 & 1) * 4 + e) ^ (k & 7)) << 4), src + e * 8);
               }
               int vflag_slot = -1;
               if (c == 0) {
@@ -625,14 +644,18 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
                   ptx::mbar_wait(&ms->vg_empty[vs], (vuse & 1) ^ 1);
                 }
                 uint8_t* vdst = vg + vs * VG_BYTES;
-                for (int x = pt; x < nf * 16; x += NPT) {
-                  const int fl = x >> 4, qq = x & 15;
-                  const int64_t col = static_cast<int64_t>(rb) * p.n2 + qq * 8;
-                  uint8_t* d = vdst + ((fl >> 3) * 2 + (qq >> 3)) * 1024 + (fl & 7) * 128 + (((qq & 7) ^ (fl & 7)) << 4);
-                  if (qq * 8 < p.n2 && col < p.ld_vtj)
-                    ptx::cp_async16(d, p.vtj + static_cast<int64_t>(tfj[fl]) * p.ld_vtj + col);
-                  else
-                    *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
+                for (int x = pt; x < nf * 4; x += NPT) {
+                  const int fl = x >> 2, q4 = x & 3;
+                  const __nv_bfloat16* vrow = p.vtj + static_cast<int64_t>(tfj[fl]) * p.ld_vtj;
+                  uint8_t* drow = vdst + ((fl >> 3) * 2 + (q4 >> 1)) * 1024 + (fl & 7) * 128;
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const int qq = q4 * 4 + e;
+                    const int64_t col = static_cast<int64_t>(rb) * p.n2 + qq * 8;
+                    uint8_t* d = drow + (((qq & 7) ^ (fl & 7)) << 4);
+                    if (qq * 8 < p.n2 && col < p.ld_vtj) ptx::cp_async16(d, vrow + col);
+                    else *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
+                  }
                 }
                 vflag_slot = static_cast<int>(vs);
               }
@@ -650,10 +673,11 @@ __global__ void __launch_bounds__(SP_NT, 1) sparse_tc_kernel(const SpTcParams p)
           while (pending > 0) retire();
         } else if (warp == 0 && lane == 0) {
           uint32_t gs = g;
+          ptx::mbar_wait(&ms->xd_full, static_cast<uint32_t>(it) & 1);
           auto mode2 = [&](int rb) {
-            const uint32_t rs = rbs + rb, vs = rs & 1;
+            const uint32_t rs = rbs + rb, vs = rs % SP_NV;
             ptx::mbar_wait(&ms->a2_full, rs & 1);
-            ptx::mbar_wait(&ms->vg_full[vs], (rs >> 1) & 1);
+            ptx::mbar_wait(&ms->vg_full[vs], (rs / SP_NV) & 1);
             ptx::mbar_wait(&ms->d2_empty, (rs & 1) ^ 1);
             ptx::tc_fence_after();
             const uint32_t a0 = ptx::smem_u32(a2), b0 = ptx::smem_u32(vg + vs * VG_BYTES);
