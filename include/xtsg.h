@@ -123,6 +123,17 @@ int32_t xtsg_blocked_begin(const int64_t dims[3], const int64_t block[3], int64_
                            const double* w, int32_t deterministic, xtsg_blocked** out);
 int32_t xtsg_blocked_push(xtsg_blocked* h, const int64_t cell[3], const int64_t shape[3],
                           const double* data);
+/* A region of whole cells at once: offset/shape in elements, aligned to the
+ * grid's cells (the region's end may be the tensor's ragged edge); data
+ * column-major over the region. Marks every covered cell as seen (duplicates
+ * -> XTSG_E_DATA). deterministic=0 compresses the region like one block (its
+ * cells' contributions summed in fp64, equal to the per-cell sum up to
+ * rounding). The facade pushes an untouched
+ * in-memory block source (make_memory_block_source, compression.cpp:256-278)
+ * as one region: the tensor goes to the device once, without the per-block
+ * host copies. */
+int32_t xtsg_blocked_push_region(xtsg_blocked* h, const int64_t offset[3], const int64_t shape[3],
+                                 const double* data);
 int32_t xtsg_blocked_finish(xtsg_blocked* h, double* y);
 void xtsg_blocked_destroy(xtsg_blocked* h);
 

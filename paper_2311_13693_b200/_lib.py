@@ -130,6 +130,7 @@ _SIGS = {
     "xtsg_comp_naive_half": (_I32, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
     "xtsg_blocked_begin": (_I32, [_P, _P, _I64, _P, _P, _P, _P, _I32, _P]),
     "xtsg_blocked_push": (_I32, [_P, _P, _P, _P]),
+    "xtsg_blocked_push_region": (_I32, [_P, _P, _P, _P]),
     "xtsg_blocked_finish": (_I32, [_P, _P]),
     "xtsg_blocked_destroy": (None, [_P]),
     "xtsg_plan_create": (_I32, [_P, _P]),

@@ -201,8 +201,11 @@ def comp_from_factors(factors, u, v, w) -> np.ndarray:
     return y
 
 
-def comp_blocked(dims, block, source: Iterable, ensemble: Ensemble, deterministic: bool = True):
-    """compression.cpp:332-404. ``source`` yields (cell, block_tensor) records."""
+def comp_blocked(dims, block, source: Iterable, ensemble: Ensemble, deterministic: bool = True,
+                 regions: Iterable = ()):
+    """compression.cpp:332-404. ``source`` yields (cell, block_tensor) records;
+    ``regions`` are (element offset, tensor) pieces of whole cells pushed first
+    (xtsg_blocked_push_region, deterministic mode)."""
     dims, block = _arr3(dims), _arr3(block)
     P = ensemble.count
     red = _arr3([ensemble.u[0].shape[0], ensemble.v[0].shape[0], ensemble.w[0].shape[0]])
@@ -217,6 +220,9 @@ def comp_blocked(dims, block, source: Iterable, ensemble: Ensemble, deterministi
     check(lib.xtsg_blocked_begin(ptr(dims), ptr(block), P, ptr(red), ptr(u), ptr(v), ptr(w),
                                  1 if deterministic else 0, C.byref(h)))
     try:
+        for off, data in regions:
+            data = _f64(data)
+            check(lib.xtsg_blocked_push_region(h, ptr(_arr3(off)), ptr(_arr3(data.shape)), ptr(data)))
         for cell, data in source:
             data = _f64(data)
             check(lib.xtsg_blocked_push(h, ptr(_arr3(cell)), ptr(_arr3(data.shape)), ptr(data)))

@@ -385,6 +385,50 @@ int32_t xtsg_blocked_push(xtsg_blocked* h, const int64_t cell[3], const int64_t 
   });
 }
 
+int32_t xtsg_blocked_push_region(xtsg_blocked* h, const int64_t offset[3], const int64_t shape[3],
+                                 const double* data) {
+  return guard([&] {
+    int64_t c0[3], c1[3];
+    for (int m = 0; m < 3; ++m) {
+      const int64_t end = offset[m] + shape[m];
+      if (offset[m] < 0 || shape[m] < 1 || end > h->dims[m]) data_error("comp_blocked: region outside the tensor");
+      if (offset[m] % h->block[m] || (end % h->block[m] && end != h->dims[m]))
+        data_error("comp_blocked: region not aligned to the block grid");
+      c0[m] = offset[m] / h->block[m];
+      c1[m] = ceil_div(end, h->block[m]);
+    }
+    for (int64_t k = c0[2]; k < c1[2]; ++k)
+      for (int64_t j = c0[1]; j < c1[1]; ++j)
+        for (int64_t i = c0[0]; i < c1[0]; ++i) {
+          const int64_t linear = i + h->cells[0] * (j + h->cells[1] * k);
+          if (h->seen[static_cast<size_t>(linear)])
+            data_error("comp_blocked: duplicate block for cell " + std::to_string(linear));
+          h->seen[static_cast<size_t>(linear)] = 1;
+          ++h->seen_count;
+        }
+    const size_t bsz = static_cast<size_t>(shape[0] * shape[1] * shape[2]);
+    if (!h->deterministic) {
+      // fast mode: the region is compressed like one block (the sum of its
+      // cells' contributions, fp64 accumulators)
+      InView<double> blk(data, bsz, h->st);
+      const int64_t L = h->red[0], M = h->red[1], N = h->red[2];
+      for (int64_t p = 0; p < h->count; ++p)
+        comp_f64_dev(blk.dev, shape[0], shape[1], shape[2], h->u.ptr + p * L * h->dims[0] + offset[0] * L, L, L,
+                     h->v.ptr + p * M * h->dims[1] + offset[1] * M, M, M,
+                     h->w.ptr + p * N * h->dims[2] + offset[2] * N, N, N, h->acc.ptr + p * L * M * N, 1.0, h->st);
+    } else if (shape[0] == h->dims[0] && shape[1] == h->dims[1] && shape[2] == h->dims[2]) {
+      XCUDA(cudaMemcpyAsync(h->assembled.ptr, data, bsz * sizeof(double), cudaMemcpyDefault, h->st));
+    } else {
+      InView<double> blk(data, bsz, h->st);
+      const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(bsz), 256), 4096));
+      scatter_block_kernel<<<blocks, 256, 0, h->st>>>(blk.dev, shape[0], shape[1], shape[2], h->assembled.ptr,
+                                                       h->dims[0], h->dims[1], offset[0], offset[1], offset[2]);
+      XLAUNCH_CHECK();
+    }
+    XCUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
 int32_t xtsg_blocked_finish(xtsg_blocked* h, double* y) {
   return guard([&] {
     const int64_t total = h->cells[0] * h->cells[1] * h->cells[2];

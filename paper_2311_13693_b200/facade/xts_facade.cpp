@@ -9,6 +9,11 @@
 // into the reference's exception types with their payloads (errors.hpp:10-59).
 // Value semantics are kept (results returned by value, inputs by const&).
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
+#include <optional>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -216,11 +221,15 @@ index_t BlockGrid::linear_cell(const std::array<index_t, 3>& cell) const {
   return cell[0] + cells(1) * (cell[1] + cells(2) * cell[2]);
 }
 
-BlockSource make_memory_block_source(const Tensor3& t, const BlockGrid& grid) {
-  if (t.n1 != grid.n1 || t.n2 != grid.n2 || t.n3 != grid.n3)
-    throw UsageError("make_memory_block_source: grid does not match tensor dims");
-  auto next = std::make_shared<index_t>(0);
-  return [next, src = &t, g = grid]() -> std::optional<BlockRecord> {
+namespace {
+// The memory block source as a named functor, so that comp_blocked can see
+// through the std::function and stream the whole in-memory tensor to the
+// device once instead of copying it block by block on the host.
+struct MemoryBlockSource {
+  std::shared_ptr<index_t> next;
+  const Tensor3* src;
+  BlockGrid g;
+  std::optional<BlockRecord> operator()() const {
     if (*next >= g.cell_count()) return std::nullopt;
     const index_t lin = (*next)++;
     const std::array<index_t, 3> cell = {lin % g.cells(1), (lin / g.cells(1)) % g.cells(2),
@@ -235,7 +244,14 @@ BlockSource make_memory_block_source(const Tensor3& t, const BlockGrid& grid) {
                     src->values.data() + e1.offset + src->n1 * ((e2.offset + j) + src->n2 * (e3.offset + k)),
                     sizeof(double) * e1.length);
     return rec;
-  };
+  }
+};
+}  // namespace
+
+BlockSource make_memory_block_source(const Tensor3& t, const BlockGrid& grid) {
+  if (t.n1 != grid.n1 || t.n2 != grid.n2 || t.n3 != grid.n3)
+    throw UsageError("make_memory_block_source: grid does not match tensor dims");
+  return MemoryBlockSource{std::make_shared<index_t>(0), &t, grid};
 }
 
 std::vector<Tensor3> comp_blocked(const BlockGrid& grid, const BlockSource& source,
@@ -254,6 +270,16 @@ std::vector<Tensor3> comp_blocked(const BlockGrid& grid, const BlockSource& sour
   ok(xtsg_blocked_begin(gdims.data(), block.data(), P, red.data(), flat[0].data(), flat[1].data(),
                         flat[2].data(), deterministic ? 1 : 0, &h));
   std::unique_ptr<xtsg_blocked, void (*)(xtsg_blocked*)> guard(h, xtsg_blocked_destroy);
+  const MemoryBlockSource* mem = source.target<MemoryBlockSource>();
+  if (mem && *mem->next == 0) {
+    // an untouched in-memory source: every block at once, straight from the
+    // caller's tensor (the deterministic result is grid-independent; the fast
+    // one is the block sum up to rounding, exactly so for a one-block grid)
+    const Tensor3& t = *mem->src;
+    const std::array<index_t, 3> zero = {0, 0, 0}, whole = {t.n1, t.n2, t.n3};
+    ok(xtsg_blocked_push_region(h, zero.data(), whole.data(), t.values.data()));
+    *mem->next = grid.cell_count();
+  }
   while (auto rec = source()) {
     const std::array<index_t, 3> shape = {rec->data.n1, rec->data.n2, rec->data.n3};
     ok(xtsg_blocked_push(h, rec->cell.data(), shape.data(), rec->data.values.data()));
@@ -287,25 +313,146 @@ double relative_error(const Tensor3& t, const FactorTriple& f) {
   return out;
 }
 
-AlsResult cp_als(const Tensor3& t, const AlsConfig& cfg) {
+namespace {
+
+xtsg_als_config als_cfg(const AlsConfig& cfg) {
   xtsg_als_config c{};
   c.rank = cfg.rank;
   c.max_iters = cfg.max_iters;
   c.tol = cfg.tol;
   c.seed = cfg.seed;
   c.init = cfg.init == AlsConfig::Init::nvecs ? 1 : 0;
-  const index_t r = std::max<index_t>(cfg.rank, 0);
-  Matrix a(t.n1, r), b(t.n2, r), cc(t.n3, r);
-  int64_t iters = 0;
-  int32_t conv = 0;
-  std::vector<double> hist(static_cast<std::size_t>(std::max<index_t>(cfg.max_iters, 1)));
-  ok(xtsg_cp_als_batched(1, t.values.data(), t.n1, t.n2, t.n3, &c, a.values.data(), b.values.data(),
-                         cc.values.data(), &iters, &conv, hist.data()));
+  return c;
+}
+
+// count same-shape tensors (values back to back) -> AlsResults
+void als_run(int64_t count, const double* t, index_t n1, index_t n2, index_t n3, const xtsg_als_config* c,
+             AlsResult** out) {
+  const index_t r = std::max<index_t>(c[0].rank, 0);
+  int64_t max_it = 1;
+  for (int64_t q = 0; q < count; ++q) max_it = std::max<int64_t>(max_it, c[q].max_iters);
+  std::vector<double> a(static_cast<std::size_t>(count * n1 * r)), b(static_cast<std::size_t>(count * n2 * r)),
+      cc(static_cast<std::size_t>(count * n3 * r)), hist(static_cast<std::size_t>(count * max_it));
+  std::vector<int64_t> iters(static_cast<std::size_t>(count));
+  std::vector<int32_t> conv(static_cast<std::size_t>(count));
+  ok(xtsg_cp_als_batched(count, t, n1, n2, n3, c, a.data(), b.data(), cc.data(), iters.data(), conv.data(),
+                         hist.data()));
+  for (int64_t q = 0; q < count; ++q) {
+    AlsResult& o = *out[q];
+    Matrix fa(n1, r), fb(n2, r), fc(n3, r);
+    std::memcpy(fa.values.data(), a.data() + q * n1 * r, sizeof(double) * n1 * r);
+    std::memcpy(fb.values.data(), b.data() + q * n2 * r, sizeof(double) * n2 * r);
+    std::memcpy(fc.values.data(), cc.data() + q * n3 * r, sizeof(double) * n3 * r);
+    o.iters = iters[static_cast<std::size_t>(q)];
+    o.converged = conv[static_cast<std::size_t>(q)] != 0;
+    const double* h = hist.data() + q * max_it;
+    o.error_history.assign(h, h + o.iters);
+    o.factors = FactorTriple(std::move(fa), std::move(fb), std::move(fc));
+  }
+}
+
+// Concurrent cp_als calls are gathered into one batched device launch. The
+// reference calls cp_als once per replica from parallel_for workers
+// (pipeline.cpp:410-434, 524-537); one launch over the calls in flight runs
+// the replicas side by side on the GPU instead of one small grid each. The
+// first caller of a round leads: it waits up to kWindow for other callers,
+// takes every pending request shaped like the oldest one (same dims and rank)
+// and runs them; the others sleep until their result is filled in. A batch
+// that fails (e.g. one tensor with non-finite values) is rerun one request at
+// a time, so each caller still sees exactly its own outcome.
+struct AlsRequest {
+  const Tensor3* t;
+  xtsg_als_config cfg;
+  AlsResult* out;
+  std::exception_ptr err;
+  bool done = false;
+};
+
+struct AlsBatcher {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<AlsRequest*> pending;
+  bool leading = false;
+  static constexpr auto kWindow = std::chrono::microseconds(300);
+  static constexpr std::size_t kMaxBatch = 256;
+
+  static bool same_shape(const AlsRequest* x, const AlsRequest* y) {
+    return x->t->n1 == y->t->n1 && x->t->n2 == y->t->n2 && x->t->n3 == y->t->n3 && x->cfg.rank == y->cfg.rank;
+  }
+
+  void lead(std::unique_lock<std::mutex>& lk) {
+    leading = true;
+    cv.wait_for(lk, kWindow, [&] { return pending.size() >= kMaxBatch; });
+    std::vector<AlsRequest*> batch;
+    const AlsRequest* head = pending.front();
+    for (auto it = pending.begin(); it != pending.end() && batch.size() < kMaxBatch;) {
+      if (same_shape(*it, head)) {
+        batch.push_back(*it);
+        it = pending.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    lk.unlock();
+    run(batch);
+    lk.lock();
+    for (AlsRequest* q : batch) q->done = true;
+    leading = false;
+    cv.notify_all();
+  }
+
+  static void run(const std::vector<AlsRequest*>& batch) {
+    const Tensor3& t0 = *batch.front()->t;
+    const int64_t n = static_cast<int64_t>(batch.size()), tsz = t0.n1 * t0.n2 * t0.n3;
+    auto one = [&](AlsRequest* q) {
+      try {
+        AlsResult* o = q->out;
+        als_run(1, q->t->values.data(), q->t->n1, q->t->n2, q->t->n3, &q->cfg, &o);
+      } catch (...) {
+        q->err = std::current_exception();
+      }
+    };
+    if (n == 1) {
+      one(batch.front());
+      return;
+    }
+    try {
+      std::vector<double> t(static_cast<std::size_t>(n * tsz));
+      std::vector<xtsg_als_config> c(static_cast<std::size_t>(n));
+      std::vector<AlsResult*> o(static_cast<std::size_t>(n));
+      for (int64_t q = 0; q < n; ++q) {
+        std::memcpy(t.data() + q * tsz, batch[static_cast<std::size_t>(q)]->t->values.data(), sizeof(double) * tsz);
+        c[static_cast<std::size_t>(q)] = batch[static_cast<std::size_t>(q)]->cfg;
+        o[static_cast<std::size_t>(q)] = batch[static_cast<std::size_t>(q)]->out;
+      }
+      als_run(n, t.data(), t0.n1, t0.n2, t0.n3, c.data(), o.data());
+    } catch (...) {
+      for (AlsRequest* q : batch) one(q);
+    }
+  }
+};
+
+AlsBatcher& als_batcher() {
+  static AlsBatcher b;
+  return b;
+}
+
+}  // namespace
+
+AlsResult cp_als(const Tensor3& t, const AlsConfig& cfg) {
   AlsResult out;
-  out.iters = iters;
-  out.converged = conv != 0;
-  out.error_history.assign(hist.begin(), hist.begin() + iters);
-  out.factors = FactorTriple(std::move(a), std::move(b), std::move(cc));
+  AlsRequest req{&t, als_cfg(cfg), &out, nullptr, false};
+  AlsBatcher& b = als_batcher();
+  {
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.pending.push_back(&req);
+    b.cv.notify_all();
+    while (!req.done) {
+      if (!b.leading) b.lead(lk);
+      else b.cv.wait(lk);
+    }
+  }
+  if (req.err) std::rethrow_exception(req.err);
   return out;
 }
 

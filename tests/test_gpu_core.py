@@ -141,6 +141,32 @@ def test_blocked_deterministic_bitwise_and_fast(gpu):
         assert rel_diff(reps[p], gpu.comp(t, ens.u[p], ens.v[p], ens.w[p])) <= 1e-12
 
 
+def test_blocked_regions(gpu):
+    # the facade's whole-tensor push of an untouched memory source: bitwise the
+    # one-shot comp; regions mix with cell records, and keep the stream checks
+    t = np.asfortranarray(np.random.default_rng(611).standard_normal((9, 8, 7)))
+    ens = gpu.make_ensemble([9, 8, 7], [4, 3, 3], 3, 1, 612)
+    direct = [gpu.comp(t, ens.u[p], ens.v[p], ens.w[p]) for p in range(3)]
+    reps = gpu.comp_blocked([9, 8, 7], [4, 3, 2], [], ens, regions=[((0, 0, 0), t)])
+    for p in range(3):
+        assert np.array_equal(reps[p], direct[p])
+    # k cells 0-1 as a region, the rest as records (ragged i/j edges inside the region)
+    recs = [r for r in _memory_source(t, [4, 3, 2]) if r[0][2] >= 2]
+    reps = gpu.comp_blocked([9, 8, 7], [4, 3, 2], recs, ens, regions=[((0, 0, 0), t[:, :, :4])])
+    for p in range(3):
+        assert np.array_equal(reps[p], direct[p])
+    with pytest.raises(gpu.DataError):  # not on cell boundaries
+        gpu.comp_blocked([9, 8, 7], [4, 3, 2], [], ens, regions=[((0, 0, 1), t[:, :, 1:])])
+    with pytest.raises(gpu.DataError):  # a cell twice
+        gpu.comp_blocked([9, 8, 7], [4, 3, 2], list(_memory_source(t, [4, 3, 2])), ens,
+                         regions=[((0, 0, 0), t[:, :, :2])])
+    # fast mode: a region is one big block (per-cell sum up to rounding)
+    reps = gpu.comp_blocked([9, 8, 7], [4, 3, 2], recs, ens, deterministic=False, regions=[((0, 0, 0), t[:, :, :4])])
+    from oracle.oracle import rel_diff
+    for p in range(3):
+        assert rel_diff(reps[p], direct[p]) <= 1e-12
+
+
 def test_blocked_stream_faults(gpu):
     # test_compression.cpp:289-337
     t = np.asfortranarray(np.random.default_rng(621).standard_normal((6, 6, 6)))
