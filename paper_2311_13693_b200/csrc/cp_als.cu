@@ -1429,12 +1429,15 @@ int als_cluster_size(int64_t n1, int64_t n2, int64_t n3, int64_t R) {
     return e ? std::atoi(e) : -1;
   }();
   if (env == 0 || R > 32 || n1 > 64 || n2 > 64 || n3 > 64 || n3 < 2) return 0;
-  for (int cl : {16, 8, 4, 2, 1}) {
-    if (env > 0 && cl != env) continue;
-    if (env <= 0 && (cl == 1 || cl == 16)) continue;  // 1 and 16 (non-portable) only on request
-    if (cl > n3) continue;
-    if (cluster_layout(int(n1), int(n2), int(n3), int(R), cl).doubles * 8 <= 110 * 1024) return cl;
-  }
+  // two CTAs per SM when the slab fits 110 KB; else one per SM (up to 200 KB:
+  // 40^3 replicas at rank 20, 155 KB with 8 CTAs) rather than the one-CTA kernel
+  for (const size_t cap : {size_t(110) * 1024, size_t(200) * 1024})
+    for (int cl : {16, 8, 4, 2, 1}) {
+      if (env > 0 && cl != env) continue;
+      if (env <= 0 && (cl == 1 || cl == 16)) continue;  // 1 and 16 (non-portable) only on request
+      if (cl > n3) continue;
+      if (cluster_layout(int(n1), int(n2), int(n3), int(R), cl).doubles * 8 <= cap) return cl;
+    }
   return 0;
 }
 
