@@ -362,17 +362,24 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   if (hf[1]) {
     DevBuf<uint64_t> keys2(static_cast<size_t>(nnz), s);
     DevBuf<uint64_t> idx2(static_cast<size_t>(nnz), s);
-    size_t tmp_bytes = 0;
     int end_bit = 1;
     while (end_bit < 64 && (uint64_t(1) << end_bit) < static_cast<uint64_t>(K) * static_cast<uint64_t>(J)) ++end_bit;
-    XCUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.ptr, keys2.ptr, idx.ptr, idx2.ptr, nnz, 0, end_bit, s));
-    DevBuf<uint8_t> tmp(tmp_bytes, s);
-    XCUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tmp_bytes, keys.ptr, keys2.ptr, idx.ptr, idx2.ptr, nnz, 0, end_bit, s));
-    count_launch();
+    {
+      // double-buffered sort: the two key/payload buffers are its ping-pong
+      // storage (small temporary instead of another 16 B per nonzero)
+      cub::DoubleBuffer<uint64_t> dkeys(keys.ptr, keys2.ptr), dpay(idx.ptr, idx2.ptr);
+      size_t tmp_bytes = 0;
+      XCUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dkeys, dpay, nnz, 0, end_bit, s));
+      DevBuf<uint8_t> tmp(tmp_bytes, s);
+      XCUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tmp_bytes, dkeys, dpay, nnz, 0, end_bit, s));
+      count_launch();
+      if (dkeys.Current() != keys2.ptr) std::swap(keys, keys2);
+      if (dpay.Current() != idx2.ptr) std::swap(idx, idx2);
+    }
+    keys.release();
+    idx.release();
     if (sparse_tc_ok()) {
-      keys.release();
-      idx.release();
-      sparse_tc_sorted(keys2.ptr, idx2.ptr, nullptr, nullptr, nnz, yo.dev, accumulate, s);
+      sparse_tc_sorted(keys2, &idx2, nullptr, nullptr, nnz, yo.dev, accumulate, s);
       if (fp16()) check_finite16(yo.dev, ysz, s);
       if (yo.host) yo.finish();
       return;
@@ -387,7 +394,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   }
   if (!hf[1] && sparse_tc_ok()) {
     idx.release();
-    sparse_tc_sorted(keys.ptr, nullptr, di.dev, dv.dev, nnz, yo.dev, accumulate, s);
+    sparse_tc_sorted(keys, nullptr, di.dev, dv.dev, nnz, yo.dev, accumulate, s);
     if (fp16()) check_finite16(yo.dev, ysz, s);
     if (yo.host) yo.finish();
     return;

@@ -115,7 +115,8 @@ struct Plan {
   void sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* slice_ptr, int64_t n_fibers,
                  const int64_t* fiber_ptr, const int32_t* fiber_j, int64_t nnz, const int32_t* nz_i,
                  const float* val, float* ydev, bool accumulate, cudaStream_t s);
-  void sparse_tc_sorted(const uint64_t* skeys, const uint64_t* spay, const int32_t* si, const float* sv,
+  // skeys / spay are consumed (released as soon as they are read)
+  void sparse_tc_sorted(DevBuf<uint64_t>& skeys, DevBuf<uint64_t>* spay, const int32_t* si, const float* sv,
                         int64_t nnz, float* ydev, bool accumulate, cudaStream_t s);
 };
 

@@ -778,6 +778,44 @@ __global__ void payload_unpack_kernel(const uint64_t* __restrict__ pay, int64_t 
   }
 }
 
+// fiber regrouping (COO input): key (k, smallest i), value = fiber index
+__global__ void fiber_group_keys_kernel(const int32_t* __restrict__ fk, const int32_t* __restrict__ fmin, int64_t nf,
+                                        uint64_t* __restrict__ key, int32_t* __restrict__ idx) {
+  for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < nf;
+       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    key[f] = (static_cast<uint64_t>(static_cast<uint32_t>(fk[f])) << 32) | static_cast<uint32_t>(fmin[f]);
+    idx[f] = static_cast<int32_t>(f);
+  }
+}
+
+__global__ void fiber_permute_kernel(const int32_t* __restrict__ perm, const int64_t* __restrict__ fptr,
+                                     const int32_t* __restrict__ fj, int64_t nf, int32_t* __restrict__ cnt,
+                                     int32_t* __restrict__ gj) {
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nf;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t f = perm[q];
+    cnt[q] = static_cast<int32_t>(fptr[f + 1] - fptr[f]);
+    gj[q] = fj[f];
+  }
+}
+
+// one warp per (new) fiber: copy its nonzeros to their new place
+__global__ void fiber_gather_kernel(const int32_t* __restrict__ perm, const int64_t* __restrict__ fptr,
+                                    const int64_t* __restrict__ gptr, int64_t nf, const int32_t* __restrict__ ni,
+                                    const float* __restrict__ nv, int32_t* __restrict__ oi, float* __restrict__ ov) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t q = w0; q < nf; q += nw) {
+    const int32_t f = perm[q];
+    const int64_t a = fptr[f], n = fptr[f + 1] - a, d = gptr[q];
+    for (int64_t e = lane; e < n; e += 32) {
+      oi[d + e] = ni[a + e];
+      ov[d + e] = nv[a + e];
+    }
+  }
+}
+
 int gridn(int64_t work) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * 16))); }
 
 // exclusive scan of cnt[0..n) into ptr[0..n] (ptr[n] = total)
@@ -867,8 +905,9 @@ void Plan::sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* sl
 
 // sorted COO (keys = k*J + j ascending, payload = (i << 32) | value bits) ->
 // CSF arrays -> sparse_tc
-void Plan::sparse_tc_sorted(const uint64_t* skeys, const uint64_t* spay, const int32_t* si_in, const float* sv_in,
-                            int64_t nnz, float* ydev, bool accumulate, cudaStream_t s) {
+void Plan::sparse_tc_sorted(DevBuf<uint64_t>& skeys_buf, DevBuf<uint64_t>* spay_buf, const int32_t* si_in,
+                            const float* sv_in, int64_t nnz, float* ydev, bool accumulate, cudaStream_t s) {
+  const uint64_t* skeys = skeys_buf.ptr;
   const int64_t J = desc.dims[1];
   // fibers: runs of equal (k, j)
   DevBuf<uint64_t> fkeys(static_cast<size_t>(nnz), s);
@@ -881,9 +920,24 @@ void Plan::sparse_tc_sorted(const uint64_t* skeys, const uint64_t* spay, const i
     XCUDA(cub::DeviceRunLengthEncode::Encode(tmp.ptr, tb, skeys, fkeys.ptr, fcnt.ptr, nruns.ptr, nnz, s));
     count_launch();
   }
+  skeys_buf.release();
+  DevBuf<int32_t> bi;
+  DevBuf<float> bv;
+  const int32_t* ni = si_in;
+  const float* nv = sv_in;
+  if (spay_buf) {
+    bi = DevBuf<int32_t>(static_cast<size_t>(nnz), s);
+    bv = DevBuf<float>(static_cast<size_t>(nnz), s);
+    payload_unpack_kernel<<<gridn(nnz), 256, 0, s>>>(spay_buf->ptr, nnz, bi.ptr, bv.ptr);
+    XLAUNCH_CHECK();
+    spay_buf->release();
+    ni = bi.ptr;
+    nv = bv.ptr;
+  }
   int64_t nf = 0;
   XCUDA(cudaMemcpyAsync(&nf, nruns.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   XCUDA(cudaStreamSynchronize(s));
+  if (nf >= (int64_t(1) << 31)) usage("plan_compress_coo: at most 2^31-1 distinct (j, k) fibers per call");
   DevBuf<int64_t> fptr(static_cast<size_t>(nf + 1), s);
   scan_ptr(fcnt.ptr, nf, fptr.ptr, s);
   fcnt.release();
@@ -905,21 +959,59 @@ void Plan::sparse_tc_sorted(const uint64_t* skeys, const uint64_t* spay, const i
   XCUDA(cudaStreamSynchronize(s));
   DevBuf<int64_t> sptr(static_cast<size_t>(kd + 1), s);
   scan_ptr(scnt.ptr, kd, sptr.ptr, s);
-  fk.release();
   scnt.release();
-  DevBuf<int32_t> bi;
-  DevBuf<float> bv;
-  const int32_t* ni = si_in;
-  const float* nv = sv_in;
-  if (spay) {
-    bi = DevBuf<int32_t>(static_cast<size_t>(nnz), s);
-    bv = DevBuf<float>(static_cast<size_t>(nnz), s);
-    payload_unpack_kernel<<<gridn(nnz), 256, 0, s>>>(spay, nnz, bi.ptr, bv.ptr);
-    XLAUNCH_CHECK();
-    ni = bi.ptr;
-    nv = bv.ptr;
+  // Regroup the fibers of every slice by their smallest i (stable in j): the
+  // (k, j) order interleaves fibers of different rank-1 blocks that share a
+  // slice, which the planner would cut into one-fiber tiles; fibers with a
+  // common i support become neighbours. Slices keep their order and extents.
+  const char* rg_env = std::getenv("XTSG_COO_REGROUP");
+  if (rg_env && std::atoi(rg_env) == 0) {  // A/B knob: keep the (k, j) fiber order
+    fk.release();
+    sparse_tc(kd, uk.ptr, sptr.ptr, nf, fptr.ptr, fj.ptr, nnz, ni, nv, ydev, accumulate, s);
+    return;
   }
-  sparse_tc(kd, uk.ptr, sptr.ptr, nf, fptr.ptr, fj.ptr, nnz, ni, nv, ydev, accumulate, s);
+  DevBuf<int32_t> fmin(static_cast<size_t>(nf), s);
+  {
+    size_t tb = 0;
+    XCUDA(cub::DeviceSegmentedReduce::Min(nullptr, tb, ni, fmin.ptr, nf, fptr.ptr, fptr.ptr + 1, s));
+    DevBuf<uint8_t> tmp(tb, s);
+    XCUDA(cub::DeviceSegmentedReduce::Min(tmp.ptr, tb, ni, fmin.ptr, nf, fptr.ptr, fptr.ptr + 1, s));
+    count_launch();
+  }
+  DevBuf<uint64_t> gk(static_cast<size_t>(nf), s), gk2(static_cast<size_t>(nf), s);
+  DevBuf<int32_t> gi(static_cast<size_t>(nf), s), gi2(static_cast<size_t>(nf), s);
+  fiber_group_keys_kernel<<<gridn(nf), 256, 0, s>>>(fk.ptr, fmin.ptr, nf, gk.ptr, gi.ptr);
+  XLAUNCH_CHECK();
+  fk.release();
+  fmin.release();
+  {
+    int end_bit = 33;
+    while (end_bit < 64 && (uint64_t(1) << (end_bit - 32)) < static_cast<uint64_t>(desc.dims[2])) ++end_bit;
+    size_t tb = 0;
+    XCUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, gk.ptr, gk2.ptr, gi.ptr, gi2.ptr, nf, 0, end_bit, s));
+    DevBuf<uint8_t> tmp(tb, s);
+    XCUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, gk.ptr, gk2.ptr, gi.ptr, gi2.ptr, nf, 0, end_bit, s));
+    count_launch();
+  }
+  gk.release();
+  gk2.release();
+  gi.release();
+  DevBuf<int32_t> gcnt(static_cast<size_t>(nf), s), gj(static_cast<size_t>(nf), s);
+  fiber_permute_kernel<<<gridn(nf), 256, 0, s>>>(gi2.ptr, fptr.ptr, fj.ptr, nf, gcnt.ptr, gj.ptr);
+  XLAUNCH_CHECK();
+  DevBuf<int64_t> gptr(static_cast<size_t>(nf + 1), s);
+  scan_ptr(gcnt.ptr, nf, gptr.ptr, s);
+  gcnt.release();
+  DevBuf<int32_t> gni(static_cast<size_t>(nnz), s);
+  DevBuf<float> gnv(static_cast<size_t>(nnz), s);
+  fiber_gather_kernel<<<gridn(nf * 32), 256, 0, s>>>(gi2.ptr, fptr.ptr, gptr.ptr, nf, ni, nv, gni.ptr, gnv.ptr);
+  XLAUNCH_CHECK();
+  gi2.release();
+  fptr.release();
+  fj.release();
+  bi.release();
+  bv.release();
+  sparse_tc(kd, uk.ptr, sptr.ptr, nf, gptr.ptr, gj.ptr, nnz, gni.ptr, gnv.ptr, ydev, accumulate, s);
 }
 
 }  // namespace xtsg

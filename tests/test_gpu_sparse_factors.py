@@ -99,16 +99,22 @@ def test_coo_rejects_out_of_range(gpu):
 
 
 def test_csf_matches_coo_bitwise_and_validates(gpu, restated):
-    # CSF input skips the sort: same fibers in the same order as the COO
-    # path's stable (k, j) sort -> the same replicas up to the order of the
-    # fiber kernel's shared-memory atomic folds (fp32 rounding only)
+    # CSF input skips the sort; the COO path also regroups each slice's fibers
+    # by their smallest i, so the two group fibers into different tiles: the
+    # replicas agree to bf16 level (duplicate coordinates are summed in bf16 in
+    # tile order), and each matches the fp64 oracle at the stated bar
     dims, red, P = (97, 88, 71), (32, 32, 16), 8
     plan = gpu.Plan(dims, red, P, 8, 77)
+    ens = gpu.make_ensemble(dims, red, P, 8, 77)
     i, j, k, v = _random_coo(dims, 20000, 3)
     y_coo = plan.compress_coo(i, j, k, v)
     csf = gpu.Plan.coo_to_csf(i, j, k, v)
     y_csf = plan.compress_csf(*csf)
-    assert rel_diff(np.asarray(y_coo, np.float64), np.asarray(y_csf, np.float64)) <= 1e-6
+    assert rel_diff(np.asarray(y_coo, np.float64), np.asarray(y_csf, np.float64)) <= 2e-3
+    t = _dense(dims, i, j, k, v)
+    got = gpu.Plan.replicas(y_csf, P, red)
+    for p in range(P):
+        assert rel_diff(restated.comp(t, ens.u[p], ens.v[p], ens.w[p]), got[p]) <= TOL
     # accumulate, and duplicate slices (the same k split in two slice records) sum
     sk, sp, fj, fp, ni, nv = csf
     y2 = plan.compress_csf(sk, sp, fj, fp, ni, nv, y=np.asarray(y_csf).copy(), accumulate=True)

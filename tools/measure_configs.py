@@ -144,6 +144,7 @@ def c4(args):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    mem_free, mem_total = torch.cuda.mem_get_info()
     launches = (xt.launch_count() - l0) / args.steps
     # exact check: comp_from_factors of the generating factors (linear in X;
     # duplicates sum), fp64 on the device, for a few replicas
@@ -164,7 +165,8 @@ def c4(args):
           "roofline": {"bound": "hbm (algorithmic 16 B/nnz) vs SIMT fp32 FMA (2*P*L = 1024 flop/nnz)",
                        "achieved_gbs": achieved, "peak_gbs": hbm, "frac": achieved / hbm,
                        "fma_tflops": 2.0 * P * red[0] * rate / 1e12, "peak_source": src},
-          "max_rel_err_vs_comp_from_factors": float(max(errs)), "tolerance": 1e-2}, args.out)
+          "max_rel_err_vs_comp_from_factors": float(max(errs)), "tolerance": 1e-2,
+          "device_mem_free_gb": mem_free / 2**30, "torch_reserved_gb": torch.cuda.memory_reserved() / 2**30}, args.out)
 
 
 def c5(args):
