@@ -58,3 +58,12 @@ def test_reference_acceptance_against_dropin(gpu):
     # with the reference, so the logged ratio is reproduced (test_output.txt:14)
     m = re.search(r"median error ratio ([0-9.eE+-]+)", r.stdout)
     assert m and abs(float(m.group(1)) - 0.000253996) < 5e-10, r.stdout
+
+
+@pytest.mark.gpu
+def test_facade_concurrent_cp_als_and_memory_source(gpu):
+    # integration/facade_concurrency.cpp: 16 threads' cp_als calls batched by
+    # the facade equal the same calls made alone (bitwise), a NaN tensor fails
+    # only its own call; comp_blocked over an in-memory source == comp
+    r = _run("facade_concurrency", 300)
+    assert r.returncode == 0 and "facade_concurrency: ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
