@@ -289,6 +289,11 @@ __global__ void __launch_bounds__(PL_NT, 4) sparse_plan_kernel(const SpPlanParam
       }
       for (int t = tid; t <= nf; t += PL_NT)
         tfp[t] = t == 0 ? 0 : static_cast<int32_t>((t == nf ? e_end : p.fiber_ptr[f + t]) - e_in);
+      if (tid == 0) {  // the next tile's i (about as many as this one's) into L2
+        const int64_t n = e_end - e_in, es1 = p.fiber_ptr[fs1];
+        const int64_t pa = (e_end + 3) & ~int64_t(3), pb = imin64(es1, e_end + n) & ~int64_t(3);
+        if (pb > pa) ptx::bulk_prefetch_l2(p.nz_i + pa, static_cast<uint32_t>(imin64((pb - pa) * 4, 1 << 20)));
+      }
       // lookup pass: id of every nonzero -> li_g, (fiber, id) occupancy ->
       // dup; an i without an id sets `miss` (and the pass stops early)
       auto lookup = [&]() {
