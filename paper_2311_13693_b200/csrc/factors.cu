@@ -188,22 +188,62 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
   const int64_t budget = std::min<int64_t>(slab_gb << 30, static_cast<int64_t>(free_b / 4));
   const int64_t planes = comp() ? 2 : 1;
   const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(k1 - k0, budget / (planes * ldi * J * 2)));
-  DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * J * ldi), s), stage_lo;
-  if (comp()) stage_lo = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
   const size_t smem = static_cast<size_t>(rank) * (TI + TJ) * sizeof(float);
   XCUDA(cudaFuncSetAttribute(gen_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  for (int64_t kb = k0; kb < k1; kb += ks) {
-    const int64_t kn = std::min(ks, k1 - kb);
+  const int64_t nslabs = ceil_div(k1 - k0, ks);
+  // Two slab buffers: the generator fills slab s+1 on the side stream while
+  // the tensor cores consume slab s (the compensated mode keeps one launch-wide
+  // max |x| per slab, so it stays serial). XTSG_GEN_OVERLAP=0 disables.
+  static const bool overlap_env = [] {
+    const char* e = std::getenv("XTSG_GEN_OVERLAP");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool overlap = overlap_env && !comp() && nslabs > 1;
+  DevBuf<__nv_bfloat16> stage[2], stage_lo;
+  stage[0] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
+  if (overlap) stage[1] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
+  if (comp()) stage_lo = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
+  auto gen = [&](int64_t sl, int b, cudaStream_t gs) {
+    const int64_t kb = k0 + sl * ks, kn = std::min(ks, k1 - kb);
     dim3 grid(static_cast<unsigned>(ceil_div(I, TI)), static_cast<unsigned>(ceil_div(J, TJ)),
               static_cast<unsigned>(kn));
-    if (comp()) XCUDA(cudaMemsetAsync(amax.ptr, 0, sizeof(unsigned), s));
-    gen_slab_kernel<<<grid, NT, smem, s>>>(fa.ptr, fb.ptr, fc.ptr, I, J, K, static_cast<int>(rank), kb, ldi,
-                                           stage.ptr, fp16(), comp() ? stage_lo.ptr : nullptr,
-                                           comp() ? amax.ptr : nullptr);
+    if (comp()) XCUDA(cudaMemsetAsync(amax.ptr, 0, sizeof(unsigned), gs));
+    gen_slab_kernel<<<grid, NT, smem, gs>>>(fa.ptr, fb.ptr, fc.ptr, I, J, K, static_cast<int>(rank), kb, ldi,
+                                            stage[b].ptr, fp16(), comp() ? stage_lo.ptr : nullptr,
+                                            comp() ? amax.ptr : nullptr);
     XLAUNCH_CHECK();
+  };
+  auto ttm = [&](int64_t sl, int b) {
+    const int64_t kb = k0 + sl * ks, kn = std::min(ks, k1 - kb);
     const int64_t off[3] = {0, 0, kb}, ext[3] = {I, J, kn};
-    run_bf16_block(stage.ptr, ldi, ldi * J, off, ext, ydst, acc, s, comp() ? stage_lo.ptr : nullptr);
+    run_bf16_block(stage[b].ptr, ldi, ldi * J, off, ext, ydst, acc, s, comp() ? stage_lo.ptr : nullptr);
     acc = true;
+  };
+  if (!overlap) {
+    for (int64_t sl = 0; sl < nslabs; ++sl) {
+      gen(sl, 0, s);
+      ttm(sl, 0);
+    }
+  } else {
+    for (int b = 0; b < 2; ++b) {
+      if (!ev_copied[b]) XCUDA(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
+      if (!ev_consumed[b]) XCUDA(cudaEventCreateWithFlags(&ev_consumed[b], cudaEventDisableTiming));
+      XCUDA(cudaEventRecord(ev_consumed[b], s));  // both buffers free; the factors are on s
+    }
+    XCUDA(cudaStreamWaitEvent(copy_st, ev_consumed[0], 0));
+    gen(0, 0, copy_st);
+    XCUDA(cudaEventRecord(ev_copied[0], copy_st));
+    for (int64_t sl = 0; sl < nslabs; ++sl) {
+      const int b = static_cast<int>(sl & 1);
+      if (sl + 1 < nslabs) {
+        XCUDA(cudaStreamWaitEvent(copy_st, ev_consumed[1 - b], 0));
+        gen(sl + 1, 1 - b, copy_st);
+        XCUDA(cudaEventRecord(ev_copied[1 - b], copy_st));
+      }
+      XCUDA(cudaStreamWaitEvent(s, ev_copied[b], 0));
+      ttm(sl, b);
+      XCUDA(cudaEventRecord(ev_consumed[b], s));
+    }
   }
   if (comp()) {
     comp_finish(y64.ptr, yo.dev, accumulate, s);
