@@ -192,31 +192,34 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
   XCUDA(cudaFuncSetAttribute(gen_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t nslabs = ceil_div(k1 - k0, ks);
   // Two slab buffers: the generator fills slab s+1 on the side stream while
-  // the tensor cores consume slab s (the compensated mode keeps one launch-wide
-  // max |x| per slab, so it stays serial). XTSG_GEN_OVERLAP=0 disables.
+  // the tensor cores consume slab s (the compensated mode's per-slab max |x|
+  // has one slot per buffer). XTSG_GEN_OVERLAP=0 disables.
   static const bool overlap_env = [] {
     const char* e = std::getenv("XTSG_GEN_OVERLAP");
     return !(e && std::atoi(e) == 0);
   }();
-  const bool overlap = overlap_env && !comp() && nslabs > 1;
-  DevBuf<__nv_bfloat16> stage[2], stage_lo;
-  stage[0] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
-  if (overlap) stage[1] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
-  if (comp()) stage_lo = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
+  const bool overlap = overlap_env && nslabs > 1;
+  DevBuf<__nv_bfloat16> stage[2], stage_lo[2];
+  for (int b = 0; b < (overlap ? 2 : 1); ++b) {
+    stage[b] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
+    if (comp()) stage_lo[b] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * J * ldi), s);
+  }
   auto gen = [&](int64_t sl, int b, cudaStream_t gs) {
     const int64_t kb = k0 + sl * ks, kn = std::min(ks, k1 - kb);
     dim3 grid(static_cast<unsigned>(ceil_div(I, TI)), static_cast<unsigned>(ceil_div(J, TJ)),
               static_cast<unsigned>(kn));
-    if (comp()) XCUDA(cudaMemsetAsync(amax.ptr, 0, sizeof(unsigned), gs));
+    if (comp()) XCUDA(cudaMemsetAsync(amax.ptr + b, 0, sizeof(unsigned), gs));
     gen_slab_kernel<<<grid, NT, smem, gs>>>(fa.ptr, fb.ptr, fc.ptr, I, J, K, static_cast<int>(rank), kb, ldi,
-                                            stage[b].ptr, fp16(), comp() ? stage_lo.ptr : nullptr,
-                                            comp() ? amax.ptr : nullptr);
+                                            stage[b].ptr, fp16(), comp() ? stage_lo[b].ptr : nullptr,
+                                            comp() ? amax.ptr + b : nullptr);
     XLAUNCH_CHECK();
   };
   auto ttm = [&](int64_t sl, int b) {
     const int64_t kb = k0 + sl * ks, kn = std::min(ks, k1 - kb);
     const int64_t off[3] = {0, 0, kb}, ext[3] = {I, J, kn};
-    run_bf16_block(stage[b].ptr, ldi, ldi * J, off, ext, ydst, acc, s, comp() ? stage_lo.ptr : nullptr);
+    cur_amax = comp() ? amax.ptr + b : nullptr;
+    run_bf16_block(stage[b].ptr, ldi, ldi * J, off, ext, ydst, acc, s, comp() ? stage_lo[b].ptr : nullptr);
+    cur_amax = nullptr;
     acc = true;
   };
   if (!overlap) {

@@ -452,7 +452,7 @@ void Plan::build_tc_operands() {
     pack3(u64.ptr, L, I, msplit, lsplit, Lv, lpad, ld_u, rows_u * ld_u, comp_bu, 0, ustack.ptr);
     pack3(v64.ptr, M, J, 1, msplit, Mv, mpad, ld_v, vP * mpad * ld_v, comp_bv, 1, vt.ptr);
     pack_virtual<float>(w64.ptr, vP, N, K, per_p, 1, 1, N, N, K, wf.ptr, st);
-    amax = DevBuf<unsigned>(1, st);
+    amax = DevBuf<unsigned>(2, st);  // one per slab buffer (overlapped staging)
   } else if (fp16()) {
     // fp16 keeps 3 more mantissa bits than bf16 but tops out at 65504: the
     // mode-1 partial sums (the mode-2 operand, |sum_i U X| ~ sqrt(I) |X|)
@@ -606,7 +606,7 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
       tl.prm.comp = 1;
       tl.prm.kpc = comp_kpc();
       tl.prm.i_chunks = static_cast<int32_t>(ceil_div(tl.prm.k_steps, tl.prm.kpc));
-      tl.prm.amax = amax.ptr;
+      tl.prm.amax = cur_amax ? cur_amax : amax.ptr;
       tl.prm.comp_c0 = comp_c0(ext[0]);
     }
     EvPair e1{}, e2{};
@@ -630,7 +630,8 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
       const int64_t mrows = mpad * lpad;
       dim3 grid(static_cast<unsigned>(ceil_div(mrows, M3_TM)), static_cast<unsigned>(ceil_div(N, M3_TN)),
                 static_cast<unsigned>(vP));
-      mode3_comp_kernel<<<grid, 256, 0, s>>>(zbuf.ptr, mrows, kc, wf.ptr + off[2] + kb, K, N * K, N, amax.ptr,
+      mode3_comp_kernel<<<grid, 256, 0, s>>>(zbuf.ptr, mrows, kc, wf.ptr + off[2] + kb, K, N * K, N,
+                                             cur_amax ? cur_amax : amax.ptr,
                                              comp_c0(ext[0]) + comp_bu + comp_bv - 22, acc ? 1 : 0, comp_y);
       XLAUNCH_CHECK();
     } else {

@@ -67,6 +67,7 @@ struct Plan {
   // the power-of-two pre-scales of U/V (kept < 16 in magnitude so hi*2^11
   // fits binary16); mode 3 accumulates in fp64 into comp_y (padded layout)
   DevBuf<unsigned> amax;
+  const unsigned* cur_amax = nullptr;  // the amax slot of the slab being consumed (null: amax.ptr)
   int comp_bu = 0, comp_bv = 0;
   double* comp_y = nullptr;
   bool comp() const { return desc.precision == XTSG_PREC_FP16X3; }

@@ -8,9 +8,10 @@ import torch
 import paper_2311_13693_b200 as xt
 
 k1 = int(sys.argv[1]) if len(sys.argv) > 1 else 400
+prec = {"bf16": xt.PREC_BF16, "fp16": xt.PREC_FP16, "fp16x3": xt.PREC_FP16X3}[sys.argv[2] if len(sys.argv) > 2 else "bf16"]
 dims, red, P, S, R = (10000, 10000, 10000), (128, 128, 128), 124, 40, 20
 f = xt.generate_factors(dims, R, seed=1)
-plan = xt.Plan(dims, red, P, S, 7, precision=xt.PREC_BF16)
+plan = xt.Plan(dims, red, P, S, 7, precision=prec)
 y = torch.zeros(P * 128 ** 3, dtype=torch.float32, device="cuda")
 plan.compress_factors(f, 0, 40, y=y, device="cuda")
 torch.cuda.synchronize()
