@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--e2e-dtype", default="f32", choices=["bf16", "f32", "f64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cp-time", action="store_true")
+    ap.add_argument("--no-c3", action="store_true",
+                    help="skip the north-star C3 decompose (10^4^3 rank 20, P = 124 x 128^3) after the C2 timing")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp16", "fp16x3"],
                     help="tensor-core operand type (fp16: 3 more mantissa bits, same speed; fp16x3: the "
                          "compensated hi/lo mode, ~1e-6 replicas at ~3x the tensor-core work)")
@@ -229,6 +231,58 @@ def cp_time_c1():
         out["reference_seconds"] = None
         out["reference_note"] = f"unavailable: {e}"
     return out
+
+
+def cp_time_c3(xt, torch, world, rank, dev):
+    """north_star: the dense 10,000^3 rank-20 tensor compressed and decomposed
+    end to end (C3: P = 124 replicas of 128^3, S = 40, blocks generated on the
+    device from the factors). One GPU: decompose on the device. N ranks:
+    mode-3 slabs per rank, one reduce-scatter of the replicas, stage 1
+    (CP-ALS) on every rank for its share, stages 2-3 on rank 0
+    (dist.decompose_distributed). bf16 compression at the relaxed replica fit
+    tolerance 1e-2 (the compensated mode meets the default 1e-6 at ~5x the
+    compression time, profiles/r2_pipeline_c3_fp16x3.json); recovered-factor
+    errors from evaluate (pipeline.cpp:577-609)."""
+    import torch.distributed as dist
+    dims, R, red, P, S = (10000, 10000, 10000), 20, (128, 128, 128), 124, 40
+    f = xt.generate_factors(dims, R, seed=1)
+    cfg = xt.PipelineConfig(reduced=red, rank=R, replicas=P, shared=S, precision=xt.PREC_BF16,
+                            replica_fit_tol=1e-2, seed=2)
+    if world == 1:
+        t0 = time.perf_counter()
+        rec, met = xt.decompose(cfg, factors=f)
+        wall = time.perf_counter() - t0
+    else:
+        from paper_2311_13693_b200.dist import decompose_distributed
+        lmn = int(np.prod(red))
+        per = -(-P // world)
+        plan = xt.Plan(dims, red, P, S, derive(2, 11), precision=xt.PREC_BF16)
+        yy = torch.zeros(per * world * lmn, dtype=torch.float32, device=dev)
+
+        def slab(k0, k1, ybuf):
+            plan.compress_factors(f, k0, k1, y=ybuf[:P * lmn], device=dev)
+            torch.cuda.synchronize()
+
+        dist.barrier()
+        t0 = time.perf_counter()
+        rec, met, t_s1 = decompose_distributed(
+            slab, dims[2], P, lmn, yy, lambda reps, ids: xt.decompose_stage1(cfg, dims, reps, ids),
+            lambda merged: xt.decompose_finish(cfg, merged, factors=f))
+        wall = time.perf_counter() - t0
+        tw = torch.tensor([wall, t_s1], device=dev, dtype=torch.float64)
+        dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        wall = float(tw[0].item())
+        plan.close()
+        if rank != 0:
+            return None
+        met.stage_seconds["decomposition"] = float(tw[1].item())
+        met.stage_seconds["compression"] = wall - sum(v for k, v in met.stage_seconds.items() if k != "compression")
+    rep = xt.evaluate(f, rec)
+    return {"config": "C3 (north_star): dense 10000^3 rank-20, P=124 x 128^3, S=40, factored source, "
+                      "bf16 compression, replica fit tol 1e-2, decompose end to end",
+            "n_gpus": world, "seconds": wall, "stage_seconds": met.stage_seconds,
+            "replicas_dropped": met.replicas_dropped, "mode_rel_err": rep.mode_rel_err,
+            "compression_elements_per_s": float(np.prod(dims)) / met.stage_seconds["compression"]}
 
 
 def _free_port():
@@ -522,6 +576,17 @@ def main():
             cpu = {"value": None, "unit": "elements/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    c3 = None
+    if not args.no_c3:
+        # free the C2 plan and block first: the C3 slabs need the HBM
+        plan.close()
+        del X
+        torch.cuda.empty_cache()
+        try:
+            c3 = cp_time_c3(xt, torch, world, rank, dev)
+        except Exception as e:
+            c3 = {"error": str(e)}
+
     if rank == 0:
         line = {
             "metric": "input tensor elements compressed/sec", "value": value, "unit": "elements/s",
@@ -535,11 +600,12 @@ def main():
                        "plan_create_s": round(t_plan, 3)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_f64_host": e2e_f64,
             "gpu_launches": int(launches),
-            "cp_time": cp, "parity": parity,
+            "cp_time": cp, "cp_time_c3": c3, "parity": parity,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    plan.close()
+    if args.no_c3:
+        plan.close()
     if world > 1:
         dist.destroy_process_group()
 
