@@ -2,33 +2,34 @@
 //
 // Eq. 3 restricted to the nonzeros (no reference counterpart):
 //   Z_k = sum_{(i,j) in slice k} x_ijk * U[:, i] (x) V_p[:, j]   (per replica)
-// then mode 3 over the slices exactly like the dense path.
+// then mode 3 over the slices exactly like the dense path (coo.cu
+// sparse_mode3).
 //
 // The SIMT fiber kernel (coo.cu) gathers a 1 KB stacked U column per nonzero
 // and spends P*L FMAs on it; nothing is reused across the fibers of a slice.
-// Here one CTA owns a slice k (dynamic slice counter, one CTA per SM) and
-// walks it in tiles of up to 64 fibers whose nonzeros touch at most 512
-// distinct i:
-//   1. densify: the tile's i are hashed in shared memory (2048 slots, open
-//      addressing) to local ids 0..ni-1 (Si = the distinct i), and the
-//      nonzeros are scattered as bf16/fp16 into a dense tile
-//      Xd[fiber][local i] (UMMA B operand, K-major SWIZZLE_128B; duplicate
-//      coordinates sum through shared-memory atomics);
-//   2. mode 1 per 128-row block rb of the stacked U (tcgen05, M = 128,
-//      N = 64 fibers, K = ni): D1 = U[rb rows, Si] * Xd^T, the U columns
-//      gathered from the i-major copy Ut[i][(p, l)] with 16-byte cp.async
-//      straight into the MN-major SWIZZLE_128B layout (a 4-slot ring, issued
-//      three chunks ahead of the MMA);
-//   3. mode 2 (tcgen05, M = 128, N = (128/Lpad)*Mpad, K = fibers): D1 drained
-//      to bf16 in shared memory (K-major) times V[(p, m), j_f] gathered from
-//      the j-major copy Vtj (MN-major); the diagonal replica blocks of D2 are
-//      added into Z[p][slice][m][l] (the slice's Z stays in L2 across tiles).
-// A tile whose i support exceeds 512 is retried with half the fibers; a
-// single fiber is cut into 512-nonzero pieces. Per nonzero the kernel reads
-// 8 B (i, value) from HBM once and the U gather is amortised over the tile's
-// fibers (C4: 464 fibers share each U column, ~16 B of L2->SM per nonzero
-// instead of 1 KB). Work per tile: 2*PL*64*ni (mode 1) + 2*PL*64*N2 (mode 2)
-// tensor flops.
+// Here a slice is cut into tiles of up to 64 fibers whose nonzeros touch at
+// most 512 distinct i, and both mode products of a tile run on the tensor
+// cores, so a U column is gathered once per tile instead of once per nonzero.
+//
+//   1. sparse_plan_kernel (several CTAs per SM, one per slice at a time): a
+//      shared-memory hash i -> local id that stays warm across the slice's
+//      tiles (one lookup pass per nonzero when the tile adds no new i; else
+//      claim + ids in slot order + lookup), table epochs whose id -> i lists
+//      go to si_g, a 16-bit code (tile fiber << 9 | id) per nonzero in li_g,
+//      a descriptor per tile; duplicate coordinates inside a tile are flagged.
+//   2. sparse_tc_kernel (one CTA per SM, 16 warps, planned tiles in a static
+//      order with the next tile prefetched to L2): warps 0-1 and 8-15 scatter
+//      the tile's values into a dense bf16 tile Xd[fiber][id] (K-major
+//      SWIZZLE_128B; CAS adds only for flagged tiles) while warps 2-7 gather
+//      the tile's U columns from the i-major copy Ut[i][(p, l)] (64-byte
+//      cp.async tasks into MN-major SWIZZLE_128B stages, 5-slot ring) and the
+//      V rows of its fibers (3 buffers); one thread issues mode 1 (M = 128
+//      stacked rows, N = 64 fibers, K = ids, A MN-major) and mode 2 (N =
+//      (128/Lpad)*Mpad, B MN-major) with mode 2 of block rb-1 after mode 1 of
+//      block rb; warps 8-15 drain D1 to bf16 and add the diagonal replica
+//      blocks of D2 into Z with fire-and-forget reductions.
+// Per nonzero: 4 B (planner) + 6 B (tensor kernel) from HBM, 2 B written;
+// per tile 2*PL*64*ni + 2*PL*64*N2 tensor flops and ni*PL*2 B of U over L2.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -40,7 +41,6 @@
 #include "gemm_simt.cuh"
 #include "plan.cuh"
 #include "sm100_ptx.cuh"
-#include "ttm_tc.cuh"
 
 namespace xtsg {
 

@@ -393,13 +393,6 @@ void launch_impl(const TtmLaunch& L, cudaStream_t st) {
 
 }  // namespace
 
-// exported for the other TMA users (sparse_tc.cu): 2-D, SWIZZLE_128B
-void make_tma_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                     uint32_t box_inner, uint32_t box_outer, bool f16) {
-  const uint64_t dims[2] = {inner, outer}, str[1] = {row_bytes};
-  const uint32_t box[2] = {box_inner, box_outer};
-  make_map(m, base, 2, dims, str, box, f16);
-}
 
 void launch_ttm_fused(const TtmLaunch& L, cudaStream_t st) {
   if (L.prm.n2 > 128 || L.prm.n2 % 16 || L.prm.lpad * L.prm.rpb != BM)

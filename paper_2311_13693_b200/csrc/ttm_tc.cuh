@@ -1,5 +1,4 @@
 #pragma once
-#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -55,7 +54,6 @@ int ttm_cluster_size();
 bool ttm_pair_supported(const TtmLaunch& l);
 void launch_ttm_pair(const TtmLaunch& l, cudaStream_t st);
 bool ttm_pair_enabled();
-void make_tma_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-                     uint32_t box_inner, uint32_t box_outer, bool f16);
+
 
 }  // namespace xtsg
