@@ -846,15 +846,27 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
     const int64_t target = int64_t(1) << 30;  // ~1 GiB of bf16 per slab
     int64_t ks = std::max<int64_t>(1, target / std::max<int64_t>(1, ldi * ext[1] * 2));
     ks = std::min(ks, ext[2]);
-    DevBuf<__nv_bfloat16> stage(static_cast<size_t>(ks * ext[1] * ldi), s), stage_lo;
-    if (comp()) stage_lo = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * ext[1] * ldi), s);
+    const int64_t nslabs = ceil_div(ext[2], ks);
+    // device input: the staging kernel fills slab s+1 on the side stream while
+    // the tensor cores consume slab s (two stage buffers, one max|x| slot each
+    // in the compensated mode); host input stages on s behind the H2D ring
+    static const bool overlap_env = [] {
+      const char* e = std::getenv("XTSG_GEN_OVERLAP");
+      return !(e && std::atoi(e) == 0);
+    }();
+    const bool overlap = x_dev && overlap_env && nslabs > 1;
+    DevBuf<__nv_bfloat16> stage[2], stage_lo[2];
+    for (int b = 0; b < (overlap ? 2 : 1); ++b) {
+      stage[b] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * ext[1] * ldi), s);
+      if (comp()) stage_lo[b] = DevBuf<__nv_bfloat16>(static_cast<size_t>(ks * ext[1] * ldi), s);
+    }
     DevBuf<uint8_t> raw[2];
+    for (int b = 0; b < 2; ++b) {
+      if (!ev_copied[b]) XCUDA(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
+      if (!ev_consumed[b]) XCUDA(cudaEventCreateWithFlags(&ev_consumed[b], cudaEventDisableTiming));
+    }
     if (!x_dev) {
-      for (int b = 0; b < 2; ++b) {
-        raw[b] = DevBuf<uint8_t>(static_cast<size_t>(ks * slab_bytes_raw), s);
-        if (!ev_copied[b]) XCUDA(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
-        if (!ev_consumed[b]) XCUDA(cudaEventCreateWithFlags(&ev_consumed[b], cudaEventDisableTiming));
-      }
+      for (int b = 0; b < 2; ++b) raw[b] = DevBuf<uint8_t>(static_cast<size_t>(ks * slab_bytes_raw), s);
       XCUDA(cudaStreamSynchronize(s));  // raw buffers allocated before copy_st uses them
     }
     const uint8_t* xb = static_cast<const uint8_t*>(x);
@@ -865,61 +877,90 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
       XCUDA(cudaMemcpyAsync(raw[b].ptr, xb + k0 * ld[1] * es, bytes, cudaMemcpyHostToDevice, copy_st));
       XCUDA(cudaEventRecord(ev_copied[b], copy_st));
     };
-    const int64_t nslabs = ceil_div(ext[2], ks);
-    if (!x_dev) {
-      // mark both buffers free
-      for (int b = 0; b < 2; ++b) XCUDA(cudaEventRecord(ev_consumed[b], s));
-      issue_copy(0, 0);
-    }
-    bool acc = acc_first;
-    for (int64_t sl = 0; sl < nslabs; ++sl) {
-      const int64_t k0 = sl * ks, kn = std::min(ks, ext[2] - k0);
-      const int b = static_cast<int>(sl & 1);
-      const uint8_t* src;
-      if (!x_dev) {
-        if (sl + 1 < nslabs) issue_copy(sl + 1, 1 - b);
-        XCUDA(cudaStreamWaitEvent(s, ev_copied[b], 0));
-        src = raw[b].ptr;
-      } else {
-        src = xb + k0 * ld[1] * es;
-      }
+    // slab sl of `src` -> stage[b] (and stage_lo[b], amax slot b) on stream ss
+    auto stage_slab = [&](int64_t sl, const uint8_t* src, int b, cudaStream_t ss) {
+      const int64_t kn = std::min(ks, ext[2] - sl * ks);
       const int64_t rows = kn * ext[1];
       const int blocks = static_cast<int>(std::min<int64_t>(rows, 148 * 8));
       const bool h = fp16();
       if (comp()) {
-        XCUDA(cudaMemsetAsync(amax.ptr, 0, sizeof(unsigned), s));
-        auto* hi = reinterpret_cast<__half*>(stage.ptr);
-        auto* lo = reinterpret_cast<__half*>(stage_lo.ptr);
+        unsigned* am = amax.ptr + b;
+        XCUDA(cudaMemsetAsync(am, 0, sizeof(unsigned), ss));
+        auto* hi = reinterpret_cast<__half*>(stage[b].ptr);
+        auto* lo = reinterpret_cast<__half*>(stage_lo[b].ptr);
         if (dtype == XTSG_DTYPE_F64)
-          split_x_kernel<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
-                                                         ld[0], ld[1], ldi, hi, lo, amax.ptr);
+          split_x_kernel<double><<<blocks, 256, 0, ss>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
+                                                          ld[0], ld[1], ldi, hi, lo, am);
         else if (dtype == XTSG_DTYPE_F32)
-          split_x_kernel<float><<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(src), ext[0], ext[1], kn,
-                                                        ld[0], ld[1], ldi, hi, lo, amax.ptr);
+          split_x_kernel<float><<<blocks, 256, 0, ss>>>(reinterpret_cast<const float*>(src), ext[0], ext[1], kn,
+                                                         ld[0], ld[1], ldi, hi, lo, am);
         else if (dtype == XTSG_DTYPE_F16)
-          split_x_kernel<__half><<<blocks, 256, 0, s>>>(reinterpret_cast<const __half*>(src), ext[0], ext[1], kn,
-                                                         ld[0], ld[1], ldi, hi, lo, amax.ptr);
+          split_x_kernel<__half><<<blocks, 256, 0, ss>>>(reinterpret_cast<const __half*>(src), ext[0], ext[1], kn,
+                                                          ld[0], ld[1], ldi, hi, lo, am);
         else
-          split_x_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(src), ext[0],
-                                                                ext[1], kn, ld[0], ld[1], ldi, hi, lo, amax.ptr);
+          split_x_kernel<__nv_bfloat16><<<blocks, 256, 0, ss>>>(reinterpret_cast<const __nv_bfloat16*>(src),
+                                                                 ext[0], ext[1], kn, ld[0], ld[1], ldi, hi, lo, am);
       } else if (dtype == XTSG_DTYPE_F64)
-        stage_x_kernel<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
-                                                       ld[0], ld[1], ldi, stage.ptr, h);
+        stage_x_kernel<double><<<blocks, 256, 0, ss>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
+                                                        ld[0], ld[1], ldi, stage[b].ptr, h);
       else if (dtype == XTSG_DTYPE_F32)
-        stage_x_kernel<float><<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(src), ext[0], ext[1], kn,
-                                                      ld[0], ld[1], ldi, stage.ptr, h);
+        stage_x_kernel<float><<<blocks, 256, 0, ss>>>(reinterpret_cast<const float*>(src), ext[0], ext[1], kn,
+                                                       ld[0], ld[1], ldi, stage[b].ptr, h);
       else if (dtype == XTSG_DTYPE_F16)
-        stage_x_kernel<__half><<<blocks, 256, 0, s>>>(reinterpret_cast<const __half*>(src), ext[0], ext[1], kn,
-                                                       ld[0], ld[1], ldi, stage.ptr, h);
+        stage_x_kernel<__half><<<blocks, 256, 0, ss>>>(reinterpret_cast<const __half*>(src), ext[0], ext[1], kn,
+                                                        ld[0], ld[1], ldi, stage[b].ptr, h);
       else
-        stage_x_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(src), ext[0],
-                                                              ext[1], kn, ld[0], ld[1], ldi, stage.ptr, h);
+        stage_x_kernel<__nv_bfloat16><<<blocks, 256, 0, ss>>>(reinterpret_cast<const __nv_bfloat16*>(src), ext[0],
+                                                               ext[1], kn, ld[0], ld[1], ldi, stage[b].ptr, h);
       XLAUNCH_CHECK();
-      if (!x_dev) XCUDA(cudaEventRecord(ev_consumed[b], s));
+    };
+    bool acc = acc_first;
+    auto ttm_slab = [&](int64_t sl, int b) {
+      const int64_t k0 = sl * ks, kn = std::min(ks, ext[2] - k0);
       const int64_t soff[3] = {off[0], off[1], off[2] + k0};
       const int64_t sext[3] = {ext[0], ext[1], kn};
-      run_bf16_block(stage.ptr, ldi, ldi * ext[1], soff, sext, ydst, acc, s, comp() ? stage_lo.ptr : nullptr);
+      cur_amax = comp() ? amax.ptr + b : nullptr;
+      run_bf16_block(stage[b].ptr, ldi, ldi * ext[1], soff, sext, ydst, acc, s,
+                     comp() ? stage_lo[b].ptr : nullptr);
+      cur_amax = nullptr;
       acc = true;
+    };
+    if (overlap) {
+      for (int b = 0; b < 2; ++b) XCUDA(cudaEventRecord(ev_consumed[b], s));
+      XCUDA(cudaStreamWaitEvent(copy_st, ev_consumed[0], 0));
+      stage_slab(0, xb, 0, copy_st);
+      XCUDA(cudaEventRecord(ev_copied[0], copy_st));
+      for (int64_t sl = 0; sl < nslabs; ++sl) {
+        const int b = static_cast<int>(sl & 1);
+        if (sl + 1 < nslabs) {
+          XCUDA(cudaStreamWaitEvent(copy_st, ev_consumed[1 - b], 0));
+          stage_slab(sl + 1, xb + (sl + 1) * ks * ld[1] * es, 1 - b, copy_st);
+          XCUDA(cudaEventRecord(ev_copied[1 - b], copy_st));
+        }
+        XCUDA(cudaStreamWaitEvent(s, ev_copied[b], 0));
+        ttm_slab(sl, b);
+        XCUDA(cudaEventRecord(ev_consumed[b], s));
+      }
+    } else {
+      if (!x_dev) {
+        // mark both raw buffers free
+        for (int b = 0; b < 2; ++b) XCUDA(cudaEventRecord(ev_consumed[b], s));
+        issue_copy(0, 0);
+      }
+      for (int64_t sl = 0; sl < nslabs; ++sl) {
+        const int b = static_cast<int>(sl & 1);
+        const uint8_t* src;
+        if (!x_dev) {
+          if (sl + 1 < nslabs) issue_copy(sl + 1, 1 - b);
+          XCUDA(cudaStreamWaitEvent(s, ev_copied[b], 0));
+          src = raw[b].ptr;
+        } else {
+          src = xb + sl * ks * ld[1] * es;
+        }
+        stage_slab(sl, src, 0, s);
+        if (!x_dev) XCUDA(cudaEventRecord(ev_consumed[b], s));
+        ttm_slab(sl, 0);
+      }
     }
   }
   if (comp()) {
