@@ -135,11 +135,6 @@ __device__ __forceinline__ int atoms_add(int* p, int v) {
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(ptx::smem_u32(p)), "r"(v) : "memory");
   return old;
 }
-__device__ __forceinline__ uint32_t atoms_or(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(ptx::smem_u32(p)), "r"(v) : "memory");
-  return old;
-}
 
 // x += v on a 16-bit float at shared address a (bf16 or fp16): CAS on its
 // 32-bit word (sm_100 has no native shared-memory float reduction)
@@ -325,16 +320,17 @@ __global__ void __launch_bounds__(PL_NT, 4) sparse_plan_kernel(const SpPlanParam
             ovf = 1;  // here: a miss
             return;
           }
-          bool d = false;
 #pragma unroll
           for (int e = 0; e < B; ++e) {
             if (e >= n) continue;
             while (tfp[fl + 1] <= xs[e]) ++fl;
             p.li_g[e_in + xs[e]] = static_cast<uint16_t>((fl << 9) | li[e]);  // fiber (6 bits) | id (9 bits)
             const int bit = fl * SP_NI + li[e];
-            d |= (atoms_or(&seen[bit >> 5], 1u << (bit & 31)) >> (bit & 31)) & 1u;
+            // occupancy of (fiber, id): fire-and-forget; duplicates show as
+            // fewer set bits than nonzeros (counted after the pass)
+            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(ptx::smem_u32(&seen[bit >> 5])), "r"(1u << (bit & 31))
+                         : "memory");
           }
-          if (d) dup = 1;
         });
       };
       bool hit = false;
@@ -440,6 +436,20 @@ __global__ void __launch_bounds__(PL_NT, 4) sparse_plan_kernel(const SpPlanParam
         __syncthreads();
       }
       committed = lds_volatile(&count);
+      {  // duplicate coordinates <=> fewer occupied (fiber, id) cells than nonzeros
+        int c = 0;
+        for (int w = tid; w < nf * (SP_NI / 32); w += PL_NT) c += __popc(seen[w]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if ((tid & 31) == 0) wsum[tid >> 5] = c;
+        __syncthreads();
+        if (tid == 0) {
+          int tot = 0;
+          for (int w = 0; w < PL_NT / 32; ++w) tot += wsum[w];
+          dup = tot != static_cast<int>(e_end - e_in);
+        }
+        __syncthreads();
+      }
       if (tid == 0) {
         const unsigned long long t = atomicAdd(p.counters + 1, 1ull);
         if (static_cast<int64_t>(t) < p.max_tiles) {
