@@ -3,7 +3,10 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -65,6 +68,37 @@ void require_device() {
     XCUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     pool_dev = dev;
   }
+}
+
+PhaseTrace::PhaseTrace(const char* n, cudaStream_t s) : name(n), st(s) {
+  const char* e = std::getenv("XTSG_TRACE");
+  on = e && std::atoi(e) != 0;
+  if (on) mark("begin");
+}
+
+void PhaseTrace::mark(const char* label) {
+  if (!on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  ev.emplace_back(label, e);
+  host.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count());
+}
+
+PhaseTrace::~PhaseTrace() {
+  if (!on) return;
+  mark("end");
+  cudaEventSynchronize(ev.back().second);
+  std::string out = std::string("[xtsg trace] ") + name + ":";
+  for (size_t q = 1; q < ev.size(); ++q) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[q - 1].second, ev[q].second);
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), " %s %.2f/%.2f", ev[q].first, ms, host[q] - host[q - 1]);
+    out += buf;
+  }
+  std::fprintf(stderr, "%s (device/host ms)\n", out.c_str());
+  for (auto& e : ev) cudaEventDestroy(e.second);
 }
 
 int sm_count() {

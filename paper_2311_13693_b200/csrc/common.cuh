@@ -154,4 +154,18 @@ struct OutView {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Phase trace (XTSG_TRACE=1): device time between marks on one stream plus
+// the host wall time, printed to stderr when the tracer goes out of scope.
+// Diagnostics only; inactive (no events recorded) unless the variable is set.
+struct PhaseTrace {
+  const char* name;
+  cudaStream_t st;
+  bool on;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  std::vector<double> host;
+  PhaseTrace(const char* n, cudaStream_t s);
+  void mark(const char* label);
+  ~PhaseTrace();
+};
+
 }  // namespace xtsg

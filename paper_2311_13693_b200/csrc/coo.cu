@@ -338,9 +338,11 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
     if (yo.host) yo.finish();
     return;
   }
+  PhaseTrace tr("compress_coo", s);
   ensure_sparse_operands(s);
   InView<int32_t> di(i, static_cast<size_t>(nnz), s), dj(j, static_cast<size_t>(nnz), s), dk(k, static_cast<size_t>(nnz), s);
   InView<float> dv(val, static_cast<size_t>(nnz), s);
+  tr.mark("inputs");
   // 1. keys, validation, sortedness
   DevBuf<uint64_t> keys(static_cast<size_t>(nnz), s);
   DevBuf<uint64_t> idx(static_cast<size_t>(nnz), s);  // packed (i, value)
@@ -354,6 +356,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   int hf[2] = {0, 0};
   XCUDA(cudaMemcpyAsync(hf, flags.ptr, sizeof(hf), cudaMemcpyDeviceToHost, s));
   XCUDA(cudaStreamSynchronize(s));
+  tr.mark("keys");
   if (hf[0]) data_error("plan_compress_coo: coordinate outside the tensor");
   const int32_t *si = di.dev, *sj = dj.dev, *sk = dk.dev;
   const float* sv = dv.dev;
@@ -376,6 +379,7 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
       if (dkeys.Current() != keys2.ptr) std::swap(keys, keys2);
       if (dpay.Current() != idx2.ptr) std::swap(idx, idx2);
     }
+    tr.mark("sort");
     keys.release();
     idx.release();
     if (sparse_tc_ok()) {

@@ -859,6 +859,7 @@ void Plan::sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* sl
                      const int64_t* fiber_ptr, const int32_t* fiber_j, int64_t nnz, const int32_t* nz_i,
                      const float* val, float* ydev, bool accumulate, cudaStream_t s) {
   const int64_t plrows = vP * lpad;
+  PhaseTrace tr("sparse_tc", s);
   DevBuf<float> z(static_cast<size_t>(vP * n_slices * mpad * lpad), s);
   z.zero();  // the tensor kernel adds every tile's contribution (empty slices stay zero)
   // 1. plan the tiles (every tile holds >= 1 nonzero and is either whole
@@ -883,8 +884,10 @@ void Plan::sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* sl
     int per_sm = 1;
     XCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sparse_plan_kernel, PL_NT, 0));
     const int grid = static_cast<int>(std::min<int64_t>(n_slices, static_cast<int64_t>(sm_count()) * std::max(1, per_sm)));
+    tr.mark("alloc");
     sparse_plan_kernel<<<grid, PL_NT, 0, s>>>(pp);
     XLAUNCH_CHECK();
+    tr.mark("plan");
   }
   // 2. tensor-core tiles
   SpTcParams prm{};
@@ -915,7 +918,9 @@ void Plan::sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* sl
   if (fp16()) launch(sparse_tc_kernel<true>);
   else launch(sparse_tc_kernel<false>);
   XLAUNCH_CHECK();
+  tr.mark("tiles");
   sparse_mode3(z.ptr, slice_k, n_slices, ydev, accumulate, s);
+  tr.mark("mode3");
 }
 
 // sorted COO (keys = k*J + j ascending, payload = (i << 32) | value bits) ->
@@ -923,6 +928,7 @@ void Plan::sparse_tc(int64_t n_slices, const int32_t* slice_k, const int64_t* sl
 void Plan::sparse_tc_sorted(DevBuf<uint64_t>& skeys_buf, DevBuf<uint64_t>* spay_buf, const int32_t* si_in,
                             const float* sv_in, int64_t nnz, float* ydev, bool accumulate, cudaStream_t s) {
   const uint64_t* skeys = skeys_buf.ptr;
+  PhaseTrace tr("sparse_tc_sorted", s);
   const int64_t J = desc.dims[1];
   // fibers: runs of equal (k, j)
   DevBuf<uint64_t> fkeys(static_cast<size_t>(nnz), s);
@@ -952,6 +958,7 @@ void Plan::sparse_tc_sorted(DevBuf<uint64_t>& skeys_buf, DevBuf<uint64_t>* spay_
   int64_t nf = 0;
   XCUDA(cudaMemcpyAsync(&nf, nruns.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   XCUDA(cudaStreamSynchronize(s));
+  tr.mark("fiber_rle+unpack");
   if (nf >= (int64_t(1) << 31)) usage("plan_compress_coo: at most 2^31-1 distinct (j, k) fibers per call");
   DevBuf<int64_t> fptr(static_cast<size_t>(nf + 1), s);
   scan_ptr(fcnt.ptr, nf, fptr.ptr, s);
@@ -972,6 +979,7 @@ void Plan::sparse_tc_sorted(DevBuf<uint64_t>& skeys_buf, DevBuf<uint64_t>* spay_
   int64_t kd = 0;
   XCUDA(cudaMemcpyAsync(&kd, nruns.ptr + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   XCUDA(cudaStreamSynchronize(s));
+  tr.mark("slices");
   DevBuf<int64_t> sptr(static_cast<size_t>(kd + 1), s);
   scan_ptr(scnt.ptr, kd, sptr.ptr, s);
   scnt.release();
@@ -1026,6 +1034,7 @@ void Plan::sparse_tc_sorted(DevBuf<uint64_t>& skeys_buf, DevBuf<uint64_t>* spay_
   fj.release();
   bi.release();
   bv.release();
+  tr.mark("regroup");
   sparse_tc(kd, uk.ptr, sptr.ptr, nf, gptr.ptr, gj.ptr, nnz, gni.ptr, gnv.ptr, ydev, accumulate, s);
 }
 
