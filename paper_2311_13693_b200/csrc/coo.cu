@@ -343,6 +343,16 @@ void Plan::compress_coo(const int32_t* i, const int32_t* j, const int32_t* k, co
   InView<int32_t> di(i, static_cast<size_t>(nnz), s), dj(j, static_cast<size_t>(nnz), s), dk(k, static_cast<size_t>(nnz), s);
   InView<float> dv(val, static_cast<size_t>(nnz), s);
   tr.mark("inputs");
+  // tile path with compact (rank k, rank j) keys: 4-byte keys make the sort
+  // half the traffic of the 8-byte (k*J + j) keys; falls back to those when
+  // the used k and j values do not fit 32 bits together (XTSG_COO_KEY64=1 forces)
+  const char* k64 = std::getenv("XTSG_COO_KEY64");
+  if (sparse_tc_ok() && !(k64 && std::atoi(k64) != 0) &&
+      sparse_tc_coo32(di.dev, dj.dev, dk.dev, dv.dev, nnz, yo.dev, accumulate, s)) {
+    if (fp16()) check_finite16(yo.dev, ysz, s);
+    if (yo.host) yo.finish();
+    return;
+  }
   // 1. keys, validation, sortedness
   DevBuf<uint64_t> keys(static_cast<size_t>(nnz), s);
   DevBuf<uint64_t> idx(static_cast<size_t>(nnz), s);  // packed (i, value)

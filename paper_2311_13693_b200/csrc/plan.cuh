@@ -119,6 +119,14 @@ struct Plan {
   // skeys / spay are consumed (released as soon as they are read)
   void sparse_tc_sorted(DevBuf<uint64_t>& skeys, DevBuf<uint64_t>* spay, const int32_t* si, const float* sv,
                         int64_t nnz, float* ydev, bool accumulate, cudaStream_t s);
+  bool sparse_tc_coo32(const int32_t* i, const int32_t* j, const int32_t* k, const float* val, int64_t nnz,
+                       float* ydev, bool accumulate, cudaStream_t s);
+  // 32-bit (rank k, rank j) keys + (i, value) payload, already sorted
+  void sparse_tc_sorted32(DevBuf<uint32_t>& skeys, DevBuf<uint64_t>& spay, const int32_t* invk, const int32_t* invj,
+                          int64_t nju, int64_t nnz, float* ydev, bool accumulate, cudaStream_t s);
+  void sparse_tc_tail(int64_t nf, DevBuf<int64_t>& fptr, DevBuf<int32_t>& fj, DevBuf<int32_t>& fk,
+                      const int32_t* ni, const float* nv, DevBuf<int32_t>& bi, DevBuf<float>& bv, int64_t nnz,
+                      float* ydev, bool accumulate, cudaStream_t s);
 };
 
 // RAII use of a plan by one C-ABI call on stream s (see Plan::mu).

@@ -831,6 +831,77 @@ __global__ void fiber_gather_kernel(const int32_t* __restrict__ perm, const int6
   }
 }
 
+// ---- COO with compact (rank k, rank j) keys ----------------------------------
+// range check, used-k / used-j bitmaps (bits set once: read before the OR, the
+// few hot words of a block-structured tensor are not hammered), (k, j) order
+__global__ void coo_scan_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                const int32_t* __restrict__ kk, int64_t nnz, int64_t I, int64_t J, int64_t K,
+                                uint32_t* __restrict__ usedk, uint32_t* __restrict__ usedj, int* __restrict__ bad) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t i = ii[e], j = jj[e], k = kk[e];
+    if (i < 0 || i >= I || j < 0 || j >= J || k < 0 || k >= K) {
+      bad[0] = 1;
+      continue;
+    }
+    const uint32_t bk = 1u << (k & 31), bj = 1u << (j & 31);
+    if (!(__ldcg(usedk + (k >> 5)) & bk)) atomicOr(usedk + (k >> 5), bk);
+    if (!(__ldcg(usedj + (j >> 5)) & bj)) atomicOr(usedj + (j >> 5), bj);
+    if (e + 1 < nnz) {
+      const int32_t k2 = kk[e + 1], j2 = jj[e + 1];
+      if (k2 < k || (k2 == k && j2 < j)) bad[1] = 1;
+    }
+  }
+}
+
+__global__ void popc_kernel(const uint32_t* __restrict__ bits, int64_t nw, int32_t* __restrict__ cnt) {
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < nw;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    cnt[w] = __popc(bits[w]);
+}
+
+// rank -> value (the used k or j values in increasing order)
+__global__ void rank_inverse_kernel(const uint32_t* __restrict__ bits, const int64_t* __restrict__ base, int64_t nw,
+                                    int32_t* __restrict__ inv) {
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < nw;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t b = bits[w];
+    int64_t r = base[w];
+    while (b) {
+      inv[r++] = static_cast<int32_t>(w * 32 + __ffs(b) - 1);
+      b &= b - 1;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t bit_rank(const uint32_t* bits, const int64_t* base, int32_t v) {
+  return static_cast<uint32_t>(base[v >> 5]) + __popc(bits[v >> 5] & ((1u << (v & 31)) - 1u));
+}
+
+// compact key rank(k) * nju + rank(j), payload (i << 32) | value bits
+__global__ void coo_ckey_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                const int32_t* __restrict__ kk, const float* __restrict__ vv, int64_t nnz,
+                                const uint32_t* __restrict__ usedk, const int64_t* __restrict__ basek,
+                                const uint32_t* __restrict__ usedj, const int64_t* __restrict__ basej, uint32_t nju,
+                                uint32_t* __restrict__ key, uint64_t* __restrict__ pay) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    key[e] = bit_rank(usedk, basek, kk[e]) * nju + bit_rank(usedj, basej, jj[e]);
+    pay[e] = (static_cast<uint64_t>(static_cast<uint32_t>(ii[e])) << 32) | __float_as_uint(vv[e]);
+  }
+}
+
+__global__ void fiber_decode32_kernel(const uint32_t* __restrict__ fkeys, int64_t nf, uint32_t nju,
+                                      const int32_t* __restrict__ invk, const int32_t* __restrict__ invj,
+                                      int32_t* __restrict__ fj, int32_t* __restrict__ fk) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nf;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t key = fkeys[e];
+    fj[e] = invj[key % nju];
+    fk[e] = invk[key / nju];
+  }
+}
+
 int gridn(int64_t work) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * 16))); }
 
 // exclusive scan of cnt[0..n) into ptr[0..n] (ptr[n] = total)
@@ -846,6 +917,68 @@ void scan_ptr(const T* cnt, int64_t n, int64_t* ptr, cudaStream_t s) {
 }
 
 }  // namespace
+
+// COO -> (validated, sorted) compact keys -> tile path. Returns false (having
+// done nothing but the validation) when rank(k) x rank(j) does not fit 32 bits.
+bool Plan::sparse_tc_coo32(const int32_t* i, const int32_t* j, const int32_t* k, const float* val, int64_t nnz,
+                           float* ydev, bool accumulate, cudaStream_t s) {
+  const int64_t I = desc.dims[0], J = desc.dims[1], K = desc.dims[2];
+  PhaseTrace tr("sparse_tc_coo32", s);
+  const int64_t nwk = ceil_div(K, 32), nwj = ceil_div(J, 32);
+  DevBuf<uint32_t> usedk(static_cast<size_t>(nwk), s), usedj(static_cast<size_t>(nwj), s);
+  usedk.zero();
+  usedj.zero();
+  DevBuf<int> flags(2, s);
+  flags.zero();
+  coo_scan_kernel<<<gridn(nnz), 256, 0, s>>>(i, j, k, nnz, I, J, K, usedk.ptr, usedj.ptr, flags.ptr);
+  XLAUNCH_CHECK();
+  DevBuf<int32_t> ck(static_cast<size_t>(nwk), s), cj(static_cast<size_t>(nwj), s);
+  DevBuf<int64_t> basek(static_cast<size_t>(nwk + 1), s), basej(static_cast<size_t>(nwj + 1), s);
+  popc_kernel<<<gridn(nwk), 256, 0, s>>>(usedk.ptr, nwk, ck.ptr);
+  XLAUNCH_CHECK();
+  popc_kernel<<<gridn(nwj), 256, 0, s>>>(usedj.ptr, nwj, cj.ptr);
+  XLAUNCH_CHECK();
+  scan_ptr(ck.ptr, nwk, basek.ptr, s);
+  scan_ptr(cj.ptr, nwj, basej.ptr, s);
+  int hf[2] = {0, 0};
+  int64_t nku = 0, nju = 0;
+  XCUDA(cudaMemcpyAsync(hf, flags.ptr, sizeof(hf), cudaMemcpyDeviceToHost, s));
+  XCUDA(cudaMemcpyAsync(&nku, basek.ptr + nwk, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  XCUDA(cudaMemcpyAsync(&nju, basej.ptr + nwj, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  XCUDA(cudaStreamSynchronize(s));
+  tr.mark("scan");
+  if (hf[0]) data_error("plan_compress_coo: coordinate outside the tensor");
+  if (nku * nju >= (int64_t(1) << 32)) return false;
+  DevBuf<int32_t> invk(static_cast<size_t>(nku), s), invj(static_cast<size_t>(nju), s);
+  rank_inverse_kernel<<<gridn(nwk), 256, 0, s>>>(usedk.ptr, basek.ptr, nwk, invk.ptr);
+  XLAUNCH_CHECK();
+  rank_inverse_kernel<<<gridn(nwj), 256, 0, s>>>(usedj.ptr, basej.ptr, nwj, invj.ptr);
+  XLAUNCH_CHECK();
+  DevBuf<uint32_t> keys(static_cast<size_t>(nnz), s);
+  DevBuf<uint64_t> pay(static_cast<size_t>(nnz), s);
+  coo_ckey_kernel<<<gridn(nnz), 256, 0, s>>>(i, j, k, val, nnz, usedk.ptr, basek.ptr, usedj.ptr, basej.ptr,
+                                             static_cast<uint32_t>(nju), keys.ptr, pay.ptr);
+  XLAUNCH_CHECK();
+  tr.mark("keys");
+  if (hf[1]) {
+    DevBuf<uint32_t> keys2(static_cast<size_t>(nnz), s);
+    DevBuf<uint64_t> pay2(static_cast<size_t>(nnz), s);
+    int end_bit = 1;
+    while (end_bit < 32 && (uint64_t(1) << end_bit) < static_cast<uint64_t>(nku * nju)) ++end_bit;
+    cub::DoubleBuffer<uint32_t> dk(keys.ptr, keys2.ptr);
+    cub::DoubleBuffer<uint64_t> dp(pay.ptr, pay2.ptr);
+    size_t tb = 0;
+    XCUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dp, nnz, 0, end_bit, s));
+    DevBuf<uint8_t> tmp(tb, s);
+    XCUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, dk, dp, nnz, 0, end_bit, s));
+    count_launch();
+    if (dk.Current() != keys.ptr) std::swap(keys, keys2);
+    if (dp.Current() != pay.ptr) std::swap(pay, pay2);
+    tr.mark("sort");
+  }
+  sparse_tc_sorted32(keys, pay, invk.ptr, invj.ptr, nju, nnz, ydev, accumulate, s);
+  return true;
+}
 
 bool Plan::sparse_tc_ok() const {
   // XTSG_SPARSE_TC=0 selects the SIMT fiber kernel (read per call: tests A/B both)
@@ -967,17 +1100,67 @@ void Plan::sparse_tc_sorted(DevBuf<uint64_t>& skeys_buf, DevBuf<uint64_t>* spay_
   fiber_split_kernel<<<gridn(nf), 256, 0, s>>>(fkeys.ptr, nf, J, fj.ptr, fk.ptr);
   XLAUNCH_CHECK();
   fkeys.release();
+  sparse_tc_tail(nf, fptr, fj, fk, ni, nv, bi, bv, nnz, ydev, accumulate, s);
+
+}
+
+
+// sorted compact keys + (i, value) payload -> CSF fibers -> the shared tail
+void Plan::sparse_tc_sorted32(DevBuf<uint32_t>& skeys, DevBuf<uint64_t>& spay, const int32_t* invk,
+                              const int32_t* invj, int64_t nju, int64_t nnz, float* ydev, bool accumulate,
+                              cudaStream_t s) {
+  PhaseTrace tr("sparse_tc_sorted32", s);
+  DevBuf<uint32_t> fkeys(static_cast<size_t>(nnz), s);
+  DevBuf<int32_t> fcnt(static_cast<size_t>(nnz), s);
+  DevBuf<int64_t> nruns(1, s);
+  {
+    size_t tb = 0;
+    XCUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, skeys.ptr, fkeys.ptr, fcnt.ptr, nruns.ptr, nnz, s));
+    DevBuf<uint8_t> tmp(tb, s);
+    XCUDA(cub::DeviceRunLengthEncode::Encode(tmp.ptr, tb, skeys.ptr, fkeys.ptr, fcnt.ptr, nruns.ptr, nnz, s));
+    count_launch();
+  }
+  skeys.release();
+  DevBuf<int32_t> bi(static_cast<size_t>(nnz), s);
+  DevBuf<float> bv(static_cast<size_t>(nnz), s);
+  payload_unpack_kernel<<<gridn(nnz), 256, 0, s>>>(spay.ptr, nnz, bi.ptr, bv.ptr);
+  XLAUNCH_CHECK();
+  spay.release();
+  int64_t nf = 0;
+  XCUDA(cudaMemcpyAsync(&nf, nruns.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  XCUDA(cudaStreamSynchronize(s));
+  tr.mark("fiber_rle+unpack");
+  if (nf >= (int64_t(1) << 31)) usage("plan_compress_coo: at most 2^31-1 distinct (j, k) fibers per call");
+  DevBuf<int64_t> fptr(static_cast<size_t>(nf + 1), s);
+  scan_ptr(fcnt.ptr, nf, fptr.ptr, s);
+  fcnt.release();
+  DevBuf<int32_t> fj(static_cast<size_t>(nf), s), fk(static_cast<size_t>(nf), s);
+  fiber_decode32_kernel<<<gridn(nf), 256, 0, s>>>(fkeys.ptr, nf, static_cast<uint32_t>(nju), invk, invj, fj.ptr,
+                                                  fk.ptr);
+  XLAUNCH_CHECK();
+  fkeys.release();
+  sparse_tc_tail(nf, fptr, fj, fk, bi.ptr, bv.ptr, bi, bv, nnz, ydev, accumulate, s);
+}
+
+// fibers (nf, fptr, fj, fk in (k, j) order) + nonzero i / values -> slices,
+// regrouping by smallest i, the tile path. bi / bv own the nonzero arrays when
+// the caller unpacked them (released once regrouped).
+void Plan::sparse_tc_tail(int64_t nf, DevBuf<int64_t>& fptr, DevBuf<int32_t>& fj, DevBuf<int32_t>& fk,
+                          const int32_t* ni, const float* nv, DevBuf<int32_t>& bi, DevBuf<float>& bv, int64_t nnz,
+                          float* ydev, bool accumulate, cudaStream_t s) {
+  PhaseTrace tr("sparse_tc_tail", s);
+  DevBuf<int64_t> nruns(2, s);
   // slices: runs of equal k over the fibers
   DevBuf<int32_t> uk(static_cast<size_t>(nf), s), scnt(static_cast<size_t>(nf), s);
   {
     size_t tb = 0;
-    XCUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, fk.ptr, uk.ptr, scnt.ptr, nruns.ptr + 1, nf, s));
+    XCUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, fk.ptr, uk.ptr, scnt.ptr, nruns.ptr, nf, s));
     DevBuf<uint8_t> tmp(tb, s);
-    XCUDA(cub::DeviceRunLengthEncode::Encode(tmp.ptr, tb, fk.ptr, uk.ptr, scnt.ptr, nruns.ptr + 1, nf, s));
+    XCUDA(cub::DeviceRunLengthEncode::Encode(tmp.ptr, tb, fk.ptr, uk.ptr, scnt.ptr, nruns.ptr, nf, s));
     count_launch();
   }
   int64_t kd = 0;
-  XCUDA(cudaMemcpyAsync(&kd, nruns.ptr + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  XCUDA(cudaMemcpyAsync(&kd, nruns.ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   XCUDA(cudaStreamSynchronize(s));
   tr.mark("slices");
   DevBuf<int64_t> sptr(static_cast<size_t>(kd + 1), s);
@@ -1036,6 +1219,11 @@ void Plan::sparse_tc_sorted(DevBuf<uint64_t>& skeys_buf, DevBuf<uint64_t>* spay_
   bv.release();
   tr.mark("regroup");
   sparse_tc(kd, uk.ptr, sptr.ptr, nf, gptr.ptr, gj.ptr, nnz, gni.ptr, gnv.ptr, ydev, accumulate, s);
+  // COO calls return with their multi-GB temporaries back in the pool: a
+  // caller that enqueues the next call at once otherwise makes the pool map
+  // new memory while these are still pending (C4 COO steps of 71 ms became
+  // 185-450 ms back to back)
+  XCUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace xtsg
