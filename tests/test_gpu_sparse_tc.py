@@ -123,7 +123,7 @@ def test_csf_empty_slices_and_fibers(gpu, restated):
     t = _dense(dims, nz_i, jj, kk, val)
     for p in range(P):
         assert rel_diff(restated.comp(t, ens.u[p], ens.v[p], ens.w[p]), y[p]) <= TOL
-    # an i outside the tensor is rejected (checked by the tile planner) before any gather
+    # an i outside the tensor is rejected (range check on the device) before any gather
     for bad in (dims[0], -1):
         bi = nz_i.copy()
         bi[nnz // 2] = bad
