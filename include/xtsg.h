@@ -248,6 +248,21 @@ int32_t xtsg_multi_compress_factors(xtsg_multi* multi, const double* a, const do
  * xtsg_plan_compress; host memory is streamed to each GPU slab by slab) */
 int32_t xtsg_multi_compress(xtsg_multi* multi, const void* x, int32_t x_dtype, const int64_t ld[2], void* y,
                             int32_t accumulate);
+/* Sparse input across the GPUs (SURVEY §8 e: C4 at 1/2/4/8 GPUs; Eq. 3 is
+ * linear in the nonzeros, so any partition sums to the whole). Arguments as
+ * xtsg_plan_compress_coo / _csf; all inputs host memory (XTSG_E_USAGE for
+ * device pointers). COO: GPU g takes nonzeros [nnz*g/G, nnz*(g+1)/G) — a
+ * k-range for a k-sorted stream. CSF: GPU g takes a contiguous slice range
+ * holding ~1/G of the nonzeros (a k-range for k-sorted slices), pointers
+ * rebased on its worker thread. Each share runs as device calls of at most
+ * XTSG_SPARSE_CHUNK nonzeros (env, default 2^31; a CSF call holds at least
+ * one whole slice), accumulated on its GPU, then the one NCCL reduce. */
+int32_t xtsg_multi_compress_coo(xtsg_multi* multi, const int32_t* i, const int32_t* j, const int32_t* k,
+                                const float* val, int64_t nnz, void* y, int32_t accumulate);
+int32_t xtsg_multi_compress_csf(xtsg_multi* multi, int64_t n_slices, const int32_t* slice_k,
+                                const int64_t* slice_ptr, int64_t n_fibers, const int32_t* fiber_j,
+                                const int64_t* fiber_ptr, int64_t nnz, const int32_t* nz_i, const float* val,
+                                void* y, int32_t accumulate);
 /* device time of the last call: max over the GPUs of compress + reduce (ms) */
 int32_t xtsg_multi_last_ms(xtsg_multi* multi, double* ms);
 /* the NCCL version the multi-GPU path resolved (e.g. 22809), or XTSG_E_CUDA */

@@ -143,6 +143,8 @@ _SIGS = {
     "xtsg_multi_destroy": (None, [_P]),
     "xtsg_multi_compress_factors": (_I32, [_P, _P, _P, _P, _I64, _P, _I32]),
     "xtsg_multi_compress": (_I32, [_P, _P, _I32, _P, _P, _I32]),
+    "xtsg_multi_compress_coo": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _I32]),
+    "xtsg_multi_compress_csf": (_I32, [_P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I32]),
     "xtsg_multi_last_ms": (_I32, [_P, _P]),
     "xtsg_nccl_version": (_I32, [_P]),
     "xtsg_plan_compress_coo": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _I32, _P]),

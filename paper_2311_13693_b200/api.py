@@ -15,7 +15,7 @@ import numpy as np
 
 from ._lib import (AlsConfig, EnsembleSpec, PlanDesc, PipelineConfigC, PipelineMetricsC, DTYPE_BF16,
                    DTYPE_F32, DTYPE_F64, KIND_GAUSSIAN, KIND_SPARSE, KIND_TWO_STAGE, LAW_DENSE, LAW_SPARSE,
-                   MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE, PREC_BF16, PREC_FP64, DTYPE_F16, check, lib, ptr)
+                   MODE_DENSE, MODE_SPARSE, MODE_TWO_STAGE, PREC_BF16, PREC_FP64, DTYPE_F16, check, lib, ptr, UsageError)
 
 _KINDS = {"gaussian": KIND_GAUSSIAN, "sparse": KIND_SPARSE, "two_stage": KIND_TWO_STAGE}
 
@@ -381,6 +381,7 @@ class Plan:
         slice_k, fiber_j, nz_i = (as_arr(v, np.int32) for v in (slice_k, fiber_j, nz_i))
         slice_ptr, fiber_ptr = (as_arr(v, np.int64) for v in (slice_ptr, fiber_ptr))
         val = as_arr(val, np.float32)
+        _csf_shape_check(slice_k, slice_ptr, fiber_j, fiber_ptr, nz_i, val)
         y = self._y(device, y)
         st = _stream_arg(stream, y, nz_i, val)
         check(lib.xtsg_plan_compress_csf(self._h, int(slice_k.shape[0]), ptr(slice_k), ptr(slice_ptr),
@@ -438,6 +439,15 @@ class Plan:
         return [y[p * n:(p + 1) * n].reshape(tuple(reduced), order="F") for p in range(count)]
 
 
+def _csf_shape_check(slice_k, slice_ptr, fiber_j, fiber_ptr, nz_i, val):
+    """The C ABI reads slice_ptr[n_slices] and fiber_ptr[n_fibers]: the pointer
+    arrays must be one longer than their index arrays."""
+    if (slice_ptr.shape[0] != slice_k.shape[0] + 1 or fiber_ptr.shape[0] != fiber_j.shape[0] + 1
+            or nz_i.shape[0] != val.shape[0]):
+        raise UsageError("compress_csf: need len(slice_ptr) = len(slice_k) + 1, "
+                         "len(fiber_ptr) = len(fiber_j) + 1 and len(nz_i) = len(val)")
+
+
 class MultiPlan:
     """xtsg_multi_*: one plan per GPU of the node, mode-3 slabs per GPU and one
     NCCL reduce of the replicas onto the first GPU (SURVEY §8 e), driven from
@@ -489,6 +499,27 @@ class MultiPlan:
         ld = np.asarray([xa.shape[0], xa.shape[0] * xa.shape[1]], np.int64)
         y = self._y(y)
         check(lib.xtsg_multi_compress(self._h, ptr(xa), code, ptr(ld), ptr(y), 1 if accumulate else 0))
+        return y
+
+    def compress_coo(self, i, j, k, val, y=None, accumulate=False):
+        """xtsg_multi_compress_coo: host COO nonzeros, contiguous nonzero ranges per GPU."""
+        i, j, k = (np.ascontiguousarray(np.asarray(a, np.int32)) for a in (i, j, k))
+        val = np.ascontiguousarray(np.asarray(val, np.float32))
+        y = self._y(y)
+        check(lib.xtsg_multi_compress_coo(self._h, ptr(i), ptr(j), ptr(k), ptr(val), int(val.shape[0]), ptr(y),
+                                          1 if accumulate else 0))
+        return y
+
+    def compress_csf(self, slice_k, slice_ptr, fiber_j, fiber_ptr, nz_i, val, y=None, accumulate=False):
+        """xtsg_multi_compress_csf: host CSF, nonzero-balanced slice ranges per GPU."""
+        slice_k, fiber_j, nz_i = (np.ascontiguousarray(np.asarray(a, np.int32)) for a in (slice_k, fiber_j, nz_i))
+        slice_ptr, fiber_ptr = (np.ascontiguousarray(np.asarray(a, np.int64)) for a in (slice_ptr, fiber_ptr))
+        val = np.ascontiguousarray(np.asarray(val, np.float32))
+        _csf_shape_check(slice_k, slice_ptr, fiber_j, fiber_ptr, nz_i, val)
+        y = self._y(y)
+        check(lib.xtsg_multi_compress_csf(self._h, int(slice_k.shape[0]), ptr(slice_k), ptr(slice_ptr),
+                                          int(fiber_j.shape[0]), ptr(fiber_j), ptr(fiber_ptr), int(val.shape[0]),
+                                          ptr(nz_i), ptr(val), ptr(y), 1 if accumulate else 0))
         return y
 
     def last_ms(self) -> float:

@@ -173,6 +173,17 @@ struct Multi {
   // every GPU's partial replicas for its mode-3 slab, one grouped reduce to
   // GPU 0, then y (host or GPU-0 memory) = / += the sum
   void run(const std::function<void(int g, int64_t k0, int64_t k1)>& slab, void* y, bool accumulate) {
+    const int64_t K = desc.dims[2];
+    run_parts([&](int g) {
+      const int64_t k0 = K * g / n, k1 = K * (g + 1) / n;
+      if (k1 > k0) slab(g, k0, k1);
+      else XCUDA(cudaMemsetAsync(ybuf[g], 0, sizeof(float) * ysz, streams[g]));
+    }, y, accumulate);
+  }
+
+  // part(g) runs on GPU g's worker and must leave GPU g's complete partial
+  // replicas in ybuf[g] (on streams[g])
+  void run_parts(const std::function<void(int g)>& part, void* y, bool accumulate) {
     std::lock_guard<std::mutex> lk(mu);
     int caller_dev = 0;
     XCUDA(cudaGetDevice(&caller_dev));
@@ -180,14 +191,11 @@ struct Multi {
       int d;
       ~Restore() { cudaSetDevice(d); }
     } restore{caller_dev};
-    const int64_t K = desc.dims[2];
     std::vector<size_t> tickets(n);
     for (int g = 0; g < n; ++g) {
-      const int64_t k0 = K * g / n, k1 = K * (g + 1) / n;
-      tickets[g] = workers[g]->submit([=] {
+      tickets[g] = workers[g]->submit([=, &part] {
         XCUDA(cudaEventRecord(ev0[g], streams[g]));
-        if (k1 > k0) slab(g, k0, k1);
-        else XCUDA(cudaMemsetAsync(ybuf[g], 0, sizeof(float) * ysz, streams[g]));
+        part(g);
       });
     }
     std::exception_ptr first;
@@ -257,6 +265,48 @@ struct Multi {
     }
     for (auto c : comms)
       if (c) nccl().comm_destroy(c);
+  }
+};
+
+// ---- sparse input across the GPUs ---------------------------------------
+// Eq. 3 is linear in the nonzeros, so any partition of them compresses to
+// partial replicas that sum to the whole. COO: GPU g takes the contiguous
+// nonzero range [nnz*g/G, nnz*(g+1)/G) (a k-range when the stream is k-sorted,
+// as CSF producers and the reference's slab writers emit it; no host pass).
+// CSF: GPU g takes a contiguous slice range holding ~1/G of the nonzeros (a
+// k-range for k-sorted slices), its pointers rebased on the worker thread.
+// Every GPU's share is further cut into device calls of at most
+// XTSG_SPARSE_CHUNK nonzeros (default 2^31: one plan call's sort keys and
+// tile lists stay within 32-bit counts), accumulated in its partial.
+
+int64_t sparse_chunk() {
+  const char* e = std::getenv("XTSG_SPARSE_CHUNK");
+  const long long v = e ? std::atoll(e) : 0;
+  return v > 0 ? static_cast<int64_t>(v) : (int64_t(1) << 31);
+}
+
+void require_host(const void* p, const char* what) {
+  if (p && is_device_ptr(p))
+    usage(std::string(what) + ": sparse inputs of a multi-GPU call must be host memory");
+}
+
+// CSF slice boundaries: first nonzero of slice q (pointers clamped so that a
+// malformed input only misplaces a split; every part is validated on its GPU)
+struct CsfIndex {
+  int64_t n_slices, n_fibers, nnz;
+  const int64_t* slice_ptr;
+  const int64_t* fiber_ptr;
+  int64_t fib(int64_t q) const { return std::min(std::max<int64_t>(slice_ptr[q], 0), n_fibers); }
+  int64_t nz(int64_t f) const { return std::min(std::max<int64_t>(fiber_ptr[f], 0), nnz); }
+  int64_t start(int64_t q) const { return nz(fib(q)); }
+  // smallest q in [lo, hi] with start(q) >= target (start is monotone for valid input)
+  int64_t lower(int64_t lo, int64_t hi, int64_t target) const {
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (start(mid) < target) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
   }
 };
 
@@ -358,6 +408,82 @@ int32_t xtsg_multi_compress(xtsg_multi* mh, const void* x, int32_t x_dtype, cons
       const void* xs = static_cast<const uint8_t*>(x) + static_cast<size_t>(k0 * ld[1]) * es;
       const int32_t rc = xtsg_plan_compress(m->plans[g], xs, x_dtype, ld, off, ext, m->ybuf[g], 0, m->streams[g]);
       if (rc != XTSG_OK) throw Status(rc, xtsg_last_error(), xtsg_last_payload(0), xtsg_last_payload(1));
+    }, y, accumulate != 0);
+  });
+}
+
+int32_t xtsg_multi_compress_coo(xtsg_multi* mh, const int32_t* i, const int32_t* j, const int32_t* k,
+                                const float* val, int64_t nnz, void* y, int32_t accumulate) {
+  return guard([&] {
+    Multi* m = reinterpret_cast<Multi*>(mh);
+    if (nnz < 0) usage("multi_compress_coo: negative nnz");
+    if (nnz > 0 && (!i || !j || !k || !val)) usage("multi_compress_coo: null input");
+    for (const void* p : {static_cast<const void*>(i), static_cast<const void*>(j), static_cast<const void*>(k),
+                          static_cast<const void*>(val)})
+      require_host(p, "multi_compress_coo");
+    const int64_t chunk = sparse_chunk();
+    m->run_parts([&](int g) {
+      const int64_t e0 = nnz * g / m->n, e1 = nnz * (g + 1) / m->n;
+      if (e1 <= e0) {
+        XCUDA(cudaMemsetAsync(m->ybuf[g], 0, sizeof(float) * m->ysz, m->streams[g]));
+        return;
+      }
+      for (int64_t a = e0; a < e1; a += chunk) {
+        const int64_t b = std::min(e1, a + chunk);
+        const int32_t rc = xtsg_plan_compress_coo(m->plans[g], i + a, j + a, k + a, val + a, b - a, m->ybuf[g],
+                                                  a > e0 ? 1 : 0, m->streams[g]);
+        if (rc != XTSG_OK) throw Status(rc, xtsg_last_error(), xtsg_last_payload(0), xtsg_last_payload(1));
+      }
+    }, y, accumulate != 0);
+  });
+}
+
+int32_t xtsg_multi_compress_csf(xtsg_multi* mh, int64_t n_slices, const int32_t* slice_k, const int64_t* slice_ptr,
+                                int64_t n_fibers, const int32_t* fiber_j, const int64_t* fiber_ptr, int64_t nnz,
+                                const int32_t* nz_i, const float* val, void* y, int32_t accumulate) {
+  return guard([&] {
+    Multi* m = reinterpret_cast<Multi*>(mh);
+    if (n_slices < 0 || n_fibers < 0 || nnz < 0) usage("multi_compress_csf: negative size");
+    if (!slice_ptr || !fiber_ptr || (n_slices > 0 && !slice_k) || (n_fibers > 0 && !fiber_j) ||
+        (nnz > 0 && (!nz_i || !val)))
+      usage("multi_compress_csf: null input");
+    for (const void* p : {static_cast<const void*>(slice_k), static_cast<const void*>(slice_ptr),
+                          static_cast<const void*>(fiber_j), static_cast<const void*>(fiber_ptr),
+                          static_cast<const void*>(nz_i), static_cast<const void*>(val)})
+      require_host(p, "multi_compress_csf");
+    const CsfIndex ix{n_slices, n_fibers, nnz, slice_ptr, fiber_ptr};
+    // GPU g: slices [qs[g], qs[g+1]), ~1/G of the nonzeros each
+    const int G = m->n;
+    std::vector<int64_t> qs(static_cast<size_t>(G) + 1, 0);
+    qs[G] = n_slices;
+    if (n_slices > 0) {
+      const int64_t E0 = ix.start(0), E1 = std::max(E0, ix.start(n_slices));
+      for (int g = 1; g < G; ++g)
+        qs[g] = std::max(qs[g - 1], ix.lower(0, n_slices, E0 + (E1 - E0) * g / G));
+    }
+    const int64_t chunk = sparse_chunk();
+    m->run_parts([&](int g) {
+      bool first = true;
+      std::vector<int64_t> lsp, lfp;
+      for (int64_t qa = qs[g]; qa < qs[g + 1];) {
+        // extend the part while it holds at most `chunk` nonzeros (at least one slice)
+        int64_t qb = ix.lower(qa + 1, qs[g + 1], ix.start(qa) + chunk + 1);
+        if (qb > qa + 1 && ix.start(qb) - ix.start(qa) > chunk) --qb;
+        qb = std::max(qb, qa + 1);
+        const int64_t f0 = ix.fib(qa), f1 = std::max(f0, ix.fib(qb));
+        const int64_t e0 = ix.nz(f0), e1 = std::max(e0, ix.nz(f1));
+        lsp.resize(static_cast<size_t>(qb - qa) + 1);
+        for (int64_t t = 0; t <= qb - qa; ++t) lsp[t] = slice_ptr[qa + t] - f0;
+        lfp.resize(static_cast<size_t>(f1 - f0) + 1);
+        for (int64_t t = 0; t <= f1 - f0; ++t) lfp[t] = fiber_ptr[f0 + t] - e0;
+        const int32_t rc = xtsg_plan_compress_csf(m->plans[g], qb - qa, slice_k + qa, lsp.data(), f1 - f0,
+                                                  fiber_j + f0, lfp.data(), e1 - e0, nz_i + e0, val + e0,
+                                                  m->ybuf[g], first ? 0 : 1, m->streams[g]);
+        if (rc != XTSG_OK) throw Status(rc, xtsg_last_error(), xtsg_last_payload(0), xtsg_last_payload(1));
+        first = false;
+        qa = qb;
+      }
+      if (first) XCUDA(cudaMemsetAsync(m->ybuf[g], 0, sizeof(float) * m->ysz, m->streams[g]));
     }, y, accumulate != 0);
   });
 }

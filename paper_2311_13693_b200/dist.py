@@ -71,6 +71,60 @@ def compress_sharded(local_compress, K: int, y, dst: int = 0, group=None):
     return y
 
 
+def coo_share(nnz: int, rank: int, world: int) -> tuple[int, int]:
+    """Nonzeros [e0, e1) of rank `rank` for COO input: contiguous ranges, as
+    xtsg_multi_compress_coo splits them across the GPUs of one process (a
+    k-range when the stream is k-sorted). Eq. 3 is linear in the nonzeros,
+    so the partials of any partition sum to the whole."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("coo_share: bad rank/world")
+    return nnz * rank // world, nnz * (rank + 1) // world
+
+
+def csf_shares(slice_ptr, fiber_ptr, world: int) -> list[int]:
+    """Slice boundaries q_0 = 0 <= ... <= q_world = n_slices: rank g takes the
+    slices [q_g, q_g+1) holding ~1/world of the nonzeros (a k-range for
+    k-sorted slices) — the split xtsg_multi_compress_csf makes
+    (csrc/multi.cu, CsfIndex::lower)."""
+    import numpy as np
+
+    slice_ptr, fiber_ptr = np.asarray(slice_ptr, np.int64), np.asarray(fiber_ptr, np.int64)
+    n_slices, n_fibers, nnz = len(slice_ptr) - 1, len(fiber_ptr) - 1, int(fiber_ptr[-1]) if len(fiber_ptr) else 0
+    start = fiber_ptr[np.clip(slice_ptr, 0, n_fibers)].clip(0, max(nnz, 0))
+    qs = [0] * (world + 1)
+    qs[world] = n_slices
+    if n_slices > 0:
+        e0, e1 = int(start[0]), max(int(start[0]), int(start[-1]))
+        for g in range(1, world):
+            target = e0 + (e1 - e0) * g // world
+            qs[g] = max(qs[g - 1], min(n_slices, int(np.searchsorted(start, target, side="left"))))
+    return qs
+
+
+def csf_part(csf, q0: int, q1: int):
+    """Slices [q0, q1) of a CSF tuple (slice_k, slice_ptr, fiber_j, fiber_ptr,
+    nz_i, val) as a CSF of their own, pointers rebased to 0."""
+    slice_k, slice_ptr, fiber_j, fiber_ptr, nz_i, val = csf
+    f0, f1 = int(slice_ptr[q0]), int(slice_ptr[q1])
+    e0, e1 = int(fiber_ptr[f0]), int(fiber_ptr[f1])
+    return (slice_k[q0:q1], slice_ptr[q0:q1 + 1] - f0, fiber_j[f0:f1], fiber_ptr[f0:f1 + 1] - e0,
+            nz_i[e0:e1], val[e0:e1])
+
+
+def compress_sparse_sharded(local_compress, y, dst: int = 0, group=None):
+    """Sparse input across ranks: ``local_compress(rank, world, y)`` writes this
+    rank's partial replicas of its share (``coo_share`` / ``csf_shares``) into
+    y, then one sum-reduce to ``dst`` (NCCL on GPUs). Returns y (complete on dst)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    local_compress(rank, world, y)
+    if world > 1:
+        dist.reduce(y, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    return y
+
+
 def decompose_sharded(compress_slab, K: int, y, decompose_replicas, dst: int = 0, group=None):
     """The multi-GPU pipeline (SURVEY §8 e): every rank compresses its mode-3
     slab into partial replicas (``compress_slab(k0, k1, y)``), one sum-reduce

@@ -210,3 +210,81 @@ def test_gloo_world2_stage_failure_raises_everywhere(where):
     assert "returned" not in (out[0], out[1])
     msg = {"sharded": "no survivors", "stage1": "every replica failed", "finish": "ill-posed"}[where]
     assert msg in out[0] and msg in out[1]
+
+
+def _sparse_csf(dims, nnz, seed):
+    from paper_2311_13693_b200.api import Plan
+    rng = np.random.default_rng(seed)
+    i, j = rng.integers(0, dims[0], nnz), rng.integers(0, dims[1], nnz)
+    k = rng.integers(0, dims[2] // 2, nnz) * 2          # odd k empty
+    k[: nnz // 3] = 4                                   # one heavy slice
+    v = rng.standard_normal(nnz).astype(np.float32)
+    return (i, j, k, v), Plan.coo_to_csf(i, j, k, v)
+
+
+def _dense(dims, i, j, k, v):
+    t = np.zeros(dims, order="F")
+    np.add.at(t, (np.asarray(i), np.asarray(j), np.asarray(k)), np.asarray(v, np.float64))
+    return t
+
+
+def test_sparse_shares_partition():
+    from paper_2311_13693_b200.dist import coo_share, csf_part, csf_shares
+    for nnz in (0, 1, 5, 1000):
+        for world in (1, 2, 3, 8):
+            spans = [coo_share(nnz, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == nnz
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    (_, _, _, v), csf = _sparse_csf((20, 15, 40), 3000, 1)
+    for world in (1, 2, 3, 8):
+        qs = csf_shares(csf[1], csf[3], world)
+        assert qs[0] == 0 and qs[-1] == len(csf[0]) and all(a <= b for a, b in zip(qs, qs[1:]))
+        parts = [csf_part(csf, a, b) for a, b in zip(qs, qs[1:])]
+        assert sum(len(p[5]) for p in parts) == len(v)
+        for p in parts:
+            assert p[1][0] == 0 and p[1][-1] == len(p[2]) and p[3][0] == 0 and p[3][-1] == len(p[5])
+        # balance: no share beyond 1/world of the nonzeros plus the heaviest slice
+        heavy = int(np.diff(csf[3][csf[1]]).max())
+        assert max(len(p[5]) for p in parts) <= len(v) / world + heavy
+    assert csf_shares(np.zeros(1, np.int64), np.zeros(1, np.int64), 4) == [0, 0, 0, 0, 0]
+
+
+def _sparse_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Restated
+    from paper_2311_13693_b200.dist import compress_sparse_sharded, coo_share, csf_part, csf_shares
+    ora = Restated()
+    dims, red, P, S, seed = (20, 15, 40), (4, 3, 5), 3, 2, 7
+    u, vv, w = ora.make_ensemble(dims, red, P, S, seed=seed)
+    (i, j, k, v), csf = _sparse_csf(dims, 3000, 1)
+
+    def comp(t):
+        return torch.from_numpy(np.concatenate([ora.comp(t, u[p], vv[p], w[p]).ravel(order="F")
+                                                for p in range(P)]))
+
+    def local_csf(r, g, y):
+        qs = csf_shares(csf[1], csf[3], g)
+        sk, sp, fj, fp, ni, val = csf_part(csf, qs[r], qs[r + 1])
+        kk = np.repeat(np.repeat(sk, np.diff(sp)), np.diff(fp))
+        jj = np.repeat(fj, np.diff(fp))
+        y.copy_(comp(_dense(dims, ni, jj, kk, val)))
+
+    def local_coo(r, g, y):
+        e0, e1 = coo_share(len(v), r, g)
+        y.copy_(comp(_dense(dims, i[e0:e1], j[e0:e1], k[e0:e1], v[e0:e1])))
+
+    full = comp(_dense(dims, i, j, k, v)).numpy()
+    for name, fn in (("csf", local_csf), ("coo", local_coo)):
+        y = torch.zeros(P * int(np.prod(red)), dtype=torch.float64)
+        compress_sparse_sharded(fn, y)
+        if rank == 0:
+            out[name] = float(np.abs(y.numpy() - full).max() / np.abs(full).max())
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sparse_shares_match_one_shot():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sparse_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out["csf"] <= 1e-12 and out["coo"] <= 1e-12
