@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -692,7 +693,84 @@ int host_threads() {
   return n;
 }
 
+constexpr size_t kStageChunk = size_t(64) << 20;
+
+// process-wide pinned staging chunks (portable: any device's copy engine)
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<void*> free;
+  void* get() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (!free.empty()) {
+        void* p = free.back();
+        free.pop_back();
+        return p;
+      }
+    }
+    void* p = nullptr;
+    XCUDA(cudaHostAlloc(&p, kStageChunk, cudaHostAllocPortable));
+    return p;
+  }
+  void put(void* p) {
+    std::lock_guard<std::mutex> g(mu);
+    free.push_back(p);
+  }
+};
+
+PinnedPool& pinned_pool() {
+  static PinnedPool* pool = new PinnedPool;  // leaked: no CUDA calls at exit
+  return *pool;
+}
+
 }  // namespace
+
+void h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  static const bool staged = [] {
+    const char* e = std::getenv("XTSG_PINNED_STAGE");
+    return !(e && e[0] == '0');
+  }();
+  cudaPointerAttributes a{};
+  const bool pinned = cudaPointerGetAttributes(&a, src) == cudaSuccess && a.type == cudaMemoryTypeHost;
+  if (!pinned) cudaGetLastError();
+  if (pinned || !staged || bytes < (size_t(8) << 20)) {
+    XCUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  struct Stage {
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~Stage() {
+      for (int b = 0; b < 2; ++b) {
+        if (ev[b]) {
+          cudaEventSynchronize(ev[b]);
+          cudaEventDestroy(ev[b]);
+        }
+        if (buf[b]) pinned_pool().put(buf[b]);
+      }
+    }
+  } st;
+  for (int b = 0; b < 2; ++b) {
+    st.buf[b] = pinned_pool().get();
+    XCUDA(cudaEventCreateWithFlags(&st.ev[b], cudaEventDisableTiming));
+  }
+  const int nthr = host_threads();
+  const char* from = static_cast<const char*>(src);
+  char* to = static_cast<char*>(dst);
+  for (size_t off = 0, c = 0; off < bytes; off += kStageChunk, ++c) {
+    const int b = static_cast<int>(c & 1);
+    const size_t n = std::min(kStageChunk, bytes - off);
+    if (c >= 2) XCUDA(cudaEventSynchronize(st.ev[b]));  // its previous chunk has landed
+    char* hb = static_cast<char*>(st.buf[b]);
+    const int nt = static_cast<int>(std::min<size_t>(nthr, std::max<size_t>(1, n >> 22)));  // >= 4 MB per thread
+    run_workers(nt, [&](int t) {
+      const size_t a0 = (n * t / nt) & ~size_t(63), a1 = t + 1 == nt ? n : (n * (t + 1) / nt) & ~size_t(63);
+      std::memcpy(hb + a0, from + off + a0, a1 - a0);
+    });
+    XCUDA(cudaMemcpyAsync(to + off, hb, n, cudaMemcpyHostToDevice, s));
+    XCUDA(cudaEventRecord(st.ev[b], s));
+  }
+}
 
 // Host f32/f64 input on a bf16 plan: the data is narrowed to bf16 ON THE HOST
 // (multi-threaded, round-to-nearest-even exactly like the device conversion)
@@ -780,7 +858,7 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
     const void* xd = x;
     if (!x_dev) {
       raw = DevBuf<uint8_t>(x_span * es, s);
-      XCUDA(cudaMemcpyAsync(raw.ptr, x, x_span * es, cudaMemcpyHostToDevice, s));
+      h2d_copy(raw.ptr, x, x_span * es, s);
       xd = raw.ptr;
     }
     DevBuf<double> x64(static_cast<size_t>(ext[0] * ext[1] * ext[2]), s);
@@ -874,7 +952,7 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
       const int64_t k0 = slab * ks, kn = std::min(ks, ext[2] - k0);
       const size_t bytes = static_cast<size_t>(((kn - 1) * ld[1] + (ext[1] - 1) * ld[0] + ext[0]) * es);
       XCUDA(cudaStreamWaitEvent(copy_st, ev_consumed[b], 0));
-      XCUDA(cudaMemcpyAsync(raw[b].ptr, xb + k0 * ld[1] * es, bytes, cudaMemcpyHostToDevice, copy_st));
+      h2d_copy(raw[b].ptr, xb + k0 * ld[1] * es, bytes, copy_st);
       XCUDA(cudaEventRecord(ev_copied[b], copy_st));
     };
     // slab sl of `src` -> stage[b] (and stage_lo[b], amax slot b) on stream ss
@@ -947,11 +1025,12 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
         for (int b = 0; b < 2; ++b) XCUDA(cudaEventRecord(ev_consumed[b], s));
         issue_copy(0, 0);
       }
+      // slab sl's work is enqueued before the host copies slab sl + 1 (a
+      // pageable source makes the copy call return only once it has landed)
       for (int64_t sl = 0; sl < nslabs; ++sl) {
         const int b = static_cast<int>(sl & 1);
         const uint8_t* src;
         if (!x_dev) {
-          if (sl + 1 < nslabs) issue_copy(sl + 1, 1 - b);
           XCUDA(cudaStreamWaitEvent(s, ev_copied[b], 0));
           src = raw[b].ptr;
         } else {
@@ -960,6 +1039,7 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
         stage_slab(sl, src, 0, s);
         if (!x_dev) XCUDA(cudaEventRecord(ev_consumed[b], s));
         ttm_slab(sl, 0);
+        if (!x_dev && sl + 1 < nslabs) issue_copy(sl + 1, 1 - b);
       }
     }
   }

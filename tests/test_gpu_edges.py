@@ -80,3 +80,25 @@ def test_als_rank_guards_and_nan(gpu):
     bad[1, 1, 1] = np.nan
     with pytest.raises(gpu.DataError):
         gpu.cp_als(bad, 2)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp16x3"])
+def test_pageable_host_input_staged_copy(gpu, prec):
+    """Pageable host input of >= 8 MB is copied by host threads through pinned
+    64 MB chunks (h2d_copy): a tensor of 2 chunks plus a ragged tail must give
+    the same replicas as the same tensor resident on the device (bitwise on
+    the fp64 path; the compensated mode's fp64 mode-3 sums may reorder)."""
+    import torch
+    dims, red, P = (257, 251, 161), (16, 16, 8), 2      # 83 MB of fp64
+    x = np.asfortranarray(np.random.default_rng(4).standard_normal(dims))
+    plan = gpu.Plan(dims, red, P, 8, 5, precision=gpu.PREC_FP64 if prec == "fp64" else gpu.PREC_FP16X3)
+    yh = np.asarray(plan.compress(x))
+    xd = torch.from_numpy(x).cuda()
+    assert xd.stride() == (1, dims[0], dims[0] * dims[1])
+    yd = plan.compress(xd)
+    yd = yd.cpu().numpy() if hasattr(yd, "cpu") else np.asarray(yd)
+    if prec == "fp64":
+        assert np.array_equal(yh.ravel(), yd.ravel())
+    else:
+        assert rel_diff(yh.ravel(), yd.ravel()) <= 1e-12
+    plan.close()

@@ -72,6 +72,7 @@ def test_multi_sparse_chunked_vs_oracle(gpu, restated, monkeypatch):
     NCCL reduce; against the oracle's Eq. 3 over the dense tensor and against
     one plan call over all nonzeros."""
     dims, red, P, S, seed = (300, 200, 60), (32, 32, 16), 5, 8, 11
+    tol = 1e-2   # the sparse bf16 bar (test_gpu_sparse_tc.TOL): 24k nonzeros average little rounding
     i, j, k, v = _sparse_case(dims, 24000, 3)
     t = _dense(dims, i, j, k, v)
     u, vv, w = restated.make_ensemble(dims, red, P, S, seed)
@@ -82,15 +83,15 @@ def test_multi_sparse_chunked_vs_oracle(gpu, restated, monkeypatch):
     for chunk in ("3001", "100000"):     # 8 accumulated calls / one call
         monkeypatch.setenv("XTSG_SPARSE_CHUNK", chunk)
         y = mp.compress_coo(i, j, k, v)
-        assert max(rel_diff(a, b) for a, b in zip(want, gpu.Plan.replicas(y, P, red))) <= 5e-3
-        assert rel_diff(y1, y) <= 5e-3
+        assert max(rel_diff(a, b) for a, b in zip(want, gpu.Plan.replicas(y, P, red))) <= tol
+        assert rel_diff(y1, y) <= tol
         csf = gpu.Plan.coo_to_csf(i, j, k, v)
         yc = mp.compress_csf(*csf)
-        assert max(rel_diff(a, b) for a, b in zip(want, gpu.Plan.replicas(yc, P, red))) <= 5e-3
+        assert max(rel_diff(a, b) for a, b in zip(want, gpu.Plan.replicas(yc, P, red))) <= tol
     # the long fiber's slice (6000 nonzeros) exceeds the chunk: it runs whole
     monkeypatch.setenv("XTSG_SPARSE_CHUNK", "1000")
     yc2 = mp.compress_csf(*csf, y=yc.copy(), accumulate=True)
-    assert max(rel_diff(2 * a, b) for a, b in zip(want, gpu.Plan.replicas(yc2, P, red))) <= 5e-3
+    assert max(rel_diff(2 * a, b) for a, b in zip(want, gpu.Plan.replicas(yc2, P, red))) <= tol
     # empty input: zero replicas
     z = mp.compress_coo(i[:0], j[:0], k[:0], v[:0])
     assert not z.any()

@@ -157,6 +157,40 @@ def c4(args):
     _, _, hbm, src = peaks()
     rate = nnz / (ms / 1e3)
     achieved = 16.0 * rate / 1e9
+    host_multi = None
+    if args.host_multi:
+        # the same nonzeros from HOST memory through xtsg_multi_compress_* on
+        # this GPU (the C++ caller's route): H2D, validation, chunked device
+        # calls, NCCL reduce and the replica read-back all inside the wall time
+        host = [t.cpu().numpy() for t in (csf if csf is not None else (ci, cj, ck, cv))]
+        del y, plan
+        if csf is not None:
+            del csf, sk, sp, fj, fp, ni, nv
+        else:
+            del ci, cj, ck, cv
+        torch.cuda.empty_cache()
+        mp = xt.MultiPlan(dims, red, P, S, derive(2, 11), gpus=[0], precision=xt.PREC_BF16)
+        host_multi = []
+        for chunk in args.chunks:
+            os.environ["XTSG_SPARSE_CHUNK"] = str(chunk)
+            run = (lambda: mp.compress_csf(*host)) if args.csf else (lambda: mp.compress_coo(*host))
+            yh = run()
+            walls, dev_ms = [], []
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                yh = run()
+                walls.append(time.perf_counter() - t0)
+                dev_ms.append(mp.last_ms())
+            got = xt.Plan.replicas(yh, P, red)
+            herr = max(rel_diff(xt.comp_from_factors(f, ens.u[p], ens.v[p], ens.w[p]), got[p])
+                       for p in range(0, P, max(1, P // 4)))
+            w = float(np.median(walls))
+            host_multi.append({"chunk_nnz": chunk, "calls_per_step": -(-nnz // chunk), "wall_s": w,
+                               "e2e_nnz_per_s": nnz / w, "device_ms_max_over_gpus": float(np.median(dev_ms)),
+                               "h2d_bytes_per_step": int(sum(a.nbytes for a in host)),
+                               "max_rel_err_vs_comp_from_factors": float(herr)})
+        os.environ.pop("XTSG_SPARSE_CHUNK", None)
+        mp.close()
     emit({"config": f"C4: sparse COO 10^6^3 rank-{R}, {npc} nnz/col -> {nnz:.4g} nonzeros "
                     f"({'CSF input, no sort' if args.csf else 'pre-sorted by (k, j)' if args.presorted else 'unsorted: sort inside the step'}), "
                     f"P={P} replicas of 32^3",
@@ -166,7 +200,8 @@ def c4(args):
                        "achieved_gbs": achieved, "peak_gbs": hbm, "frac": achieved / hbm,
                        "fma_tflops": 2.0 * P * red[0] * rate / 1e12, "peak_source": src},
           "max_rel_err_vs_comp_from_factors": float(max(errs)), "tolerance": 1e-2,
-          "device_mem_free_gb": mem_free / 2**30, "torch_reserved_gb": torch.cuda.memory_reserved() / 2**30}, args.out)
+          "device_mem_free_gb": mem_free / 2**30, "torch_reserved_gb": torch.cuda.memory_reserved() / 2**30,
+          "host_input_multi_api": host_multi}, args.out)
 
 
 def c5(args):
@@ -317,6 +352,9 @@ def main():
     ap.add_argument("--nnz-per-col", type=int, default=464)
     ap.add_argument("--presorted", action="store_true")
     ap.add_argument("--csf", action="store_true")
+    ap.add_argument("--host-multi", action="store_true",
+                    help="c4: also time host input through xtsg_multi_compress_* (1 GPU)")
+    ap.add_argument("--chunks", type=int, nargs="+", default=[2 ** 31, 250_000_000])
     ap.add_argument("--n", type=int, default=4000)
     ap.add_argument("--L", type=int, nargs="+", default=[32, 64, 128])
     ap.add_argument("--P", type=int, nargs="+", default=[16, 32, 64, 128])
