@@ -77,6 +77,8 @@ def parse():
     ap.add_argument("--no-cp-time", action="store_true")
     ap.add_argument("--no-c3", action="store_true",
                     help="skip the north-star C3 decompose (10^4^3 rank 20, P = 124 x 128^3) after the C2 timing")
+    ap.add_argument("--no-c4", action="store_true",
+                    help="skip the sparse C4 line (10^6^3, 1e9 nonzeros as CSF; one GPU runs only)")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp16", "fp16x3"],
                     help="tensor-core operand type (fp16: 3 more mantissa bits, same speed; fp16x3: the "
                          "compensated hi/lo mode, ~1e-6 replicas at ~3x the tensor-core work)")
@@ -283,6 +285,80 @@ def cp_time_c3(xt, torch, world, rank, dev):
             "n_gpus": world, "seconds": wall, "stage_seconds": met.stage_seconds,
             "replicas_dropped": met.replicas_dropped, "mode_rel_err": rep.mode_rel_err,
             "compression_elements_per_s": float(np.prod(dims)) / met.stage_seconds["compression"]}
+
+
+def sparse_c4(xt, torch, dev):
+    """north_star config 4 (one GPU): the sparse 10^6 x 10^6 x 10^6 rank-10
+    tensor (464 nonzeros per factor column -> 10 dense 464^3 sub-cubes,
+    9.99e8 nonzeros), P = 16 replicas of 32^3, as CSF resident on the device
+    (tile planner + dense-tile tensor kernel, CUDA events on the call's
+    stream), then the same CSF from host memory through the multi-GPU C ABI
+    (xtsg_multi_compress_csf: pinned-staged H2D + NCCL reduce in the wall
+    time). Checked against comp_from_factors of the generating factors."""
+    dims, R, npc, red, P, S = (10 ** 6,) * 3, 10, 464, (32, 32, 32), 16, 8
+    f = xt.generate_factors(dims, R, law="sparse", nnz_per_col=npc, seed=1)
+    sk, fj, ni, nv = [], [], [], []
+    for r in range(R):
+        sup = [np.nonzero(f[m][:, r])[0] for m in range(3)]
+        val = [torch.tensor(f[m][sup[m], r], dtype=torch.float32, device=dev) for m in range(3)]
+        idx = [torch.tensor(x, dtype=torch.int32, device=dev) for x in sup]
+        na, nb, nc = (len(x) for x in sup)
+        sk.append(idx[2])
+        fj.append(idx[1].repeat(nc))
+        ni.append(idx[0].repeat(nc * nb))
+        nv.append((val[2].view(nc, 1, 1) * val[1].view(1, nb, 1) * val[0].view(1, 1, na)).reshape(-1))
+    sk, fj, ni, nv = (torch.cat(x) for x in (sk, fj, ni, nv))
+    sp = torch.arange(0, sk.numel() + 1, dtype=torch.int64, device=dev) * (fj.numel() // sk.numel())
+    fp = torch.arange(0, fj.numel() + 1, dtype=torch.int64, device=dev) * (ni.numel() // fj.numel())
+    csf = (sk, sp, fj, fp, ni, nv)
+    nnz = int(nv.numel())
+    seed = derive(2, 11)
+    plan = xt.Plan(dims, red, P, S, seed, precision=xt.PREC_BF16)
+    y = torch.zeros(P * int(np.prod(red)), dtype=torch.float32, device=dev)
+    st = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(st):
+        for _ in range(2):
+            plan.compress_csf(*csf, y=y, stream=st)
+        steps = 5
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            plan.compress_csf(*csf, y=y, stream=st)
+        e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ens = xt.make_ensemble(dims, red, P, S, seed)
+    from oracle.oracle import rel_diff
+    got = xt.Plan.replicas(y.cpu().numpy(), P, red)
+    err = max(rel_diff(xt.comp_from_factors(f, ens.u[p], ens.v[p], ens.w[p]), got[p]) for p in (0, P - 1))
+    plan.close()
+    host = [t.cpu().numpy() for t in csf]
+    del csf, sk, sp, fj, fp, ni, nv, y
+    torch.cuda.empty_cache()
+    mp = xt.MultiPlan(dims, red, P, S, seed, gpus=[dev.index or 0], precision=xt.PREC_BF16)
+    mp.compress_csf(*host)
+    walls = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        yh = mp.compress_csf(*host)
+        walls.append(time.perf_counter() - t0)
+    mp.close()
+    got = xt.Plan.replicas(yh, P, red)
+    herr = max(rel_diff(xt.comp_from_factors(f, ens.u[p], ens.v[p], ens.w[p]), got[p]) for p in (0, P - 1))
+    hbm = peaks()[2]
+    rate = nnz / (ms / 1e3)
+    wall = float(np.median(walls))
+    return {"config": "C4: sparse 10^6^3 rank-10, 464 nnz/col -> %.4g nonzeros as CSF, P=16 replicas of 32^3, "
+                      "bf16 tile path" % nnz,
+            "metric": "nonzeros compressed/sec", "value": rate, "unit": "nnz/s", "ms_per_step": ms,
+            "steps": steps, "roofline": {"bound": "hbm", "algorithmic_bytes_per_nnz": 16,
+                                         "achieved": 16.0 * rate / 1e9, "peak": hbm, "unit": "GB/s",
+                                         "frac": 16.0 * rate / 1e9 / hbm},
+            "max_rel_err_vs_comp_from_factors": float(err),
+            "e2e_host_csf_multi_api": {"value": nnz / wall, "unit": "nnz/s", "wall_s": wall,
+                                       "h2d_bytes_per_step": int(sum(a.nbytes for a in host)),
+                                       "d2h_bytes_per_step": int(yh.nbytes),
+                                       "max_rel_err_vs_comp_from_factors": float(herr)}}
 
 
 def _free_port():
@@ -587,6 +663,17 @@ def main():
         except Exception as e:
             c3 = {"error": str(e)}
 
+    c4 = None
+    if world == 1 and not args.no_c4:
+        if args.no_c3:
+            plan.close()
+            del X
+            torch.cuda.empty_cache()
+        try:
+            c4 = sparse_c4(xt, torch, dev)
+        except Exception as e:
+            c4 = {"error": str(e)}
+
     if rank == 0:
         line = {
             "metric": "input tensor elements compressed/sec", "value": value, "unit": "elements/s",
@@ -600,11 +687,11 @@ def main():
                        "plan_create_s": round(t_plan, 3)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_f64_host": e2e_f64,
             "gpu_launches": int(launches),
-            "cp_time": cp, "cp_time_c3": c3, "parity": parity,
+            "cp_time": cp, "cp_time_c3": c3, "sparse_c4": c4, "parity": parity,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if args.no_c3:
+    if args.no_c3 and not (world == 1 and not args.no_c4):
         plan.close()
     if world > 1:
         dist.destroy_process_group()
