@@ -1120,30 +1120,33 @@ namespace cg = cooperative_groups;
 // init (cp_als.cpp:62-76): normals, nvecs on attempt 1, and ||T||
 __global__ void __launch_bounds__(NT) als_init_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3,
                                                       double* ia, double* ib, double* ic, double* tnorm) {
+  // one CTA per (instance, mode): the three modes' normals and nvecs
+  // eigenproblems are independent, and the Gram + Jacobi workspace (2 rows^2,
+  // rows <= 64 on this path) lives in shared memory — the same arithmetic in
+  // the same order as the one-CTA in-kernel version, without an L2 round trip
+  // between the three barriers of every Jacobi rotation step
   extern __shared__ double sm[];
   const AlsInst in = insts[blockIdx.x];
+  const int mode = static_cast<int>(blockIdx.y);
   const int R = static_cast<int>(in.cfg.rank);
   const int mx = max(n1, max(n2, n3));
+  const int jac = max(mx, R) / 2 + 2;
   Smem s{};
   double* q = sm;
   s.red = q; q += 64;
-  s.cs = q; q += max(mx, R) / 2 + 2;
-  s.sn = q; q += max(mx, R) / 2 + 2;
-  s.pp = reinterpret_cast<int*>(q); q += max(mx, R) / 2 + 2;
-  s.qq = reinterpret_cast<int*>(q);
-  double* A = ia + static_cast<int64_t>(blockIdx.x) * n1 * R;
-  double* B = ib + static_cast<int64_t>(blockIdx.x) * n2 * R;
-  double* C = ic + static_cast<int64_t>(blockIdx.x) * n3 * R;
+  s.cs = q; q += jac;
+  s.sn = q; q += jac;
+  s.pp = reinterpret_cast<int*>(q); q += jac;
+  s.qq = reinterpret_cast<int*>(q); q += jac;
+  double* ws = q;  // G, V: rows x rows each
+  const int rows = mode == 0 ? n1 : mode == 1 ? n2 : n3;
+  double* F = mode == 0 ? ia + static_cast<int64_t>(blockIdx.x) * n1 * R
+            : mode == 1 ? ib + static_cast<int64_t>(blockIdx.x) * n2 * R
+                        : ic + static_cast<int64_t>(blockIdx.x) * n3 * R;
   const double tn = sqrt(norm_sq(in.t, static_cast<int64_t>(n1) * n2 * n3, s.red));
-  block_normals(derive(in.cfg.seed, 1), n1 * R, A, s.red);
-  block_normals(derive(in.cfg.seed, 2), n2 * R, B, s.red);
-  block_normals(derive(in.cfg.seed, 3), n3 * R, C, s.red);
-  if (in.cfg.init == 1 && tn > 0.0) {
-    nvecs_init(in.t, n1, n2, n3, 0, R, A, in.nvec_ws, s);
-    nvecs_init(in.t, n1, n2, n3, 1, R, B, in.nvec_ws, s);
-    nvecs_init(in.t, n1, n2, n3, 2, R, C, in.nvec_ws, s);
-  }
-  if (threadIdx.x == 0) tnorm[blockIdx.x] = tn;
+  block_normals(derive(in.cfg.seed, 1 + static_cast<uint64_t>(mode)), rows * R, F, s.red);
+  if (in.cfg.init == 1 && tn > 0.0) nvecs_init(in.t, n1, n2, n3, mode, R, F, ws, s);
+  if (mode == 0 && threadIdx.x == 0) tnorm[blockIdx.x] = tn;
 }
 
 struct ClusterLayout {
@@ -1445,8 +1448,10 @@ void launch_als_cluster(const AlsInst* din, int64_t count, int n1, int n2, int n
   DevBuf<double> ia(static_cast<size_t>(count * n1 * R), st), ib(static_cast<size_t>(count * n2 * R), st),
       ic(static_cast<size_t>(count * n3 * R), st), tn(static_cast<size_t>(count), st);
   const int mx = std::max(n1, std::max(n2, n3));
-  const size_t ismem = sizeof(double) * (64 + 4 * (std::max(mx, R) / 2 + 2));
-  als_init_kernel<<<static_cast<unsigned>(count), NT, ismem, st>>>(din, n1, n2, n3, ia.ptr, ib.ptr, ic.ptr, tn.ptr);
+  const size_t ismem = sizeof(double) * (64 + 4 * (std::max(mx, R) / 2 + 2) + 2 * static_cast<size_t>(mx) * mx);
+  XCUDA(cudaFuncSetAttribute(als_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ismem)));
+  als_init_kernel<<<dim3(static_cast<unsigned>(count), 3), NT, ismem, st>>>(din, n1, n2, n3, ia.ptr, ib.ptr, ic.ptr,
+                                                                           tn.ptr);
   XLAUNCH_CHECK();
   const size_t smem = cluster_layout(n1, n2, n3, R, CL).doubles * 8;
   auto go = [&](auto kern) {
