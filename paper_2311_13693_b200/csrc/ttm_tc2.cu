@@ -575,7 +575,12 @@ void launch_pair(const TtmLaunch& L, cudaStream_t st) {
     const char* e = std::getenv("XTSG_TTM_SYNCJ");
     return e ? std::atoi(e) : 0;
   }();
-  prm.sync_j = syncj_env > 0 ? syncj_env : prm.j_tiles;
+  // lane barrier spacing: once per slice when a slice is a few j tiles (C2:
+  // 8), every 4 j tiles for large slices (C3: 40 tiles, 200 MB per slice; the
+  // group's clusters drift apart within a slice and re-read X from DRAM).
+  // Measured at C3 (tools/c3_syncj_ab.sh, c3_traffic_sweep.sh): DRAM reads
+  // 190 -> 161 GB per 40-slice launch, 1072 -> 1091 TF/s (3 alternating reps)
+  prm.sync_j = syncj_env > 0 ? syncj_env : (prm.j_tiles >= 16 ? 4 : prm.j_tiles);
   if (prm.lanes && sched_env == 2 && L.sync) {
     XCUDA(cudaMemsetAsync(L.sync, 0, sizeof(unsigned) * prm.lanes, st));
     prm.sync = L.sync;
