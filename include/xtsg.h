@@ -182,11 +182,12 @@ int32_t xtsg_comp_naive_half(const double* t, int64_t n1, int64_t n2, int64_t n3
 #define XTSG_PREC_FP16 2   /* tcgen05 kind::f16, fp16 operands (3 more mantissa bits, range 65504:
                               U scaled by 2^-s / W by 2^s internally; overflow -> XTSG_E_HALFRANGE) */
 #define XTSG_PREC_FP16X3 3 /* compensated tensor-core mode (the reference's Eq. 5 split, mixed.cpp:18-24,
-                              done on tcgen05): every operand is an fp16 pair (hi, lo' = (x - hi) * 2^11)
-                              and each mode product is hi*hi + hi*lo + lo*hi (3 MMAs; lo*lo dropped,
-                              2^-22 relative), the mode-1 sum over i in chunks, the mode-3 sum over k in
-                              fp64; replicas ~1e-7 relative vs fp64. |x| must fit binary16
-                              (else XTSG_E_HALFRANGE); output fp32 like the other tensor-core modes */
+                              done on tcgen05): every operand is an fp16 pair (hi, lo = x - hi) after a
+                              power-of-two pre-scale that puts its max |x| in [2^13, 2^14) (any input
+                              magnitude), each mode product is hi*hi + hi*lo + lo*hi (3 MMAs; lo*lo
+                              dropped, 2^-22 relative), the mode-1 sum over i in chunks, the mode-3 sum
+                              over k in fp64; replicas ~2.5e-6 relative vs fp64 at C2/C3; output fp32
+                              like the other tensor-core modes */
 
 #define XTSG_DTYPE_BF16 0
 #define XTSG_DTYPE_F32 1

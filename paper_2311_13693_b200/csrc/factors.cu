@@ -23,13 +23,14 @@ namespace {
 constexpr int TI = 128, TJ = 64, NT = 256;
 
 // X[kk][j][i] (ld_i) = sum_r A[i,r] B[j,r] C[k0+kk,r]; A/B/C fp32 column-major.
-// Compensated plans (X_lo != null): fp16 hi into X, lo' = (x - hi) * 2^11
-// into X_lo, and the slab's max |x| into *amax (float bits).
+// Compensated plans (X_lo != null): x scaled by 2^comp_x_shift(amax) (amax: an
+// upper bound of |x| over the call, factor_bound_kernel), fp16 hi into X and
+// lo = x - hi into X_lo.
 __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                       const float* __restrict__ Cm, int64_t I, int64_t J, int64_t K,
                                                       int R, int64_t k0, int64_t ldi,
                                                       __nv_bfloat16* __restrict__ X, bool f16,
-                                                      __nv_bfloat16* __restrict__ X_lo, unsigned* __restrict__ amax) {
+                                                      __nv_bfloat16* __restrict__ X_lo, const unsigned* __restrict__ amax) {
   extern __shared__ float sm[];
   float* As = sm;            // R x TI
   float* Bs = sm + R * TI;   // R x TJ (already scaled by c_k)
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ 
       for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(av[a], bv[b], acc[a][b]);
   }
   if (X_lo) {
-    float m = 0.f;
+    const float sc = ldexpf(1.f, comp_x_shift(amax));
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int64_t j = j0 + ty + 16 * b;
@@ -70,17 +71,14 @@ __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ 
       const int64_t o = (kk * J + j) * ldi + i0 + tx * 8;
       float v8[8];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        v8[a] = i0 + tx * 8 + a < I ? acc[a][b] : 0.f;
-        m = fmaxf(m, fabsf(v8[a]));
-      }
+      for (int a = 0; a < 8; ++a) v8[a] = i0 + tx * 8 + a < I ? acc[a][b] * sc : 0.f;
       if (i0 + tx * 8 + 8 <= ldi) {
         uint32_t wh[4], wl[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const __half2 h = __floats2half2_rn(v8[2 * q], v8[2 * q + 1]);
           const float2 hf = __half22float2(h);
-          const __half2 l = __floats2half2_rn((v8[2 * q] - hf.x) * 2048.f, (v8[2 * q + 1] - hf.y) * 2048.f);
+          const __half2 l = __floats2half2_rn(v8[2 * q] - hf.x, v8[2 * q + 1] - hf.y);
           wh[q] = *reinterpret_cast<const uint32_t*>(&h);
           wl[q] = *reinterpret_cast<const uint32_t*>(&l);
         }
@@ -91,15 +89,12 @@ __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ 
         for (int a = 0; a < 8; ++a) {
           if (i0 + tx * 8 + a >= ldi) continue;
           const __half h = __float2half_rn(v8[a]);
-          const __half l = __float2half_rn((v8[a] - __half2float(h)) * 2048.f);
+          const __half l = __float2half_rn(v8[a] - __half2float(h));
           X[o + a] = __ushort_as_bfloat16(__half_as_ushort(h));
           X_lo[o + a] = __ushort_as_bfloat16(__half_as_ushort(l));
         }
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
     return;
   }
 #pragma unroll
@@ -120,6 +115,41 @@ __global__ void __launch_bounds__(NT) gen_slab_kernel(const float* __restrict__ 
           row[a] = f16 ? __ushort_as_bfloat16(__half_as_ushort(__float2half_rn(v))) : __float2bfloat16(v);
         }
     }
+  }
+}
+
+// |x_ijk| <= sum_r max_i |a_ir| max_j |b_jr| max_(k0 <= k < k1) |c_kr| (fp32
+// factors), stored as float bits in both amax slots: the compensated split's
+// scale for every slab of the call (one block)
+__global__ void factor_bound_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                    const float* __restrict__ Cm, int64_t I, int64_t J, int64_t K, int R, int64_t k0,
+                                    int64_t k1, unsigned* __restrict__ amax) {
+  __shared__ float red[3][32];
+  float total = 0.f;
+  for (int r = 0; r < R; ++r) {
+    float m[3] = {0.f, 0.f, 0.f};
+    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) m[0] = fmaxf(m[0], fabsf(A[i + I * r]));
+    for (int64_t j = threadIdx.x; j < J; j += blockDim.x) m[1] = fmaxf(m[1], fabsf(B[j + J * r]));
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) m[2] = fmaxf(m[2], fabsf(Cm[k + K * r]));
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m[q] = fmaxf(m[q], __shfl_xor_sync(0xffffffffu, m[q], o));
+      if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = m[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float mm[3] = {0.f, 0.f, 0.f};
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
+        for (int q = 0; q < 3; ++q) mm[q] = fmaxf(mm[q], red[q][w]);
+      total += mm[0] * mm[1] * mm[2];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const unsigned bits = __float_as_uint(total * 1.0001f);  // the generator's fp32 sums round
+    amax[0] = bits;
+    amax[1] = bits;
   }
 }
 
@@ -191,9 +221,13 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
   const size_t smem = static_cast<size_t>(rank) * (TI + TJ) * sizeof(float);
   XCUDA(cudaFuncSetAttribute(gen_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t nslabs = ceil_div(k1 - k0, ks);
+  if (comp()) {
+    factor_bound_kernel<<<1, 1024, 0, s>>>(fa.ptr, fb.ptr, fc.ptr, I, J, K, static_cast<int>(rank), k0, k1, amax.ptr);
+    XLAUNCH_CHECK();
+  }
   // Two slab buffers: the generator fills slab s+1 on the side stream while
-  // the tensor cores consume slab s (the compensated mode's per-slab max |x|
-  // has one slot per buffer). XTSG_GEN_OVERLAP=0 disables.
+  // the tensor cores consume slab s (the compensated mode's |x| bound sits in
+  // both amax slots). XTSG_GEN_OVERLAP=0 disables.
   static const bool overlap_env = [] {
     const char* e = std::getenv("XTSG_GEN_OVERLAP");
     return !(e && std::atoi(e) == 0);
@@ -208,7 +242,6 @@ void Plan::compress_factors(const double* a, const double* b, const double* c, i
     const int64_t kb = k0 + sl * ks, kn = std::min(ks, k1 - kb);
     dim3 grid(static_cast<unsigned>(ceil_div(I, TI)), static_cast<unsigned>(ceil_div(J, TJ)),
               static_cast<unsigned>(kn));
-    if (comp()) XCUDA(cudaMemsetAsync(amax.ptr + b, 0, sizeof(unsigned), gs));
     gen_slab_kernel<<<grid, NT, smem, gs>>>(fa.ptr, fb.ptr, fc.ptr, I, J, K, static_cast<int>(rank), kb, ldi,
                                             stage[b].ptr, fp16(), comp() ? stage_lo[b].ptr : nullptr,
                                             comp() ? amax.ptr + b : nullptr);

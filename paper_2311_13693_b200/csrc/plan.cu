@@ -78,13 +78,11 @@ void pack_virtual(const double* src, int64_t vcount, int64_t rows, int64_t cols,
 }
 
 // Compensated operands: like pack_virtual_kernel, but each value v (scaled
-// by 2^-b so |v| < 16) becomes three fp16 planes, plane_stride elements
-// apart: (hi * 2^11, hi, lo' = (v - hi) * 2^11) for U (hi_first = true:
-// products (Uh*2^11, Xh), (Uh, Xl'), (Ul', Xh)), and (hi * 2^11, lo', hi) for
-// V (products (Th, Vh*2^11), (Th, Vl'), (Tl', Vh)).
+// by 2^-b so max |v| is in [2^13, 2^14)) becomes two fp16 planes,
+// plane_stride elements apart: hi = fp16(v), lo = fp16(v - hi).
 __global__ void pack_split_kernel(const double* __restrict__ src, int64_t rows, int64_t cols, int64_t per_p,
                                   int64_t sdiv, int64_t smod, int64_t srows, int64_t rows_pad, int64_t ld,
-                                  double scale, int64_t plane_stride, int32_t v_order, __half* __restrict__ dst) {
+                                  double scale, int64_t plane_stride, __half* __restrict__ dst) {
   __shared__ double tile[32][33];
   const int64_t q = blockIdx.z;
   const int64_t p = q / per_p, split = (q / sdiv) % smod;
@@ -101,12 +99,10 @@ __global__ void pack_split_kernel(const double* __restrict__ src, int64_t rows, 
     if (r < srows && rbase + r < rows && c < cols) {
       const double v = tile[threadIdx.x][dy] * scale;
       const __half hi = __double2half(v);
-      const __half lo = __double2half((v - static_cast<double>(__half2float(hi))) * 2048.0);
-      const __half hi2 = __float2half_rn(__half2float(hi) * 2048.f);  // exact: |hi| < 16
+      const __half lo = __double2half(v - static_cast<double>(__half2float(hi)));
       __half* o = dst + (q * rows_pad + r) * ld + c;
-      o[0] = hi2;
-      o[plane_stride] = v_order ? lo : hi;
-      o[2 * plane_stride] = v_order ? hi : lo;
+      o[0] = hi;
+      o[plane_stride] = lo;
     }
   }
 }
@@ -174,36 +170,19 @@ __global__ void stage_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj
   }
 }
 
-// Compensated staging: X block -> fp16 planes hi = fp16(x), lo' =
-// fp16((x - hi) * 2^11) in the TMA layout, plus max |x| of the block
-// (float bits; atomicMax on non-negative floats orders like their bits).
+// Compensated staging, pass 1: max |x| of the X block (float bits; atomicMax
+// on non-negative floats orders like their bits).
 template <class T>
-__global__ void split_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj, int64_t nk, int64_t ld0,
-                               int64_t ld1, int64_t ldi, __half* __restrict__ hi, __half* __restrict__ lo,
-                               unsigned* __restrict__ amax) {
+__global__ void amax_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj, int64_t nk, int64_t ld0, int64_t ld1,
+                              unsigned* __restrict__ amax) {
   const int64_t rows = nj * nk;
   float m = 0.f;
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const int64_t j = row % nj, k = row / nj;
     const T* s = src + j * ld0 + k * ld1;
-    for (int64_t i = threadIdx.x; i < ldi; i += blockDim.x) {
-      float v = 0.f, r = 0.f;
-      if (i < ni) {
-        if constexpr (std::is_same<T, double>::value) {
-          const double d = s[i];
-          const __half h = __double2half(d);
-          v = __half2float(h);
-          r = static_cast<float>((d - static_cast<double>(v)) * 2048.0);
-          m = fmaxf(m, static_cast<float>(fabs(d)));
-        } else {
-          const float f = to_f(s[i]);
-          v = __half2float(__float2half_rn(f));
-          r = (f - v) * 2048.f;
-          m = fmaxf(m, fabsf(f));
-        }
-      }
-      hi[row * ldi + i] = __float2half_rn(v);
-      lo[row * ldi + i] = __float2half_rn(r);
+    for (int64_t i = threadIdx.x; i < ni; i += blockDim.x) {
+      if constexpr (std::is_same<T, double>::value) m = fmaxf(m, static_cast<float>(fabs(s[i])));
+      else m = fmaxf(m, fabsf(to_f(s[i])));
     }
   }
 #pragma unroll
@@ -211,11 +190,66 @@ __global__ void split_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj
   if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
 }
 
+// the same over a contiguous block of n elements, 16-byte loads (n * sizeof(T)
+// a multiple of 16, 16-byte aligned base)
+template <class T>
+__global__ void amax_flat_kernel(const T* __restrict__ src, int64_t n, unsigned* __restrict__ amax) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t nv = n / V;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  float m = 0.f;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nv;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint4 w = __ldcs(s4 + e);
+    const T* t = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      if constexpr (std::is_same<T, double>::value) m = fmaxf(m, static_cast<float>(fabs(t[q])));
+      else m = fmaxf(m, fabsf(to_f(t[q])));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
+}
+
+// Compensated staging, pass 2: X block scaled by 2^(13 - exponent of max |x|)
+// (max |x'| in [2^13, 2^14)) -> fp16 planes hi = fp16(x'), lo = fp16(x' - hi)
+// in the TMA layout.
+template <class T>
+__global__ void split_x_kernel(const T* __restrict__ src, int64_t ni, int64_t nj, int64_t nk, int64_t ld0,
+                               int64_t ld1, int64_t ldi, __half* __restrict__ hi, __half* __restrict__ lo,
+                               const unsigned* __restrict__ amax) {
+  const int64_t rows = nj * nk;
+  const int sh = comp_x_shift(amax);
+  const float scf = ldexpf(1.f, sh);
+  const double scd = ldexp(1.0, sh);
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t j = row % nj, k = row / nj;
+    const T* s = src + j * ld0 + k * ld1;
+    for (int64_t i = threadIdx.x; i < ldi; i += blockDim.x) {
+      float v = 0.f, r = 0.f;
+      if (i < ni) {
+        if constexpr (std::is_same<T, double>::value) {
+          const double d = static_cast<double>(s[i]) * scd;
+          v = __half2float(__double2half(d));
+          r = static_cast<float>(d - static_cast<double>(v));
+        } else {
+          const float f = to_f(s[i]) * scf;
+          v = __half2float(__float2half_rn(f));
+          r = f - v;
+        }
+      }
+      hi[row * ldi + i] = __float2half_rn(v);
+      lo[row * ldi + i] = __float2half_rn(r);
+    }
+  }
+}
+
 // Compensated mode 3: Y64[q] (mrows x N) (+)= 2^e * Z[q] (mrows x kc, fp32)
 // * W[q][:, k0:k0+kc]^T (fp32, row n at W + n*ldw), fp64 accumulation. e =
 // e0 + exponent(max |x| of the launch) undoes the power-of-two operand
-// scales (U, V pre-scales, the 2^11 of the hi*2^11 products, the split
-// scale of the mode-1 result).
+// scales (U, V and X pre-scales, the split scale of the mode-1 result).
 constexpr int M3_TM = 64, M3_TN = 32, M3_TK = 32;
 __global__ void __launch_bounds__(256) mode3_comp_kernel(const float* __restrict__ Z, int64_t mrows, int64_t kc,
                                                          const float* __restrict__ W, int64_t ldw, int64_t wstride,
@@ -417,7 +451,7 @@ void Plan::build_tc_operands() {
   rows_u = round_up(vP * lpad, comp() ? 256 : 128);
   ld_u = round_up(I, 8);
   ld_v = round_up(J, 8);
-  const int planes = comp() ? 3 : 1;
+  const int planes = comp() ? 2 : 1;
   ustack = DevBuf<__nv_bfloat16>(static_cast<size_t>(planes * rows_u * ld_u), st);
   ustack.zero();
   vt = DevBuf<__nv_bfloat16>(static_cast<size_t>(planes * vP * mpad * ld_v), st);
@@ -426,7 +460,8 @@ void Plan::build_tc_operands() {
   const int64_t per_p = lsplit * msplit;
   // U rows of virtual replica q: split a = (q / msplit) % lsplit; V rows: b = q % msplit
   if (comp()) {
-    // pre-scales 2^-b with max |u| * 2^-b < 16 (so hi * 2^11 < 2^15 fits binary16)
+    // pre-scales 2^-b with max |u| * 2^-b in [2^13, 2^14): hi and lo stay
+    // normal binary16 numbers for every entry within 2^16 of the maximum
     auto prescale = [&](const double* m, int64_t n) {
       DevBuf<unsigned long long> mx(1, st);
       mx.zero();
@@ -437,21 +472,21 @@ void Plan::build_tc_operands() {
       XCUDA(cudaStreamSynchronize(st));
       double v;
       std::memcpy(&v, &bits, sizeof(v));
-      return v > 0.0 ? std::max(0, std::ilogb(v) - 3) : 0;
+      return v > 0.0 ? std::ilogb(v) - 13 : 0;
     };
     comp_bu = prescale(u64.ptr, P * L * I);
     comp_bv = prescale(v64.ptr, P * M * J);
     auto pack3 = [&](const double* src, int64_t rows, int64_t cols, int64_t sdiv, int64_t smod, int64_t srows,
-                     int64_t rows_pad, int64_t ld, int64_t plane, int b, int v_order, __nv_bfloat16* dst) {
+                     int64_t rows_pad, int64_t ld, int64_t plane, int b, __nv_bfloat16* dst) {
       dim3 grid(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(srows, 32)),
                 static_cast<unsigned>(vP));
       pack_split_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, per_p, sdiv, smod, srows, rows_pad, ld,
-                                                      std::ldexp(1.0, -b), plane, v_order,
+                                                      std::ldexp(1.0, -b), plane,
                                                       reinterpret_cast<__half*>(dst));
       XLAUNCH_CHECK();
     };
-    pack3(u64.ptr, L, I, msplit, lsplit, Lv, lpad, ld_u, rows_u * ld_u, comp_bu, 0, ustack.ptr);
-    pack3(v64.ptr, M, J, 1, msplit, Mv, mpad, ld_v, vP * mpad * ld_v, comp_bv, 1, vt.ptr);
+    pack3(u64.ptr, L, I, msplit, lsplit, Lv, lpad, ld_u, rows_u * ld_u, comp_bu, ustack.ptr);
+    pack3(v64.ptr, M, J, 1, msplit, Mv, mpad, ld_v, vP * mpad * ld_v, comp_bv, vt.ptr);
     pack_virtual<float>(w64.ptr, vP, N, K, per_p, 1, 1, N, N, K, wf.ptr, st);
     amax = DevBuf<unsigned>(2, st);  // one per slab buffer (overlapped staging)
   } else if (fp16()) {
@@ -528,7 +563,7 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
   const int64_t L = desc.reduced[0], M = desc.reduced[1], N = desc.reduced[2], P = desc.count;
   const int64_t K = desc.dims[2];
   if (comp() && !x_lo) usage("plan: the compensated mode needs the X lo plane");
-  const int planes = comp() ? 3 : 1;
+  const int planes = comp() ? 2 : 1;
   // Operand slices; TMA needs 16-byte aligned bases, so unaligned offsets get
   // an aligned copy of the slice (every plane).
   const __nv_bfloat16* uop = ustack.ptr + off[0];
@@ -633,7 +668,7 @@ void Plan::run_bf16_block(const __nv_bfloat16* x, int64_t ld0, int64_t ld1, cons
                 static_cast<unsigned>(vP));
       mode3_comp_kernel<<<grid, 256, 0, s>>>(zbuf.ptr, mrows, kc, wf.ptr + off[2] + kb, K, N * K, N,
                                              cur_amax ? cur_amax : amax.ptr,
-                                             comp_c0(ext[0]) + comp_bu + comp_bv - 22, acc ? 1 : 0, comp_y);
+                                             comp_c0(ext[0]) + comp_bu + comp_bv - 14, acc ? 1 : 0, comp_y);
       XLAUNCH_CHECK();
     } else {
     GemmArgs<float> g;
@@ -966,18 +1001,21 @@ void Plan::compress(const void* x, int32_t dtype, const int64_t ld[2], const int
         XCUDA(cudaMemsetAsync(am, 0, sizeof(unsigned), ss));
         auto* hi = reinterpret_cast<__half*>(stage[b].ptr);
         auto* lo = reinterpret_cast<__half*>(stage_lo[b].ptr);
-        if (dtype == XTSG_DTYPE_F64)
-          split_x_kernel<double><<<blocks, 256, 0, ss>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
-                                                          ld[0], ld[1], ldi, hi, lo, am);
-        else if (dtype == XTSG_DTYPE_F32)
-          split_x_kernel<float><<<blocks, 256, 0, ss>>>(reinterpret_cast<const float*>(src), ext[0], ext[1], kn,
-                                                         ld[0], ld[1], ldi, hi, lo, am);
-        else if (dtype == XTSG_DTYPE_F16)
-          split_x_kernel<__half><<<blocks, 256, 0, ss>>>(reinterpret_cast<const __half*>(src), ext[0], ext[1], kn,
-                                                          ld[0], ld[1], ldi, hi, lo, am);
-        else
-          split_x_kernel<__nv_bfloat16><<<blocks, 256, 0, ss>>>(reinterpret_cast<const __nv_bfloat16*>(src),
-                                                                 ext[0], ext[1], kn, ld[0], ld[1], ldi, hi, lo, am);
+        auto split = [&](auto tag) {
+          using T = decltype(tag);
+          const T* sp = reinterpret_cast<const T*>(src);
+          const int64_t n = ext[0] * ext[1] * kn;
+          if (ld[0] == ext[0] && ld[1] == ext[0] * ext[1] && (n * static_cast<int64_t>(sizeof(T))) % 16 == 0 &&
+              reinterpret_cast<uintptr_t>(sp) % 16 == 0)
+            amax_flat_kernel<T><<<148 * 8, 256, 0, ss>>>(sp, n, am);
+          else
+            amax_x_kernel<T><<<blocks, 256, 0, ss>>>(sp, ext[0], ext[1], kn, ld[0], ld[1], am);
+          split_x_kernel<T><<<blocks, 256, 0, ss>>>(sp, ext[0], ext[1], kn, ld[0], ld[1], ldi, hi, lo, am);
+        };
+        if (dtype == XTSG_DTYPE_F64) split(double{});
+        else if (dtype == XTSG_DTYPE_F32) split(float{});
+        else if (dtype == XTSG_DTYPE_F16) split(__half{});
+        else split(__nv_bfloat16{});
       } else if (dtype == XTSG_DTYPE_F64)
         stage_x_kernel<double><<<blocks, 256, 0, ss>>>(reinterpret_cast<const double*>(src), ext[0], ext[1], kn,
                                                         ld[0], ld[1], ldi, stage[b].ptr, h);
@@ -1081,12 +1119,13 @@ int Plan::comp_kpc() const {
   return v;
 }
 
-// the split of the mode-1 result (~2^11 * 2^-bu * sqrt(ni) * max|x| at most
-// in rms) is scaled by 2^-(c0 + e_x), e_x = exponent of max |x|, to ~2^10
+// the mode-1 result U'X' (operands scaled to [2^13, 2^14), rms of the sum
+// <= 2^28 * 2^c with 2^c >= sqrt(ni)) is scaled by 2^-c0, c0 = c + 18, to
+// ~2^10 at most in rms before its hi/lo split
 int Plan::comp_c0(int64_t ni) const {
   int c = 0;
   while ((int64_t(1) << (2 * c)) < ni) ++c;  // 2^c >= sqrt(ni)
-  return 1 - comp_bu + c;
+  return c + 18;
 }
 
 // fp16 plans: a binary16 overflow anywhere in the chain shows up as a

@@ -10,6 +10,12 @@
 
 namespace xtsg {
 
+// compensated mode: X is scaled by 2^comp_x_shift(amax) before its hi/lo split
+// so that max |x| lands in [2^13, 2^14)
+__device__ __forceinline__ int comp_x_shift(const unsigned* amax) {
+  return 13 - ilogbf(fmaxf(__uint_as_float(*amax), 1e-30f));
+}
+
 struct Plan {
   xtsg_plan_desc desc;
   // Calls on one plan serialise: the host side under `mu`, the device side
@@ -61,11 +67,12 @@ struct Plan {
   DevBuf<double> outer[3];
   int64_t inner_dims[3] = {0, 0, 0};
 
-  // compensated fp16 hi/lo mode (XTSG_PREC_FP16X3): U and V as three fp16
-  // planes each, X staged as two; `amax` holds the current launch's max |x|
-  // (float bits) that scales the split of the mode-1 result; comp_bu/bv are
-  // the power-of-two pre-scales of U/V (kept < 16 in magnitude so hi*2^11
-  // fits binary16); mode 3 accumulates in fp64 into comp_y (padded layout)
+  // compensated fp16 hi/lo mode (XTSG_PREC_FP16X3): U, V and X as two fp16
+  // planes each (hi, lo = v - hi); `amax` holds the current launch's max |x|
+  // (float bits, or an upper bound for factored sources) that sets X's
+  // power-of-two pre-scale (comp_x_shift) and mode 3's undo; comp_bu/bv are
+  // the pre-scales 2^-b of U/V (max in [2^13, 2^14)); mode 3 accumulates in
+  // fp64 into comp_y (padded layout)
   DevBuf<unsigned> amax;
   const unsigned* cur_amax = nullptr;  // the amax slot of the slab being consumed (null: amax.ptr)
   int comp_bu = 0, comp_bv = 0;

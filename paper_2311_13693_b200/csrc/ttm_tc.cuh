@@ -26,11 +26,11 @@ struct TtmParams {
   int32_t f16;             // operands are fp16 (XTSG_PREC_FP16) instead of bf16
   // compensated fp16 hi/lo mode (XTSG_PREC_FP16X3, pair kernel only)
   int32_t comp;            // 1: three products per mode, planes below
-  int32_t u_plane_rows;    // rows between the U planes (Uh*2^11, Uh, Ul')
-  int32_t v_plane_rows;    // rows between the V planes (Vh*2^11, Vl', Vh)
+  int32_t u_plane_rows;    // rows between the U planes (Uh, Ul)
+  int32_t v_plane_rows;    // rows between the V planes (Vh, Vl)
   int32_t i_chunks, kpc;   // i steps split into i_chunks chunks of kpc (0: one chunk)
-  const unsigned* amax;    // max |x| of this launch's X (float bits), sets the mode-2 operand scale
-  int32_t comp_c0;         // 2^-(comp_c0 + exponent(max|x|)) scales the mode-1 result before its split
+  const unsigned* amax;    // max |x| of this launch's X (float bits; mode 3's scale)
+  int32_t comp_c0;         // 2^-comp_c0 scales the mode-1 result before its split
   float* z;          // out: Z[p][kk][m][l], kk in [0, kc)
 };
 

@@ -43,18 +43,21 @@ constexpr int A2_BYTES = BM * 64 * 2;   // 16 KB
 constexpr int B2_BYTES = 128 * 64 * 2;  // 16 KB (n2 <= 128 rows per CTA)
 constexpr int CHUNKS = BN / 64;
 // Compensated mode (XTSG_PREC_FP16X3): every operand is an fp16 pair
-// (hi, lo' = (x - hi) * 2^11) and each product is hi*hi*2^11 + hi*lo' + lo'*hi
-// (the dropped lo*lo term is 2^-22 relative). Mode 1 streams three (U plane,
-// X plane) stages per 64-wide i step — (Uh*2^11, Xh), (Uh, Xl'), (Ul', Xh) —
-// into the same accumulator; the epilogue splits the fp32 mode-1 result into
-// an A2 (hi, lo') pair and mode 2 issues (Th, Vh*2^11), (Th, Vl'), (Tl', Vh).
-// S TMA stages, A2_SLOTS mode-1 chunks in flight to mode 2 (a pair of tiles
-// each when compensated), B2_SLOTS V chunks (three planes when compensated).
+// (hi, lo = x - hi), each operand pre-scaled by a power of two so its largest
+// value sits in [2^13, 2^14) (lo then stays a normal binary16 for every value
+// within 2^16 of the maximum), and each product is hi*hi + hi*lo + lo*hi (the
+// dropped lo*lo term is 2^-22 relative). One ring stage holds a whole 64-wide
+// i step — (Uh, Ul, Xh, Xl), 64 KB per CTA — and the MMA issuer runs the three
+// products (Uh, Xh), (Uh, Xl), (Ul, Xh) from it into the same accumulator; the
+// epilogue splits the fp32 mode-1 result into an A2 (hi, lo) pair and mode 2
+// issues (Th, Vh), (Th, Vl), (Tl, Vh) from a two-plane V slot.
+// S ring stages, A2_SLOTS mode-1 chunks in flight to mode 2, B2_SLOTS V chunks.
 constexpr int smem_total(int S, int A2_SLOTS, bool COMP = false, int B2_SLOTS = 2) {
-  return S * STAGE_BYTES + A2_SLOTS * A2_BYTES * (COMP ? 2 : 1) + B2_SLOTS * B2_BYTES * (COMP ? 3 : 1) + 1024 + 512;
+  return S * STAGE_BYTES * (COMP ? 2 : 1) + A2_SLOTS * A2_BYTES * (COMP ? 2 : 1) +
+         B2_SLOTS * B2_BYTES * (COMP ? 2 : 1) + 1024 + 512;
 }
 static_assert(smem_total(4, 4) <= 232448 && smem_total(5, 2) <= 232448, "shared memory budget");
-static_assert(smem_total(3, 2, true, 1) <= 232448, "shared memory budget (compensated)");
+static_assert(smem_total(2, 2, true, 1) <= 232448, "shared memory budget (compensated)");
 constexpr uint32_t IDESC1 = ptx::idesc_bf16(2 * BM, BN);
 constexpr uint16_t PAIR = 0x3;
 
@@ -133,14 +136,14 @@ struct Bars2 {
   uint32_t tmem_base;
 };
 
-// split of an fp32 value into the fp16 pair (hi, lo' = (v - hi) * 2^11)
+// split of an fp32 value into the fp16 pair (hi, lo = v - hi)
 __device__ __forceinline__ void split16x2(const float* v, uint4& hi, uint4& lo) {
   uint32_t wh[4], wl[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const __half2 h = __floats2half2_rn(v[2 * q], v[2 * q + 1]);
     const float2 hf = __half22float2(h);
-    const __half2 l = __floats2half2_rn((v[2 * q] - hf.x) * 2048.f, (v[2 * q + 1] - hf.y) * 2048.f);
+    const __half2 l = __floats2half2_rn(v[2 * q] - hf.x, v[2 * q + 1] - hf.y);
     wh[q] = *reinterpret_cast<const uint32_t*>(&h);
     wl[q] = *reinterpret_cast<const uint32_t*>(&l);
   }
@@ -154,13 +157,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_xl,
                     const TtmParams p) {
   static_assert(!COMP || LOCAL2, "the compensated mode runs mode 2 per CTA");
-  constexpr int NC = COMP ? 3 : 1;                      // mode-1 products per i step
-  constexpr int A2_SLOT = A2_BYTES * (COMP ? 2 : 1);    // (hi[, lo']) mode-2 A tiles
-  constexpr int B2_SLOT = B2_BYTES * (COMP ? 3 : 1);    // (Vh*2^11, Vl', Vh) planes
+  constexpr int NC = COMP ? 3 : 1;                      // products per i step / per mode-2 chunk
+  constexpr int CSTAGE = STAGE_BYTES * (COMP ? 2 : 1);  // (U[, Ul], X[, Xl]) tiles of one i step
+  constexpr int A2_SLOT = A2_BYTES * (COMP ? 2 : 1);    // (Th[, Tl]) mode-2 A tiles
+  constexpr int B2_SLOT = B2_BYTES * (COMP ? 2 : 1);    // (Vh[, Vl]) planes
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
-  uint8_t* a2_base = smem + S * STAGE_BYTES;
+  uint8_t* a2_base = smem + S * CSTAGE;
   uint8_t* b2_base = a2_base + A2_SLOTS * A2_SLOT;
   auto* bars = reinterpret_cast<Bars2<S, A2_SLOTS, B2_SLOTS>*>(b2_base + B2_SLOTS * B2_SLOT);
 
@@ -230,20 +234,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (p.sync && ic == 0 && jt % p.sync_j == 0) lane_barrier(p.sync + us.lane, 2u * us.group * ++sync_no);
           if (!act) continue;
           const int ks1 = min(k_steps, (ic + 1) * kpc);
+          // the last j tile runs with N = n_last: each CTA holds n_last / 2 of its j
+          const int half = jt == j_tiles - 1 ? (p.n_last >> 1) : BNC;
           for (int ks = ic * kpc; ks < ks1; ++ks) {
+            ptx::mbar_wait(&bars->empty1[s], ph ^ 1);
+            uint8_t* st = stage_base + s * CSTAGE;
+            if (leader) ptx::mbar_arrive_expect_tx(&bars->full1[s], 2 * CSTAGE);
+            const uint32_t fb = ptx::mapa_shared(&bars->full1[s], 0);
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              ptx::mbar_wait(&bars->empty1[s], ph ^ 1);
-              uint8_t* st = stage_base + s * STAGE_BYTES;
-              if (leader) ptx::mbar_arrive_expect_tx(&bars->full1[s], 2 * STAGE_BYTES);
-              const uint32_t fb = ptx::mapa_shared(&bars->full1[s], 0);
-              ptx::tma_load_2d_pair_hint(st, &tm_u, fb, ks * BK, urow + c * p.u_plane_rows, p.u_policy);
-              // the last j tile runs with N = n_last: each CTA holds n_last / 2 of its j
-              const int half = jt == j_tiles - 1 ? (p.n_last >> 1) : BNC;
-              ptx::tma_load_3d_pair_hint(st + A_BYTES, (COMP && c == 1) ? &tm_xl : &tm_x, fb, ks * BK,
-                                         jt * BN + crank * half, p.k_first + kk, p.x_policy);
-              if (++s == S) { s = 0; ph ^= 1; }
-            }
+            for (int c = 0; c < (COMP ? 2 : 1); ++c)
+              ptx::tma_load_2d_pair_hint(st + c * A_BYTES, &tm_u, fb, ks * BK, urow + c * p.u_plane_rows, p.u_policy);
+            uint8_t* xs = st + (COMP ? 2 : 1) * A_BYTES;
+            ptx::tma_load_3d_pair_hint(xs, &tm_x, fb, ks * BK, jt * BN + crank * half, p.k_first + kk, p.x_policy);
+            if (COMP)
+              ptx::tma_load_3d_pair_hint(xs + B_BYTES, &tm_xl, fb, ks * BK, jt * BN + crank * half, p.k_first + kk,
+                                         p.x_policy);
+            if (++s == S) { s = 0; ph ^= 1; }
           }
         }
       }
@@ -269,20 +275,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const int ks0 = ic * kpc, ks1 = min(k_steps, ks0 + kpc);
           for (int ks = ks0; ks < ks1; ++ks) {
             const int nk16 = ks == k_steps - 1 ? p.k16_last : BK / 16;
+            ptx::mbar_wait(&bars->full1[s], ph);
+            ptx::tc_fence_after();
+            const uint32_t st0 = ptx::smem_u32(stage_base + s * CSTAGE);
+            const uint32_t xs0 = st0 + (COMP ? 2 : 1) * A_BYTES;
+            // products (U plane, X plane): (h, h)[, (h, l), (l, h)]
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-              ptx::mbar_wait(&bars->full1[s], ph);
-              ptx::tc_fence_after();
-              const uint32_t a0 = ptx::smem_u32(stage_base + s * STAGE_BYTES);
-              const uint32_t b0 = a0 + A_BYTES;
+              const uint32_t a0 = st0 + (c == 2 ? A_BYTES : 0);
+              const uint32_t b0 = xs0 + (c == 1 ? B_BYTES : 0);
 #pragma unroll
               for (int k4 = 0; k4 < BK / 16; ++k4)
                 if (k4 < nk16)
                   ptx::mma_bf16_pair(d, ptx::sw128_desc(a0 + k4 * 32), ptx::sw128_desc(b0 + k4 * 32), idesc1,
                                      (ks != ks0 || c != 0 || k4 != 0));
-              ptx::mma_commit_pair(&bars->empty1[s], PAIR);
-              if (++s == S) { s = 0; ph ^= 1; }
             }
+            ptx::mma_commit_pair(&bars->empty1[s], PAIR);
+            if (++s == S) { s = 0; ph ^= 1; }
           }
           ptx::mma_commit_pair(&bars->tmem_full[b], PAIR);
         }
@@ -306,9 +315,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             const int slot = g % B2_SLOTS;
             ptx::mbar_wait(&bars->b2_empty[slot], ((g / B2_SLOTS) & 1) ^ 1);
             if (LOCAL2) {
-              ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], bytes * NC);
+              ptx::mbar_arrive_expect_tx(&bars->b2_full[slot], bytes * (COMP ? 2 : 1));
 #pragma unroll
-              for (int pl = 0; pl < NC; ++pl)
+              for (int pl = 0; pl < (COMP ? 2 : 1); ++pl)
                 ptx::tma_load_2d(b2_base + slot * B2_SLOT + pl * B2_BYTES, &tm_v, &bars->b2_full[slot],
                                  jt * BN + c * 64, vrow + pl * p.v_plane_rows);
             } else {
@@ -355,10 +364,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             const uint32_t b0 = ptx::smem_u32(b2_base + bslot * B2_SLOT);
             const int nk16 = (last && c == nch - 1) ? p.k16_chunk_last : 4;
             if (LOCAL2) {
-              // (A2 tile, V plane) per product: (Th, Vh*2^11), (Th, Vl'), (Tl', Vh)
+              // (A2 tile, V plane) per product: (Th, Vh)[, (Th, Vl), (Tl, Vh)]
 #pragma unroll
               for (int q = 0; q < NC; ++q) {
-                const uint32_t aq = a0 + (q == 2 ? A2_BYTES : 0), bq = b0 + q * B2_BYTES;
+                const uint32_t aq = a0 + (q == 2 ? A2_BYTES : 0), bq = b0 + (q == 1 ? B2_BYTES : 0);
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4)
                   if (k4 < nk16)
@@ -396,13 +405,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     UnitSched us(cid, n_clusters, n_rb2, p);
     int kk, rb2;
     bool act;
-    // compensated: the mode-1 result (2^11 * 2^-bu * U X) is scaled by 2^-a
-    // into the fp16 range before the split, a from this launch's max |x|
-    float t_scale = 1.f;
-    if (COMP) {
-      const int ex = p.amax ? ilogbf(fmaxf(__uint_as_float(*p.amax), 1e-30f)) + 1 : 0;
-      t_scale = exp2f(static_cast<float>(-(p.comp_c0 + ex)));
-    }
+    // compensated: the mode-1 result (2^-(bu+sx) U X, operands scaled to
+    // [2^13, 2^14)) is scaled by 2^-c0 into the binary16 range before the split
+    const float t_scale = COMP ? exp2f(static_cast<float>(-p.comp_c0)) : 1.f;
     while (us.next(act, kk, rb2)) {
       if (!act) continue;
       float zacc[MPAD];
@@ -533,8 +538,8 @@ template <int MPAD, bool LOCAL2, int S, int A2_SLOTS, bool COMP = false, int B2_
 void launch_pair(const TtmLaunch& L, cudaStream_t st) {
   CUtensorMap mu, mx, mv, mxl;
   {
-    // compensated: three U planes of rows_u rows each, stacked
-    const uint64_t dims[2] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.rows_u * (COMP ? 3 : 1))};
+    // compensated: two U planes (hi, lo) of rows_u rows each, stacked
+    const uint64_t dims[2] = {static_cast<uint64_t>(L.ni), static_cast<uint64_t>(L.rows_u * (COMP ? 2 : 1))};
     const uint64_t str[1] = {static_cast<uint64_t>(L.ld_u) * 2};
     const uint32_t box[2] = {BK, BM};
     map_bf16(&mu, L.u, 2, dims, str, box, L.prm.f16 != 0);
@@ -548,7 +553,7 @@ void launch_pair(const TtmLaunch& L, cudaStream_t st) {
     else mxl = mx;
   }
   {
-    const uint64_t dims[2] = {static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.rows_v * (COMP ? 3 : 1))};
+    const uint64_t dims[2] = {static_cast<uint64_t>(L.nj), static_cast<uint64_t>(L.rows_v * (COMP ? 2 : 1))};
     const uint64_t str[1] = {static_cast<uint64_t>(L.ld_v) * 2};
     const uint32_t box[2] = {64, static_cast<uint32_t>(L.prm.n2)};
     map_bf16(&mv, L.v, 2, dims, str, box, L.prm.f16 != 0);
@@ -610,7 +615,7 @@ void launch_ttm_pair(const TtmLaunch& L, cudaStream_t st) {
   auto go = [&](auto mpad_tag) {
     constexpr int MP = decltype(mpad_tag)::value;
     if (L.prm.comp)
-      launch_pair<MP, true, 3, 2, true, 1>(L, st);
+      launch_pair<MP, true, 2, 2, true, 1>(L, st);
     else if (variant == 0)
       launch_pair<MP, false, 4, 4>(L, st);
     else if (variant == 1)

@@ -1,7 +1,11 @@
 """Compensated tensor-core compression (XTSG_PREC_FP16X3) against the fp64
-oracle: the reference's Eq. 5 operand split (mixed.cpp:18-24: x = hi + lo with
-the residual stored as fp16 of residual * 2^11) carried onto tcgen05 — each
-mode product is hi*hi + hi*lo + lo*hi over fp16 pairs.
+oracle: the reference's Eq. 5 operand split (mixed.cpp:18-24: x = hi + lo,
+the residual stored in fp16) carried onto tcgen05 — each mode product is
+hi*hi + hi*lo + lo*hi over fp16 pairs. Every operand (U, V, each X launch,
+the mode-1 result) is pre-scaled by a power of two that puts its largest
+value in [2^13, 2^14), so lo stays a normal binary16 number and inputs of any
+magnitude compress (the reference's mixed path, half.cpp, raises
+HalfRangeError instead; that path is replayed bit-exactly in mixed.cu).
 
 Stated tolerance: per-replica relative Frobenius error <= COMP_TOL vs the
 reference's fp64 comp / comp_from_factors. What bounds it is the fp32
@@ -87,13 +91,20 @@ def test_comp_factored_vs_comp_from_factors(gpu, restated):
     plan.close()
 
 
-def test_comp_out_of_binary16_range_raises(gpu):
-    dims, red = (64, 64, 8), (32, 32, 8)
-    t = np.asfortranarray(np.random.default_rng(0).standard_normal(dims))
-    t[3, 4, 5] = 1e6
-    plan = gpu.Plan(dims, red, 2, 4, 1, precision=gpu.PREC_FP16X3)
-    with pytest.raises(gpu.HalfRangeError):
-        plan.compress(t)
+@pytest.mark.parametrize("scale,outlier", [(1.0, 1e6), (1e-9, None), (1e12, None)])
+def test_comp_any_magnitude(gpu, restated, scale, outlier):
+    """Values outside binary16 (an outlier at 1e6, a tensor at 1e12) and far
+    below its normal range (1e-9) compress to the oracle's tolerance: the
+    power-of-two pre-scale of each X launch keeps hi and lo in range."""
+    dims, red, P, S, seed = (64, 64, 8), (32, 32, 8), 2, 4, 1
+    t = np.asfortranarray(np.random.default_rng(0).standard_normal(dims)) * scale
+    if outlier is not None:
+        t[3, 4, 5] = outlier
+    ens = restated.make_ensemble(dims, red, P, S, seed)
+    want = [restated.comp(t, ens[0][p], ens[1][p], ens[2][p]) for p in range(P)]
+    plan = gpu.Plan(dims, red, P, S, seed, precision=gpu.PREC_FP16X3)
+    errs = _errs(want, plan.compress(t), P, red)
+    assert max(errs) <= COMP_TOL, errs
     plan.close()
 
 
