@@ -1173,7 +1173,7 @@ template <int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     als_cluster_kernel(const AlsInst* __restrict__ insts, int n1, int n2, int n3, const double* __restrict__ ia,
                        const double* __restrict__ ib, const double* __restrict__ ic,
-                       const double* __restrict__ tnorm) {
+                       const double* __restrict__ tnorm, int dbg) {
   extern __shared__ double sm[];
   __shared__ int s_ok;
   cg::cluster_group cl = cg::this_cluster();
@@ -1229,6 +1229,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
   int64_t it = 0;
   bool converged = false;
   double prev = 0.0;
+  // dbg: per-phase SM cycles of crank 0 / thread 0 (tools/als_small_probe.py)
+  long long tph[7] = {0, 0, 0, 0, 0, 0, 0}, tl = clock64(), tsub[4] = {0, 0, 0, 0}, tl2 = 0;
+  auto phase = [&](int ph) {
+    if (dbg) {
+      const long long t = clock64();
+      tph[ph] += t - tl;
+      tl = t;
+    }
+  };
   for (; it < in.cfg.max_iters; ++it) {
     // ---- A update: slab partial of T(1) (C kr B) on the fp64 tensor cores
     // (DMMA m8n8k4: 8 i x 8 r tiles, K = the slab's (j, kk) fibers),
@@ -1260,8 +1269,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
         }
       }
     }
+    phase(0);
+    tl2 = clock64();
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
     cl.sync();
+    if (dbg) { const long long t = clock64(); tsub[0] += t - tl2; tl2 = t; }
     for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
       double v = 0.0;
 #pragma unroll
@@ -1269,10 +1281,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       s.M[e] = v;
     }
     __syncthreads();
+    if (dbg) { const long long t = clock64(); tsub[1] += t - tl2; tl2 = t; }
     solve_gram(s.M, n1, R, s, s.A, &s_ok);
     __syncthreads();
+    if (dbg) { const long long t = clock64(); tsub[2] += t - tl2; tl2 = t; }
     gram(s.A, n1, R, s.G1);
     __syncthreads();
+    if (dbg) { const long long t = clock64(); tsub[3] += t - tl2; tl2 = t; }
+    phase(1);
     // ---- P = A' T_c on the slab (DMMA: 8 r x 8 fibers tiles, K = i), M_B partial
     {
       const int ntr = (R + 7) / 8, ntf = (nf + 7) / 8;
@@ -1294,6 +1310,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       }
     }
     __syncthreads();
+    phase(2);
     for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
       const int j = e % n2, r = e / n2;
       const double* pr = Pl + static_cast<int64_t>(r) * n2 * kc + j;
@@ -1314,6 +1331,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     __syncthreads();
     gram(s.B, n2, R, s.G2);
     __syncthreads();
+    phase(3);
     // ---- C rows of this slab: M_C[kk, r] = sum_j B[j, r] P[r][kk][j]
     for (int e = threadIdx.x; e < nk * R; e += blockDim.x) {
       const int kk = e % nk, r = e / nk;
@@ -1335,6 +1353,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       s.C[e] = cl.map_shared_rank(Cown, c)[kk + nkc * r];
     }
     __syncthreads();
+    phase(4);
     // ---- move a/b column norms into c (cp_als.cpp:84-96)
     for (int r = threadIdx.x; r < R; r += blockDim.x) {
       double na = 0.0, nb = 0.0;
@@ -1360,6 +1379,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     gram(s.A, n1, R, s.G1);
     gram(s.B, n2, R, s.G2);
     gram(s.C, n3, R, s.G3);
+    phase(5);
     // ---- residual of the slab: X^ = A (C kr B)' tile by tile on DMMA
     // (8 i x 8 fibers, K = r), compared with the resident T
     {
@@ -1401,6 +1421,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     for (int c = 0; c < CL; ++c) res2 += cl.map_shared_rank(rs, c)[0];
     const double res = sqrt(res2);
     const double err = tn > 0.0 ? res / tn : res;
+    phase(6);
     if (crank == 0 && threadIdx.x == 0) in.hist[it] = err;
     if (it >= 1 && fabs(prev - err) < in.cfg.tol) {
       converged = true;
@@ -1408,6 +1429,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       break;
     }
     prev = err;
+  }
+  if (dbg && crank == 0 && threadIdx.x == 0 && in.cfg.max_iters >= 8) {
+    for (int ph = 0; ph < 7; ++ph) in.hist[ph] = static_cast<double>(tph[ph]);
+    in.hist[7] = static_cast<double>(it);
+    if (in.cfg.max_iters >= 12)
+      for (int q = 0; q < 4; ++q) in.hist[8 + q] = static_cast<double>(tsub[q]);
   }
   if (crank == 0) {
     for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) in.a[e] = s.A[e];
@@ -1457,7 +1484,11 @@ void launch_als_cluster(const AlsInst* din, int64_t count, int n1, int n2, int n
   auto go = [&](auto kern) {
     XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (CL > 8) XCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    kern<<<static_cast<unsigned>(count * CL), NT, smem, st>>>(din, n1, n2, n3, ia.ptr, ib.ptr, ic.ptr, tn.ptr);
+    static const int dbg = [] {
+      const char* e = std::getenv("XTSG_ALS_CL_DBG");  // per-phase cycles into history[0..7]
+      return e ? std::atoi(e) : 0;
+    }();
+    kern<<<static_cast<unsigned>(count * CL), NT, smem, st>>>(din, n1, n2, n3, ia.ptr, ib.ptr, ic.ptr, tn.ptr, dbg);
   };
   if (CL == 16) go(als_cluster_kernel<16>);
   else if (CL == 1) go(als_cluster_kernel<1>);

@@ -28,3 +28,13 @@ check(lib.xtsg_cp_als_batched(cnt, ptr(td), n, n, n, cfgs, ptr(fa), ptr(fb), ptr
 ev1.record()
 torch.cuda.synchronize()
 print(f"{cnt} x {n}^3 R={R}: iters {it.cpu().tolist()}, {ev0.elapsed_time(ev1) / max(1, int(it.max())) * 1e3:.1f} us/sweep")
+if __import__("os").environ.get("XTSG_ALS_CL_DBG"):
+    hh = h.view(cnt, its)[:, :8].cpu().numpy()
+    names = ["mttkrp_A", "reduce+solve+gram_A", "P=A'T", "M_B reduce+solve+gram_B", "C rows+solve+allgather",
+             "norms+grams", "residual+sync"]
+    sw = hh[:, 7]
+    print("cycles per sweep (mean over instances):", {n_: round(float(np.mean(hh[:, q] / sw))) for q, n_ in enumerate(names)},
+          "total", round(float(np.mean(hh[:, :7].sum(1) / sw))))
+    hs = h.view(cnt, its)[:, 8:12].cpu().numpy()
+    print("A update split:", {n_: round(float(np.mean(hs[:, q] / sw))) for q, n_ in
+                              enumerate(["H + cluster sync", "DSMEM reduce", "solve_gram", "gram"])})
