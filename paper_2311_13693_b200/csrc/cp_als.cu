@@ -366,7 +366,35 @@ __device__ void apply_pinv(const double* Mt, int rows, int R, const double* P, d
 // safely positive definite (a pivot below 1e-11 of the largest diagonal —
 // well above the reference's rcond = 1e-12 of sigma_max cut, linalg.cpp:56)
 // it falls back to the Jacobi pseudo-inverse, i.e. the reference semantics.
+// Cholesky trailing update of row i: L(i, j) -= L(i, k) L(j, k) for k < j <= i.
+// The row (stride R) and column k never share an element, and saying so
+// (__restrict__) lets the loads of successive j issue ahead of the stores.
+__device__ __forceinline__ void chol_row_update(double* __restrict__ row, const double* __restrict__ colk, int R, int k,
+                                                int i, double lik) {
+  int j = k + 1;
+  for (; j + 3 <= i; j += 4) {
+    const double c0 = colk[j], c1 = colk[j + 1], c2 = colk[j + 2], c3 = colk[j + 3];
+    const double r0 = row[R * j], r1 = row[R * (j + 1)], r2 = row[R * (j + 2)], r3 = row[R * (j + 3)];
+    row[R * j] = fma(-lik, c0, r0);
+    row[R * (j + 1)] = fma(-lik, c1, r1);
+    row[R * (j + 2)] = fma(-lik, c2, r2);
+    row[R * (j + 3)] = fma(-lik, c3, r3);
+  }
+  for (; j <= i; ++j) row[R * j] = fma(-lik, colk[j], row[R * j]);
+}
+
+__device__ long long g_sg_cycles[5];  // diagnostics: solve_gram split of block 0 (XTSG_ALS_CL_DBG)
+
 __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, double* F, int* ok) {
+  const bool tw = blockIdx.x == 0 && threadIdx.x == 0;
+  long long t0 = tw ? clock64() : 0;
+  auto tmark = [&](int q) {
+    if (tw) {
+      const long long t = clock64();
+      g_sg_cycles[q] += t - t0;
+      t0 = t;
+    }
+  };
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     double* Lm = s.P;  // lower triangle, column-major R x R
@@ -376,8 +404,11 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
     // right-looking Cholesky in place (lower triangle of s.P), warp-synchronous
     for (int e = lane; e < R * R; e += 32) Lm[e] = s.H[e];
     __syncwarp();
+    // largest diagonal: one load per lane and a warp max (not R dependent loads)
     double mxd = 0.0;
-    for (int i = 0; i < R; ++i) mxd = fmax(mxd, Lm[i + R * i]);
+    for (int i = lane; i < R; i += 32) mxd = fmax(mxd, Lm[i + R * i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mxd = fmax(mxd, __shfl_xor_sync(0xffffffffu, mxd, o));
     bool good = mxd > 0.0;
     for (int k = 0; k < R && good; ++k) {
       const double d = Lm[k + R * k];
@@ -395,14 +426,14 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
         s.V[k + R * k] = rl;
       }
       __syncwarp();
-      const int m = R - k - 1;
-      for (int t = lane; t < m * m; t += 32) {
-        const int i = k + 1 + t % m, j = k + 1 + t / m;
-        if (i >= j) Lm[i + R * j] = fma(-Lm[i + R * k], Lm[j + R * k], Lm[i + R * j]);
-      }
+      // trailing update, lane over rows i (the same fma per element as a
+      // flat (i, j) walk, without an integer division per element; a row's
+      // columns are independent, so their loads overlap)
+      for (int i = k + 1 + lane; i < R; i += 32) chol_row_update(Lm + i, Lm + R * k, R, k, i, Lm[i + R * k]);
       __syncwarp();
     }
-    if (good) {
+    tmark(0);
+    if (good && R > 16) {
       // L^-1 column by column (lane c), still inside warp 0: H^-1 = L^-T L^-1
       for (int c = lane; c < R; c += 32)
         for (int i = c + 1; i < R; ++i) {
@@ -412,10 +443,45 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
         }
     }
     if (lane == 0) *ok = good ? 1 : 0;
+    tmark(1);
     }
   }
   __syncthreads();
-  if (*ok) {
+  tmark(2);
+  if (*ok && R <= 16) {
+    // R <= 16: one forward and one back substitution per row of Mt
+    // (L y = m_x, L' f = y; 1 / L(k,k) on the diagonal of s.V), every
+    // thread a row, the R values of the row in registers
+    const double* Lm = s.P;
+    for (int x = threadIdx.x; x < rows; x += blockDim.x) {
+      double y[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (k < R) {
+          double acc = Mt[x + rows * k];
+#pragma unroll
+          for (int j = 0; j < k; ++j) acc = fma(-Lm[k + R * j], y[j], acc);
+          y[k] = acc * s.V[k + R * k];
+        } else {
+          y[k] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int k = 15; k >= 0; --k) {
+        if (k < R) {
+          double acc = y[k];
+#pragma unroll
+          for (int j = k + 1; j < 16; ++j)
+            if (j < R) acc = fma(-Lm[j + R * k], y[j], acc);
+          y[k] = acc * s.V[k + R * k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (k < R) F[x + rows * k] = y[k];
+    }
+    tmark(4);
+  } else if (*ok) {
     // H^-1 (into s.H) and F = Mt H^-1 over all threads
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
       const int a = e % R, b = e / R;
@@ -424,12 +490,14 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
       s.H[e] = acc;
     }
     __syncthreads();
+    tmark(3);
     for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
       const int x = e % rows, r = e / rows;
       double acc = 0.0;
       for (int q = 0; q < R; ++q) acc = fma(Mt[x + rows * q], s.H[q + R * r], acc);
       F[e] = acc;
     }
+    tmark(4);
   } else {
     pinv_sym(s.H, R, s);
     apply_pinv(Mt, rows, R, s.P, F);
@@ -1430,6 +1498,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     }
     prev = err;
   }
+  if (dbg && blockIdx.x == 0 && threadIdx.x == 0)
+    printf("solve_gram cycles per call (block 0): chol %lld, L^-1 %lld, sync %lld, H^-1+sync %lld, apply %lld\n",
+           g_sg_cycles[0] / (3 * it), g_sg_cycles[1] / (3 * it), g_sg_cycles[2] / (3 * it),
+           g_sg_cycles[3] / (3 * it), g_sg_cycles[4] / (3 * it));
   if (dbg && crank == 0 && threadIdx.x == 0 && in.cfg.max_iters >= 8) {
     for (int ph = 0; ph < 7; ++ph) in.hist[ph] = static_cast<double>(tph[ph]);
     in.hist[7] = static_cast<double>(it);
