@@ -331,6 +331,28 @@ def sparse_c4(xt, torch, dev):
     from oracle.oracle import rel_diff
     got = xt.Plan.replicas(y.cpu().numpy(), P, red)
     err = max(rel_diff(xt.comp_from_factors(f, ens.u[p], ens.v[p], ens.w[p]), got[p]) for p in (0, P - 1))
+    # the same nonzeros as unsorted COO (north_star config 4's input format):
+    # a random permutation, so every call groups them into fibers itself
+    nf_per_slice = fj.numel() // sk.numel()
+    npf = ni.numel() // fj.numel()
+    perm = torch.randperm(nnz, device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+    ck = sk.repeat_interleave(nf_per_slice * npf)[perm]
+    cj = fj.repeat_interleave(npf)[perm]
+    ci, cv = ni[perm], nv[perm]
+    del perm
+    yc = torch.zeros_like(y)
+    with torch.cuda.stream(st):
+        plan.compress_coo(ci, cj, ck, cv, y=yc, stream=st)
+        csteps = 3
+        e0.record(st)
+        for _ in range(csteps):
+            plan.compress_coo(ci, cj, ck, cv, y=yc, stream=st)
+        e1.record(st)
+    torch.cuda.synchronize()
+    coo_ms = e0.elapsed_time(e1) / csteps
+    got = xt.Plan.replicas(yc.cpu().numpy(), P, red)
+    coo_err = max(rel_diff(xt.comp_from_factors(f, ens.u[p], ens.v[p], ens.w[p]), got[p]) for p in (0, P - 1))
+    del ci, cj, ck, cv, yc
     plan.close()
     host = [t.cpu().numpy() for t in csf]
     del csf, sk, sp, fj, fp, ni, nv, y
@@ -355,6 +377,10 @@ def sparse_c4(xt, torch, dev):
                                          "achieved": 16.0 * rate / 1e9, "peak": hbm, "unit": "GB/s",
                                          "frac": 16.0 * rate / 1e9 / hbm},
             "max_rel_err_vs_comp_from_factors": float(err),
+            "coo_unsorted": {"value": nnz / (coo_ms / 1e3), "unit": "nnz/s", "ms_per_step": coo_ms, "steps": 3,
+                             "input": "the same nonzeros as device COO in random order (grouped into fibers "
+                                      "inside every call: 25-bit radix sort of compact (rank k, rank j) keys)",
+                             "max_rel_err_vs_comp_from_factors": float(coo_err)},
             "e2e_host_csf_multi_api": {"value": nnz / wall, "unit": "nnz/s", "wall_s": wall,
                                        "h2d_bytes_per_step": int(sum(a.nbytes for a in host)),
                                        "d2h_bytes_per_step": int(yh.nbytes),
