@@ -108,6 +108,23 @@ def test_comp_any_magnitude(gpu, restated, scale, outlier):
     plan.close()
 
 
+@pytest.mark.parametrize("scale", [1e-12, 1e9])
+def test_comp_factored_any_magnitude(gpu, restated, scale):
+    """Factored sources take X's pre-scale from the factor bound
+    sum_r max|a_r| max|b_r| max|c_r| (no pass over the slabs); tiny and huge
+    factors compress to the same tolerance."""
+    dims, red, P, S, R = (300, 260, 90), (32, 32, 32), 6, 8, 5
+    seed = restated.derive(2, 11)
+    a, b, c = restated.generate_dense(dims, R, 3)
+    f = (np.asfortranarray(a * scale), b, c)
+    ens = restated.ensemble_cols(dims, red, P, S, seed)
+    want = [restated.comp_from_factors(*f, ens[0][p], ens[1][p], ens[2][p]) for p in range(P)]
+    plan = gpu.Plan(dims, red, P, S, seed, precision=gpu.PREC_FP16X3)
+    errs = _errs(want, plan.compress_factors(f), P, red)
+    assert max(errs) <= COMP_TOL, errs
+    plan.close()
+
+
 def test_comp_sparse_input_rejected(gpu):
     plan = gpu.Plan((64, 64, 8), (32, 32, 8), 2, 4, 1, precision=gpu.PREC_FP16X3)
     with pytest.raises(gpu.UsageError):
