@@ -854,6 +854,68 @@ __global__ void coo_scan_kernel(const int32_t* __restrict__ ii, const int32_t* _
   }
 }
 
+// Random-order COO: the same checks and bitmaps split by mode so that each
+// used-value bitmap (<= 200 KB) sits in one CTA's shared memory — no random
+// L2 read per nonzero and mode. coo_check_kernel: range and (k, j) order;
+// coo_bits_kernel: one mode's used bits, ORed into the global bitmap once per
+// non-zero word per CTA.
+__global__ void coo_check_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                 const int32_t* __restrict__ kk, int64_t nnz, int64_t I, int64_t J, int64_t K,
+                                 int* __restrict__ bad) {
+  bool b0 = false, b1 = false;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t i = ii[e], j = jj[e], k = kk[e];
+    b0 |= i < 0 || i >= I || j < 0 || j >= J || k < 0 || k >= K;
+    if (e + 1 < nnz) {
+      const int32_t k2 = kk[e + 1], j2 = jj[e + 1];
+      b1 |= k2 < k || (k2 == k && j2 < j);
+    }
+  }
+  if (__any_sync(0xffffffffu, b0) && (threadIdx.x & 31) == 0) bad[0] = 1;
+  if (__any_sync(0xffffffffu, b1) && (threadIdx.x & 31) == 0) bad[1] = 1;
+}
+
+__global__ void __launch_bounds__(1024) coo_bits_kernel(const int32_t* __restrict__ v, int64_t nnz, int64_t n,
+                                                        uint32_t* __restrict__ used) {
+  extern __shared__ uint32_t sb[];
+  const int64_t nw = (n + 31) / 32;
+  for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) sb[w] = 0u;
+  __syncthreads();
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t x = v[e];
+    if (x < 0 || x >= n) continue;  // reported by coo_check_kernel
+    const uint32_t bit = 1u << (x & 31);
+    if (!(sb[x >> 5] & bit)) atomicOr(&sb[x >> 5], bit);
+  }
+  __syncthreads();
+  for (int64_t w = threadIdx.x; w < nw; w += blockDim.x)
+    if (sb[w]) atomicOr(used + w, sb[w]);
+}
+
+// rank of every value v < n in the used set (-1 when unused): one 4-byte
+// lookup per nonzero instead of a bitmap word + a base
+__global__ void rank_table_kernel(const uint32_t* __restrict__ bits, const int64_t* __restrict__ base, int64_t n,
+                                  int32_t* __restrict__ rank) {
+  for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < n;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t w = bits[x >> 5], bit = 1u << (x & 31);
+    rank[x] = (w & bit) ? static_cast<int32_t>(base[x >> 5] + __popc(w & (bit - 1u))) : -1;
+  }
+}
+
+__global__ void coo_tkey_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                const int32_t* __restrict__ kk, const float* __restrict__ vv, int64_t nnz,
+                                const int32_t* __restrict__ rk, const int32_t* __restrict__ rj, uint32_t nju,
+                                uint32_t* __restrict__ key, uint64_t* __restrict__ pay) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    key[e] = static_cast<uint32_t>(rk[kk[e]]) * nju + static_cast<uint32_t>(rj[jj[e]]);
+    pay[e] = (static_cast<uint64_t>(static_cast<uint32_t>(ii[e])) << 32) | __float_as_uint(vv[e]);
+  }
+}
+
 __global__ void popc_kernel(const uint32_t* __restrict__ bits, int64_t nw, int32_t* __restrict__ cnt) {
   for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < nw;
        w += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -930,8 +992,21 @@ bool Plan::sparse_tc_coo32(const int32_t* i, const int32_t* j, const int32_t* k,
   usedj.zero();
   DevBuf<int> flags(2, s);
   flags.zero();
-  coo_scan_kernel<<<gridn(nnz), 256, 0, s>>>(i, j, k, nnz, I, J, K, usedk.ptr, usedj.ptr, flags.ptr);
-  XLAUNCH_CHECK();
+  // per-mode shared-memory bitmaps when both fit a CTA (C4: 10^6 values, 122 KB)
+  const size_t bmk = static_cast<size_t>(nwk) * 4, bmj = static_cast<size_t>(nwj) * 4;
+  const bool smem_bits = bmk <= 200 * 1024 && bmj <= 200 * 1024;
+  if (smem_bits) {
+    coo_check_kernel<<<gridn(nnz), 256, 0, s>>>(i, j, k, nnz, I, J, K, flags.ptr);
+    XLAUNCH_CHECK();
+    XCUDA(cudaFuncSetAttribute(coo_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    coo_bits_kernel<<<sm_count(), 1024, bmk, s>>>(k, nnz, K, usedk.ptr);
+    XLAUNCH_CHECK();
+    coo_bits_kernel<<<sm_count(), 1024, bmj, s>>>(j, nnz, J, usedj.ptr);
+    XLAUNCH_CHECK();
+  } else {
+    coo_scan_kernel<<<gridn(nnz), 256, 0, s>>>(i, j, k, nnz, I, J, K, usedk.ptr, usedj.ptr, flags.ptr);
+    XLAUNCH_CHECK();
+  }
   DevBuf<int32_t> ck(static_cast<size_t>(nwk), s), cj(static_cast<size_t>(nwj), s);
   DevBuf<int64_t> basek(static_cast<size_t>(nwk + 1), s), basej(static_cast<size_t>(nwj + 1), s);
   popc_kernel<<<gridn(nwk), 256, 0, s>>>(usedk.ptr, nwk, ck.ptr);
@@ -956,9 +1031,21 @@ bool Plan::sparse_tc_coo32(const int32_t* i, const int32_t* j, const int32_t* k,
   XLAUNCH_CHECK();
   DevBuf<uint32_t> keys(static_cast<size_t>(nnz), s);
   DevBuf<uint64_t> pay(static_cast<size_t>(nnz), s);
-  coo_ckey_kernel<<<gridn(nnz), 256, 0, s>>>(i, j, k, val, nnz, usedk.ptr, basek.ptr, usedj.ptr, basej.ptr,
-                                             static_cast<uint32_t>(nju), keys.ptr, pay.ptr);
-  XLAUNCH_CHECK();
+  if (K + J <= (int64_t(1) << 27)) {
+    // rank tables (4 bytes per index value, L2-resident at C4's 2 x 10^6)
+    DevBuf<int32_t> rk(static_cast<size_t>(K), s), rj(static_cast<size_t>(J), s);
+    rank_table_kernel<<<gridn(K), 256, 0, s>>>(usedk.ptr, basek.ptr, K, rk.ptr);
+    XLAUNCH_CHECK();
+    rank_table_kernel<<<gridn(J), 256, 0, s>>>(usedj.ptr, basej.ptr, J, rj.ptr);
+    XLAUNCH_CHECK();
+    coo_tkey_kernel<<<gridn(nnz), 256, 0, s>>>(i, j, k, val, nnz, rk.ptr, rj.ptr, static_cast<uint32_t>(nju),
+                                               keys.ptr, pay.ptr);
+    XLAUNCH_CHECK();
+  } else {
+    coo_ckey_kernel<<<gridn(nnz), 256, 0, s>>>(i, j, k, val, nnz, usedk.ptr, basek.ptr, usedj.ptr, basej.ptr,
+                                               static_cast<uint32_t>(nju), keys.ptr, pay.ptr);
+    XLAUNCH_CHECK();
+  }
   tr.mark("keys");
   if (hf[1]) {
     DevBuf<uint32_t> keys2(static_cast<size_t>(nnz), s);
