@@ -383,18 +383,7 @@ __device__ __forceinline__ void chol_row_update(double* __restrict__ row, const 
   for (; j <= i; ++j) row[R * j] = fma(-lik, colk[j], row[R * j]);
 }
 
-__device__ long long g_sg_cycles[5];  // diagnostics: solve_gram split of block 0 (XTSG_ALS_CL_DBG)
-
 __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, double* F, int* ok) {
-  const bool tw = blockIdx.x == 0 && threadIdx.x == 0;
-  long long t0 = tw ? clock64() : 0;
-  auto tmark = [&](int q) {
-    if (tw) {
-      const long long t = clock64();
-      g_sg_cycles[q] += t - t0;
-      t0 = t;
-    }
-  };
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     double* Lm = s.P;  // lower triangle, column-major R x R
@@ -432,7 +421,6 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
       for (int i = k + 1 + lane; i < R; i += 32) chol_row_update(Lm + i, Lm + R * k, R, k, i, Lm[i + R * k]);
       __syncwarp();
     }
-    tmark(0);
     if (good && R > 16) {
       // L^-1 column by column (lane c), still inside warp 0: H^-1 = L^-T L^-1
       for (int c = lane; c < R; c += 32)
@@ -443,11 +431,9 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
         }
     }
     if (lane == 0) *ok = good ? 1 : 0;
-    tmark(1);
     }
   }
   __syncthreads();
-  tmark(2);
   if (*ok && R <= 16) {
     // R <= 16: one forward and one back substitution per row of Mt
     // (L y = m_x, L' f = y; 1 / L(k,k) on the diagonal of s.V), every
@@ -480,7 +466,6 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
       for (int k = 0; k < 16; ++k)
         if (k < R) F[x + rows * k] = y[k];
     }
-    tmark(4);
   } else if (*ok) {
     // H^-1 (into s.H) and F = Mt H^-1 over all threads
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -490,14 +475,12 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
       s.H[e] = acc;
     }
     __syncthreads();
-    tmark(3);
     for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
       const int x = e % rows, r = e / rows;
       double acc = 0.0;
       for (int q = 0; q < R; ++q) acc = fma(Mt[x + rows * q], s.H[q + R * r], acc);
       F[e] = acc;
     }
-    tmark(4);
   } else {
     pinv_sym(s.H, R, s);
     apply_pinv(Mt, rows, R, s.P, F);
@@ -1498,10 +1481,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     }
     prev = err;
   }
-  if (dbg && blockIdx.x == 0 && threadIdx.x == 0)
-    printf("solve_gram cycles per call (block 0): chol %lld, L^-1 %lld, sync %lld, H^-1+sync %lld, apply %lld\n",
-           g_sg_cycles[0] / (3 * it), g_sg_cycles[1] / (3 * it), g_sg_cycles[2] / (3 * it),
-           g_sg_cycles[3] / (3 * it), g_sg_cycles[4] / (3 * it));
   if (dbg && crank == 0 && threadIdx.x == 0 && in.cfg.max_iters >= 8) {
     for (int ph = 0; ph < 7; ++ph) in.hist[ph] = static_cast<double>(tph[ph]);
     in.hist[7] = static_cast<double>(it);
