@@ -1321,7 +1321,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       }
     }
     phase(0);
-    tl2 = clock64();
+    if (dbg) tl2 = clock64();
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G2[e];
     cl.sync();
     if (dbg) { const long long t = clock64(); tsub[0] += t - tl2; tl2 = t; }
