@@ -383,9 +383,23 @@ __device__ __forceinline__ void chol_row_update(double* __restrict__ row, const 
   for (; j <= i; ++j) row[R * j] = fma(-lik, colk[j], row[R * j]);
 }
 
+// solve_gram in two halves: gram_factor_warp0 (warp 0: Cholesky of s.H into
+// s.P / s.V, *ok) and gram_solve_factored (every thread, after a barrier:
+// substitution, or the Jacobi pseudo-inverse when the factor failed). The
+// cluster kernel runs the first half for the B update while the other warps
+// compute P = A' T, since its input G3 .* G1 is known one phase early.
+__device__ void gram_factor_warp0(int R, const Smem& s, int* ok);
+__device__ void gram_solve_factored(const double* Mt, int rows, int R, const Smem& s, double* F, const int* ok);
+
 __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, double* F, int* ok) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
+  if (threadIdx.x < 32) gram_factor_warp0(R, s, ok);
+  __syncthreads();
+  gram_solve_factored(Mt, rows, R, s, F, ok);
+}
+
+__device__ void gram_factor_warp0(int R, const Smem& s, int* ok) {
+  {
+    const int lane = threadIdx.x & 31;
     double* Lm = s.P;  // lower triangle, column-major R x R
     if (R > 64) {  // the per-row substitution keeps R values in registers/local memory
       if (lane == 0) *ok = 0;
@@ -433,7 +447,9 @@ __device__ void solve_gram(const double* Mt, int rows, int R, const Smem& s, dou
     if (lane == 0) *ok = good ? 1 : 0;
     }
   }
-  __syncthreads();
+}
+
+__device__ void gram_solve_factored(const double* Mt, int rows, int R, const Smem& s, double* F, const int* ok) {
   if (*ok && R <= 16) {
     // R <= 16: one forward and one back substitution per row of Mt
     // (L y = m_x, L' f = y; 1 / L(k,k) on the diagonal of s.V), every
@@ -1340,10 +1356,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     __syncthreads();
     if (dbg) { const long long t = clock64(); tsub[3] += t - tl2; tl2 = t; }
     phase(1);
-    // ---- P = A' T_c on the slab (DMMA: 8 r x 8 fibers tiles, K = i), M_B partial
-    {
+    // ---- P = A' T_c on the slab (DMMA: 8 r x 8 fibers tiles, K = i) by warps
+    // 1..7 while warp 0 factors the B update's Gram H = G3 .* G1 (known now:
+    // the same Cholesky solve_gram would run after the M_B reduction)
+    if (warp == 0) {
+      for (int e = lane; e < R * R; e += 32) s.H[e] = s.G3[e] * s.G1[e];
+      __syncwarp();
+      gram_factor_warp0(R, s, &s_ok);
+    } else {
       const int ntr = (R + 7) / 8, ntf = (nf + 7) / 8;
-      for (int tile = warp; tile < ntr * ntf; tile += nwarps) {
+      for (int tile = warp - 1; tile < ntr * ntf; tile += nwarps - 1) {
         const int r0 = (tile % ntr) * 8, f0 = (tile / ntr) * 8;
         const int ra = r0 + lr, fb = f0 + lr;
         double d0 = 0.0, d1 = 0.0;
@@ -1369,7 +1391,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       for (int kk = 0; kk < nk; ++kk) acc = fma(s.C[(k0 + kk) + n3 * r], pr[n2 * kk], acc);
       MBp[e] = acc;
     }
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G3[e] * s.G1[e];
     cl.sync();
     for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
       double v = 0.0;
@@ -1378,7 +1399,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       s.M[e] = v;
     }
     __syncthreads();
-    solve_gram(s.M, n2, R, s, s.B, &s_ok);
+    gram_solve_factored(s.M, n2, R, s, s.B, &s_ok);
     __syncthreads();
     gram(s.B, n2, R, s.G2);
     __syncthreads();
