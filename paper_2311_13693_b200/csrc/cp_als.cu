@@ -1404,18 +1404,24 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     gram(s.B, n2, R, s.G2);
     __syncthreads();
     phase(3);
-    // ---- C rows of this slab: M_C[kk, r] = sum_j B[j, r] P[r][kk][j]
-    for (int e = threadIdx.x; e < nk * R; e += blockDim.x) {
-      const int kk = e % nk, r = e / nk;
-      const double* pr = Pl + static_cast<int64_t>(r) * n2 * kc + n2 * kk;
-      const double* Br = s.B + n2 * r;
-      double acc = 0.0;
-      for (int j = 0; j < n2; ++j) acc = fma(Br[j], pr[j], acc);
-      s.M[e] = acc;
+    // ---- C rows of this slab: M_C[kk, r] = sum_j B[j, r] P[r][kk][j] by
+    // warps 1..7 while warp 0 factors H = G2 .* G1
+    if (warp == 0) {
+      for (int e = lane; e < R * R; e += 32) s.H[e] = s.G2[e] * s.G1[e];
+      __syncwarp();
+      gram_factor_warp0(R, s, &s_ok);
+    } else {
+      for (int e = threadIdx.x - 32; e < nk * R; e += blockDim.x - 32) {
+        const int kk = e % nk, r = e / nk;
+        const double* pr = Pl + static_cast<int64_t>(r) * n2 * kc + n2 * kk;
+        const double* Br = s.B + n2 * r;
+        double acc = 0.0;
+        for (int j = 0; j < n2; ++j) acc = fma(Br[j], pr[j], acc);
+        s.M[e] = acc;
+      }
     }
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) s.H[e] = s.G2[e] * s.G1[e];
     __syncthreads();
-    solve_gram(s.M, nk, R, s, Cown, &s_ok);
+    gram_solve_factored(s.M, nk, R, s, Cown, &s_ok);
     cl.sync();
     // all-gather the new C rows from their owners
     for (int e = threadIdx.x; e < n3 * R; e += blockDim.x) {
